@@ -1,0 +1,303 @@
+"""kkgen — seeded synthetic KK-link input generator (transmitter + linear channel + ADC).
+
+This module is the ONLY code shared by the oracle side (tests, bench `cpu_baseline`)
+and the CUDA side (tests, bench). It holds none of the receiver method's arithmetic:
+it builds the *input* of the method — the int16 ADC codes of a minimum-phase KK
+photocurrent — and the transmitted labels, exactly as the paper's transmitter and
+link describe them (§2 "Experimental setup"):
+
+  * 1 GBaud QAM (4/8/16/32/64) labels from a counter-based hash keyed by
+    (seed, global symbol index) — chunk- and shard-invariant;
+  * 1 %-roll-off RRC pulse shaping at 4 sps, span 256 symbols;
+  * chromatic dispersion as the all-pass exp(+i·β₂L/2·ω²) on the data field,
+    ω the optical angular offset from the laser/tone;
+  * carrier tone A at the field DC, data at +0.516 GHz;
+  * complex AWGN on the field before square law ("white" over the 4 GHz
+    simulation band, or "analytic" = positive frequencies only);
+  * square-law detection |E|² and an ideal DC-coupled int16 ADC.
+
+Everything is fp64 and device-agnostic torch (CPU for tests; CUDA for the bench's
+multi-GiB streams). Random numbers come from a counter-based integer hash so the
+sample at global index n never depends on how the stream is chunked or sharded.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+import torch
+from scipy.fft import next_fast_len
+
+FS = 4.0e9          # ADC rate ("4 GS/s ADC")
+BAUD = 1.0e9        # symbol rate ("1 GBaud")
+SPS = 4
+F_C = 0.516e9       # tone offset ("carrier tone at 0.516 GHz")
+LO_NUM, LO_DEN = 129, 1000   # F_C / FS = 0.129 exactly
+ROLLOFF = 0.01      # PAPER.md:50 "1% roll-off"
+RRC_SPAN = 256
+LAMBDA_M = 1550.51e-9  # PAPER.md:50 ECL wavelength
+C_LIGHT = 299792458.0
+FRAME_SYMBOLS = 4096  # SURVEY R23 (used only to place the per-segment format schedule)
+
+# ----------------------------------------------------------------------------------
+# counter-based hash (murmur3 fmix32 on int64 tensors, overflow-free 32-bit multiply)
+# ----------------------------------------------------------------------------------
+_M32 = 0xFFFFFFFF
+
+
+def _mul32(x: torch.Tensor, c: int) -> torch.Tensor:
+    lo, hi = c & 0xFFFF, c >> 16
+    return (x * lo + (((x * hi) & 0xFFFF) << 16)) & _M32
+
+
+def _fmix32(x: torch.Tensor) -> torch.Tensor:
+    x = x ^ (x >> 16)
+    x = _mul32(x, 0x85EBCA6B)
+    x = x ^ (x >> 13)
+    x = _mul32(x, 0xC2B2AE35)
+    x = x ^ (x >> 16)
+    return x
+
+
+def hash_u32(seed: int, stream: int, idx: torch.Tensor) -> torch.Tensor:
+    """32-bit hash of (seed, stream, idx) for int64 idx (any sign)."""
+    key = _fmix32(torch.tensor(((seed * 0x9E3779B1) ^ (stream * 0x7F4A7C15)) & _M32,
+                               dtype=torch.int64, device=idx.device))
+    lo = idx & _M32
+    hi = (idx >> 32) & _M32
+    h = _fmix32(lo ^ key)
+    h = _fmix32(h ^ hi ^ 0x68E31DA4)
+    return _fmix32(h ^ key)
+
+
+def uniform01(seed: int, stream: int, idx: torch.Tensor) -> torch.Tensor:
+    return (hash_u32(seed, stream, idx).to(torch.float64) + 0.5) * (1.0 / 4294967296.0)
+
+
+def gauss_complex(seed: int, idx: torch.Tensor) -> torch.Tensor:
+    """Unit-variance circular complex Gaussian per index (Box-Muller, E|n|^2 = 1)."""
+    u1 = uniform01(seed, 11, idx)
+    u2 = uniform01(seed, 12, idx)
+    r = torch.sqrt(-torch.log(u1))          # |n|^2 ~ Exp(1)
+    ph = 2.0 * math.pi * u2
+    return torch.complex(r * torch.cos(ph), r * torch.sin(ph))
+
+
+# ----------------------------------------------------------------------------------
+# transmitter alphabets (labels -> points), SURVEY R13
+# ----------------------------------------------------------------------------------
+_CROSS32_ROWS = [  # rows Q=+5..-5, columns I=-5..+5; -1 = empty corner
+    [-1, 3, 2, 18, 19, -1],
+    [6, 14, 10, 26, 30, 22],
+    [7, 15, 11, 27, 31, 23],
+    [5, 13, 9, 25, 29, 21],
+    [4, 12, 8, 24, 28, 20],
+    [-1, 0, 1, 17, 16, -1],
+]
+
+
+def tx_alphabet(M: int) -> np.ndarray:
+    """points[label] (complex128, unit mean energy) for the transmitter mapper."""
+    pts = np.zeros(M, np.complex128)
+    gray = lambda i: i ^ (i >> 1)
+    if M in (4, 16, 64):
+        m = int(round(math.sqrt(M)))
+        b2 = int(round(math.log2(m)))
+        sc = 1.0 / math.sqrt(2.0 * (M - 1) / 3.0)
+        for iI in range(m):
+            for iQ in range(m):
+                pts[(gray(iI) << b2) | gray(iQ)] = sc * complex(2 * iI - (m - 1), 2 * iQ - (m - 1))
+    elif M == 8:
+        sc = 1.0 / math.sqrt(6.0)
+        for iI in range(4):
+            for iQ in range(2):
+                pts[(gray(iI) << 1) | iQ] = sc * complex(2 * iI - 3, 2 * iQ - 1)
+    elif M == 32:
+        sc = 1.0 / math.sqrt(20.0)
+        for r, row in enumerate(_CROSS32_ROWS):
+            for c, lab in enumerate(row):
+                if lab >= 0:
+                    pts[lab] = sc * complex(2 * c - 5, 5 - 2 * r)
+    else:
+        raise ValueError(f"unsupported QAM order {M}")
+    return pts
+
+
+def rrc_taps_tx(rolloff: float = ROLLOFF, span: int = RRC_SPAN, sps: int = SPS) -> np.ndarray:
+    """Transmit RRC taps (unit energy, length span*sps+1, centred); textbook RRC impulse response."""
+    n = np.arange(-span * sps // 2, span * sps // 2 + 1, dtype=np.float64)
+    t = n / sps
+    b = rolloff
+    h = np.empty_like(t)
+    for i, ti in enumerate(t):
+        if ti == 0.0:
+            h[i] = 1.0 + b * (4.0 / math.pi - 1.0)
+        elif abs(abs(4.0 * b * ti) - 1.0) < 1e-12:
+            h[i] = (b / math.sqrt(2.0)) * ((1 + 2 / math.pi) * math.sin(math.pi / (4 * b))
+                                           + (1 - 2 / math.pi) * math.cos(math.pi / (4 * b)))
+        else:
+            h[i] = (math.sin(math.pi * ti * (1 - b)) + 4 * b * ti * math.cos(math.pi * ti * (1 + b))) / (
+                math.pi * ti * (1 - (4 * b * ti) ** 2))
+    return h / math.sqrt(np.sum(h * h))
+
+
+# ----------------------------------------------------------------------------------
+# link configuration
+# ----------------------------------------------------------------------------------
+@dataclass
+class LinkConfig:
+    formats: Sequence[int] = (4,)         # QAM order per segment (cycled)
+    segment_frames: int = 1 << 30         # frames per segment (format constant within)
+    cspr_db: float = 12.0
+    esn0_db: Optional[float] = None       # nominal Es/N0 (None = noiseless)
+    noise: str = "white"                  # "white" | "analytic"
+    dl_ps_nm: float = 0.0                 # accumulated dispersion D*L
+    seed: int = 101
+    wander_rad: float = 0.0               # optional data-vs-tone phase wander amplitude (CPR fixtures)
+    wander_hz: float = 50e3
+    sideband: int = +1
+
+    @property
+    def px(self) -> float:  # mean |x|^2 of the shaped data at 4 sps with unit-energy taps
+        return 1.0 / SPS
+
+    @property
+    def amp(self) -> float:  # tone amplitude from CSPR = A^2 / P_x
+        return math.sqrt(self.px * 10.0 ** (self.cspr_db / 10.0))
+
+    @property
+    def sigma2(self) -> float:  # complex noise variance per 4-GS/s sample
+        if self.esn0_db is None:
+            return 0.0
+        return SPS * self.px / 10.0 ** (self.esn0_db / 10.0)
+
+    @property
+    def i_clip(self) -> float:  # ADC full scale: fixed by the config (chunk-invariant)
+        return (self.amp + 6.0 * math.sqrt(self.px + self.sigma2)) ** 2
+
+    @property
+    def adc_scale(self) -> float:
+        return self.i_clip / 32767.0
+
+    @property
+    def i_ref(self) -> float:  # expected mean intensity
+        return self.amp ** 2 + self.px + self.sigma2
+
+    def format_of_symbols(self, k: torch.Tensor) -> torch.Tensor:
+        seg = torch.div(torch.div(k, FRAME_SYMBOLS, rounding_mode="floor"), self.segment_frames,
+                        rounding_mode="floor")
+        sched = torch.tensor(list(self.formats), dtype=torch.int64, device=k.device)
+        return sched[torch.remainder(seg, len(self.formats))]
+
+
+def esn0_from_osnr(osnr_db: float, cspr_db: float) -> float:
+    """E_s/N_0 of the data part at a given OSNR (0.1 nm, single pol) and CSPR."""
+    return osnr_db + 10 * math.log10(12.5) - 10 * math.log10(1 + 10 ** (cspr_db / 10))
+
+
+def beta2_l(dl_ps_nm: float, lam: float = LAMBDA_M) -> float:
+    """beta_2 * L in s^2 from accumulated D*L in ps/nm (beta_2 = -D lambda^2 / (2 pi c))."""
+    return -(dl_ps_nm * 1e-3) * lam ** 2 / (2 * math.pi * C_LIGHT)
+
+
+# ----------------------------------------------------------------------------------
+# generation
+# ----------------------------------------------------------------------------------
+def symbol_labels(cfg: LinkConfig, k: torch.Tensor) -> torch.Tensor:
+    M = cfg.format_of_symbols(k)
+    return (hash_u32(cfg.seed, 1, k) & (M - 1)).to(torch.uint8)
+
+
+def _symbols(cfg: LinkConfig, k: torch.Tensor) -> torch.Tensor:
+    lab = symbol_labels(cfg, k).to(torch.int64)
+    M = cfg.format_of_symbols(k)
+    out = torch.zeros(k.shape, dtype=torch.complex128, device=k.device)
+    for m in sorted(set(int(x) for x in cfg.formats)):
+        tab = torch.from_numpy(tx_alphabet(m)).to(k.device)
+        sel = M == m
+        out[sel] = tab[lab[sel]]
+    return out
+
+
+def _data_field(cfg: LinkConfig, s0: int, s1: int, device, guard_sym: int = 1024) -> torch.Tensor:
+    """Dispersed, tone-shifted data field x_s[n] for global samples [s0, s1) (multiples of 4)."""
+    assert s0 % SPS == 0 and s1 % SPS == 0
+    k0, k1 = s0 // SPS - guard_sym, s1 // SPS + guard_sym
+    k = torch.arange(k0, k1, dtype=torch.int64, device=device)
+    sym = _symbols(cfg, k)
+    nfft = next_fast_len((k1 - k0) * SPS)
+    u = torch.zeros(nfft, dtype=torch.complex128, device=device)
+    u[: (k1 - k0) * SPS: SPS] = sym
+    h = rrc_taps_tx()
+    half = (len(h) - 1) // 2
+    hc = np.zeros(nfft, np.float64)   # circularly centred taps
+    hc[: half + 1] = h[half:]
+    hc[-half:] = h[:half]
+    Hf = torch.fft.fft(torch.from_numpy(hc).to(device))
+    nu = torch.fft.fftfreq(nfft, d=1.0 / FS, device=device).to(torch.float64)
+    w = 2 * math.pi * (nu + cfg.sideband * F_C)      # optical offset of each data bin
+    cd = torch.exp(1j * (beta2_l(cfg.dl_ps_nm) / 2.0) * w * w)
+    x = torch.fft.ifft(torch.fft.fft(u) * Hf * cd)
+    g = guard_sym * SPS
+    x = x[g: g + (s1 - s0)]
+    n = torch.arange(s0, s1, dtype=torch.int64, device=device)
+    q = torch.remainder(torch.remainder(n, LO_DEN) * LO_NUM, LO_DEN).to(torch.float64)
+    ph = cfg.sideband * 2 * math.pi * q / LO_DEN
+    if cfg.wander_rad:
+        ph = ph + cfg.wander_rad * torch.sin(2 * math.pi * cfg.wander_hz * n.to(torch.float64) / FS)
+    return x * torch.exp(1j * ph)
+
+
+def generate(cfg: LinkConfig, s0: int, s1: int, device="cpu", chunk: int = 1 << 24,
+             return_field: bool = False):
+    """int16 ADC codes for global samples [s0, s1) and labels for symbols [s0/4, s1/4).
+
+    Returns dict(codes=int16[s1-s0], labels=uint8[(s1-s0)/4], and the sidecar numbers).
+    With return_field=True also the noiseless transmitted field E (complex128).
+    """
+    device = torch.device(device)
+    codes = torch.empty(s1 - s0, dtype=torch.int16, device=device)
+    fields = []
+    if cfg.noise == "analytic" and cfg.sigma2 > 0:
+        chunk = max(chunk, s1 - s0)   # analytic noise is a non-local filter: one chunk only
+    for c0 in range(s0, s1, chunk):
+        c1 = min(s1, c0 + chunk)
+        E = cfg.amp + _data_field(cfg, c0, c1, device)
+        if return_field:
+            fields.append(E.clone())
+        if cfg.sigma2 > 0:
+            n = torch.arange(c0, c1, dtype=torch.int64, device=device)
+            nz = gauss_complex(cfg.seed, n)
+            if cfg.noise == "analytic":
+                Nf = torch.fft.fft(nz)
+                nu = torch.fft.fftfreq(c1 - c0, device=device)
+                keep = (nu * cfg.sideband) > 0
+                nz = torch.fft.ifft(torch.where(keep, Nf, torch.zeros_like(Nf)))  # same PSD on f>0
+            E = E + math.sqrt(cfg.sigma2) * nz
+        inten = E.real * E.real + E.imag * E.imag
+        code = torch.clamp(torch.round(inten * (32767.0 / cfg.i_clip)), 0, 32767)
+        codes[c0 - s0: c1 - s0] = code.to(torch.int16)
+    k = torch.arange(s0 // SPS, s1 // SPS, dtype=torch.int64, device=device)
+    out = dict(codes=codes, labels=symbol_labels(cfg, k), adc_scale=cfg.adc_scale,
+               adc_offset=0.0, i_ref=cfg.i_ref, amp=cfg.amp, px=cfg.px, sigma2=cfg.sigma2)
+    if return_field:
+        out["field"] = torch.cat(fields)
+    return out
+
+
+# ----------------------------------------------------------------------------------
+# named workloads (BASELINE.json configs)
+# ----------------------------------------------------------------------------------
+WORKLOADS = {
+    "C1": dict(cfg=LinkConfig(formats=(4,), dl_ps_nm=0.0, cspr_db=12.0, seed=101), samples=1 << 16),
+    "C2": dict(cfg=LinkConfig(formats=(16,), dl_ps_nm=112000.0, cspr_db=6.0,
+                              esn0_db=esn0_from_osnr(17.0, 6.0), seed=201), samples=1 << 22),
+    "C3": dict(cfg=LinkConfig(formats=(64,), dl_ps_nm=32000.0, cspr_db=12.0, esn0_db=26.0, seed=301),
+               samples=1 << 24),
+    "C4": dict(cfg=LinkConfig(formats=(4,), dl_ps_nm=200000.0, cspr_db=12.0, esn0_db=12.0, seed=401),
+               samples=1 << 26),
+    "C5": dict(cfg=LinkConfig(formats=(4, 8, 16, 32, 64), segment_frames=256, dl_ps_nm=32000.0,
+                              cspr_db=12.0, esn0_db=26.0, seed=501), samples=1 << 32),
+}

@@ -1,0 +1,321 @@
+"""The KK receive chain, step by step in fp64 (oracle; TEST INFRASTRUCTURE ONLY).
+
+Steps O1–O11 follow PAPER.md:82 (§2, DSP chain of Fig. 1b) in the paper's order, with
+the north-star changes (BASELINE.json: carrier removal, block-adaptive FIR absorbing CD,
+carrier-phase recovery) and the readings R1–R27 of SURVEY.md §8(c):
+
+  O1  I[n] = s·(c[n] − o)                                   PAPER.md:82 "converts the samples to floating point"
+  O2  a[n] = ½·ln max(I[n], ε), ε = clamp_rel·I_ref         PAPER.md:82 "square-root and logarithm"; R7
+  O3  φ = σ·Hilbert(a) by 1024-pt OLS, hop 512, centre kept   PAPER.md:82 "pair of 1024-point 100% overlap-save FFTs"; R1, R2
+  O4  E[n] = √max(I,ε)·e^{iφ[n]}                              PAPER.md:82 "combined with the amplitude ... reconstruct the optical field"
+  O5  A_f = mean_{n∈f} E[n];  e[n] = E[n] − A_{f(n)}           BASELINE.json north_star "carrier removal"; R8
+  O6  b[n] = e[n]·exp(−2πiσ·((lo_num·n) mod lo_den)/lo_den)    PAPER.md:82 "downshifted to DC"; R9
+  O7  y[m] = Σ_{j=−512}^{512} h[j]·b[2m − j]                    PAPER.md:82 "static equalization and downsampling from 4 to 2"; R4, R5, R6
+  O8  per-frame widely-linear DD least-squares FIR              PAPER.md:82 "adaptive ... DDLMS widely-linear"; north_star; R10, R25, R27
+  O9  CPR: ϑ_b = arg Σ_{k∈b} v_k·conj(D(v_k)); z = v·e^{−iϑ_b}   north_star "carrier-phase recovery"; R12
+  O10 decisions and error counts                             PAPER.md:82 "decisions ... are demapped"; PAPER.md:112
+  O11 Q = 20·log10(√2·erfcinv(2·BER))                        PAPER.md:112; SPEC S:71 (theory.q_from_ber)
+
+Library primitives used as single steps: numpy.fft (O3), scipy.signal.fftconvolve (O7),
+numpy.linalg.lstsq (CD-init fit), dense Φ̃ᴴΦ̃ and numpy.linalg.cholesky/solve (O8),
+brute-force nearest point (O8–O10).
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+from scipy import signal
+
+from .constellation import nearest, popcount
+
+C_LIGHT = 299792458.0
+
+
+@dataclass
+class OracleConfig:
+    fs_hz: float = 4e9
+    baud_hz: float = 1e9
+    lo_num: int = 129                 # f_c / f_s = 129/1000 ("0.516 GHz" at 4 GS/s)
+    lo_den: int = 1000
+    sideband: int = +1                # data above the tone (R2, R3)
+    rolloff: float = 0.01             # PAPER.md:50 "1% roll-off"
+    rrc_span_sym: int = 256           # R4
+    hilbert_n: int = 1024             # PAPER.md:82 "1024-point"
+    hilbert_hop: int = 512            # R1
+    frame_symbols: int = 4096         # R23
+    eq_taps: int = 0                  # 0 = tap-count rule
+    eq_widely_linear: bool = True     # PAPER.md:82 "widely-linear"
+    eq_ridge: float = 1e-3            # R10
+    cpr_window: int = 256             # R12
+    dispersion_ps_per_nm: float = 0.0
+    lambda_m: float = 1550.51e-9
+    adc_scale: float = 1.0
+    adc_offset: float = 0.0
+    ref_intensity: float = 1.0
+    clamp_rel: float = 1e-12          # R7
+    formats: Sequence[int] = (4,)     # per-segment QAM order (R26)
+    segment_frames: int = 1 << 30
+
+    @property
+    def sps(self) -> int:
+        return int(round(self.fs_hz / self.baud_hz))
+
+    @property
+    def frame_samples(self) -> int:
+        return self.frame_symbols * self.sps
+
+    def fmt_of_frame(self, f: int) -> int:
+        return int(self.formats[(f // self.segment_frames) % len(self.formats)])
+
+
+# ------------------------------------------------------------------------------------------
+# init-time constants
+# ------------------------------------------------------------------------------------------
+def rrc_taps(cfg: OracleConfig) -> np.ndarray:
+    """Unit-energy RRC, span `rrc_span_sym` symbols at 4 sps, index j = −span·2 .. +span·2 (R4)."""
+    sps = cfg.sps
+    half = cfg.rrc_span_sym * sps // 2
+    b = cfg.rolloff
+    h = np.zeros(2 * half + 1)
+    for idx in range(2 * half + 1):
+        t = (idx - half) / sps                     # in symbol periods
+        if t == 0:
+            h[idx] = 1 - b + 4 * b / math.pi
+        elif abs(4 * b * abs(t) - 1) < 1e-12:
+            h[idx] = b / math.sqrt(2) * ((1 + 2 / math.pi) * math.sin(math.pi / (4 * b))
+                                         + (1 - 2 / math.pi) * math.cos(math.pi / (4 * b)))
+        else:
+            num = math.sin(math.pi * t * (1 - b)) + 4 * b * t * math.cos(math.pi * t * (1 + b))
+            h[idx] = num / (math.pi * t * (1 - (4 * b * t) ** 2))
+    return h / np.sqrt(np.sum(h ** 2))
+
+
+def beta2L(cfg: OracleConfig) -> float:
+    """β₂·L (s²) from accumulated dispersion D·L (ps/nm): β₂ = −D·λ²/(2πc)."""
+    dl_si = cfg.dispersion_ps_per_nm * 1e-12 / 1e-9
+    return -dl_si * cfg.lambda_m ** 2 / (2 * math.pi * C_LIGHT)
+
+
+def tap_count(cfg: OracleConfig) -> int:
+    """L = 2·⌈τ_max/(T/2)⌉ + 7, τ_max = |β₂L|·2π·(f_c + (1+β)R_s/2) (SURVEY §8(a) tap-count rule)."""
+    if cfg.eq_taps:
+        return cfg.eq_taps
+    f_c = cfg.fs_hz * cfg.lo_num / cfg.lo_den
+    tau = abs(beta2L(cfg)) * 2 * math.pi * (f_c + (1 + cfg.rolloff) * cfg.baud_hz / 2)
+    return 2 * int(math.ceil(tau / (0.5 / cfg.baud_hz) - 1e-12)) + 7
+
+
+def cd_init_taps(cfg: OracleConfig) -> np.ndarray:
+    """w_cd = argmin Σ_ν |Σ_j w_j e^{−i2πνj/(2R_s)} − C(ν)|², j = −K..K, 2001 ν on ±(1+β)R_s/2,
+    C(ν) = exp(−i·(β₂L/2)·(2π(ν + σf_c))²) — the CD inverse referenced to the tone."""
+    L = tap_count(cfg)
+    K = (L - 1) // 2
+    f_c = cfg.fs_hz * cfg.lo_num / cfg.lo_den
+    nu = np.linspace(-(1 + cfg.rolloff) * cfg.baud_hz / 2, (1 + cfg.rolloff) * cfg.baud_hz / 2, 2001)
+    j = np.arange(-K, K + 1)
+    A = np.exp(-2j * np.pi * np.outer(nu, j) / (2 * cfg.baud_hz))
+    C = np.exp(-1j * (beta2L(cfg) / 2) * (2 * np.pi * (nu + cfg.sideband * f_c)) ** 2)
+    w, *_ = np.linalg.lstsq(A, C, rcond=None)
+    return w
+
+
+# ------------------------------------------------------------------------------------------
+# O1–O7: sample-rate stages on a contiguous global range
+# ------------------------------------------------------------------------------------------
+def o1_intensity(codes: np.ndarray, cfg: OracleConfig) -> np.ndarray:
+    return cfg.adc_scale * (codes.astype(np.float64) - cfg.adc_offset)
+
+
+def o2_front_end(I: np.ndarray, cfg: OracleConfig):
+    eps = cfg.clamp_rel * cfg.ref_intensity
+    clamped = I < eps
+    Ic = np.maximum(I, eps)
+    return 0.5 * np.log(Ic), np.sqrt(Ic), clamped
+
+
+def o3_hilbert_ols(a: np.ndarray, g0: int, out0: int, out1: int, cfg: OracleConfig) -> np.ndarray:
+    """φ[n] for global n ∈ [out0, out1) from a over global [g0, g0+len(a)). Block j keeps
+    [hop·j, hop·j+hop) of the circular Hilbert of a[hop·j − (N−hop)/2, +N); multiplier −i·sgn(q),
+    zero at q ∈ {0, N/2} (R1, R2)."""
+    N, hop = cfg.hilbert_n, cfg.hilbert_hop
+    lead = (N - hop) // 2
+    assert out0 % hop == 0 and out1 % hop == 0
+    q = np.arange(N)
+    mult = np.where((q > 0) & (q < N // 2), -1j, np.where(q > N // 2, 1j, 0.0))
+    phi = np.empty(out1 - out0)
+    for jb in range(out0 // hop, out1 // hop):
+        s = hop * jb - lead - g0
+        assert s >= 0 and s + N <= len(a), "Hilbert input outside the provided range"
+        blk = np.fft.ifft(np.fft.fft(a[s:s + N]) * mult).real
+        phi[hop * jb - out0: hop * jb - out0 + hop] = blk[lead:lead + hop]
+    return cfg.sideband * phi
+
+
+def o5_carrier_removal(E: np.ndarray, e0: int, cfg: OracleConfig):
+    """A_f = mean of E over frame f (global 16384-sample grid); e = E − A_{f(n)} (R8)."""
+    F = cfg.frame_samples
+    assert e0 % F == 0 and len(E) % F == 0
+    A = E.reshape(-1, F).mean(axis=1)
+    return E - np.repeat(A, F), A
+
+
+def o6_mixer(e: np.ndarray, e0: int, cfg: OracleConfig) -> np.ndarray:
+    n = np.arange(e0, e0 + len(e), dtype=np.int64)
+    q = np.mod(cfg.lo_num * np.mod(n, cfg.lo_den), cfg.lo_den)
+    return e * np.exp(-2j * np.pi * cfg.sideband * q / cfg.lo_den)
+
+
+def o7_matched_filter(b: np.ndarray, b0: int, m0: int, m1: int, h: np.ndarray) -> np.ndarray:
+    """y[m] = Σ_j h[j]·b[2m − j] for m ∈ [m0, m1) (exact decimated linear convolution; R6)."""
+    half = (len(h) - 1) // 2
+    c = signal.fftconvolve(b, h, mode="full")          # c[i] = Σ_t h_arr[t]·b[i − t]
+    n = 2 * np.arange(m0, m1, dtype=np.int64)
+    assert n[0] - half >= b0 and n[-1] + half < b0 + len(b), "MF input outside provided range"
+    return c[n - b0 + half]
+
+
+# ------------------------------------------------------------------------------------------
+# O8–O10: per-frame equalizer, CPR, decisions
+# ------------------------------------------------------------------------------------------
+def o8_equalize_frame(yf: np.ndarray, K: int, w_cd: np.ndarray, M: int, cfg: OracleConfig,
+                      widely_linear: Optional[bool] = None):
+    """One frame. yf = y[2k0 − K, 2k0 + 2F − 2 + K] (length 2F − 1 + 2K). Returns (u, info) with
+    u the unbiased pass-2 output of the frame's F symbols (SURVEY §8(a) a7 steps 1–7)."""
+    wl = cfg.eq_widely_linear if widely_linear is None else widely_linear
+    L = 2 * K + 1
+    F = (len(yf) - 2 * K + 1) // 2
+    # (1) regressor φ̃_k = [y[2k − j]]_{j=−K..K} ‖ conj(·)
+    kk = np.arange(F)
+    idx = 2 * kk[:, None] - np.arange(-K, K + 1)[None, :] + K
+    U = yf[idx]
+    Phi = np.concatenate([U, np.conj(U)], axis=1) if wl else U
+    n_par = Phi.shape[1]
+    # (2) θ₀ = [w_cd; 0]
+    th0 = np.concatenate([w_cd, np.zeros(L, complex)]) if wl else w_cd.astype(complex)
+    # (3) AGC: g = (mean |φ̃ᵀθ₀|²)^(−½) ; θ₀ ← g·θ₀   (R25)
+    y0 = Phi @ th0
+    P0 = np.mean(np.abs(y0) ** 2)
+    bad = False
+    g = 1.0 / math.sqrt(P0) if (P0 > 0 and np.isfinite(P0)) else float("nan")
+    if not np.isfinite(g):
+        g, bad = 1.0, True
+    th0 = g * th0
+    # (4) pass 1 and decisions
+    y0 = Phi @ th0
+    d, _ = nearest(y0, M)
+    # (5) DD least squares with ridge toward θ₀: θ₁ = (R + λI)^(−1)(p + λθ₀), λ = ridge·tr(R)/(2L)
+    R = Phi.conj().T @ Phi
+    p = Phi.conj().T @ d
+    lam = cfg.eq_ridge * np.real(np.trace(R)) / n_par
+    Areg = R + lam * np.eye(n_par)
+    try:
+        Lc = np.linalg.cholesky(Areg)
+        th1 = np.linalg.solve(Lc.conj().T, np.linalg.solve(Lc, p + lam * th0))
+        if not np.all(np.isfinite(th1)):
+            raise np.linalg.LinAlgError
+    except np.linalg.LinAlgError:
+        th1, bad = th0, True
+    # (6) pass 2
+    y1 = Phi @ th1
+    # (7) gain unbias: γ = Σ y¹·conj(D(y¹)) / Σ|D(y¹)|² ; y¹ ← y¹/|γ|   (R27)
+    d1, _ = nearest(y1, M)
+    gam = np.sum(y1 * np.conj(d1)) / np.sum(np.abs(d1) ** 2)
+    if abs(gam) > 0 and np.isfinite(abs(gam)):
+        u = y1 / abs(gam)
+    else:
+        u, bad = y1, True
+    return u, dict(theta0=th0, theta1=th1, g=g, gamma=gam, bad=bad, R=R, p=p, lam=lam)
+
+
+def o9_cpr(u: np.ndarray, M: int, W: int):
+    """ϑ_b = arg Σ_{k∈b} u_k·conj(D(u_k)) per W-symbol window aligned to the frame; z = u·e^{−iϑ_b} (R12)."""
+    d, _ = nearest(u, M)
+    s = (u * np.conj(d)).reshape(-1, W).sum(axis=1)
+    th = np.where(s != 0, np.angle(s), 0.0)
+    return u * np.repeat(np.exp(-1j * th), W), th
+
+
+# ------------------------------------------------------------------------------------------
+# the whole chain over a shard
+# ------------------------------------------------------------------------------------------
+def halo(cfg: OracleConfig) -> int:
+    """Samples needed on each side of the core: one neighbour frame + half a Hilbert block."""
+    return cfg.frame_samples + (cfg.hilbert_n - cfg.hilbert_hop) // 2
+
+
+def receive(codes: np.ndarray, first: int, n: int, cfg: OracleConfig, ref: Optional[np.ndarray] = None,
+            keep: bool = True) -> dict:
+    """Run O1–O10 on the core [first, first+n) given codes for [first − H, first + n + H)."""
+    F = cfg.frame_samples
+    H = halo(cfg)
+    assert first % F == 0 and n % F == 0 and n > 0
+    assert len(codes) == n + 2 * H
+    g0 = first - H
+    # O1, O2
+    I = o1_intensity(np.asarray(codes), cfg)
+    a, amp, clamped = o2_front_end(I, cfg)
+    # O3, O4 over core ± one frame
+    e0, e1 = first - F, first + n + F
+    phi = o3_hilbert_ols(a, g0, e0, e1, cfg)
+    E = amp[e0 - g0:e1 - g0] * np.exp(1j * phi)
+    # O5, O6
+    e, A = o5_carrier_removal(E, e0, cfg)
+    b = o6_mixer(e, e0, cfg)
+    # O7 over the 2-sps range the frames need
+    L = tap_count(cfg)
+    K = (L - 1) // 2
+    m0, m1 = first // 2 - K, (first + n) // 2 + K
+    h = rrc_taps(cfg)
+    y = o7_matched_filter(b, e0, m0, m1, h)
+    # O8–O10 per frame
+    w_cd = cd_init_taps(cfg)
+    Fs = cfg.frame_symbols
+    nfr = n // F
+    z = np.zeros(n // cfg.sps, complex)
+    dec = np.zeros(n // cfg.sps, np.int64)
+    counts = dict(sym=np.zeros(5, np.int64), sym_err=np.zeros(5, np.int64), bits=np.zeros(5, np.int64),
+                  bit_err=np.zeros(5, np.int64), clamped=int(clamped[H:H + n].sum()), frames=nfr,
+                  dead_frames=0, bad_frames=0)
+    infos = []
+    for fi in range(nfr):
+        f = first // F + fi
+        M = cfg.fmt_of_frame(f)
+        k0 = fi * Fs                                    # local symbol index
+        dead = bool(np.all(clamped[H + fi * F: H + (fi + 1) * F]))
+        if dead:
+            counts["dead_frames"] += 1
+            zf = np.zeros(Fs, complex)
+            _, lab = nearest(np.full(Fs, -1e-9 - 1e-9j), M)   # D(0) with ties to the lower level (R15)
+            info = dict(dead=True, bad=False)
+        else:
+            yf = y[2 * k0: 2 * k0 + 2 * Fs - 1 + 2 * K]
+            u, info = o8_equalize_frame(yf, K, w_cd, M, cfg)
+            zf, th = o9_cpr(u, M, cfg.cpr_window)
+            info["cpr"] = th
+            counts["bad_frames"] += int(info["bad"])
+            _, lab = nearest(zf, M)
+        z[k0:k0 + Fs] = zf
+        dec[k0:k0 + Fs] = lab
+        bi = int(round(math.log2(M))) - 2
+        counts["sym"][bi] += Fs
+        counts["bits"][bi] += Fs * (bi + 2)
+        if ref is not None:
+            r = np.asarray(ref[k0:k0 + Fs]).astype(np.int64)
+            counts["sym_err"][bi] += int(np.sum(lab != r))
+            counts["bit_err"][bi] += int(np.sum(popcount(lab ^ r)))
+        if keep:
+            infos.append(info)
+    out = dict(z=z, dec=dec, counts=counts, A=A, K=K, L=L)
+    if keep:
+        out.update(E=E, E0=e0, y=y, m0=m0, a=a, phi=phi, b=b, frames=infos, w_cd=w_cd, h=h)
+    return out
+
+
+def o11_q(counts: dict, fmt_index: Optional[int] = None) -> float:
+    from .theory import q_from_ber
+    be = counts["bit_err"] if fmt_index is None else counts["bit_err"][fmt_index]
+    bt = counts["bits"] if fmt_index is None else counts["bits"][fmt_index]
+    return q_from_ber(float(np.sum(be)) / float(np.sum(bt)))

@@ -1,0 +1,59 @@
+"""Checks of the shared seeded input generator (kkgen) against the transmitter definitions."""
+import math
+
+import numpy as np
+import torch
+
+import kkgen
+
+
+def test_cspr_amplitude_definition():
+    # cspr_db = 10 with mean|x|^2 = 0.1 gives A = 1.0 (CSPR = A^2 / P_x)
+    assert abs(math.sqrt(0.1 * 10 ** (10 / 10)) - 1.0) < 1e-15
+    c = kkgen.LinkConfig(cspr_db=10.0)
+    assert abs(c.amp ** 2 / c.px - 10.0) < 1e-12
+
+
+def test_field_power_cspr_and_single_sidedness():
+    cfg = kkgen.LinkConfig(formats=(16,), cspr_db=12.0, seed=5)
+    g = kkgen.generate(cfg, 0, 1 << 16, return_field=True)
+    E = g["field"].numpy()
+    x = E - cfg.amp
+    assert abs(np.mean(np.abs(x) ** 2) / cfg.px - 1) < 0.05
+    X = np.abs(np.fft.fft(x)) ** 2
+    f = np.fft.fftfreq(len(x), d=0.25)              # GHz
+    assert np.sum(X[f > 0]) / np.sum(X) > 0.999      # data strictly above the tone (R3)
+    band = X[(f > 0.011) & (f < 1.021)].sum() / X.sum()
+    assert band > 0.999
+    # Parseval on the detected intensity: mean(I) = mean|E|^2
+    I = np.abs(E) ** 2
+    assert abs(np.mean(I) - np.mean(np.abs(np.fft.fft(E)) ** 2) / len(E)) < 1e-9
+
+
+def test_chunk_invariance():
+    cfg = kkgen.LinkConfig(formats=(4, 16), segment_frames=1, cspr_db=12.0, esn0_db=20.0,
+                           dl_ps_nm=200000.0, seed=9)
+    a = kkgen.generate(cfg, -4096, 1 << 17, chunk=1 << 20)
+    b = kkgen.generate(cfg, -4096, 1 << 17, chunk=1 << 14)
+    assert torch.equal(a["labels"], b["labels"])
+    assert int((a["codes"].to(torch.int32) - b["codes"].to(torch.int32)).abs().max()) <= 1
+
+
+def test_labels_follow_schedule():
+    cfg = kkgen.LinkConfig(formats=(4, 8, 16, 32, 64), segment_frames=2)
+    k = torch.arange(0, 4096 * 20)
+    lab = kkgen.symbol_labels(cfg, k)
+    M = cfg.format_of_symbols(k)
+    assert torch.all(lab.to(torch.int64) < M)
+    assert M[0] == 4 and M[4096 * 2] == 8 and M[4096 * 10] == 4
+    # roughly uniform
+    h = torch.bincount(lab[:4096 * 2].to(torch.int64), minlength=4).double()
+    assert float(h.min() / h.max()) > 0.9
+
+
+def test_white_noise_statistics():
+    cfg = kkgen.LinkConfig(esn0_db=10.0, seed=3)
+    n = kkgen.gauss_complex(3, torch.arange(1 << 18))
+    assert abs(float((n.abs() ** 2).mean()) - 1) < 0.01
+    assert abs(float((n * n).mean().abs())) < 0.01                      # circular
+    assert abs(cfg.sigma2 - 4 * 0.25 / 10.0) < 1e-15                    # σ² = 4·P_x/(Es/N0) (R14)

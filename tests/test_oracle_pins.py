@@ -1,0 +1,426 @@
+"""Pins of the fp64 oracle against what the paper and the mathematics fix (SURVEY §8(c) P1–P14).
+
+None of these re-type the oracle's formula: each checks a closed form, an invariant, a
+textbook special case, brute force on a tiny input, or a value printed in the spec/paper.
+"""
+import math
+import os
+
+import numpy as np
+import pytest
+from scipy import special
+
+import kkgen
+from oracle import constellation as C
+from oracle import receiver as R
+from oracle import theory as T
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+# ------------------------------------------------------------------ P1: Q(BER)
+def test_p1_q_from_ber_golden():
+    for line in open(os.path.join(GOLD, "q_from_ber.txt")):
+        if line.startswith("#") or not line.strip():
+            continue
+        ber, q, tol, _src = line.split()
+        assert abs(T.q_from_ber(float(ber)) - float(q)) <= float(tol)
+
+
+def test_p1_q_roundtrip_erfc():
+    # BER = ½·erfc(Q_lin/√2) with Q_lin = 10^(Q/20): the Gaussian-tail definition, via erfc (not erfcinv)
+    for ber in (3e-2, 1e-2, 1e-3, 2.27e-4, 1e-6, 1e-9):
+        qlin = 10 ** (T.q_from_ber(ber) / 20)
+        assert abs(0.5 * special.erfc(qlin / math.sqrt(2)) / ber - 1) < 1e-9
+
+
+def test_p1_q_domain_and_monotone():
+    for bad in (0.0, 0.5, 0.7, -1e-3):
+        with pytest.raises(ValueError):
+            T.q_from_ber(bad)
+    bers = np.logspace(-9, np.log10(0.4), 50)
+    q = [T.q_from_ber(b) for b in bers]
+    assert np.all(np.diff(q) < 0)
+
+
+# ------------------------------------------------------------------ P2: constellations
+@pytest.mark.parametrize("M", C.FORMATS)
+def test_p2_constellation_invariants(M):
+    pts, labs = C.constellation(M)
+    assert len(pts) == M
+    assert abs(np.mean(np.abs(pts) ** 2) - 1) < 1e-12                       # unit energy
+    assert sorted(labs.tolist()) == list(range(M))                         # bijective labels
+    _, l2 = C.nearest(pts, M)
+    assert np.array_equal(l2, labs)                                        # map∘demap = identity
+    # the transmitter's independent restatement of the alphabet agrees point by point
+    assert np.allclose(kkgen.tx_alphabet(M)[labs], pts, atol=1e-15)
+    # Gray: nearest-neighbour pairs differ in one bit for 4/8/16/64; 32-cross quasi-Gray
+    d = np.abs(pts[:, None] - pts[None, :])
+    dmin = np.min(d[d > 1e-9])
+    pairs = [(i, j) for i in range(M) for j in range(i + 1, M) if abs(d[i, j] - dmin) < 1e-9]
+    hd = [bin(labs[i] ^ labs[j]).count("1") for i, j in pairs]
+    if M == 32:
+        assert len(pairs) == 52 and abs(np.mean(hd) - 1.154) < 1e-3       # SURVEY R13 exhaustive fold
+    else:
+        assert max(hd) == 1
+
+
+def test_p2_cross32_structure():
+    pts, _ = C.constellation(32)
+    g = np.round(pts * math.sqrt(20)).astype(complex)
+    assert set(np.abs(g.real).astype(int)) == {1, 3, 5} and set(np.abs(g.imag).astype(int)) == {1, 3, 5}
+    assert not np.any((np.abs(g.real) == 5) & (np.abs(g.imag) == 5))       # corners removed
+
+
+# ------------------------------------------------------------------ theory special cases
+def test_theory_qpsk_textbook():
+    for es in (0.0, 6.0, 10.0):
+        g = 10 ** (es / 10)
+        assert abs(T.ber_awgn(4, es) / (0.5 * special.erfc(math.sqrt(g / 2))) - 1) < 1e-12
+
+
+@pytest.mark.parametrize("M,es", [(16, 14.0), (8, 12.0), (32, 16.0), (64, 20.0)])
+def test_theory_vs_montecarlo_slicer(M, es):
+    rng = np.random.default_rng(5)
+    n = 400_000
+    pts, labs = C.constellation(M)
+    i = rng.integers(0, M, n)
+    s = math.sqrt(10 ** (-es / 10) / 2)
+    z = pts[i] + s * (rng.standard_normal(n) + 1j * rng.standard_normal(n))
+    _, l = C.nearest(z, M)
+    ber = C.popcount(l ^ labs[i]).sum() / (n * math.log2(M))
+    th = T.ber_awgn(M, es)
+    se = math.sqrt(th / (n * math.log2(M)))
+    assert abs(ber - th) < 5 * se + 0.05 * th
+
+
+# ------------------------------------------------------------------ helpers
+def _cfg(**kw):
+    return R.OracleConfig(**kw)
+
+
+def _run_float_intensity(I_float, cfg, first):
+    """Run O1–O4 on float intensities (adc_scale 1, offset 0) and return E over core ± 1 frame."""
+    H = R.halo(cfg)
+    n = len(I_float) - 2 * H
+    a, amp, _ = R.o2_front_end(R.o1_intensity(I_float, cfg), cfg)
+    F = cfg.frame_samples
+    phi = R.o3_hilbert_ols(a, first - H, first - F, first + n + F, cfg)
+    return amp[H - F: H + n + F] * np.exp(1j * phi)
+
+
+# ------------------------------------------------------------------ P3: exp-construction (exact KK)
+def test_p3_exp_construction_exact():
+    rng = np.random.default_rng(1)
+    N = 1024
+    q = np.arange(3, 262)                                      # bins of (0.011, 1.021) GHz on the 1024-grid
+    c = (rng.standard_normal(len(q)) + 1j * rng.standard_normal(len(q)))
+    cfg = _cfg(ref_intensity=1.0)
+    H, F = R.halo(cfg), cfg.frame_samples
+    n = 2 * F
+    first = 3 * F
+    g = np.arange(first - H, first + n + H)
+    z = (c[None, :] * np.exp(2j * np.pi * np.outer(g, q) / N)).sum(axis=1)
+    z *= 0.6 / np.max(np.abs(z))                              # depth 0.6
+    E = 2.0 * np.exp(z)
+    Erec = _run_float_intensity(np.abs(E) ** 2, cfg, first)
+    Etrue = E[H - F: H + n + F]
+    assert np.linalg.norm(Erec - Etrue) / np.linalg.norm(Etrue) < 1e-12
+
+
+# ------------------------------------------------------------------ P4: KK at high CSPR (north_star <1e-9)
+@pytest.mark.parametrize("cspr_db,bound", [(60, 1e-7), (80, 1e-9), (90, 1e-10)])
+def test_p4_kk_high_cspr(cspr_db, bound):
+    rng = np.random.default_rng(2)
+    N = 1024
+    q = np.arange(3, 262)
+    c = rng.standard_normal(len(q)) + 1j * rng.standard_normal(len(q))
+    cfg = _cfg(ref_intensity=1.0)
+    H, F = R.halo(cfg), cfg.frame_samples
+    n, first = F, 2 * F
+    g = np.arange(first - H, first + n + H)
+    x = (c[None, :] * np.exp(2j * np.pi * np.outer(g, q) / N)).sum(axis=1)
+    x /= np.sqrt(np.mean(np.abs(x) ** 2))
+    A = np.sqrt(10 ** (cspr_db / 10))
+    E = A + x
+    Erec = _run_float_intensity(np.abs(E) ** 2, cfg, first)
+    Et = E[H - F: H + n + F]
+    err = np.linalg.norm(Erec - Et) / np.linalg.norm(Et)
+    assert err < bound
+    if cspr_db == 60:   # the periodic A + x construction is not exactly minimum-phase-exact: error is real, not 0
+        assert err > 1e-10
+
+
+# ------------------------------------------------------------------ P5: Hilbert OLS pins
+def test_p5_hilbert_cos_to_sin_on_grid():
+    cfg = _cfg()
+    N = cfg.hilbert_n
+    g0 = -256
+    n = np.arange(g0, g0 + 8192 + 512)
+    for q in (1, 7, 100, 511):
+        a = np.cos(2 * np.pi * ((q * n) % N) / N + 0.3)
+        phi = R.o3_hilbert_ols(a, g0, 0, 8192, cfg)
+        assert np.max(np.abs(phi - np.sin(2 * np.pi * ((q * np.arange(8192)) % N) / N + 0.3))) < 1e-12
+
+
+def test_p5_hilbert_dc_nyquist_zero():
+    cfg = _cfg()
+    n = np.arange(-256, 4096 + 256)
+    for a in (np.full(len(n), 3.7), np.cos(np.pi * n)):
+        assert np.max(np.abs(R.o3_hilbert_ols(a, -256, 0, 4096, cfg))) < 1e-12
+
+
+def test_p5_parseval_and_involution_periodic():
+    # For a 1024-periodic input every OLS block sees a cyclic shift of one period, so the OLS output over
+    # one period IS the circular Hilbert transform: Σφ² = Σa² − (|A_0|²+|A_{N/2}|²)/N, H[H[a]] = −(a − DC − Nyq).
+    rng = np.random.default_rng(3)
+    cfg = _cfg()
+    N = cfg.hilbert_n
+    per = rng.standard_normal(N)
+    n = np.arange(-256, 2048 + 256)
+    a = per[n % N]
+    phi = R.o3_hilbert_ols(a, -256, 0, 2048, cfg)[:N]
+    Af = np.fft.fft(per)
+    assert abs(np.sum(phi ** 2) - (np.sum(per ** 2) - (abs(Af[0]) ** 2 + abs(Af[N // 2]) ** 2) / N)) < 1e-10
+    a2 = phi[n % N]                                                   # periodic extension of φ
+    hh = R.o3_hilbert_ols(a2, -256, 0, 2048, cfg)[:N]
+    dc = Af[0].real / N
+    nyq = Af[N // 2].real / N * np.cos(np.pi * np.arange(N))
+    assert np.max(np.abs(hh + (per - dc - nyq))) < 1e-12
+
+
+def test_p5_ols_vs_full_length_hilbert_realistic():
+    cfg_l = kkgen.LinkConfig(formats=(16,), cspr_db=12.0, seed=11)
+    F = 16384
+    H = F + 256
+    first, n = F, 4 * F
+    g = kkgen.generate(cfg_l, first - H, first + n + H)
+    ocfg = _cfg(adc_scale=cfg_l.adc_scale, ref_intensity=cfg_l.i_ref)
+    a, _, _ = R.o2_front_end(R.o1_intensity(g["codes"].numpy(), ocfg), ocfg)
+    phi = R.o3_hilbert_ols(a, first - H, first, first + n, ocfg)
+    Af = np.fft.fft(a)
+    f = np.fft.fftfreq(len(a))
+    full = np.fft.ifft(Af * (-1j * np.sign(f))).real[H:H + n]
+    rms = np.sqrt(np.mean((phi - full) ** 2)) / np.sqrt(np.mean(full ** 2))
+    assert rms < 1e-2                                                  # ~4e-3 at CSPR 12
+
+
+# ------------------------------------------------------------------ P6: matched filter + decimation
+def test_p6_rrc_taps_properties():
+    h = R.rrc_taps(_cfg())
+    assert len(h) == 1025
+    assert np.max(np.abs(h - h[::-1])) < 1e-12                        # symmetry
+    assert abs(np.sum(h ** 2) - 1) < 1e-9                             # unit energy
+    assert np.allclose(h, kkgen.rrc_taps_tx(), atol=1e-15)            # transmitter restatement agrees
+    # Nyquist (raised-cosine) property of h*h at the symbol spacing: ISI −54 dB at span 256
+    rc = np.convolve(h, h)
+    c = len(rc) // 2
+    isi = rc[c % 4::4]
+    isi = np.delete(isi, c // 4)
+    assert abs(rc[c] - 1) < 1e-12
+    assert 10 * np.log10(np.sum(isi ** 2) / rc[c] ** 2) < -50
+    # stop band: |H| at 0.6 GHz below −60 dB, pass band flat to 0.45 GHz
+    Hf = np.abs(np.fft.fft(h, 1 << 16))
+    fr = np.fft.fftfreq(1 << 16, d=0.25)                              # GHz at 4 GS/s
+    assert np.max(Hf[np.abs(fr) > 0.6]) / np.max(Hf) < 10 ** (-60 / 20)
+    passb = Hf[np.abs(fr) < 0.45]
+    assert np.max(passb) / np.min(passb) < 1.01
+
+
+def test_p6_mf_brute_force():
+    rng = np.random.default_rng(4)
+    h = R.rrc_taps(_cfg())
+    b0 = -700
+    b = rng.standard_normal(3000) + 1j * rng.standard_normal(3000)
+    m0, m1 = (b0 + 512) // 2 + 1, (b0 + 3000 - 513) // 2
+    y = R.o7_matched_filter(b, b0, m0, m1, h)
+    brute = np.array([sum(h[j + 512] * b[2 * m - j - b0] for j in range(-512, 513)) for m in range(m0, m1)])
+    assert np.max(np.abs(y - brute)) < 1e-12 * np.max(np.abs(brute)) * 10
+
+
+# ------------------------------------------------------------------ P7: mixer
+def test_p7_mixer_tone_to_dc_and_period():
+    cfg = _cfg()
+    e0 = (1 << 40) + 12345
+    n = np.arange(e0, e0 + 5000, dtype=np.int64)
+    tone = np.exp(2j * np.pi * ((129 * n) % 1000) / 1000)
+    b = R.o6_mixer(tone, e0, cfg)
+    assert np.max(np.abs(b - 1)) < 1e-12
+    # period 1000 of the LO
+    one = R.o6_mixer(np.ones(3000, complex), 0, cfg)
+    assert np.max(np.abs(one[:1000] - one[1000:2000])) < 1e-15
+    # equals exp(−i2π·0.129·n) for moderate n
+    assert np.max(np.abs(one - np.exp(-2j * np.pi * 0.129 * np.arange(3000)))) < 1e-9
+
+
+# ------------------------------------------------------------------ P8: CD-init taps and tap rule
+@pytest.mark.parametrize("dl,L,maxdb", [(0.0, 7, -200), (32000.0, 9, -80), (112000.0, 11, -93),
+                                        (200000.0, 15, -110)])
+def test_p8_cd_fit(dl, L, maxdb):
+    cfg = _cfg(dispersion_ps_per_nm=dl)
+    assert R.tap_count(cfg) == L
+    w = R.cd_init_taps(cfg)
+    K = (L - 1) // 2
+    # β₂ from D = 20 ps/nm/km at 1550.51 nm is −25.53 ps²/km
+    assert abs(R.beta2L(_cfg(dispersion_ps_per_nm=20.0)) / 1e-24 + 25.53) < 0.01
+    nu = np.linspace(-0.505e9, 0.505e9, 4001)
+    Wf = np.exp(-2j * np.pi * np.outer(nu, np.arange(-K, K + 1)) / 2e9) @ w
+    Cf = np.exp(-1j * (R.beta2L(cfg) / 2) * (2 * np.pi * (nu + 0.516e9)) ** 2)
+    err_db = 10 * np.log10(np.mean(np.abs(Wf - Cf) ** 2) + 1e-300)
+    assert err_db < maxdb
+    # the inverse cancels the channel's all-pass: |W·CD| = 1 and the group delay offset is removed
+    if dl:
+        cd = np.exp(1j * (R.beta2L(cfg) / 2) * (2 * np.pi * (nu + 0.516e9)) ** 2)
+        assert np.max(np.abs(Wf * cd - 1)) < 10 ** (maxdb / 20) * 30
+
+
+# ------------------------------------------------------------------ chain helpers
+def _chain(M, dl=0.0, cspr=12.0, esn0=None, n=1 << 16, seed=7, noise="white", first=2 * 16384, **ocfg):
+    lc = kkgen.LinkConfig(formats=(M,), dl_ps_nm=dl, cspr_db=cspr, esn0_db=esn0, seed=seed, noise=noise,
+                          **{k: ocfg.pop(k) for k in ("wander_rad", "wander_hz") if k in ocfg})
+    cfg = _cfg(dispersion_ps_per_nm=dl, adc_scale=lc.adc_scale, ref_intensity=lc.i_ref, formats=(M,), **ocfg)
+    H = R.halo(cfg)
+    g = kkgen.generate(lc, first - H, first + n + H)
+    ref = g["labels"].numpy()[H // 4:(H + n) // 4]
+    return R.receive(g["codes"].numpy(), first, n, cfg, ref=ref), cfg, g, ref
+
+
+def _evm_db(z, M):
+    d, _ = C.nearest(z, M)
+    return 10 * np.log10(np.mean(np.abs(z - d) ** 2))
+
+
+# ------------------------------------------------------------------ P9: equalizer LS
+def test_p9_normal_equations_equal_lstsq():
+    out, cfg, _, _ = _chain(16, dl=32000.0, esn0=18.0, n=16384)
+    K = out["K"]
+    yf = out["y"][0: 2 * 4096 - 1 + 2 * K]
+    _, info = R.o8_equalize_frame(yf, K, out["w_cd"], 16, cfg)
+    kk = np.arange(4096)
+    U = yf[2 * kk[:, None] - np.arange(-K, K + 1)[None, :] + K]
+    Phi = np.hstack([U, U.conj()])
+    th0 = info["theta0"]
+    y0 = Phi @ th0
+    d, _ = C.nearest(y0, 16)
+    lam = info["lam"]
+    Aaug = np.vstack([Phi, math.sqrt(lam) * np.eye(Phi.shape[1])])
+    baug = np.concatenate([d, math.sqrt(lam) * th0])
+    th_ls, *_ = np.linalg.lstsq(Aaug, baug, rcond=None)
+    assert np.linalg.norm(th_ls - info["theta1"]) / np.linalg.norm(th_ls) < 1e-10
+    assert abs(lam - 1e-3 * np.sum(np.abs(Phi) ** 2) / Phi.shape[1]) < 1e-9 * lam
+
+
+def test_p9_zero_km_noiseless_taps_near_identity():
+    out, _, _, _ = _chain(4, dl=0.0, n=16384)
+    th = out["frames"][0]["theta1"]
+    L = out["L"]
+    c = th[(L - 1) // 2]
+    assert np.linalg.norm(th) ** 2 / abs(c) ** 2 < 1.01                 # ≥ 99 % of the tap energy on w_0
+
+
+@pytest.mark.parametrize("M", [16, 64])
+def test_p9b_widely_linear_branch(M):
+    out, cfg, _, ref = _chain(M, dl=32000.0, cspr=16.0, n=2 * 16384)
+    y = out["y"] + 0.1 * np.conj(out["y"])                              # conjugate leakage after the MF
+    K = out["K"]
+    res = {}
+    for wl in (True, False):
+        zs = []
+        for fi in range(2):
+            yf = y[2 * 4096 * fi: 2 * 4096 * fi + 2 * 4096 - 1 + 2 * K]
+            u, _ = R.o8_equalize_frame(yf, K, out["w_cd"], M, cfg, widely_linear=wl)
+            z, _ = R.o9_cpr(u, M, 256)
+            zs.append(z)
+        res[wl] = _evm_db(np.concatenate(zs), M)
+    assert res[True] < res[False] - 10
+
+
+# ------------------------------------------------------------------ P10: noiseless end to end
+@pytest.mark.parametrize("M,dl,cspr", [(4, 0.0, 10.0), (8, 0.0, 10.0), (16, 0.0, 12.0), (32, 0.0, 12.0),
+                                       (64, 0.0, 12.0), (4, 200000.0, 12.0), (8, 200000.0, 10.0),
+                                       (16, 112000.0, 12.0), (32, 200000.0, 12.0), (64, 32000.0, 12.0)])
+def test_p10_noiseless_zero_errors(M, dl, cspr):
+    out, _, _, _ = _chain(M, dl=dl, cspr=cspr, n=2 * 16384)
+    c = out["counts"]
+    assert c["sym_err"].sum() == 0 and c["bit_err"].sum() == 0
+    assert c["bits"].sum() == 2 * 4096 * int(math.log2(M))
+    assert c["bad_frames"] == 0 and c["dead_frames"] == 0
+    assert _evm_db(out["z"], M) < -35
+
+
+# ------------------------------------------------------------------ P11: AWGN calibration against theory
+@pytest.mark.parametrize("M,es,noise,shift,tol", [
+    (4, 9.0, "analytic", 0.0, 0.12), (16, 15.0, "analytic", 0.0, 0.12), (64, 21.0, "analytic", 0.0, 0.12),
+    (16, 18.0, "white", -10 * math.log10(2), 0.2)])
+def test_p11_awgn_q_vs_theory(M, es, noise, shift, tol):
+    n = 1 << 21                                                         # 2^19 symbols
+    out, _, _, _ = _chain(M, cspr=16.0, esn0=es, noise=noise, n=n, seed=17)
+    c = out["counts"]
+    ber = c["bit_err"].sum() / c["bits"].sum()
+    assert 5e-4 < ber < 3e-2
+    q_or = T.q_from_ber(ber)
+    q_th = T.q_from_ber(T.ber_awgn(M, es + shift))
+    assert abs(q_or - q_th) <= tol, (q_or, q_th)
+
+
+# ------------------------------------------------------------------ P12: CPR
+@pytest.mark.parametrize("M,th", [(4, 0.5), (16, 0.18), (64, 0.08)])
+def test_p12_cpr_exact_rotation(M, th):
+    rng = np.random.default_rng(9)
+    pts, _ = C.constellation(M)
+    u = pts[rng.integers(0, M, 4096)]
+    rot = th * np.repeat(rng.uniform(-1, 1, 16), 256)
+    z, est = R.o9_cpr(u * np.exp(1j * rot), M, 256)
+    assert np.max(np.abs(est - rot[::256])) < 1e-12
+    assert np.max(np.abs(z - u)) < 1e-12
+
+
+def test_p12_cpr_tracks_phase_wander():
+    out_on, _, _, _ = _chain(16, dl=32000.0, cspr=16.0, n=4 * 16384, wander_rad=0.05, wander_hz=50e3)
+    out_off, _, _, _ = _chain(16, dl=32000.0, cspr=16.0, n=4 * 16384, wander_rad=0.05, wander_hz=50e3,
+                              cpr_window=4096)
+    on, off = _evm_db(out_on["z"], 16), _evm_db(out_off["z"], 16)
+    assert on < -45 and off > on + 6, (on, off)
+
+
+# ------------------------------------------------------------------ P13: shard / halo invariance
+def test_p13_shard_invariance():
+    lc = kkgen.LinkConfig(formats=(16,), dl_ps_nm=112000.0, cspr_db=10.0, esn0_db=16.0, seed=23)
+    cfg = _cfg(dispersion_ps_per_nm=112000.0, adc_scale=lc.adc_scale, ref_intensity=lc.i_ref, formats=(16,))
+    F, H = cfg.frame_samples, R.halo(cfg)
+    first, n = 5 * F, 4 * F
+    g = kkgen.generate(lc, first - H, first + n + H)
+    codes, lab = g["codes"].numpy(), g["labels"].numpy()
+    whole = R.receive(codes, first, n, cfg, ref=lab[H // 4:(H + n) // 4], keep=False)
+    parts = []
+    for s in range(2):
+        f0 = first + s * 2 * F
+        o = f0 - (first - H)
+        parts.append(R.receive(codes[o - H:o + 2 * F + H], f0, 2 * F, cfg,
+                               ref=lab[o // 4:(o + 2 * F) // 4], keep=False))
+    assert np.array_equal(np.concatenate([p["dec"] for p in parts]), whole["dec"])
+    assert np.max(np.abs(np.concatenate([p["z"] for p in parts]) - whole["z"])) < 1e-9
+    for key in ("sym_err", "bit_err", "bits"):
+        assert np.array_equal(parts[0]["counts"][key] + parts[1]["counts"][key], whole["counts"][key])
+
+
+# ------------------------------------------------------------------ P14: CSPR behaviour
+def test_p14_evm_nonincreasing_in_cspr():
+    ev = [_evm_db(_chain(16, dl=32000.0, cspr=c, n=16384)[0]["z"], 16) for c in (8.0, 10.0, 12.0, 14.0, 16.0)]
+    assert all(b <= a + 0.5 for a, b in zip(ev, ev[1:])), ev
+    assert ev[-1] < ev[0] - 5
+
+
+# ------------------------------------------------------------------ dead frames (input-level rule)
+def test_dead_frame_counted():
+    lc = kkgen.LinkConfig(formats=(4,), cspr_db=12.0, seed=3)
+    cfg = _cfg(adc_scale=lc.adc_scale, ref_intensity=lc.i_ref)
+    F, H = cfg.frame_samples, R.halo(cfg)
+    first, n = 2 * F, 3 * F
+    g = kkgen.generate(lc, first - H, first + n + H)
+    codes = g["codes"].numpy().copy()
+    codes[H + F: H + 2 * F] = 0                                          # frame 1 of the core is dark
+    out = R.receive(codes, first, n, cfg, ref=g["labels"].numpy()[H // 4:(H + n) // 4])
+    assert out["counts"]["dead_frames"] == 1
+    assert out["counts"]["clamped"] == F
+    assert np.all(out["z"][4096:8192] == 0)
