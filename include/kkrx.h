@@ -1,0 +1,173 @@
+/*
+ * kkrx.h — C ABI of libkkrx.so, the B200 (sm_100a) Kramers-Kronig receive chain.
+ *
+ * What the library computes (§2 "DSP chain", Fig. 1b; BASELINE.json north_star;
+ * readings R1–R27 of SURVEY.md §8(c), restated in DESIGN.md §3): from int16 ADC codes of a
+ * minimum-phase KK photocurrent sampled at 4 GS/s it recovers
+ *     a = ½ ln max(I, ε)            sqrt/log front end
+ *     φ = σ·H[a]                     1024-pt 50 %-hop overlap-save Hilbert FFT pair (R1, R2)
+ *     E = √max(I,ε)·e^{iφ}           field reconstruction
+ *     b = (E − A_f)·e^{−2πiσ f_c n/f_s}   carrier removal + downshift (north_star; R8, R9)
+ *     y[m] = Σ h[j] b[2m−j]          RRC 1 % matched filter at 2 sps via FFT4096/fold/IFFT2048 (R4–R6)
+ *     per 4096-symbol frame: widely-linear block-adaptive FIR absorbing CD (DD least squares),
+ *     carrier-phase recovery, QAM decision, bit/symbol error counting (north_star; R10–R27)
+ * Q = 20·log10(√2·erfcinv(2·BER)) is computed on the host by kk_q_from_ber.
+ *
+ * Conventions
+ *  - Global indices: sample n (int64, 4 GS/s), symbol k = n/4 (sample 4k is the centre of symbol k),
+ *    frame f = samples [16384 f, 16384 f + 16384). All block/tile/frame grids are anchored at n = 0,
+ *    so any chunking or sharding of a stream gives bit-identical decisions.
+ *  - Device pointers are plain CUDA device addresses (e.g. torch.Tensor.data_ptr()). The caller owns
+ *    every buffer passed in; the context owns its constants, scratch and counters. The library never
+ *    frees caller memory. Buffers must stay valid until the stream passes the call.
+ *  - Every call returns a kk_status; nothing throws across the ABI. Asynchronous kernel faults are
+ *    reported at the next synchronising call (kk_stats) as KK_ERR_CUDA.
+ *  - One context per (device, stream); calls on one context are not re-entrant.
+ */
+#ifndef KKRX_H
+#define KKRX_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct kk_ctx kk_ctx;          /* opaque */
+typedef void* kk_stream_t;             /* a cudaStream_t (NULL = legacy default stream) */
+
+typedef enum {
+  KK_OK = 0,
+  KK_ERR_CONFIG = -1,   /* invalid or unsupported configuration            */
+  KK_ERR_ALIGN = -2,    /* first_sample / n_samples not on the frame grid, or pointer not 16-B aligned */
+  KK_ERR_SHORT = -3,    /* n_samples < one frame (SPEC.md:307 analogue)                               */
+  KK_ERR_NULL = -4,     /* required pointer is NULL                                                   */
+  KK_ERR_NOMEM = -5,    /* device allocation failed                                                   */
+  KK_ERR_CUDA = -6,     /* CUDA launch / runtime error (sticky errors surface at kk_stats)            */
+  KK_ERR_DOMAIN = -7,   /* kk_q_from_ber outside 0 < BER < 0.5                           */
+  KK_ERR_STATE = -8     /* call out of order (e.g. intermediate not kept / no call yet)               */
+} kk_status;
+
+enum { KK_IN_INT16 = 0, KK_IN_FLOAT32 = 1 };                  /* input_dtype */
+enum { KK_STAGE_FIELD = 0, KK_STAGE_MF = 1, KK_STAGE_EQ = 2 }; /* kk_get_intermediate stages */
+
+/* Receiver configuration. kk_config_default() fills the paper's values; fields marked [fixed] must
+ * keep them (the kernels are specialised for them) or kk_init returns KK_ERR_CONFIG. */
+typedef struct kk_config {
+  double  fs_hz;                 /* 4e9  ADC rate; fs/baud must be 4 [fixed]              */
+  double  baud_hz;               /* 1e9  symbol rate                                       */
+  int32_t lo_num, lo_den;        /* f_c/f_s as a reduced rational: 129/1000 = 0.516 GHz / 4 GS/s; den ≤ 4096 */
+  int32_t sideband;              /* +1: data above the tone (φ = +H[a]); −1 mirrors φ and the LO (R2)   */
+  int32_t rrc_span_sym;          /* 256 → 1025 taps (R4); span·4 ≤ mf_fft_n − mf_hop                    */
+  double  rolloff;               /* 0.01 ("1% roll-off")                                     */
+  int32_t hilbert_n, hilbert_hop;/* 1024, 512 [fixed] ("1024-point 100% overlap-save"; R1)  */
+  int32_t mf_fft_n, mf_hop;      /* 4096, 3072 [fixed] (FFT4096 → fold → IFFT2048; R6)                 */
+  int32_t frame_symbols;         /* 4096 [fixed] (R23)                                                   */
+  int32_t eq_taps;               /* 0 = tap-count rule of SURVEY §8(a); else odd L in [3, 25]           */
+  int32_t eq_widely_linear;      /* 1 = widely linear ("widely-linear"), 0 = linear only    */
+  int32_t cpr_window;            /* 256 symbols; one of 16,32,64,128,256,512 (R12)                       */
+  double  eq_ridge;              /* 1e-3: λ = ridge·tr(R)/(2L) (R10)                                     */
+  double  dispersion_ps_per_nm;  /* accumulated D·L, e.g. 200000 for 10,000 km at 20 ps/nm/km          */
+  double  lambda_m;              /* 1550.51e-9                                             */
+  int32_t input_dtype;           /* KK_IN_INT16 (ADC codes) | KK_IN_FLOAT32 (intensities, for tests)    */
+  float   adc_scale, adc_offset; /* I = adc_scale·(code − adc_offset)                                    */
+  float   ref_intensity;         /* I_ref > 0; ε = clamp_rel·I_ref (R7)                                  */
+  float   clamp_rel;             /* 1e-12                                                                */
+  const uint8_t* format_schedule;/* host array of n_segments QAM orders in {4,8,16,32,64}; NULL → default_format */
+  int32_t n_segments;            /* entries in format_schedule (copied at kk_init)                       */
+  int32_t default_format;        /* M when format_schedule is NULL                                       */
+  int64_t segment_frames;        /* frames per schedule entry; format(f) = schedule[(f/segment_frames) mod n_segments] (R26) */
+  int64_t max_samples_per_call;  /* sizes the scratch; multiple of 16384                                 */
+  int32_t device;                /* CUDA device ordinal the context lives on                             */
+  int32_t keep_intermediate;     /* 1: K3 also stores z (EQ stage) for kk_get_intermediate               */
+} kk_config;
+
+/* Counters (all uint64, summed over calls until kk_reset_stats; index i = log2(M) − 2 for M = 4..64).
+ * Layout is fixed: 24 consecutive uint64 — the same layout kk_stats_device writes. */
+typedef struct kk_stats_t {
+  uint64_t sym[5], sym_err[5], bits[5], bit_err[5];
+  uint64_t clamped;       /* core samples with I < ε (R7)                                   */
+  uint64_t frames;        /* frames processed                                               */
+  uint64_t dead_frames;   /* frames whose 16384 samples are all clamped (signal loss)        */
+  uint64_t bad_frames;    /* frames whose LS solve failed (fell back to the CD-init taps)    */
+} kk_stats_t;
+#define KK_STATS_WORDS 24
+
+/* Fill *cfg with the paper's defaults (4 GS/s, 1 GBaud, 0.516 GHz tone, 1 % RRC span 256, 1024/512 Hilbert,
+ * 4096/3072 MF, 4096-symbol frames, rule-based L, widely linear, W = 256, λ = 1e-3, 4-QAM, 0 ps/nm). */
+void kk_config_default(kk_config* cfg);
+/* sizeof(kk_config) and sizeof(kk_stats_t) as compiled into the library (lets bindings check their layout). */
+size_t kk_config_sizeof(void);
+size_t kk_stats_sizeof(void);
+
+/* Validate cfg, compute the fp64 constants (RRC taps → MF spectrum, LO table, CD-inverse LS taps, tap
+ * count, FFT twiddles), upload them and allocate scratch + counters on cfg->device. No kernel runs.
+ * Errors: KK_ERR_NULL, KK_ERR_CONFIG, KK_ERR_NOMEM, KK_ERR_CUDA. On error *out is NULL. */
+kk_status kk_init(const kk_config* cfg, kk_ctx** out);
+
+/* Samples that must be readable before (left) and after (right) the core of every call:
+ * one neighbour frame (its carrier estimate A_f and MF support) + half a Hilbert block = 16640. */
+kk_status kk_halo(const kk_ctx* ctx, int64_t* left, int64_t* right);
+
+/* Equalizer taps L actually used (rule or override). */
+kk_status kk_eq_taps(const kk_ctx* ctx, int32_t* taps);
+
+/* Process the core [first_sample, first_sample + n_samples) of the stream; asynchronous on `stream`.
+ *   d_adc       device pointer to the CORE start (global sample first_sample); the range
+ *               [d_adc − left, d_adc + n_samples + right) must be readable (kk_halo). int16 or float32
+ *               per cfg.input_dtype; must be 16-byte aligned.
+ *   first_sample global index, multiple of 16384 (frame grid), ≥ 0.
+ *   n_samples   multiple of 16384, 16384 ≤ n_samples ≤ max_samples_per_call.
+ *   d_ref       nullable device uint8[n_samples/4]: transmitted labels; if given, error counters update.
+ *   d_decisions nullable device uint8[n_samples/4]: decided labels out.
+ * Symbol/bit/frame/clamp counters always update. Errors: KK_ERR_NULL, KK_ERR_ALIGN, KK_ERR_SHORT,
+ * KK_ERR_CONFIG (n_samples too large), KK_ERR_CUDA (launch failure). */
+kk_status kk_process_frames(kk_ctx* ctx, const void* d_adc, int64_t first_sample, int64_t n_samples,
+                            const uint8_t* d_ref, uint8_t* d_decisions, kk_stream_t stream);
+
+/* End-to-end variant with HOST buffers (pinned recommended): copies [h_adc − left, h_adc + n + right)
+ * host→device, runs kk_process_frames, copies decisions device→host, in chunks of ≤ max_samples_per_call
+ * with two internal streams so the copies of chunk i+1 overlap the kernels of chunk i. Blocks until done.
+ * h_ref / h_decisions nullable host uint8[n_samples/4]. Same constraints/errors as kk_process_frames,
+ * except n_samples may exceed max_samples_per_call (it must be a multiple of 16384). */
+kk_status kk_process_frames_host(kk_ctx* ctx, const void* h_adc, int64_t first_sample, int64_t n_samples,
+                                 const uint8_t* h_ref, uint8_t* h_decisions);
+
+/* Synchronise the context's last stream and copy the counters to *host_out. KK_ERR_CUDA on sticky error. */
+kk_status kk_stats(kk_ctx* ctx, kk_stats_t* host_out);
+/* Asynchronously copy the 24 counters (kk_stats_t layout) to device memory d_out (e.g. for NCCL allreduce). */
+kk_status kk_stats_device(kk_ctx* ctx, uint64_t* d_out, kk_stream_t stream);
+/* Zero the counters (asynchronous on stream). */
+kk_status kk_reset_stats(kk_ctx* ctx, kk_stream_t stream);
+
+/* Describe / copy the last call's intermediate of a stage (device→device, async on stream):
+ *   KK_STAGE_FIELD: E (complex64 interleaved) for samples [first − 16384, first + n + 16384)
+ *   KK_STAGE_MF   : y (complex64) for 2-sps indices [first/2 − K, (first + n)/2 + K), K = (L−1)/2
+ *   KK_STAGE_EQ   : z (complex64) for symbols [first/4, (first + n)/4); needs keep_intermediate
+ * kk_intermediate_range gives (first global index, count) of the stage. KK_ERR_STATE if no call yet /
+ * not kept; KK_ERR_CONFIG if bytes < count·8. */
+kk_status kk_intermediate_range(const kk_ctx* ctx, int stage, int64_t* first_index, int64_t* count);
+kk_status kk_get_intermediate(kk_ctx* ctx, int stage, void* d_dst, size_t bytes, kk_stream_t stream);
+
+/* Per-kernel timing (measurement support). When enabled, kk_process_frames records CUDA
+ * events around each of its kernel launches (K1 KK, K2 MF, K3 EQ) on the call's stream. kk_kernel_times
+ * synchronises those events and returns, per kernel, the summed device time in ms and the launch count
+ * since the last reset (reset = 1 clears them after reading). */
+kk_status kk_enable_timing(kk_ctx* ctx, int enable);
+kk_status kk_kernel_times(kk_ctx* ctx, double ms_out[3], int64_t launches_out[3], int reset);
+
+/* Q = 20·log10(√2·erfcinv(2·BER)) in dB; KK_ERR_DOMAIN unless 0 < ber < 0.5. */
+kk_status kk_q_from_ber(double ber, double* q_db);
+
+/* Free everything the context owns (synchronises its device first). NULL is a no-op. */
+void kk_destroy(kk_ctx* ctx);
+
+const char* kk_strerror(kk_status status);
+/* Last error message of the context, with (stage, frame) where known; "" if none. */
+const char* kk_last_error(const kk_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KKRX_H */

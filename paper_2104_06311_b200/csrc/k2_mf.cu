@@ -1,0 +1,156 @@
+// k2_mf.cu — K2: carrier removal, downshift to DC, RRC matched filter and 4→2 sps decimation.
+//
+// PAPER.md:82 (§2): the reconstructed field "is subsequently downshifted to DC for further processing.
+// Frequency-domain static equalization and downsampling from 4 to 2 samples-per-symbol is performed by
+// multiplication with an offline-optimized filter enabled by another FFT and IFFT pair." With the
+// north-star carrier removal and SURVEY readings R4 (RRC 1 %, span 256 = 1025 taps), R5 (static filter =
+// RRC MF), R6 (exact decimation by spectral fold), R8 (A_f = per-frame mean of E), R9 (LO indexed by the
+// global sample: exp(−2πiσ·((lo_num·n) mod lo_den)/lo_den)):
+//     b[n] = (E[n] − A_{f(n)})·LO[n]
+//     tile t (global grid): x = b[3072t − 512, 3072t + 3584)
+//     Y = FFT4096(x)·H   (H = DFT of the circularly centred taps, real, ×1/4096 folded in)
+//     Y2[q] = Y[q] + Y[q + 2048], q < 2048            (fold = decimation by 2 in frequency)
+//     y[1536t − 256 + p] = IFFT2048(Y2)[p], p ∈ [256, 1792)   (the alias-free, non-wrapped outputs)
+// which equals y[m] = Σ_{j=−512}^{512} h[j]·b[2m − j] exactly (up to fp32 rounding).
+//
+// Mapping: persistent CTAs of 128 threads, one 4096-point tile at a time in shared memory (34.8 KB,
+// padded 1 float2 per 16 to make the radix-16 Stockham scatter conflict-free); LO table resident in
+// shared memory for the CTA's lifetime; H and the twiddles read through the read-only path (L1-resident).
+// E is read with 16-byte vector loads; the 1536 kept outputs are written coalesced.
+#include "kk_device.cuh"
+#include "kk_params.h"
+
+namespace kk {
+
+constexpr int K2_THREADS = 128;
+constexpr int K2_BUF = 4096 + 256;
+
+__device__ __forceinline__ int pad16(int i) { return i + (i >> 4); }
+
+// One radix-R Stockham pass over an N-point array in shared memory (in place, barrier-separated).
+// tw: table of W_{Ns·R}^{r·k} laid out [r][k] (k < Ns), conjugated when DIR = +1.
+template <int N, int R, int Ns, int DIR>
+__device__ __forceinline__ void stockham_pass(float2* buf, const float2* __restrict__ tw, int tid) {
+  constexpr int NJ = N / R;
+  constexpr int PER = NJ / K2_THREADS;
+  static_assert(PER >= 1 && NJ % K2_THREADS == 0, "pass shape");
+  float2 v[PER][R];
+#pragma unroll
+  for (int it = 0; it < PER; ++it) {
+    const int j = tid + it * K2_THREADS;
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[it][r] = buf[pad16(j + r * NJ)];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int it = 0; it < PER; ++it) {
+    const int j = tid + it * K2_THREADS;
+    const int k = j & (Ns - 1);
+    if (Ns > 1) {
+#pragma unroll
+      for (int r = 1; r < R; ++r) {
+        const float2 w = __ldg(&tw[r * Ns + k]);
+        v[it][r] = DIR < 0 ? cmul(v[it][r], w) : cmulc(v[it][r], w);
+      }
+    }
+    dft_reg<R, DIR>(v[it]);
+    const int idxD = (j / Ns) * Ns * R + k;
+#pragma unroll
+    for (int r = 0; r < R; ++r) buf[pad16(idxD + r * Ns)] = v[it][r];
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ int64_t floordiv(int64_t a, int64_t b) {
+  int64_t q = a / b;
+  return (a % b != 0 && ((a < 0) != (b < 0))) ? q - 1 : q;
+}
+
+__global__ void __launch_bounds__(K2_THREADS, 4)
+k2_mf_kernel(const float2* __restrict__ E, int64_t E_first, const float2* __restrict__ part, int64_t jb0,
+             int64_t tile0, int64_t n_tiles, float2* __restrict__ y, int64_t y_first, int64_t y_count,
+             const float* __restrict__ Hs, const float2* __restrict__ lo_tab, const float2* __restrict__ tw256,
+             const float2* __restrict__ tw4096, const float2* __restrict__ tw2048, K2Params p) {
+  __shared__ __align__(16) float2 buf[K2_BUF];
+  __shared__ float2 A_s[2];
+  extern __shared__ float2 lo_s[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = tid; i < p.lo_den; i += K2_THREADS) lo_s[i] = lo_tab[i];
+  const int lo_step = (int)(((int64_t)2 * K2_THREADS * p.lo_num) % p.lo_den);
+
+  for (int64_t ti = blockIdx.x; ti < n_tiles; ti += gridDim.x) {
+    const int64_t t = tile0 + ti;
+    const int64_t s0 = t * kMfHop - kMfLead;                 // global sample of x[0]
+    const int64_t fa = floordiv(s0, kFrameSamp);
+    const int64_t fsplit = (fa + 1) * kFrameSamp;            // first sample of frame fa+1
+    // carrier estimates A_fa, A_fa+1 from K1's per-512-block sums (fixed order → deterministic)
+    if (warp < 2) {
+      const int64_t f = fa + warp;
+      float2 v = make_float2(0.f, 0.f);
+      if (warp == 0 || s0 + kMfN > fsplit) v = part[f * 32 - jb0 + lane];
+      v.x = warp_sum(v.x); v.y = warp_sum(v.y);
+      if (lane == 0) A_s[warp] = make_float2(v.x * (1.0f / kFrameSamp), v.y * (1.0f / kFrameSamp));
+    }
+    __syncthreads();
+    // a5: b = (E − A_f)·LO, two samples per thread per step (16-B loads)
+    {
+      const int64_t sA = s0 + 2 * tid;
+      int q = (int)(((sA % p.lo_den) + p.lo_den) % p.lo_den);
+      q = (int)(((int64_t)q * p.lo_num) % p.lo_den);
+      const float4* src = reinterpret_cast<const float4*>(E + (s0 - E_first)) + tid;
+      const float2 A0 = A_s[0], A1 = A_s[1];
+#pragma unroll 4
+      for (int it = 0; it < kMfN / (2 * K2_THREADS); ++it) {
+        const int i = 2 * (tid + K2_THREADS * it);
+        const float4 e = __ldg(src + it * K2_THREADS);
+        const int64_t s = s0 + i;
+        const float2 A = (s < fsplit) ? A0 : A1;             // s and s+1 lie in the same frame (s even)
+        int q1 = q + p.lo_num; q1 -= (q1 >= p.lo_den) ? p.lo_den : 0;
+        buf[pad16(i)] = cmul(make_float2(e.x - A.x, e.y - A.y), lo_s[q]);
+        buf[pad16(i + 1)] = cmul(make_float2(e.z - A.x, e.w - A.y), lo_s[q1]);
+        q += lo_step; q -= (q >= p.lo_den) ? p.lo_den : 0;
+      }
+    }
+    __syncthreads();
+    // a6: FFT4096 (radix 16 × 3)
+    stockham_pass<4096, 16, 1, -1>(buf, nullptr, tid);
+    stockham_pass<4096, 16, 16, -1>(buf, tw256, tid);
+    stockham_pass<4096, 16, 256, -1>(buf, tw4096, tid);
+    // × H (real) and fold: Y2[q] = Y[q]H[q] + Y[q+2048]H[q+2048]
+#pragma unroll 4
+    for (int it = 0; it < 2048 / K2_THREADS; ++it) {
+      const int qq = tid + it * K2_THREADS;
+      const float2 a = buf[pad16(qq)], b = buf[pad16(qq + 2048)];
+      const float ha = __ldg(&Hs[qq]), hb = __ldg(&Hs[qq + 2048]);
+      buf[pad16(qq)] = make_float2(fmaf(a.x, ha, b.x * hb), fmaf(a.y, ha, b.y * hb));
+    }
+    __syncthreads();
+    // IFFT2048 (radix 16, 16, 8)
+    stockham_pass<2048, 16, 1, +1>(buf, nullptr, tid);
+    stockham_pass<2048, 16, 16, +1>(buf, tw256, tid);
+    stockham_pass<2048, 8, 256, +1>(buf, tw2048, tid);
+    // keep p ∈ [256, 1792) → y[1536t − 256 + p]
+    const int64_t m_base = t * kMfKeep - kMfKeep0;
+#pragma unroll 4
+    for (int it = 0; it < kMfKeep / K2_THREADS; ++it) {
+      const int pp = kMfKeep0 + tid + it * K2_THREADS;
+      const int64_t m = m_base + pp;
+      if (m >= y_first && m < y_first + y_count) y[m - y_first] = buf[pad16(pp)];
+    }
+    __syncthreads();
+  }
+}
+
+void launch_k2(const float2* E, int64_t E_first, const float2* part, const int* /*clampcnt*/, int64_t jb0,
+               int64_t tile0, int64_t n_tiles, float2* y, int64_t y_first, int64_t y_count, const float* Hs,
+               const float2* lo_tab, const float2* tw256, const float2* tw4096, const float2* tw2048,
+               const K2Params& p, int num_sms, cudaStream_t s) {
+  int per_sm = 4;
+  int64_t grid = (int64_t)num_sms * per_sm;
+  if (grid > n_tiles) grid = n_tiles;
+  const size_t dyn = (size_t)p.lo_den * sizeof(float2);
+  k2_mf_kernel<<<(unsigned)grid, K2_THREADS, dyn, s>>>(E, E_first, part, jb0, tile0, n_tiles, y, y_first, y_count,
+                                                       Hs, lo_tab, tw256, tw4096, tw2048, p);
+}
+
+}  // namespace kk

@@ -1,0 +1,191 @@
+// kk_device.cuh — device helpers shared by the KK kernels (K1, K2, K3): complex arithmetic,
+// register-resident radix-2 DFT-R (R = 8/16/32) used by the shared-memory Stockham FFTs,
+// the QAM slicers and TMA 1-D bulk-copy / mbarrier wrappers (sm_100a).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace kk {
+
+// ------------------------------------------------------------------ complex float2 helpers
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+  return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+}
+__device__ __forceinline__ float2 cmulc(float2 a, float2 b) {  // a * conj(b)
+  return make_float2(fmaf(a.x, b.x, a.y * b.y), fmaf(a.y, b.x, -a.x * b.y));
+}
+__device__ __forceinline__ float2 cconj(float2 a) { return make_float2(a.x, -a.y); }
+__device__ __forceinline__ float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
+// acc += a * b
+__device__ __forceinline__ void cmac(float2& acc, float2 a, float2 b) {
+  acc.x = fmaf(a.x, b.x, acc.x); acc.x = fmaf(-a.y, b.y, acc.x);
+  acc.y = fmaf(a.x, b.y, acc.y); acc.y = fmaf(a.y, b.x, acc.y);
+}
+// acc += conj(a) * b
+__device__ __forceinline__ void cmac_conj(float2& acc, float2 a, float2 b) {
+  acc.x = fmaf(a.x, b.x, acc.x); acc.x = fmaf(a.y, b.y, acc.x);
+  acc.y = fmaf(a.x, b.y, acc.y); acc.y = fmaf(-a.y, b.x, acc.y);
+}
+
+// ------------------------------------------------------------------ register DFT
+// cos(2πk/32) for k = 0..8 (quarter wave); other angles by symmetry. Folded to immediates after unroll.
+__device__ __forceinline__ float cos32q(int k) {
+  const float q[9] = {1.0f, 0.98078528040323044913f, 0.92387953251128675613f, 0.83146961230254523708f,
+                      0.70710678118654752440f, 0.55557023301960222474f, 0.38268343236508977173f,
+                      0.19509032201612826785f, 0.0f};
+  return q[k];
+}
+// exp(2πi e/R) for R | 32 (angle in units of 1/32 turn: u = e·32/R)
+template <int R>
+__device__ __forceinline__ float2 unit_root(int e) {
+  int u = (e * (32 / R)) & 31;
+  float c, s;
+  if (u <= 8) { c = cos32q(u); s = cos32q(8 - u); }
+  else if (u <= 16) { c = -cos32q(16 - u); s = cos32q(u - 8); }
+  else if (u <= 24) { c = -cos32q(u - 16); s = -cos32q(24 - u); }
+  else { c = cos32q(32 - u); s = -cos32q(u - 24); }
+  return make_float2(c, s);
+}
+__host__ __device__ constexpr int ilog2c(int n) { return n <= 1 ? 0 : 1 + ilog2c(n >> 1); }
+// non-recursive so that it folds to a constant after loop unrolling (recursion would block inlining)
+__host__ __device__ __forceinline__ constexpr int bitrevc(int x, int bits) {
+  int r = 0;
+  for (int b = 0; b < bits; ++b) r |= ((x >> b) & 1) << (bits - 1 - b);
+  return r;
+}
+
+// In-register DFT of length R (power of two ≤ 32), natural order in and out, unnormalised.
+// DIR = −1: X[k] = Σ x[n] e^{−2πi nk/R} (forward);  DIR = +1: inverse (no 1/R).
+template <int R, int DIR>
+__device__ __forceinline__ void dft_reg(float2 (&v)[R]) {
+  constexpr int LOGR = ilog2c(R);
+#pragma unroll
+  for (int st = 0; st < LOGR; ++st) {
+    const int half = R >> (st + 1);
+#pragma unroll
+    for (int i = 0; i < R / 2; ++i) {
+      const int j = i & (half - 1);                  // position inside the butterfly group
+      const int start = (i - j) * 2;                 // group start
+      float2 a = v[start + j], b = v[start + j + half];
+      v[start + j] = cadd(a, b);
+      float2 d = csub(a, b);
+      const int e = j << st;                         // twiddle W_R^{e}, e < R/2
+      if (e == 0) {
+        v[start + j + half] = d;
+      } else if (4 * e == R) {                       // ±i
+        v[start + j + half] = DIR < 0 ? make_float2(d.y, -d.x) : make_float2(-d.y, d.x);
+      } else {
+        float2 w = unit_root<R>(e);
+        if (DIR < 0) w.y = -w.y;
+        v[start + j + half] = cmul(d, w);
+      }
+    }
+  }
+  // DIF leaves bit-reversed order: permute back (compile-time renaming)
+  float2 t[R];
+#pragma unroll
+  for (int i = 0; i < R; ++i) t[i] = v[bitrevc(i, LOGR)];
+#pragma unroll
+  for (int i = 0; i < R; ++i) v[i] = t[i];
+}
+
+// ------------------------------------------------------------------ reductions
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// ------------------------------------------------------------------ QAM slicer
+// Decision regions: per axis, a value exactly on a boundary goes to the lower level; the 32-cross
+// corner cells go to the nearer of the two adjacent points (ties to the lower label).
+struct Decision { float2 pt; int lab; };
+
+__device__ __forceinline__ int gray(int i) { return i ^ (i >> 1); }
+// level index of a PAM slicer with m levels at odd integers −(m−1)..(m−1), x in grid units
+__device__ __forceinline__ int pam_index(float x, int m) {
+  int i = (int)ceilf(0.5f * (x + (float)(m - 2)));
+  return min(max(i, 0), m - 1);
+}
+// 32-cross label of grid cell (iI, iQ) (level index 0 = −5); corners unused.
+// rows iQ = 0..5 (Q = −5..+5), 5 bits per column iI = 0..5.
+__device__ __forceinline__ int cross32_label(int iI, int iQ) {
+  const unsigned long long rows[6] = {
+      (0ull) | (0ull << 5) | (1ull << 10) | (17ull << 15) | (16ull << 20) | (0ull << 25),
+      (4ull) | (12ull << 5) | (8ull << 10) | (24ull << 15) | (28ull << 20) | (20ull << 25),
+      (5ull) | (13ull << 5) | (9ull << 10) | (25ull << 15) | (29ull << 20) | (21ull << 25),
+      (7ull) | (15ull << 5) | (11ull << 10) | (27ull << 15) | (31ull << 20) | (23ull << 25),
+      (6ull) | (14ull << 5) | (10ull << 10) | (26ull << 15) | (30ull << 20) | (22ull << 25),
+      (0ull) | (3ull << 5) | (2ull << 10) | (18ull << 15) | (19ull << 20) | (0ull << 25)};
+  unsigned long long r = rows[0];
+#pragma unroll
+  for (int q = 1; q < 6; ++q) r = (iQ == q) ? rows[q] : r;
+  return (int)((r >> (5 * iI)) & 31ull);
+}
+
+template <int M>
+__device__ __forceinline__ Decision slice(float2 z) {
+  Decision d;
+  if constexpr (M == 4 || M == 16 || M == 64) {
+    constexpr int m = M == 4 ? 2 : (M == 16 ? 4 : 8);
+    constexpr int hb = M == 4 ? 1 : (M == 16 ? 2 : 3);
+    constexpr float s = M == 4 ? 1.41421356237309505f : (M == 16 ? 3.16227766016837933f : 6.48074069840786023f);
+    int iI = pam_index(z.x * s, m), iQ = pam_index(z.y * s, m);
+    d.lab = (gray(iI) << hb) | gray(iQ);
+    d.pt = make_float2((float)(2 * iI - (m - 1)) * (1.0f / s), (float)(2 * iQ - (m - 1)) * (1.0f / s));
+  } else if constexpr (M == 8) {
+    constexpr float s = 2.44948974278317810f;   // √6
+    int iI = pam_index(z.x * s, 4), iQ = pam_index(z.y * s, 2);
+    d.lab = (gray(iI) << 1) | iQ;
+    d.pt = make_float2((float)(2 * iI - 3) * (1.0f / s), (float)(2 * iQ - 1) * (1.0f / s));
+  } else {  // 32-cross
+    constexpr float s = 4.47213595499957940f;   // √20
+    float xu = z.x * s, yu = z.y * s;
+    int iI = pam_index(xu, 6), iQ = pam_index(yu, 6);
+    if ((iI == 0 || iI == 5) && (iQ == 0 || iQ == 5)) {
+      float ax = fabsf(xu), ay = fabsf(yu);
+      int iI_a = iI, iQ_a = (iQ == 0) ? 1 : 4;     // (±5, ±3): keep I, move Q inward
+      int iI_b = (iI == 0) ? 1 : 4, iQ_b = iQ;     // (±3, ±5)
+      if (ax > ay) { iQ = iQ_a; }
+      else if (ay > ax) { iI = iI_b; }
+      else {
+        int la = cross32_label(iI_a, iQ_a), lb = cross32_label(iI_b, iQ_b);
+        if (la < lb) iQ = iQ_a; else iI = iI_b;
+      }
+    }
+    d.lab = cross32_label(iI, iQ);
+    d.pt = make_float2((float)(2 * iI - 5) * (1.0f / s), (float)(2 * iQ - 5) * (1.0f / s));
+  }
+  return d;
+}
+
+// ------------------------------------------------------------------ TMA 1-D bulk copy (cp.async.bulk) + mbarrier
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void tma_bulk_g2s(void* dst_smem, const void* src_gmem, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst_smem)),
+      "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(
+          smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+
+}  // namespace kk

@@ -1,0 +1,57 @@
+// kk_params.h — plain-old-data launch parameters and launch wrappers shared by the host library and
+// the kernels (no torch, no CUDA types beyond cudaStream_t / float2).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace kk {
+
+constexpr int kHilbertN = 1024;      // PAPER.md:82 "1024-point"
+constexpr int kHilbertHop = 512;     // R1: 100 % overlap of the hop, central 512 kept
+constexpr int kHilbertLead = 256;    // (N − hop)/2 discarded at each block end
+constexpr int kFrameSym = 4096;      // R23
+constexpr int kFrameSamp = 16384;
+constexpr int kMfN = 4096;           // R6: FFT4096 → ×H → fold → IFFT2048
+constexpr int kMfHop = 3072;
+constexpr int kMfLead = 512;         // input of tile t starts at 3072 t − 512
+constexpr int kMfKeep0 = 256;        // IFFT2048 outputs kept: [256, 1792)
+constexpr int kMfKeep = 1536;
+constexpr int kHalo = kFrameSamp + kHilbertLead;   // 16640
+constexpr int kMaxK = 12;            // L = 2K + 1 ≤ 25
+constexpr int kNumCounters = 24;     // kk_stats_t layout
+
+struct K1Params {
+  float adc_scale, adc_offset;       // I = scale·(code − offset)
+  float inv_iref;                    // 1/I_ref
+  float clamp_rel;                   // ε / I_ref
+  float half_ln_iref;                // ½·ln I_ref
+  float sideband;                    // ±1
+};
+
+struct K2Params {
+  int lo_num, lo_den;
+};
+
+struct K3Params {
+  const uint8_t* schedule;           // device, n_segments entries
+  int n_segments;
+  int64_t segment_frames;
+  float ridge;
+  int widely_linear;
+  int cpr_window;                    // symbols
+};
+
+// K1: KK front end + Hilbert + field; one warp per pair of 512-blocks, 8 warps per CTA.
+void launch_k1(const void* adc_cta0, int input_float, int64_t n_pairs, float2* E, float2* part, int* clampcnt,
+               const float2* tw1024, const K1Params& p, cudaStream_t s);
+// K2: carrier removal + mixer + RRC MF + decimation by 2 on the global tile grid.
+void launch_k2(const float2* E, int64_t E_first, const float2* part, const int* clampcnt, int64_t jb0,
+               int64_t tile0, int64_t n_tiles, float2* y, int64_t y_first, int64_t y_count, const float* Hs,
+               const float2* lo_tab, const float2* tw256, const float2* tw4096, const float2* tw2048,
+               const K2Params& p, int num_sms, cudaStream_t s);
+// K3: per-frame widely-linear DD-LS equalizer, CPR, decisions, counters.
+void launch_k3(const float2* y, int64_t frame0, int64_t n_frames, int K, const float2* w_cd, const int* clampcnt,
+               int64_t clamp_frame_off, const uint8_t* ref, uint8_t* dec, float2* z, unsigned long long* counters,
+               const K3Params& p, cudaStream_t s);
+
+}  // namespace kk

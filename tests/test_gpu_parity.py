@@ -1,0 +1,201 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle on identical seeded int16 inputs.
+
+Tolerances (BASELINE.json north_star): reconstructed field within 1e-4 relative RMS (relative to
+the signal part E − A_f), MF output within 1e-4, equalizer output within 1e-4, decided symbols ≥ 99.99 %
+identical, Q within 0.05 dB, error counts bit-exact in the noiseless case.
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from gpu_case import F, HALO, field_rel_err, make_case, rel, run_gpu, run_oracle
+
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover - CPU box
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2104_06311_b200 as P  # noqa: E402
+from oracle import theory  # noqa: E402
+
+
+def _check_all(case, gpu, orc, dec_min=0.9999, z_tol=1e-4):
+    fe = field_rel_err(gpu, orc)
+    assert fe <= 1e-4, f"field rel err {fe:.3e}"
+    assert gpu["m0"] == orc["m0"]
+    ye = rel(gpu["y"], orc["y"])
+    assert ye <= 1e-4, f"MF rel err {ye:.3e}"
+    ze = rel(gpu["z"], orc["z"])
+    assert ze <= z_tol, f"EQ rel err {ze:.3e}"
+    agree = np.mean(gpu["dec"] == orc["dec"])
+    assert agree >= dec_min, f"decision agreement {agree}"
+    return fe, ye, ze, agree
+
+
+# ----------------------------------------------------------------------------- C1 (BASELINE configs[0])
+def test_c1_b2b_noiseless_parity_and_exact_counts():
+    case = make_case(M=4, n=1 << 16, seed=101)
+    gpu, orc = run_gpu(case), run_oracle(case)
+    _check_all(case, gpu, orc, dec_min=1.0)
+    s, c = gpu["stats"], orc["counts"]
+    assert s["sym_err"] == list(c["sym_err"]) and s["bit_err"] == list(c["bit_err"]) == [0] * 5
+    assert s["bits"] == list(c["bits"]) and s["sym"] == list(c["sym"])
+    assert s["frames"] == 4 and s["clamped"] == c["clamped"] and s["dead_frames"] == 0 and s["bad_frames"] == 0
+
+
+@pytest.mark.parametrize("esn0,noise", [(8.0, "white"), (10.0, "white"), (12.0, "white"), (5.0, "analytic"),
+                                        (7.0, "analytic")])
+def test_c1_awgn_parity(esn0, noise):
+    case = make_case(M=4, n=1 << 18, esn0=esn0, noise=noise, seed=102)
+    gpu, orc = run_gpu(case), run_oracle(case)
+    _check_all(case, gpu, orc)
+    be_g, be_o = sum(gpu["stats"]["bit_err"]), int(orc["counts"]["bit_err"].sum())
+    bits = sum(gpu["stats"]["bits"])
+    assert abs(theory.q_from_ber(be_g / bits) - theory.q_from_ber(be_o / bits)) <= 0.05
+
+
+# ----------------------------------------------------------------------------- every format, CD, noise
+@pytest.mark.parametrize("M,dl,cspr,esn0", [
+    (8, 0.0, 12.0, None), (16, 112000.0, 12.0, None), (32, 200000.0, 12.0, None), (64, 32000.0, 12.0, None),
+    (4, 200000.0, 12.0, None), (16, 112000.0, 6.0, 17.0 + 10 * math.log10(12.5) - 10 * math.log10(1 + 10 ** 0.6)),
+    (64, 32000.0, 12.0, 26.0), (32, 32000.0, 14.0, 22.0), (8, 200000.0, 10.0, 16.0)])
+def test_format_parity(M, dl, cspr, esn0):
+    case = make_case(M=M, dl=dl, cspr=cspr, esn0=esn0, n=1 << 17, seed=200 + M)
+    gpu, orc = run_gpu(case), run_oracle(case)
+    _check_all(case, gpu, orc, dec_min=1.0 if esn0 is None else 0.9999)
+    if esn0 is None:
+        assert gpu["stats"]["bit_err"] == [0] * 5 == list(orc["counts"]["bit_err"])
+    else:
+        bits = sum(gpu["stats"]["bits"])
+        bg, bo = sum(gpu["stats"]["bit_err"]), int(orc["counts"]["bit_err"].sum())
+        if 0 < bg and 0 < bo:
+            assert abs(theory.q_from_ber(bg / bits) - theory.q_from_ber(bo / bits)) <= 0.05
+
+
+def test_q_parity_large_64qam():
+    case = make_case(M=64, dl=32000.0, cspr=12.0, esn0=24.0, n=1 << 20, seed=301)
+    gpu, orc = run_gpu(case), run_oracle(case, keep=True)
+    _check_all(case, gpu, orc)
+    bits = sum(gpu["stats"]["bits"])
+    qg = theory.q_from_ber(sum(gpu["stats"]["bit_err"]) / bits)
+    qo = theory.q_from_ber(int(orc["counts"]["bit_err"].sum()) / bits)
+    assert abs(qg - qo) <= 0.05
+
+
+# ----------------------------------------------------------------------------- mixed formats (C5 shape)
+def test_mixed_format_schedule():
+    case = make_case(formats=(4, 8, 16, 32, 64), segment_frames=1, dl=32000.0, cspr=12.0, esn0=26.0,
+                     n=10 * F, seed=501)
+    gpu, orc = run_gpu(case), run_oracle(case)
+    _check_all(case, gpu, orc)
+    s, c = gpu["stats"], orc["counts"]
+    assert s["sym"] == list(c["sym"]) and s["bits"] == list(c["bits"])
+    assert all(v == 2 * 4096 for v in s["sym"])
+
+
+# ----------------------------------------------------------------------------- KK exactness on GPU (P3 analogue)
+def test_exp_construction_float_input():
+    from paper_2104_06311_b200 import KK_STAGE_FIELD, Receiver
+    rng = np.random.default_rng(1)
+    N, first, n = 1024, 3 * F, 2 * F
+    q = np.arange(3, 262)
+    c = rng.standard_normal(len(q)) + 1j * rng.standard_normal(len(q))
+    gidx = np.arange(first - HALO, first + n + HALO)
+    z = (c[None, :] * np.exp(2j * np.pi * np.outer(gidx % N, q) / N)).sum(axis=1)
+    z *= 0.6 / np.max(np.abs(z))
+    E = 2.0 * np.exp(z)
+    I = torch.tensor(np.abs(E) ** 2, dtype=torch.float32, device="cuda")
+    rx = Receiver(adc_scale=1.0, ref_intensity=4.0, input_float=True, max_samples_per_call=n, keep_intermediate=True)
+    rx.process(I, first, n)
+    e0, Eg = rx.intermediate(KK_STAGE_FIELD)
+    Et = E[HALO - F: HALO + n + F]
+    assert e0 == first - F
+    err = np.linalg.norm(Eg.cpu().numpy() - Et) / np.linalg.norm(Et)
+    assert err <= 1e-5, err
+
+
+# ----------------------------------------------------------------------------- determinism / sharding (P13)
+def test_chunk_and_shard_invariance():
+    case = make_case(M=16, dl=112000.0, cspr=10.0, esn0=16.0, n=8 * F, seed=13)
+    whole = run_gpu(case, keep=True)
+    chunked = run_gpu(case, keep=True, chunk=2 * F)
+    assert np.array_equal(whole["dec"], chunked["dec"])
+    assert np.array_equal(whole["z"], chunked["z"])                 # bit-identical
+    for k in ("sym", "sym_err", "bits", "bit_err", "clamped", "frames"):
+        assert whole["stats"][k] == chunked["stats"][k]
+    # two "ranks": separate contexts on the two halves of the stream
+    from paper_2104_06311_b200 import Receiver
+    o = case["ocfg"]
+    codes = case["codes"].cuda()
+    decs = []
+    for r in range(2):
+        rx = Receiver(adc_scale=o.adc_scale, ref_intensity=o.ref_intensity, dispersion_ps_per_nm=case["dl"],
+                      formats=case["formats"], max_samples_per_call=4 * F)
+        d = torch.zeros(4 * 4096, dtype=torch.uint8, device="cuda")
+        rx.process(codes, case["first"] + r * 4 * F, 4 * F, decisions=d, offset=r * 4 * F)
+        decs.append(d.cpu().numpy())
+    assert np.array_equal(np.concatenate(decs), whole["dec"])
+
+
+# ----------------------------------------------------------------------------- edge cases
+def test_single_frame_and_stream_start():
+    case = make_case(M=4, n=F, first=0, esn0=10.0, seed=5)        # first frame of the stream, n = one frame
+    gpu, orc = run_gpu(case), run_oracle(case)
+    _check_all(case, gpu, orc)
+
+
+def test_dead_frame():
+    case = make_case(M=16, n=3 * F, seed=3)
+    case["codes"] = case["codes"].clone()
+    case["codes"][HALO + F: HALO + 2 * F] = 0
+    gpu, orc = run_gpu(case), run_oracle(case)
+    s = gpu["stats"]
+    assert s["dead_frames"] == 1 == orc["counts"]["dead_frames"] and s["clamped"] == F
+    assert np.array_equal(gpu["dec"], orc["dec"])
+    assert np.all(gpu["z"][4096:8192] == 0)
+
+
+def test_linear_only_and_cpr_windows():
+    case = make_case(M=16, dl=32000.0, cspr=14.0, esn0=20.0, n=4 * F, seed=8, eq_widely_linear=False,
+                     cpr_window=1024)
+    gpu, orc = run_gpu(case), run_oracle(case)
+    _check_all(case, gpu, orc)
+
+
+def test_host_path_matches_device_path():
+    case = make_case(M=16, dl=112000.0, cspr=10.0, esn0=16.0, n=8 * F, seed=21)
+    dev = run_gpu(case, keep=False)
+    from gpu_case import receiver_for
+    rx = receiver_for(case, keep=False, max_samples=2 * F)        # forces 4 pipelined chunks
+    codes = case["codes"].pin_memory()
+    ref = case["ref"].pin_memory()
+    dec = torch.zeros(case["n"] // 4, dtype=torch.uint8).pin_memory()
+    rx.process_host(codes, case["first"], case["n"], ref=ref, decisions=dec)
+    assert np.array_equal(dec.numpy().astype(np.int64), dev["dec"])
+    s = rx.stats()
+    for k in ("sym", "sym_err", "bits", "bit_err", "frames"):
+        assert s[k] == dev["stats"][k]
+
+
+def test_call_errors():
+    case = make_case(M=4, n=2 * F, seed=1)
+    from gpu_case import receiver_for
+    rx = receiver_for(case, keep=False)
+    codes = case["codes"].cuda()
+    with pytest.raises(P.KKError) as e:
+        rx.process(codes, case["first"] + 4, 2 * F)
+    assert e.value.status == P.KK_ERR_ALIGN
+    with pytest.raises(P.KKError) as e:
+        rx.process(codes, case["first"], 4 * F)
+    assert e.value.status == P.KK_ERR_CONFIG
+    with pytest.raises(P.KKError) as e:
+        P.kk_process_frames(rx.ctx, codes.data_ptr() + HALO * 2, case["first"], 100)
+    assert e.value.status == P.KK_ERR_SHORT
+    with pytest.raises(P.KKError) as e:
+        P.kk_process_frames(rx.ctx, codes.data_ptr() + HALO * 2 + 2, case["first"], 2 * F)
+    assert e.value.status == P.KK_ERR_ALIGN
+    with pytest.raises(P.KKError) as e:
+        P.kk_intermediate_range(rx.ctx, P.KK_STAGE_EQ)
+    assert e.value.status == P.KK_ERR_STATE
