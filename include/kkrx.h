@@ -64,7 +64,7 @@ typedef struct kk_config {
   int32_t hilbert_n, hilbert_hop;/* 1024, 512 [fixed] ("1024-point 100% overlap-save"; R1)  */
   int32_t mf_fft_n, mf_hop;      /* 4096, 3072 [fixed] (FFT4096 → fold → IFFT2048; R6)                 */
   int32_t frame_symbols;         /* 4096 [fixed] (R23)                                                   */
-  int32_t eq_taps;               /* 0 = tap-count rule of SURVEY §8(a); else odd L in [3, 25]           */
+  int32_t eq_taps;               /* 0 = tap-count rule of SURVEY §8(a); else odd L in [3, 15]           */
   int32_t eq_widely_linear;      /* 1 = widely linear ("widely-linear"), 0 = linear only    */
   int32_t cpr_window;            /* 256 symbols; one of 16,32,64,128,256,512 (R12)                       */
   double  eq_ridge;              /* 1e-3: λ = ridge·tr(R)/(2L) (R10)                                     */

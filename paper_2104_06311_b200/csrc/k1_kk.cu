@@ -54,16 +54,36 @@ k1_kk_kernel(const Tin* __restrict__ adc0, float2* __restrict__ E, float2* __res
   mbar_wait(bar, 0);
 
   // ---- a1/a2: int → float, I/I_ref, ε-clamp, a = ½ ln(.)  (one MUFU.LG2 per staged sample)
-  for (int i = tid; i < K1_SAMPLES; i += K1_THREADS) {
-    float I = p.adc_scale * ((float)stage[i] - p.adc_offset);
-    float x = I * p.inv_iref;
-    bool cl = !(x >= p.clamp_rel);
-    x = cl ? p.clamp_rel : x;
-    a_s[i] = 0.34657359027997264f * __log2f(x);   // ½·ln 2·log2 x
-    unsigned bal = __ballot_sync(0xffffffffu, cl);
-    if (bal != 0u && lane == 0) {
-      int o = i - kHilbertLead;                    // output position inside the CTA (32-aligned group)
-      if (o >= 0 && o < K1_WARPS * 1024) atomicAdd(&cblk[o >> 9], __popc(bal));
+  // 8 consecutive samples per thread per step: one 16-B (int16) or two 16-B (float) shared loads, two
+  // 16-B stores; the group never straddles a 512-block, so its clamp count goes to one block counter.
+  const float sc_in = p.adc_scale * p.inv_iref, off_in = -p.adc_offset * p.adc_scale * p.inv_iref;
+  for (int gi = tid; gi < K1_SAMPLES / 8; gi += K1_THREADS) {
+    float x[8];
+    if constexpr (sizeof(Tin) == 2) {
+      const int4 raw = reinterpret_cast<const int4*>(stage)[gi];
+      const short* h = reinterpret_cast<const short*>(&raw);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) x[j] = fmaf((float)h[j], sc_in, off_in);
+    } else {
+      const float4 r0 = reinterpret_cast<const float4*>(stage)[2 * gi];
+      const float4 r1 = reinterpret_cast<const float4*>(stage)[2 * gi + 1];
+      const float rr[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+#pragma unroll
+      for (int j = 0; j < 8; ++j) x[j] = fmaf(rr[j], sc_in, off_in);
+    }
+    int ncl = 0;
+    float av[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const bool cl = !(x[j] >= p.clamp_rel);
+      ncl += cl;
+      av[j] = 0.34657359027997264f * __log2f(cl ? p.clamp_rel : x[j]);   // ½·ln 2·log2 x
+    }
+    reinterpret_cast<float4*>(a_s)[2 * gi] = make_float4(av[0], av[1], av[2], av[3]);
+    reinterpret_cast<float4*>(a_s)[2 * gi + 1] = make_float4(av[4], av[5], av[6], av[7]);
+    if (ncl) {
+      const int o = 8 * gi - kHilbertLead;        // output position inside the CTA
+      if (o >= 0 && o < K1_WARPS * 1024) atomicAdd(&cblk[o >> 9], ncl);
     }
   }
   __syncthreads();

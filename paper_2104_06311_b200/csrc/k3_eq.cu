@@ -10,23 +10,29 @@
 //   per frame f (4096 symbols k, regressor φ̃_k = [y[2k − j]]_{j=−K..K} ‖ conj(·)):
 //   (1) y⁰ = φ̃ᵀθ₀, θ₀ = [w_cd; 0];  g = (mean|y⁰|²)^{−½};  θ₀ ← gθ₀          (AGC)
 //   (2) d_k = D(g·y⁰_k)
-//   (3) R = Σ conj(φ̃)φ̃ᵀ, p = Σ conj(φ̃)d;  θ₁ = (R + λI)⁻¹(p + λθ₀)        (fp64 Cholesky)
+//   (3) R = Σ conj(φ̃)φ̃ᵀ, p = Σ conj(φ̃)d;  θ₁ = (R + λI)⁻¹(p + λθ₀)
 //   (4) y¹ = φ̃ᵀθ₁;  γ = Σ y¹·conj(D(y¹)) / Σ|D(y¹)|²;  u = y¹/|γ|           (unbias)
 //   (5) per window b: c_b = Σ u·conj(D(u)),  z = u·conj(c_b)/|c_b|           (CPR: e^{−i·arg c_b})
 //   (6) label = D(z); counts vs reference labels.
 //
-// R is assembled from its structure instead of a dense 2L×2L accumulation: with u_k[j] = y[2k − j],
-//   R11[i][j] = S(i, j−i) (j ≥ i), S(i,d) = Σ_k conj(y[2k−i])·y[2k−i−d];   R22 = conj(R11)
-//   R21[i][j] = T(min(i,j), |j−i|),  T(i,d) = Σ_k y[2k−i]·y[2k−i−d];      R12 = conj(R21)
-// The CTA accumulates S and T only for i ∈ {−K, −K+1} (all lags d), i.e. 4L complex MACs per symbol,
-// and walks i upward by 2 with the exact sliding-window correction
-//   S(i+2, d) = S(i, d) + term_i(k0 − 1) − term_i(k1 − 1).
-// Exactly the same matrix as the dense sum (up to rounding order).
+// Structure used (exact identities):
+//  * R from lag sums: with a_j = y[2k − j],  S(i,d) = Σ_k conj(a_i)·a_{i+d},  T(i,d) = Σ_k a_i·a_{i+d}.
+//    Only the bases i = −K, −K+1 are accumulated (4L complex MACs per symbol); every other S(i,d), T(i,d)
+//    follows from the exact sliding-window recurrence S(i+2,d) = S(i,d) + term_i(k0−1) − term_i(k1−1).
+//  * Real form of the widely-linear normal equations: with x_k = [Re a; Im a] ∈ R^{2L}, the complex
+//    augmented ridge system (R + λI)θ = p + λθ₀ is the same problem as two real systems
+//    (G + λ/2·I)m_r = q_r + λ/2·m_r0 (r = 1, 2; G = Σ x xᵀ, q_1 = Σ x·Re d, q_2 = Σ x·Im d) with
+//    m_1 = [w_r + v_r; v_i − w_i], m_2 = [w_i + v_i; w_r − v_r]. G and q are read off S, T and p.
+//    Linear-only mode solves the real 2L form [[Re R, −Im R],[Im R, Re R]] of the Hermitian system.
+//    Both are solved in fp64 by one warp with one matrix row per lane (Gauss–Jordan, no pivoting on an
+//    SPD matrix; failure ⇒ fall back to θ₀ and count a bad frame).
 //
-// Mapping: one CTA (256 threads) per frame; thread t owns symbols t + 256·s (s < 16) so that every warp
-// access to the frame's 2-sps samples is a contiguous 256-B shared-memory load (the samples are stored
-// de-interleaved by parity). Block reductions: in-warp transpose-reduce (31 shuffles for 32 values),
-// then an fp64 sum over the 8 warps in fixed order (deterministic).
+// Mapping: one CTA (256 threads) per frame; thread t owns symbols t + 256·s (s < 16). The frame's 2-sps
+// samples are stored de-interleaved by parity so each symbol's tap window is a set of shared-memory loads
+// with compile-time offsets (K is a template parameter) and every warp load is a contiguous 256-B access.
+// Each sweep loads a symbol's window once into registers and does all its MACs from registers.
+// Reductions: in-warp transpose-reduce (31 shuffles per 32 values), then fp64 over the 8 warps in fixed
+// order (deterministic).
 #include "kk_device.cuh"
 #include "kk_params.h"
 
@@ -35,36 +41,50 @@ namespace kk {
 constexpr int K3_THREADS = 256;
 constexpr int K3_WARPS = 8;
 constexpr int K3_SPT = kFrameSym / K3_THREADS;   // 16 symbols per thread
-constexpr int K3_G = 8;                          // lags / taps per accumulation pass
+constexpr int K3_RED = 256;                      // max reduced floats per frame (padded)
 
-struct K3Smem {
-  // dynamic layout offsets (bytes)
-  int ye, yo, red, dred, S, T, P1, P2, A, rhs, th, misc, total;
+// runtime-uniform QAM slicer parameters (CTA-uniform: one format per frame, R26)
+struct Slicer {
+  int mI, mQ, hb, cross;
+  float s, inv_s;
+  __device__ __forceinline__ void init(int M) {
+    cross = (M == 32);
+    if (M == 8) { mI = 4; mQ = 2; hb = 1; s = 2.44948974278317810f; }
+    else if (M == 32) { mI = 6; mQ = 6; hb = 0; s = 4.47213595499957940f; }
+    else {
+      mI = mQ = (M == 4) ? 2 : (M == 16) ? 4 : 8;
+      hb = (M == 4) ? 1 : (M == 16) ? 2 : 3;
+      s = (M == 4) ? 1.41421356237309505f : (M == 16) ? 3.16227766016837933f : 6.48074069840786023f;
+    }
+    inv_s = 1.0f / s;
+  }
+  __device__ __forceinline__ void levels(float2 z, int& iI, int& iQ) const {
+    const float xu = z.x * s, yu = z.y * s;
+    iI = pam_index(xu, mI);
+    iQ = pam_index(yu, mQ);
+    if (cross && (iI == 0 || iI == 5) && (iQ == 0 || iQ == 5)) {
+      const float ax = fabsf(xu), ay = fabsf(yu);
+      const int iQa = (iQ == 0) ? 1 : 4, iIb = (iI == 0) ? 1 : 4;
+      if (ax > ay) iQ = iQa;
+      else if (ay > ax) iI = iIb;
+      else if (cross32_label(iI, iQa) < cross32_label(iIb, iQ)) iQ = iQa;
+      else iI = iIb;
+    }
+  }
+  __device__ __forceinline__ float2 point(float2 z) const {
+    int iI, iQ;
+    levels(z, iI, iQ);
+    return make_float2((float)(2 * iI - (mI - 1)) * inv_s, (float)(2 * iQ - (mQ - 1)) * inv_s);
+  }
+  __device__ __forceinline__ int label(float2 z) const {
+    int iI, iQ;
+    levels(z, iI, iQ);
+    return cross ? cross32_label(iI, iQ) : ((gray(iI) << hb) | gray(iQ));
+  }
 };
 
-__host__ __device__ inline K3Smem k3_layout(int K) {
-  K3Smem l;
-  const int L = 2 * K + 1, n = 2 * L, nd = 2 * K + 1;
-  int o = 0;
-  auto take = [&](int bytes) { int r = o; o += (bytes + 15) & ~15; return r; };
-  l.ye = take((kFrameSym + K + 1) * 8);
-  l.yo = take((kFrameSym + K + 1) * 8);
-  l.red = take(K3_WARPS * 32 * 4);
-  l.dred = take(32 * 8);
-  l.S = take(2 * nd * 16);
-  l.T = take(2 * nd * 16);
-  l.P1 = take(L * 16);
-  l.P2 = take(L * 16);
-  l.A = take(n * n * 16);
-  l.rhs = take(n * 16);
-  l.th = take(n * 8);
-  l.misc = take(64 * 4);
-  l.total = o;
-  return l;
-}
-
-// Sum 32 per-thread floats over the CTA: result (fp64) in dres[0..31] for all threads after return.
-__device__ __forceinline__ void block_reduce32(float (&v)[32], float* red, double* dres, int lane, int warp) {
+// In-warp transpose-reduce of 32 floats: afterwards lane l holds the warp sum of element l.
+__device__ __forceinline__ float warp_transpose_reduce(float (&v)[32], int lane) {
 #pragma unroll
   for (int off = 16; off >= 1; off >>= 1) {
     const bool up = (lane & off) != 0;
@@ -75,355 +95,410 @@ __device__ __forceinline__ void block_reduce32(float (&v)[32], float* red, doubl
       v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
     }
   }
-  red[warp * 32 + lane] = v[0];   // lane l holds the warp sum of element l
-  __syncthreads();
-  if (warp == 0) {
+  return v[0];
+}
+
+// Write this warp's sums of acc[0..N) to red[warp*K3_RED + base + i].
+template <int N>
+__device__ __forceinline__ void warp_partials(const float (&acc)[N], float* red_w, int base, int lane) {
+#pragma unroll
+  for (int b = 0; b < (N + 31) / 32; ++b) {
+    float t[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) t[i] = (b * 32 + i < N) ? acc[b * 32 + i] : 0.f;
+    const float r = warp_transpose_reduce(t, lane);
+    if (b * 32 + lane < N) red_w[base + b * 32 + lane] = r;
+  }
+}
+
+// fp64 sum over the 8 warp partials of values [0, n) into dres (call after a __syncthreads).
+__device__ __forceinline__ void cross_warp_sum(const float* red, double* dres, int n, int tid) {
+  for (int v = tid; v < n; v += K3_THREADS) {
     double s = 0.0;
 #pragma unroll
-    for (int w = 0; w < K3_WARPS; ++w) s += (double)red[w * 32 + lane];
-    dres[lane] = s;
-  }
-  __syncthreads();
-}
-
-__device__ __forceinline__ double2 dmulc(double2 a, double2 b) {  // a * conj(b)
-  return make_double2(a.x * b.x + a.y * b.y, a.y * b.x - a.x * b.y);
-}
-__device__ __forceinline__ double2 dmul(double2 a, double2 b) {
-  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
-}
-
-template <int M>
-__device__ __forceinline__ Decision slice_m(float2 z) { return slice<M>(z); }
-
-__device__ __forceinline__ Decision slice_rt(float2 z, int M) {
-  switch (M) {
-    case 4: return slice<4>(z);
-    case 8: return slice<8>(z);
-    case 16: return slice<16>(z);
-    case 32: return slice<32>(z);
-    default: return slice<64>(z);
+    for (int w = 0; w < K3_WARPS; ++w) s += (double)red[w * K3_RED + v];
+    dres[v] = s;
   }
 }
 
+// Gauss–Jordan elimination step KS on an N×N system with (W − N) right-hand sides, one row per lane,
+// unrolled at compile time (keeps `row` in registers). SPD ⇒ no pivoting; non-positive pivot ⇒ fail.
+template <int N, int W, int KS>
+__device__ __forceinline__ void gj_step(double (&row)[W], int lane, int& fail) {
+  if constexpr (KS < N) {
+    const double piv = __shfl_sync(0xffffffffu, row[KS], KS);
+    fail |= !(piv > 0.0) || !isfinite(piv);
+    const double inv = 1.0 / piv;
+    if (lane == KS) {
+#pragma unroll
+      for (int c = KS; c < W; ++c) row[c] *= inv;
+    }
+    const double fct = row[KS];
+#pragma unroll
+    for (int c = KS + 1; c < W; ++c) {
+      const double pc = __shfl_sync(0xffffffffu, row[c], KS);
+      if (lane != KS) row[c] = fma(-fct, pc, row[c]);
+    }
+    gj_step<N, W, KS + 1>(row, lane, fail);
+  }
+}
+
+template <int K>
+struct K3Layout {
+  static constexpr int L = 2 * K + 1;
+  static constexpr int ND = 2 * K + 1;             // lags 0..2K for base i = −K (ρ = 0); 0..2K−1 for ρ = 1
+  static constexpr int N = 2 * L;                  // real system size
+  static constexpr int NP = 4 * L;                 // p floats: p1, p2 complex
+  static constexpr int NR = 4 * ND + 4 * (ND - 1); // S0,T0 (ND complex each) + S1,T1 (ND−1 complex each)
+  static constexpr int NRED = NP + NR;
+  static constexpr int RG = 5;                     // lags per R sweep (register budget)
+  // shared memory (bytes)
+  static constexpr int YE = 0;
+  static constexpr int YN = kFrameSym + K + 1;     // float2 per parity plane
+  static constexpr int YO = YE + YN * 8;
+  static constexpr int RED = ((YO + YN * 8 + 15) / 16) * 16;
+  static constexpr int DRES = RED + K3_WARPS * K3_RED * 4;
+  static constexpr int MAT = DRES + K3_RED * 8;    // real system rows (N × (N + 2) doubles)
+  static constexpr int TH = MAT + N * (N + 2) * 8; // θ₁ as float2 [w(L), v(L)]
+  static constexpr int ROT = TH + 2 * L * 8;       // 16 CPR rotations
+  static constexpr int US = ROT + 16 * 8;          // per-symbol y⁰ / y¹ / z (float2 × 4096)
+  static constexpr int REF = US + kFrameSym * 8;   // reference labels (TMA bulk copy, 4096 B)
+  static constexpr int BAR = REF + kFrameSym;      // mbarrier
+  static constexpr int MISC = BAR + 16;
+  static constexpr int TOTAL = MISC + 64 * 4;
+  static_assert(NRED <= K3_RED, "reduction buffer");
+  static_assert(N <= 32, "one matrix row per lane");
+};
+
+template <int K>
 __global__ void __launch_bounds__(K3_THREADS, 2)
-k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int K, const float2* __restrict__ w_cd,
+k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, const float2* __restrict__ w_cd,
              const int* __restrict__ clampcnt, int64_t clamp_frame_off, const uint8_t* __restrict__ ref,
              uint8_t* __restrict__ dec, float2* __restrict__ zout, unsigned long long* __restrict__ counters,
              K3Params p) {
+  using Lay = K3Layout<K>;
+  constexpr int L = Lay::L, ND = Lay::ND, N = Lay::N;
   extern __shared__ __align__(16) unsigned char smem[];
-  const K3Smem lay = k3_layout(K);
-  float2* ye = reinterpret_cast<float2*>(smem + lay.ye);
-  float2* yo = reinterpret_cast<float2*>(smem + lay.yo);
-  float* red = reinterpret_cast<float*>(smem + lay.red);
-  double* dred = reinterpret_cast<double*>(smem + lay.dred);
-  double2* Sd = reinterpret_cast<double2*>(smem + lay.S);
-  double2* Td = reinterpret_cast<double2*>(smem + lay.T);
-  double2* P1 = reinterpret_cast<double2*>(smem + lay.P1);
-  double2* P2 = reinterpret_cast<double2*>(smem + lay.P2);
-  double2* Am = reinterpret_cast<double2*>(smem + lay.A);
-  double2* rhs = reinterpret_cast<double2*>(smem + lay.rhs);
-  float2* th = reinterpret_cast<float2*>(smem + lay.th);
-  int* misc = reinterpret_cast<int*>(smem + lay.misc);
+  float2* ye = reinterpret_cast<float2*>(smem + Lay::YE);
+  float2* yo = reinterpret_cast<float2*>(smem + Lay::YO);
+  float* red = reinterpret_cast<float*>(smem + Lay::RED);
+  double* dres = reinterpret_cast<double*>(smem + Lay::DRES);
+  double* mat = reinterpret_cast<double*>(smem + Lay::MAT);
+  float2* th = reinterpret_cast<float2*>(smem + Lay::TH);
+  float2* rot = reinterpret_cast<float2*>(smem + Lay::ROT);
+  float2* us = reinterpret_cast<float2*>(smem + Lay::US);
+  uint8_t* ref_s = smem + Lay::REF;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + Lay::BAR);
+  int* misc = reinterpret_cast<int*>(smem + Lay::MISC);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int fl = blockIdx.x;
   const int64_t f = frame0 + fl;
-  const int L = 2 * K + 1, nd = 2 * K + 1;
   const bool wl = p.widely_linear != 0;
-  const int n = wl ? 2 * L : L;
   const int M = (int)p.schedule[(int)(((f / p.segment_frames) % p.n_segments + p.n_segments) % p.n_segments)];
   const int bi = (M == 4) ? 0 : (M == 8) ? 1 : (M == 16) ? 2 : (M == 32) ? 3 : 4;
-  const int nbits = bi + 2;
+  Slicer sl;
+  sl.init(M);
+  float* red_w = red + warp * K3_RED;
+  const int64_t sym0 = (int64_t)fl * kFrameSym;
 
-  // ---- frame-level clamp count (K1 per-block counts) → dead-frame rule
-  int ccount = 0;
+  // ---- reference labels: one TMA bulk copy of the frame's 4096 labels into shared memory (consumed at the end)
+  const bool ref_tma = ref && ((reinterpret_cast<uintptr_t>(ref + sym0) & 15) == 0);
+  if (tid == 0 && ref_tma) mbar_init(bar, 1);
+  __syncthreads();
+  if (tid == 0 && ref_tma) {
+    mbar_arrive_expect_tx(bar, kFrameSym);
+    tma_bulk_g2s(ref_s, ref + sym0, kFrameSym, bar);
+  }
+  // ---- frame clamp count (K1 per-block counts) → dead-frame rule
   if (warp == 0) {
     int c = clampcnt[clamp_frame_off + (int64_t)fl * 32 + lane];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
     if (lane == 0) misc[0] = c;
   }
-  // ---- load the frame's 2-sps samples y[2k0 − K .. 2k0 + 8190 + K], de-interleaved by parity
+  // ---- the frame's 2-sps samples y_s[i] = y[2k0 − K + i], i < 8191 + 2K, de-interleaved by parity
   const float4* yf = reinterpret_cast<const float4*>(y + (int64_t)fl * (2 * kFrameSym));
-  const int npair = kFrameSym + K;   // pairs (ys[2c], ys[2c+1]); the last odd element is unused padding
-  for (int c = tid; c < npair; c += K3_THREADS) {
+  for (int c = tid; c < kFrameSym + K; c += K3_THREADS) {
     const float4 v = __ldg(yf + c);
     ye[c] = make_float2(v.x, v.y);
     yo[c] = make_float2(v.z, v.w);
   }
   __syncthreads();
-  ccount = misc[0];
+  const int ccount = misc[0];
   const bool dead = (ccount >= kFrameSamp);
-  // y_s[i] (i = tap-local index, y_s[i] = y[2k0 − K + i]) for local symbol kl: y_s[2kl + i]
-  auto Y = [&](int idx) -> float2 { return (idx & 1) ? yo[idx >> 1] : ye[idx >> 1]; };
 
-  float2 u[K3_SPT];
+  // tap window of local symbol kl: w[e] = y_s[2kl + 2K − e] = y[2k − (e − K)], e = 0..2K (tap j = e − K)
+  auto load_window = [&](int kl, float2 (&w)[L]) {
+#pragma unroll
+    for (int e = 0; e < L; ++e) w[e] = (e & 1) ? yo[kl + K - (e + 1) / 2] : ye[kl + K - e / 2];
+  };
+
   int bad = 0;
   if (!dead) {
-    // ---- (1) pass 1 with θ₀ = [w_cd; 0]: y⁰_k = Σ_j w_j y[2k − j] = Σ_{a} w_cd[a]·y_s[2kl + 2K − a]
+    // ---- (1) pass 1 with θ₀ = [w_cd; 0] and the frame power
+    float2 wc[L];
 #pragma unroll
-    for (int s = 0; s < K3_SPT; ++s) u[s] = make_float2(0.f, 0.f);
-    for (int a = 0; a < L; ++a) {
-      const float2 w = __ldg(&w_cd[a]);
-      const int off = 2 * K - a;
-#pragma unroll
-      for (int s = 0; s < K3_SPT; ++s) cmac(u[s], w, Y(2 * (tid + K3_THREADS * s) + off));
-    }
-    float pw[32];
-#pragma unroll
-    for (int i = 0; i < 32; ++i) pw[i] = 0.f;
-#pragma unroll
-    for (int s = 0; s < K3_SPT; ++s) pw[0] = fmaf(u[s].x, u[s].x, fmaf(u[s].y, u[s].y, pw[0]));
-    block_reduce32(pw, red, dred, lane, warp);
-    const double P0 = dred[0] / (double)kFrameSym;
-    float g = (P0 > 0.0 && isfinite(P0)) ? (float)(1.0 / sqrt(P0)) : 1.0f;
-    if (!(P0 > 0.0 && isfinite(P0))) bad = 1;
-    // ---- (2) decisions on the AGC'd pass-1 output
-    float2 dk[K3_SPT];
-#pragma unroll
-    for (int s = 0; s < K3_SPT; ++s) dk[s] = slice_rt(cscale(u[s], g), M).pt;
-
-    // ---- (3a) structured R: S(i,d), T(i,d) for base i = −K + rho (rho ∈ {0,1}), lags d in groups of 8
-    //      y[2k − i] = y_s[2kl + K − i] = y_s[2kl + 2K − rho];   y[2k − i − d] = y_s[2kl + 2K − rho − d]
-    for (int rho = 0; rho < 2; ++rho) {
-      for (int d0 = 0; d0 < nd; d0 += K3_G) {
-        float acc[32];
-#pragma unroll
-        for (int i = 0; i < 32; ++i) acc[i] = 0.f;
+    for (int e = 0; e < L; ++e) wc[e] = __ldg(&w_cd[e]);    // w_cd[a], a = j + K; tap j ↔ e = j + K
+    float pw = 0.f;
 #pragma unroll 2
-        for (int s = 0; s < K3_SPT; ++s) {
-          const int ia = 2 * (tid + K3_THREADS * s) + 2 * K - rho;
-          const float2 ya = Y(ia);
+    for (int s = 0; s < K3_SPT; ++s) {
+      const int kl = tid + K3_THREADS * s;
+      float2 w[L];
+      load_window(kl, w);
+      float2 acc = make_float2(0.f, 0.f);
 #pragma unroll
-          for (int g8 = 0; g8 < K3_G; ++g8) {
-            const int d = d0 + g8;
-            if (d < nd) {
-              const float2 yb = Y(ia - d);
-              float2 sacc = make_float2(acc[4 * g8], acc[4 * g8 + 1]);
-              float2 tacc = make_float2(acc[4 * g8 + 2], acc[4 * g8 + 3]);
-              cmac_conj(sacc, ya, yb);
-              cmac(tacc, ya, yb);
-              acc[4 * g8] = sacc.x; acc[4 * g8 + 1] = sacc.y; acc[4 * g8 + 2] = tacc.x; acc[4 * g8 + 3] = tacc.y;
+      for (int e = 0; e < L; ++e) cmac(acc, wc[e], w[e]);
+      us[kl] = acc;
+      pw = fmaf(acc.x, acc.x, fmaf(acc.y, acc.y, pw));
+    }
+    pw = warp_sum(pw);
+    if (lane == 0) red_w[0] = pw;
+    __syncthreads();
+    double P0 = 0.0;
+#pragma unroll
+    for (int w8 = 0; w8 < K3_WARPS; ++w8) P0 += (double)red[w8 * K3_RED];
+    P0 /= (double)kFrameSym;
+    const bool p0ok = (P0 > 0.0) && isfinite(P0);
+    const float g = p0ok ? (float)(1.0 / sqrt(P0)) : 1.0f;
+    bad |= !p0ok;
+    __syncthreads();   // red is reused below
+
+    // ---- (3a) p1[e] = Σ conj(a_j)·d, p2[e] = Σ a_j·d  (a_j = w[e])
+    {
+      float acc[Lay::NP];
+#pragma unroll
+      for (int i = 0; i < Lay::NP; ++i) acc[i] = 0.f;
+#pragma unroll 2
+      for (int s = 0; s < K3_SPT; ++s) {
+        const int kl = tid + K3_THREADS * s;
+        const float2 d = sl.point(cscale(us[kl], g));
+        float2 w[L];
+        load_window(kl, w);
+#pragma unroll
+        for (int e = 0; e < L; ++e) {
+          float2 p1 = make_float2(acc[4 * e], acc[4 * e + 1]), p2 = make_float2(acc[4 * e + 2], acc[4 * e + 3]);
+          cmac_conj(p1, w[e], d);
+          cmac(p2, w[e], d);
+          acc[4 * e] = p1.x; acc[4 * e + 1] = p1.y; acc[4 * e + 2] = p2.x; acc[4 * e + 3] = p2.y;
+        }
+      }
+      warp_partials<Lay::NP>(acc, red_w, 0, lane);
+    }
+    // ---- (3b) lag sums for bases ρ = 0 (i = −K, e = 0) and ρ = 1 (i = −K+1, e = 1), lags in groups of RG
+    //      S_ρ(d) = Σ conj(w[ρ])·w[ρ + d],  T_ρ(d) = Σ w[ρ]·w[ρ + d]
+#pragma unroll
+    for (int d0 = 0; d0 < ND; d0 += Lay::RG) {
+      constexpr int G = Lay::RG;
+      float acc[8 * G];
+#pragma unroll
+      for (int i = 0; i < 8 * G; ++i) acc[i] = 0.f;
+#pragma unroll 2
+      for (int s = 0; s < K3_SPT; ++s) {
+        float2 w[L];
+        load_window(tid + K3_THREADS * s, w);
+#pragma unroll
+        for (int gg = 0; gg < G; ++gg) {
+          const int d = d0 + gg;
+          if (d < ND) {
+            float2 s0 = make_float2(acc[8 * gg], acc[8 * gg + 1]), t0 = make_float2(acc[8 * gg + 2], acc[8 * gg + 3]);
+            cmac_conj(s0, w[0], w[d]);
+            cmac(t0, w[0], w[d]);
+            acc[8 * gg] = s0.x; acc[8 * gg + 1] = s0.y; acc[8 * gg + 2] = t0.x; acc[8 * gg + 3] = t0.y;
+            if (d < ND - 1) {
+              float2 s1 = make_float2(acc[8 * gg + 4], acc[8 * gg + 5]), t1 = make_float2(acc[8 * gg + 6], acc[8 * gg + 7]);
+              cmac_conj(s1, w[1], w[1 + d]);
+              cmac(t1, w[1], w[1 + d]);
+              acc[8 * gg + 4] = s1.x; acc[8 * gg + 5] = s1.y; acc[8 * gg + 6] = t1.x; acc[8 * gg + 7] = t1.y;
             }
           }
         }
-        block_reduce32(acc, red, dred, lane, warp);
-        if (tid < K3_G) {
-          const int d = d0 + tid;
-          if (d < nd) {
-            Sd[rho * nd + d] = make_double2(dred[4 * tid], dred[4 * tid + 1]);
-            Td[rho * nd + d] = make_double2(dred[4 * tid + 2], dred[4 * tid + 3]);
-          }
-        }
       }
-    }
-    // ---- (3b) p1[j] = Σ conj(y[2k−j])·d_k, p2[j] = Σ y[2k−j]·d_k; y[2k − j] = y_s[2kl + K − j], a = j + K
-    for (int a0 = 0; a0 < L; a0 += K3_G) {
-      float acc[32];
-#pragma unroll
-      for (int i = 0; i < 32; ++i) acc[i] = 0.f;
-#pragma unroll
-      for (int s = 0; s < K3_SPT; ++s) {
-        const int base = 2 * (tid + K3_THREADS * s) + 2 * K;
-        const float2 dd = dk[s];
-#pragma unroll
-        for (int g8 = 0; g8 < K3_G; ++g8) {
-          const int a = a0 + g8;
-          if (a < L) {
-            const float2 yv = Y(base - a);
-            float2 p1 = make_float2(acc[4 * g8], acc[4 * g8 + 1]);
-            float2 p2 = make_float2(acc[4 * g8 + 2], acc[4 * g8 + 3]);
-            cmac_conj(p1, yv, dd);
-            cmac(p2, yv, dd);
-            acc[4 * g8] = p1.x; acc[4 * g8 + 1] = p1.y; acc[4 * g8 + 2] = p2.x; acc[4 * g8 + 3] = p2.y;
-          }
-        }
-      }
-      block_reduce32(acc, red, dred, lane, warp);
-      if (tid < K3_G && a0 + tid < L) {
-        P1[a0 + tid] = make_double2(dred[4 * tid], dred[4 * tid + 1]);
-        P2[a0 + tid] = make_double2(dred[4 * tid + 2], dred[4 * tid + 3]);
-      }
+      // layout in red: [NP + 8·d + {S0re, S0im, T0re, T0im, S1re, S1im, T1re, T1im}]
+      warp_partials<8 * G>(acc, red_w, Lay::NP + 8 * d0, lane);
     }
     __syncthreads();
+    cross_warp_sum(red, dres, Lay::NP + 8 * ND, tid);
+    __syncthreads();
 
-    // ---- (3c) assemble R + λI and rhs = p + λθ₀ (fp64), then Cholesky solve — warp 0
+    // ---- (3c) assemble the real system and solve (warp 0)
     if (warp == 0) {
-      // S(i,d) for all i ∈ [−K, K − d] by the sliding recurrence; store R11 / R21 blocks directly.
-      // y_s local index of y[2k − i] for the edge symbols: k0 − 1 → K − 2 − i ; k1 − 1 → 8192 + K − 2 − i
-      for (int d = lane; d < nd; d += 32) {
-        for (int rho = 0; rho < 2; ++rho) {
-          double2 sv = Sd[rho * nd + d], tv = Td[rho * nd + d];
-          for (int i = -K + rho; i + d <= K; i += 2) {
-            const int r = i + K, c = i + d + K;     // R11[r][c] (c ≥ r), R21[r][c]
-            Am[r * n + c] = sv;
-            Am[c * n + r] = make_double2(sv.x, -sv.y);
-            if (wl) {
-              // R21 = T_sym, R12 = conj(T_sym), R22 = conj(R11)
-              Am[(L + r) * n + c] = tv; Am[(L + c) * n + r] = tv;
-              Am[r * n + (L + c)] = make_double2(tv.x, -tv.y); Am[c * n + (L + r)] = make_double2(tv.x, -tv.y);
-              Am[(L + r) * n + (L + c)] = make_double2(sv.x, -sv.y);
-              Am[(L + c) * n + (L + r)] = sv;
-            }
-            // advance i → i + 2
-            if (i + 2 + d > K) break;
-            const int lo1 = K - 2 - i, lo2 = lo1 - d;
-            const int hi1 = 2 * kFrameSym + K - 2 - i, hi2 = hi1 - d;
-            const float2 a1 = Y(lo1), a2 = Y(lo2), b1 = Y(hi1), b2 = Y(hi2);
-            sv.x += (double)a1.x * a2.x + (double)a1.y * a2.y - ((double)b1.x * b2.x + (double)b1.y * b2.y);
-            sv.y += (double)a1.x * a2.y - (double)a1.y * a2.x - ((double)b1.x * b2.y - (double)b1.y * b2.x);
-            tv.x += (double)a1.x * a2.x - (double)a1.y * a2.y - ((double)b1.x * b2.x - (double)b1.y * b2.y);
-            tv.y += (double)a1.x * a2.y + (double)a1.y * a2.x - ((double)b1.x * b2.y + (double)b1.y * b2.x);
+      // complex S(i, i+d), T(i, i+d) for all i ∈ [−K, K − d] via the sliding recurrence. Local y_s index
+      // of y[2k − i] at the edge symbols k0 − 1 → K − 2 − i; k1 − 1 → 8190 + K − i.
+      auto Ys = [&](int idx) -> double2 {
+        const float2 v = (idx & 1) ? yo[idx >> 1] : ye[idx >> 1];
+        return make_double2((double)v.x, (double)v.y);
+      };
+      // lane l < 2·ND walks one (ρ, d) chain and writes the matrix entries it owns
+      double* A = mat;   // row-major N × (N + 2)
+      constexpr int W = N + 2;
+      for (int c = lane; c < 2 * ND; c += 32) {
+        const int rho = c / ND, d = c % ND;
+        if (rho == 1 && d == ND - 1) continue;
+        double sr = dres[Lay::NP + 8 * d + 4 * rho], si = dres[Lay::NP + 8 * d + 4 * rho + 1];
+        double tr_ = dres[Lay::NP + 8 * d + 4 * rho + 2], ti = dres[Lay::NP + 8 * d + 4 * rho + 3];
+        for (int i = -K + rho; i + d <= K; i += 2) {
+          const int r = i + K, q = i + d + K;     // S(r, q) = Σ conj(a_r)·a_q, T(r, q) = Σ a_r·a_q
+          if (wl) {
+            // G = [[Σ ar arᵀ, Σ ar aiᵀ], [Σ ai arᵀ, Σ ai aiᵀ]] from S and T (both orders of (r, q))
+            const double rr = 0.5 * (sr + tr_), ii = 0.5 * (sr - tr_);
+            const double ri = 0.5 * (si + ti), ir = 0.5 * (ti - si);   // Σ ar_r·ai_q, Σ ai_r·ar_q
+            A[r * W + q] = rr;             A[q * W + r] = rr;
+            A[(L + r) * W + (L + q)] = ii; A[(L + q) * W + (L + r)] = ii;
+            A[r * W + (L + q)] = ri;       A[(L + q) * W + r] = ri;
+            A[(L + r) * W + q] = ir;       A[q * W + (L + r)] = ir;
+          } else {
+            // real form of the Hermitian R11: [[Re R, −Im R], [Im R, Re R]], R[r][q] = S, R[q][r] = conj(S)
+            A[r * W + q] = sr;             A[q * W + r] = sr;
+            A[(L + r) * W + (L + q)] = sr; A[(L + q) * W + (L + r)] = sr;
+            A[(L + r) * W + q] = si;       A[(L + q) * W + r] = -si;
+            A[r * W + (L + q)] = -si;      A[q * W + (L + r)] = si;
           }
+          if (i + 2 + d > K) break;
+          const double2 a1 = Ys(K - 2 - i), a2 = Ys(K - 2 - i - d);
+          const double2 b1 = Ys(8190 + K - i), b2 = Ys(8190 + K - i - d);
+          sr += a1.x * a2.x + a1.y * a2.y - (b1.x * b2.x + b1.y * b2.y);
+          si += a1.x * a2.y - a1.y * a2.x - (b1.x * b2.y - b1.y * b2.x);
+          tr_ += a1.x * a2.x - a1.y * a2.y - (b1.x * b2.x - b1.y * b2.y);
+          ti += a1.x * a2.y + a1.y * a2.x - (b1.x * b2.y + b1.y * b2.x);
         }
       }
       __syncwarp();
-      double tr = 0.0;
-      for (int a = 0; a < n; ++a) tr += Am[a * n + a].x;
-      const double lam = (double)p.ridge * tr / (double)n;
-      for (int a = lane; a < n; a += 32) {
-        Am[a * n + a].x += lam;
-        const double2 pv = (a < L) ? P1[a] : P2[a - L];
-        double2 t0 = make_double2(0.0, 0.0);
-        if (a < L) { const float2 w = w_cd[a]; t0 = make_double2((double)g * w.x, (double)g * w.y); }
-        rhs[a] = make_double2(pv.x + lam * t0.x, pv.y + lam * t0.y);
-      }
-      __syncwarp();
-      // right-looking Cholesky A = L·Lᴴ (lower), in place
-      int fail = 0;
-      for (int k = 0; k < n; ++k) {
-        const double dkk = Am[k * n + k].x;
-        fail |= !(dkk > 0.0) || !isfinite(dkk);
-        const double lkk = sqrt(fabs(dkk) + 1e-300);
-        const double inv = 1.0 / lkk;
-        __syncwarp();
-        for (int i = k + 1 + lane; i < n; i += 32) {
-          Am[i * n + k] = make_double2(Am[i * n + k].x * inv, Am[i * n + k].y * inv);
-        }
-        if (lane == 0) Am[k * n + k] = make_double2(lkk, 0.0);
-        __syncwarp();
-        for (int i = k + 1 + lane; i < n; i += 32) {
-          const double2 lik = Am[i * n + k];
-          for (int j = k + 1; j <= i; ++j) {
-            const double2 t = dmulc(lik, Am[j * n + k]);
-            Am[i * n + j].x -= t.x; Am[i * n + j].y -= t.y;
-          }
-        }
-        __syncwarp();
-      }
-      // forward: L z = rhs ; backward: Lᴴ θ = z  (column-oriented, lanes over rows)
-      for (int k = 0; k < n; ++k) {
-        const double inv = 1.0 / Am[k * n + k].x;
-        if (lane == 0) rhs[k] = make_double2(rhs[k].x * inv, rhs[k].y * inv);
-        __syncwarp();
-        const double2 zk = rhs[k];
-        for (int i = k + 1 + lane; i < n; i += 32) {
-          const double2 t = dmul(Am[i * n + k], zk);
-          rhs[i].x -= t.x; rhs[i].y -= t.y;
-        }
-        __syncwarp();
-      }
-      for (int k = n - 1; k >= 0; --k) {
-        const double inv = 1.0 / Am[k * n + k].x;
-        if (lane == 0) rhs[k] = make_double2(rhs[k].x * inv, rhs[k].y * inv);
-        __syncwarp();
-        const double2 xk = rhs[k];
-        for (int i = lane; i < k; i += 32) {   // rhs[i] -= conj(L[k][i]) · x_k
-          const double2 lki = Am[k * n + i];
-          const double2 t = make_double2(lki.x * xk.x + lki.y * xk.y, lki.x * xk.y - lki.y * xk.x);
-          rhs[i].x -= t.x; rhs[i].y -= t.y;
-        }
-        __syncwarp();
-      }
-      for (int a = 0; a < n; ++a) fail |= !isfinite(rhs[a].x) || !isfinite(rhs[a].y);
-      for (int a = lane; a < 2 * L; a += 32) {
-        float2 v;
-        if (fail) {
-          v = (a < L) ? make_float2(g * w_cd[a].x, g * w_cd[a].y) : make_float2(0.f, 0.f);
+      // ridge and right-hand sides (R27/R10: λ_c = ridge·tr(R)/n_c; real form uses λ_c/2 for WL)
+      double trG = 0.0;
+#pragma unroll
+      for (int r = 0; r < N; ++r) trG += A[r * W + r];
+      const double lam = wl ? (double)p.ridge * trG / (double)N          // = λ_c / 2, tr(R) = 2 tr(G)
+                            : (double)p.ridge * 0.5 * trG / (double)L;   // real form doubles tr(R11)
+      if (lane < L) {
+        const int e = lane;
+        const double p1r = dres[4 * e], p1i = dres[4 * e + 1], p2r = dres[4 * e + 2], p2i = dres[4 * e + 3];
+        const double w0r = (double)g * (double)__ldg(&w_cd[e]).x, w0i = (double)g * (double)__ldg(&w_cd[e]).y;
+        if (wl) {
+          // q1 = [Σ ar·dr; Σ ai·dr], q2 = [Σ ar·di; Σ ai·di];  m1₀ = [w0r; −w0i], m2₀ = [w0i; w0r]
+          A[e * W + N] = 0.5 * (p1r + p2r) + lam * w0r;
+          A[(L + e) * W + N] = 0.5 * (p2i - p1i) - lam * w0i;
+          A[e * W + N + 1] = 0.5 * (p1i + p2i) + lam * w0i;
+          A[(L + e) * W + N + 1] = 0.5 * (p1r - p2r) + lam * w0r;
         } else {
-          v = (a < n) ? make_float2((float)rhs[a].x, (float)rhs[a].y) : make_float2(0.f, 0.f);
+          A[e * W + N] = p1r + lam * w0r;
+          A[(L + e) * W + N] = p1i + lam * w0i;
+          A[e * W + N + 1] = 0.0;
+          A[(L + e) * W + N + 1] = 0.0;
         }
-        th[a] = v;
+      }
+      __syncwarp();
+      // Gauss–Jordan with one row per lane (SPD ⇒ no pivoting)
+      double row[W];
+#pragma unroll
+      for (int c = 0; c < W; ++c) row[c] = (lane < N) ? A[lane * W + c] : 0.0;
+#pragma unroll
+      for (int c = 0; c < N; ++c) row[c] += (c == lane) ? lam : 0.0;   // ridge (compile-time register index)
+      int fail = 0;
+      gj_step<N, W, 0>(row, lane, fail);
+      fail |= !isfinite(row[N]) || !isfinite(row[N + 1]);
+      fail = __any_sync(0xffffffffu, fail && lane < N) ? 1 : 0;
+      // θ₁ from m1, m2 (lane e holds m1[e], m2[e]; lane L+e holds m1[L+e], m2[L+e])
+      const double m1 = row[N], m2 = row[N + 1];
+      const double m1b = __shfl_down_sync(0xffffffffu, m1, L), m2b = __shfl_down_sync(0xffffffffu, m2, L);
+      if (lane < L) {
+        float2 wv, vv;
+        if (fail) {
+          const float2 w0 = __ldg(&w_cd[lane]);
+          wv = make_float2(g * w0.x, g * w0.y);
+          vv = make_float2(0.f, 0.f);
+        } else if (wl) {
+          wv = make_float2((float)(0.5 * (m1 + m2b)), (float)(0.5 * (m2 - m1b)));
+          vv = make_float2((float)(0.5 * (m1 - m2b)), (float)(0.5 * (m2 + m1b)));
+        } else {
+          wv = make_float2((float)m1, (float)m1b);
+          vv = make_float2(0.f, 0.f);
+        }
+        th[lane] = wv;
+        th[L + lane] = vv;
       }
       if (lane == 0) misc[1] = fail;
     }
     __syncthreads();
     bad |= misc[1];
 
-    // ---- (4) pass 2: y¹_k = Σ_a w_a·y_s[2kl + 2K − a] + v_a·conj(y_s[...])
-#pragma unroll
-    for (int s = 0; s < K3_SPT; ++s) u[s] = make_float2(0.f, 0.f);
-    for (int a = 0; a < L; ++a) {
-      const float2 w = th[a], v = th[L + a];
-      const int off = 2 * K - a;
-#pragma unroll
-      for (int s = 0; s < K3_SPT; ++s) {
-        const float2 yv = Y(2 * (tid + K3_THREADS * s) + off);
-        cmac(u[s], w, yv);
-        cmac(u[s], v, cconj(yv));
-      }
-    }
-    // gain unbias γ = Σ y¹·conj(D(y¹)) / Σ|D(y¹)|²
+    // ---- (4) pass 2: y¹ = Σ_e w_e·a + v_e·conj(a)
     {
+      float2 tw[L], tv[L];
+#pragma unroll
+      for (int e = 0; e < L; ++e) { tw[e] = th[e]; tv[e] = th[L + e]; }
       float acc[32];
-#pragma unroll
-      for (int i = 0; i < 32; ++i) acc[i] = 0.f;
-#pragma unroll
+      float gr = 0.f, gi = 0.f, gd = 0.f;
+#pragma unroll 2
       for (int s = 0; s < K3_SPT; ++s) {
-        const float2 dd = slice_rt(u[s], M).pt;
-        const float2 c = cmulc(u[s], dd);
-        acc[0] += c.x; acc[1] += c.y; acc[2] = fmaf(dd.x, dd.x, fmaf(dd.y, dd.y, acc[2]));
+        const int kl = tid + K3_THREADS * s;
+        float2 w[L];
+        load_window(kl, w);
+        float2 o = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int e = 0; e < L; ++e) {
+          cmac(o, tw[e], w[e]);
+          cmac(o, tv[e], cconj(w[e]));
+        }
+        us[kl] = o;
+        // gain unbias γ = Σ y¹·conj(D(y¹)) / Σ|D(y¹)|²
+        const float2 dd = sl.point(o);
+        const float2 c = cmulc(o, dd);
+        gr += c.x; gi += c.y; gd = fmaf(dd.x, dd.x, fmaf(dd.y, dd.y, gd));
       }
-      block_reduce32(acc, red, dred, lane, warp);
-      const double gr = dred[0] / dred[2], gi = dred[1] / dred[2];
-      const double ag = sqrt(gr * gr + gi * gi);
+      gr = warp_sum(gr); gi = warp_sum(gi); gd = warp_sum(gd);
+      if (lane == 0) { red_w[0] = gr; red_w[1] = gi; red_w[2] = gd; }
+      __syncthreads();
+      double Gr = 0, Gi = 0, Gd = 0;
+#pragma unroll
+      for (int w8 = 0; w8 < K3_WARPS; ++w8) { Gr += red[w8 * K3_RED]; Gi += red[w8 * K3_RED + 1]; Gd += red[w8 * K3_RED + 2]; }
+      const double ag = sqrt(Gr * Gr + Gi * Gi) / Gd;
       float sc = 1.0f;
       if (ag > 0.0 && isfinite(ag)) sc = (float)(1.0 / ag); else bad = 1;
-#pragma unroll
-      for (int s = 0; s < K3_SPT; ++s) u[s] = cscale(u[s], sc);
-    }
-    // ---- (5) CPR: window index of symbol tid + 256 s is s / (W/256)
-    {
-      float acc[32];
+      __syncthreads();
+      // ---- (5) CPR: c_s = Σ_t u·conj(D(u)) for window s (W = 256 ⇒ one window per s), u = y¹/|γ|
 #pragma unroll
       for (int s = 0; s < K3_SPT; ++s) {
-        const float2 dd = slice_rt(u[s], M).pt;
-        const float2 c = cmulc(u[s], dd);
+        const int kl = tid + K3_THREADS * s;
+        const float2 uu = cscale(us[kl], sc);
+        us[kl] = uu;
+        const float2 c = cmulc(uu, sl.point(uu));
         acc[2 * s] = c.x; acc[2 * s + 1] = c.y;
       }
-      block_reduce32(acc, red, dred, lane, warp);
-      const int per = p.cpr_window / K3_THREADS;   // s-values per window (1, 2, 4, 8, 16)
-#pragma unroll
-      for (int s = 0; s < K3_SPT; ++s) {
-        const int w0 = (s / per) * per;
+      warp_partials<32>(acc, red_w, 0, lane);
+      __syncthreads();
+      if (tid < K3_SPT) {
+        const int per = p.cpr_window / K3_THREADS;     // s-values per window (1, 2, 4, 8, 16)
+        const int w0 = (tid / per) * per;
         double cr = 0.0, ci = 0.0;
-        for (int q = 0; q < per; ++q) { cr += dred[2 * (w0 + q)]; ci += dred[2 * (w0 + q) + 1]; }
-        const double mag = sqrt(cr * cr + ci * ci);
-        float2 rot = make_float2(1.f, 0.f);
-        if (mag > 0.0) rot = make_float2((float)(cr / mag), (float)(-ci / mag));
-        u[s] = cmul(u[s], rot);
-      }
-    }
-  } else {
+        for (int q = 0; q < per; ++q)
 #pragma unroll
-    for (int s = 0; s < K3_SPT; ++s) u[s] = make_float2(0.f, 0.f);
+          for (int w8 = 0; w8 < K3_WARPS; ++w8) {
+            cr += (double)red[w8 * K3_RED + 2 * (w0 + q)];
+            ci += (double)red[w8 * K3_RED + 2 * (w0 + q) + 1];
+          }
+        const double mag = sqrt(cr * cr + ci * ci);
+        rot[tid] = (mag > 0.0) ? make_float2((float)(cr / mag), (float)(-ci / mag)) : make_float2(1.f, 0.f);
+      }
+      __syncthreads();
+    }
   }
 
   // ---- (6) decisions, counts, outputs
+  if (ref_tma) mbar_wait(bar, 0);
   int serr = 0, berr = 0;
-  const int64_t sym0 = (int64_t)fl * kFrameSym;
-#pragma unroll
+#pragma unroll 4
   for (int s = 0; s < K3_SPT; ++s) {
     const int kl = tid + K3_THREADS * s;
-    const int lab = slice_rt(u[s], M).lab;
+    const float2 zz = dead ? make_float2(0.f, 0.f) : cmul(us[kl], rot[s]);
+    const int lab = sl.label(zz);
     if (ref) {
-      const int r = ref[sym0 + kl];
+      const int r = ref_tma ? (int)ref_s[kl] : (int)__ldg(&ref[sym0 + kl]);
       serr += (lab != r);
       berr += __popc(lab ^ r);
     }
     if (dec) dec[sym0 + kl] = (uint8_t)lab;
-    if (zout) zout[sym0 + kl] = u[s];
+    if (zout) zout[sym0 + kl] = zz;
   }
   if (ref) {
 #pragma unroll
@@ -437,12 +512,12 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int K, const float2* 
   if (tid == 0) {
     if (ref) {
       long long se = 0, be = 0;
-      for (int w = 0; w < K3_WARPS; ++w) { se += misc[8 + w]; be += misc[16 + w]; }
+      for (int w8 = 0; w8 < K3_WARPS; ++w8) { se += misc[8 + w8]; be += misc[16 + w8]; }
       if (se) atomicAdd(&counters[5 + bi], (unsigned long long)se);
       if (be) atomicAdd(&counters[15 + bi], (unsigned long long)be);
     }
     atomicAdd(&counters[bi], (unsigned long long)kFrameSym);
-    atomicAdd(&counters[10 + bi], (unsigned long long)kFrameSym * nbits);
+    atomicAdd(&counters[10 + bi], (unsigned long long)kFrameSym * (bi + 2));
     if (ccount) atomicAdd(&counters[20], (unsigned long long)ccount);
     atomicAdd(&counters[21], 1ull);
     if (dead) atomicAdd(&counters[22], 1ull);
@@ -450,15 +525,38 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int K, const float2* 
   }
 }
 
-size_t k3_smem_bytes(int K) { return (size_t)k3_layout(K).total; }
+template <int K>
+static void launch_k3_t(const float2* y, int64_t frame0, int64_t n_frames, const float2* w_cd, const int* clampcnt,
+                        int64_t clamp_frame_off, const uint8_t* ref, uint8_t* dec, float2* z,
+                        unsigned long long* counters, const K3Params& p, cudaStream_t s) {
+  constexpr int smem = K3Layout<K>::TOTAL;
+  cudaFuncSetAttribute(k3_eq_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  k3_eq_kernel<K><<<(unsigned)n_frames, K3_THREADS, smem, s>>>(y, frame0, w_cd, clampcnt, clamp_frame_off, ref, dec,
+                                                               z, counters, p);
+}
+
+size_t k3_smem_bytes(int K) {
+  switch (K) {
+    case 1: return K3Layout<1>::TOTAL;
+    case 2: return K3Layout<2>::TOTAL;
+    case 3: return K3Layout<3>::TOTAL;
+    case 4: return K3Layout<4>::TOTAL;
+    case 5: return K3Layout<5>::TOTAL;
+    case 6: return K3Layout<6>::TOTAL;
+    case 7: return K3Layout<7>::TOTAL;
+    default: return 0;
+  }
+}
 
 void launch_k3(const float2* y, int64_t frame0, int64_t n_frames, int K, const float2* w_cd, const int* clampcnt,
                int64_t clamp_frame_off, const uint8_t* ref, uint8_t* dec, float2* z, unsigned long long* counters,
                const K3Params& p, cudaStream_t s) {
-  const size_t smem = k3_smem_bytes(K);
-  cudaFuncSetAttribute(k3_eq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k3_eq_kernel<<<(unsigned)n_frames, K3_THREADS, smem, s>>>(y, frame0, K, w_cd, clampcnt, clamp_frame_off, ref, dec,
-                                                            z, counters, p);
+#define KK_K3(KV) case KV: launch_k3_t<KV>(y, frame0, n_frames, w_cd, clampcnt, clamp_frame_off, ref, dec, z, counters, p, s); break;
+  switch (K) {
+    KK_K3(1) KK_K3(2) KK_K3(3) KK_K3(4) KK_K3(5) KK_K3(6) KK_K3(7)
+    default: break;
+  }
+#undef KK_K3
 }
 
 }  // namespace kk

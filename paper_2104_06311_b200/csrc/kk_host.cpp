@@ -217,7 +217,7 @@ kk_status validate(const kk_config& c, std::string& why) {
   if (c.mf_fft_n != kk::kMfN || c.mf_hop != kk::kMfHop) return bad("kernels are built for MF 4096/3072");
   if (c.rrc_span_sym < 8 || c.rrc_span_sym * 4 > c.mf_fft_n - c.mf_hop) return bad("rrc span: taps-1 must fit the MF overlap");
   if (c.frame_symbols != kk::kFrameSym) return bad("kernels are built for 4096-symbol frames");
-  if (c.eq_taps != 0 && (c.eq_taps < 3 || c.eq_taps > 2 * kk::kMaxK + 1 || (c.eq_taps % 2) == 0)) return bad("eq_taps must be 0 or odd in [3,25]");
+  if (c.eq_taps != 0 && (c.eq_taps < 3 || c.eq_taps > 2 * kk::kMaxK + 1 || (c.eq_taps % 2) == 0)) return bad("eq_taps must be 0 or odd in [3,15]");
   if (c.cpr_window != 256 && c.cpr_window != 512 && c.cpr_window != 1024 && c.cpr_window != 2048 && c.cpr_window != 4096)
     return bad("cpr_window must be one of 256,512,1024,2048,4096");
   if (!(c.eq_ridge >= 0)) return bad("eq_ridge must be >= 0");
@@ -324,7 +324,7 @@ kk_status kk_init(const kk_config* cfg, kk_ctx** out) {
   }
   const int L = tap_rule(*cfg);
   if (L < 3 || L > 2 * kk::kMaxK + 1 || (L % 2) == 0) {
-    std::fprintf(stderr, "kk_init: tap-count rule gives L=%d outside [3,25]\n", L);
+    std::fprintf(stderr, "kk_init: tap-count rule gives L=%d outside [3,15]\n", L);
     return KK_ERR_CONFIG;
   }
   kk_ctx* c = new kk_ctx();

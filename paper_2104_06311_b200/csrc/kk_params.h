@@ -17,7 +17,7 @@ constexpr int kMfLead = 512;         // input of tile t starts at 3072 t − 512
 constexpr int kMfKeep0 = 256;        // IFFT2048 outputs kept: [256, 1792)
 constexpr int kMfKeep = 1536;
 constexpr int kHalo = kFrameSamp + kHilbertLead;   // 16640
-constexpr int kMaxK = 12;            // L = 2K + 1 ≤ 25
+constexpr int kMaxK = 7;             // L = 2K + 1 ≤ 15 (one real-system row per lane: 2L ≤ 32)
 constexpr int kNumCounters = 24;     // kk_stats_t layout
 
 struct K1Params {
