@@ -76,10 +76,11 @@ k2_mf_kernel(const float2* __restrict__ E, int64_t E_first, const float2* __rest
   extern __shared__ float2 lo_s[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int i = tid; i < p.lo_den; i += K2_THREADS) lo_s[i] = lo_tab[i];
-  const int lo_step = (int)(((int64_t)2 * K2_THREADS * p.lo_num) % p.lo_den);
 
+  // tiles are visited from the END of the range: K1 wrote E front to back, so its most recent (L2-resident)
+  // output is consumed first; K3 then walks y front to back, again reading K2's most recent writes first.
   for (int64_t ti = blockIdx.x; ti < n_tiles; ti += gridDim.x) {
-    const int64_t t = tile0 + ti;
+    const int64_t t = tile0 + (n_tiles - 1 - ti);
     const int64_t s0 = t * kMfHop - kMfLead;                 // global sample of x[0]
     const int64_t fa = floordiv(s0, kFrameSamp);
     const int64_t fsplit = (fa + 1) * kFrameSamp;            // first sample of frame fa+1
@@ -92,23 +93,27 @@ k2_mf_kernel(const float2* __restrict__ E, int64_t E_first, const float2* __rest
       if (lane == 0) A_s[warp] = make_float2(v.x * (1.0f / kFrameSamp), v.y * (1.0f / kFrameSamp));
     }
     __syncthreads();
-    // a5: b = (E − A_f)·LO, two samples per thread per step (16-B loads)
+    // next tile's input (32 KiB of E) → L2 while this tile computes
+    if (tid == 0 && ti + gridDim.x < n_tiles) {
+      const int64_t s0n = (t - gridDim.x) * kMfHop - kMfLead;
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(E + (s0n - E_first)), "r"(kMfN * 8) : "memory");
+    }
+    // a5: b = (E − A_f)·LO, one sample per thread per step: 256-B coalesced loads, conflict-free stores
     {
-      const int64_t sA = s0 + 2 * tid;
+      const int64_t sA = s0 + tid;
       int q = (int)(((sA % p.lo_den) + p.lo_den) % p.lo_den);
       q = (int)(((int64_t)q * p.lo_num) % p.lo_den);
-      const float4* src = reinterpret_cast<const float4*>(E + (s0 - E_first)) + tid;
+      const int lo_step1 = (int)(((int64_t)K2_THREADS * p.lo_num) % p.lo_den);
+      const float2* src = E + (s0 - E_first) + tid;
       const float2 A0 = A_s[0], A1 = A_s[1];
-#pragma unroll 4
-      for (int it = 0; it < kMfN / (2 * K2_THREADS); ++it) {
-        const int i = 2 * (tid + K2_THREADS * it);
-        const float4 e = __ldg(src + it * K2_THREADS);
-        const int64_t s = s0 + i;
-        const float2 A = (s < fsplit) ? A0 : A1;             // s and s+1 lie in the same frame (s even)
-        int q1 = q + p.lo_num; q1 -= (q1 >= p.lo_den) ? p.lo_den : 0;
+      const int isplit = (int)(fsplit - s0);                 // first local sample of frame fa+1
+#pragma unroll 8
+      for (int it = 0; it < kMfN / K2_THREADS; ++it) {
+        const int i = tid + K2_THREADS * it;
+        const float2 e = __ldg(src + it * K2_THREADS);
+        const float2 A = (i < isplit) ? A0 : A1;
         buf[pad16(i)] = cmul(make_float2(e.x - A.x, e.y - A.y), lo_s[q]);
-        buf[pad16(i + 1)] = cmul(make_float2(e.z - A.x, e.w - A.y), lo_s[q1]);
-        q += lo_step; q -= (q >= p.lo_den) ? p.lo_den : 0;
+        q += lo_step1; q -= (q >= p.lo_den) ? p.lo_den : 0;
       }
     }
     __syncthreads();

@@ -27,10 +27,13 @@
 //    Both are solved in fp64 by one warp with one matrix row per lane (Gauss–Jordan, no pivoting on an
 //    SPD matrix; failure ⇒ fall back to θ₀ and count a bad frame).
 //
-// Mapping: one CTA (256 threads) per frame; thread t owns symbols t + 256·s (s < 16). The frame's 2-sps
-// samples are stored de-interleaved by parity so each symbol's tap window is a set of shared-memory loads
-// with compile-time offsets (K is a template parameter) and every warp load is a contiguous 256-B access.
-// Each sweep loads a symbol's window once into registers and does all its MACs from registers.
+// Mapping: persistent CTAs (256 threads, 2 per SM), one frame at a time; thread t owns symbols t + 256·s
+// (s < 16). Each frame's 2-sps samples (64 KiB) and reference labels (4 KiB) arrive by one TMA bulk copy
+// (cp.async.bulk + mbarrier) from L2, where the CTA prefetched them (cp.async.bulk.prefetch.L2) while it was
+// working on its previous frame. A symbol's tap window y_s[2kl .. 2kl + 2K] is K+1 16-byte shared loads
+// (each warp load a contiguous 512-B access, conflict-free) with compile-time offsets (K is a template
+// parameter); every sweep does all of a symbol's MACs from registers. Sweeps: (A) lag sums + frame power,
+// (B) decisions + p, (C) pass 2 — y¹ stays in registers through unbias, CPR and the decisions.
 // Reductions: in-warp transpose-reduce (31 shuffles per 32 values), then fp64 over the 8 warps in fixed
 // order (deterministic).
 #include "kk_device.cuh"
@@ -149,323 +152,336 @@ struct K3Layout {
   static constexpr int ND = 2 * K + 1;             // lags 0..2K for base i = −K (ρ = 0); 0..2K−1 for ρ = 1
   static constexpr int N = 2 * L;                  // real system size
   static constexpr int NP = 4 * L;                 // p floats: p1, p2 complex
-  static constexpr int NR = 4 * ND + 4 * (ND - 1); // S0,T0 (ND complex each) + S1,T1 (ND−1 complex each)
-  static constexpr int NRED = NP + NR;
   static constexpr int RG = 5;                     // lags per R sweep (register budget)
+  static constexpr int NRG = (ND + RG - 1) / RG;   // R sweeps
+  static constexpr int NR = 8 * RG * NRG;          // S0,T0,S1,T1 per lag (padded to whole groups)
+  static constexpr int NRED = ((NP + NR + 1 + 31) / 32) * 32;   // + frame power
+  static constexpr int IPOW = NP + NR;             // index of the frame power in the reduction
+  static constexpr int YS = 2 * kFrameSym + 2 * K; // float2 loaded per frame (y_s[0 .. 8191 + 2K])
   // shared memory (bytes)
-  static constexpr int YE = 0;
-  static constexpr int YN = kFrameSym + K + 1;     // float2 per parity plane
-  static constexpr int YO = YE + YN * 8;
-  static constexpr int RED = ((YO + YN * 8 + 15) / 16) * 16;
-  static constexpr int DRES = RED + K3_WARPS * K3_RED * 4;
-  static constexpr int MAT = DRES + K3_RED * 8;    // real system rows (N × (N + 2) doubles)
+  static constexpr int Y = 0;
+  static constexpr int REF = Y + YS * 8;
+  static constexpr int RED = REF + kFrameSym;
+  static constexpr int DRES = RED + K3_WARPS * NRED * 4;
+  static constexpr int MAT = DRES + NRED * 8;      // real system rows (N × (N + 2) doubles)
   static constexpr int TH = MAT + N * (N + 2) * 8; // θ₁ as float2 [w(L), v(L)]
   static constexpr int ROT = TH + 2 * L * 8;       // 16 CPR rotations
-  static constexpr int US = ROT + 16 * 8;          // per-symbol y⁰ / y¹ / z (float2 × 4096)
-  static constexpr int REF = US + kFrameSym * 8;   // reference labels (TMA bulk copy, 4096 B)
-  static constexpr int BAR = REF + kFrameSym;      // mbarrier
+  static constexpr int BAR = ROT + 16 * 8;         // mbarrier
   static constexpr int MISC = BAR + 16;
   static constexpr int TOTAL = MISC + 64 * 4;
-  static_assert(NRED <= K3_RED, "reduction buffer");
   static_assert(N <= 32, "one matrix row per lane");
+  static_assert((YS * 8) % 16 == 0, "TMA size");
 };
+
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
 
 template <int K>
 __global__ void __launch_bounds__(K3_THREADS, 2)
-k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, const float2* __restrict__ w_cd,
+k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const float2* __restrict__ w_cd,
              const int* __restrict__ clampcnt, int64_t clamp_frame_off, const uint8_t* __restrict__ ref,
              uint8_t* __restrict__ dec, float2* __restrict__ zout, unsigned long long* __restrict__ counters,
              K3Params p) {
   using Lay = K3Layout<K>;
-  constexpr int L = Lay::L, ND = Lay::ND, N = Lay::N;
-  extern __shared__ __align__(16) unsigned char smem[];
-  float2* ye = reinterpret_cast<float2*>(smem + Lay::YE);
-  float2* yo = reinterpret_cast<float2*>(smem + Lay::YO);
+  constexpr int L = Lay::L, ND = Lay::ND, N = Lay::N, NRED = Lay::NRED;
+  extern __shared__ __align__(128) unsigned char smem[];
+  float2* ys = reinterpret_cast<float2*>(smem + Lay::Y);
+  const float4* ys4 = reinterpret_cast<const float4*>(smem + Lay::Y);
+  uint8_t* ref_s = smem + Lay::REF;
   float* red = reinterpret_cast<float*>(smem + Lay::RED);
   double* dres = reinterpret_cast<double*>(smem + Lay::DRES);
   double* mat = reinterpret_cast<double*>(smem + Lay::MAT);
   float2* th = reinterpret_cast<float2*>(smem + Lay::TH);
   float2* rot = reinterpret_cast<float2*>(smem + Lay::ROT);
-  float2* us = reinterpret_cast<float2*>(smem + Lay::US);
-  uint8_t* ref_s = smem + Lay::REF;
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + Lay::BAR);
   int* misc = reinterpret_cast<int*>(smem + Lay::MISC);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int fl = blockIdx.x;
-  const int64_t f = frame0 + fl;
   const bool wl = p.widely_linear != 0;
-  const int M = (int)p.schedule[(int)(((f / p.segment_frames) % p.n_segments + p.n_segments) % p.n_segments)];
-  const int bi = (M == 4) ? 0 : (M == 8) ? 1 : (M == 16) ? 2 : (M == 32) ? 3 : 4;
-  Slicer sl;
-  sl.init(M);
-  float* red_w = red + warp * K3_RED;
-  const int64_t sym0 = (int64_t)fl * kFrameSym;
+  float* red_w = red + warp * NRED;
+  const bool ref_tma = ref && ((reinterpret_cast<uintptr_t>(ref) & 15) == 0);
+  constexpr uint32_t YBYTES = Lay::YS * 8;
 
-  // ---- reference labels: one TMA bulk copy of the frame's 4096 labels into shared memory (consumed at the end)
-  const bool ref_tma = ref && ((reinterpret_cast<uintptr_t>(ref + sym0) & 15) == 0);
-  if (tid == 0 && ref_tma) mbar_init(bar, 1);
+  auto issue = [&](int fl) {   // thread 0: TMA the frame (and its labels) into shared memory
+    const uint32_t bytes = YBYTES + (ref_tma ? (uint32_t)kFrameSym : 0u);
+    mbar_arrive_expect_tx(bar, bytes);
+    tma_bulk_g2s(ys, y + (int64_t)fl * (2 * kFrameSym), YBYTES, bar);
+    if (ref_tma) tma_bulk_g2s(ref_s, ref + (int64_t)fl * kFrameSym, kFrameSym, bar);
+  };
+  auto prefetch = [&](int fl) {
+    prefetch_l2(y + (int64_t)fl * (2 * kFrameSym), YBYTES);
+    if (ref_tma) prefetch_l2(ref + (int64_t)fl * kFrameSym, kFrameSym);
+  };
+  if (tid == 0) mbar_init(bar, 1);
   __syncthreads();
-  if (tid == 0 && ref_tma) {
-    mbar_arrive_expect_tx(bar, kFrameSym);
-    tma_bulk_g2s(ref_s, ref + sym0, kFrameSym, bar);
+  if (tid == 0 && (int)blockIdx.x < n_frames) {
+    issue(blockIdx.x);
+    if ((int)blockIdx.x + (int)gridDim.x < n_frames) prefetch(blockIdx.x + gridDim.x);
   }
-  // ---- frame clamp count (K1 per-block counts) → dead-frame rule
-  if (warp == 0) {
-    int c = clampcnt[clamp_frame_off + (int64_t)fl * 32 + lane];
+  float2 wc[L];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-    if (lane == 0) misc[0] = c;
-  }
-  // ---- the frame's 2-sps samples y_s[i] = y[2k0 − K + i], i < 8191 + 2K, de-interleaved by parity
-  const float4* yf = reinterpret_cast<const float4*>(y + (int64_t)fl * (2 * kFrameSym));
-  for (int c = tid; c < kFrameSym + K; c += K3_THREADS) {
-    const float4 v = __ldg(yf + c);
-    ye[c] = make_float2(v.x, v.y);
-    yo[c] = make_float2(v.z, v.w);
-  }
-  __syncthreads();
-  const int ccount = misc[0];
-  const bool dead = (ccount >= kFrameSamp);
+  for (int e = 0; e < L; ++e) wc[e] = __ldg(&w_cd[e]);    // w_cd[a], a = j + K; tap j ↔ window index e
 
-  // tap window of local symbol kl: w[e] = y_s[2kl + 2K − e] = y[2k − (e − K)], e = 0..2K (tap j = e − K)
+  // tap window of local symbol kl: w[e] = y_s[2kl + 2K − e] = y[2k − (e − K)], e = 0..2K;
+  // loaded as K+1 16-B pairs (y_s[2kl + 2m], y_s[2kl + 2m + 1]) = (w[2K − 2m], w[2K − 2m − 1])
   auto load_window = [&](int kl, float2 (&w)[L]) {
 #pragma unroll
-    for (int e = 0; e < L; ++e) w[e] = (e & 1) ? yo[kl + K - (e + 1) / 2] : ye[kl + K - e / 2];
+    for (int m = 0; m <= K; ++m) {
+      const float4 v = ys4[kl + m];
+      w[2 * K - 2 * m] = make_float2(v.x, v.y);
+      if (m < K) w[2 * K - 2 * m - 1] = make_float2(v.z, v.w);
+    }
   };
 
-  int bad = 0;
-  if (!dead) {
-    // ---- (1) pass 1 with θ₀ = [w_cd; 0] and the frame power
-    float2 wc[L];
+  int it = 0;
+  for (int fl = blockIdx.x; fl < n_frames; fl += gridDim.x, ++it) {
+    const int64_t f = frame0 + fl;
+    const int M = (int)p.schedule[(int)(((f / p.segment_frames) % p.n_segments + p.n_segments) % p.n_segments)];
+    const int bi = (M == 4) ? 0 : (M == 8) ? 1 : (M == 16) ? 2 : (M == 32) ? 3 : 4;
+    Slicer sl;
+    sl.init(M);
+    const int64_t sym0 = (int64_t)fl * kFrameSym;
+    // frame clamp count (K1 per-block counts) → dead-frame rule
+    if (warp == 0) {
+      int c = __ldg(&clampcnt[clamp_frame_off + (int64_t)fl * 32 + lane]);
 #pragma unroll
-    for (int e = 0; e < L; ++e) wc[e] = __ldg(&w_cd[e]);    // w_cd[a], a = j + K; tap j ↔ e = j + K
-    float pw = 0.f;
-#pragma unroll 2
-    for (int s = 0; s < K3_SPT; ++s) {
-      const int kl = tid + K3_THREADS * s;
-      float2 w[L];
-      load_window(kl, w);
-      float2 acc = make_float2(0.f, 0.f);
-#pragma unroll
-      for (int e = 0; e < L; ++e) cmac(acc, wc[e], w[e]);
-      us[kl] = acc;
-      pw = fmaf(acc.x, acc.x, fmaf(acc.y, acc.y, pw));
+      for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+      if (lane == 0) misc[0] = c;
     }
-    pw = warp_sum(pw);
-    if (lane == 0) red_w[0] = pw;
+    mbar_wait(bar, it & 1);
     __syncthreads();
-    double P0 = 0.0;
-#pragma unroll
-    for (int w8 = 0; w8 < K3_WARPS; ++w8) P0 += (double)red[w8 * K3_RED];
-    P0 /= (double)kFrameSym;
-    const bool p0ok = (P0 > 0.0) && isfinite(P0);
-    const float g = p0ok ? (float)(1.0 / sqrt(P0)) : 1.0f;
-    bad |= !p0ok;
-    __syncthreads();   // red is reused below
+    const int ccount = misc[0];
+    const bool dead = (ccount >= kFrameSamp);
 
-    // ---- (3a) p1[e] = Σ conj(a_j)·d, p2[e] = Σ a_j·d  (a_j = w[e])
-    {
-      float acc[Lay::NP];
+    float2 u[K3_SPT];
+    int bad = 0;
+    if (!dead) {
+      // ---- sweep A: lag sums for bases ρ = 0 (i = −K, w[0]) and ρ = 1 (i = −K+1, w[1]) + pass-1 power
+      //      S_ρ(d) = Σ conj(w[ρ])·w[ρ + d],  T_ρ(d) = Σ w[ρ]·w[ρ + d];  y⁰ = Σ_e w_cd[e]·w[e]
 #pragma unroll
-      for (int i = 0; i < Lay::NP; ++i) acc[i] = 0.f;
+      for (int grp = 0; grp < Lay::NRG; ++grp) {
+        constexpr int G = Lay::RG;
+        const int d0 = grp * G;
+        float acc[8 * G];
+#pragma unroll
+        for (int i = 0; i < 8 * G; ++i) acc[i] = 0.f;
+        float pw = 0.f;
 #pragma unroll 2
-      for (int s = 0; s < K3_SPT; ++s) {
-        const int kl = tid + K3_THREADS * s;
-        const float2 d = sl.point(cscale(us[kl], g));
-        float2 w[L];
-        load_window(kl, w);
+        for (int s = 0; s < K3_SPT; ++s) {
+          float2 w[L];
+          load_window(tid + K3_THREADS * s, w);
 #pragma unroll
-        for (int e = 0; e < L; ++e) {
-          float2 p1 = make_float2(acc[4 * e], acc[4 * e + 1]), p2 = make_float2(acc[4 * e + 2], acc[4 * e + 3]);
-          cmac_conj(p1, w[e], d);
-          cmac(p2, w[e], d);
-          acc[4 * e] = p1.x; acc[4 * e + 1] = p1.y; acc[4 * e + 2] = p2.x; acc[4 * e + 3] = p2.y;
-        }
-      }
-      warp_partials<Lay::NP>(acc, red_w, 0, lane);
-    }
-    // ---- (3b) lag sums for bases ρ = 0 (i = −K, e = 0) and ρ = 1 (i = −K+1, e = 1), lags in groups of RG
-    //      S_ρ(d) = Σ conj(w[ρ])·w[ρ + d],  T_ρ(d) = Σ w[ρ]·w[ρ + d]
-#pragma unroll
-    for (int d0 = 0; d0 < ND; d0 += Lay::RG) {
-      constexpr int G = Lay::RG;
-      float acc[8 * G];
-#pragma unroll
-      for (int i = 0; i < 8 * G; ++i) acc[i] = 0.f;
-#pragma unroll 2
-      for (int s = 0; s < K3_SPT; ++s) {
-        float2 w[L];
-        load_window(tid + K3_THREADS * s, w);
-#pragma unroll
-        for (int gg = 0; gg < G; ++gg) {
-          const int d = d0 + gg;
-          if (d < ND) {
-            float2 s0 = make_float2(acc[8 * gg], acc[8 * gg + 1]), t0 = make_float2(acc[8 * gg + 2], acc[8 * gg + 3]);
-            cmac_conj(s0, w[0], w[d]);
-            cmac(t0, w[0], w[d]);
-            acc[8 * gg] = s0.x; acc[8 * gg + 1] = s0.y; acc[8 * gg + 2] = t0.x; acc[8 * gg + 3] = t0.y;
-            if (d < ND - 1) {
-              float2 s1 = make_float2(acc[8 * gg + 4], acc[8 * gg + 5]), t1 = make_float2(acc[8 * gg + 6], acc[8 * gg + 7]);
-              cmac_conj(s1, w[1], w[1 + d]);
-              cmac(t1, w[1], w[1 + d]);
-              acc[8 * gg + 4] = s1.x; acc[8 * gg + 5] = s1.y; acc[8 * gg + 6] = t1.x; acc[8 * gg + 7] = t1.y;
+          for (int gg = 0; gg < G; ++gg) {
+            const int d = d0 + gg;
+            if (d < ND) {
+              float2 s0 = make_float2(acc[8 * gg], acc[8 * gg + 1]), t0 = make_float2(acc[8 * gg + 2], acc[8 * gg + 3]);
+              cmac_conj(s0, w[0], w[d]);
+              cmac(t0, w[0], w[d]);
+              acc[8 * gg] = s0.x; acc[8 * gg + 1] = s0.y; acc[8 * gg + 2] = t0.x; acc[8 * gg + 3] = t0.y;
+              if (d < ND - 1) {
+                float2 s1 = make_float2(acc[8 * gg + 4], acc[8 * gg + 5]), t1 = make_float2(acc[8 * gg + 6], acc[8 * gg + 7]);
+                cmac_conj(s1, w[1], w[1 + d]);
+                cmac(t1, w[1], w[1 + d]);
+                acc[8 * gg + 4] = s1.x; acc[8 * gg + 5] = s1.y; acc[8 * gg + 6] = t1.x; acc[8 * gg + 7] = t1.y;
+              }
             }
           }
-        }
-      }
-      // layout in red: [NP + 8·d + {S0re, S0im, T0re, T0im, S1re, S1im, T1re, T1im}]
-      warp_partials<8 * G>(acc, red_w, Lay::NP + 8 * d0, lane);
-    }
-    __syncthreads();
-    cross_warp_sum(red, dres, Lay::NP + 8 * ND, tid);
-    __syncthreads();
-
-    // ---- (3c) assemble the real system and solve (warp 0)
-    if (warp == 0) {
-      // complex S(i, i+d), T(i, i+d) for all i ∈ [−K, K − d] via the sliding recurrence. Local y_s index
-      // of y[2k − i] at the edge symbols k0 − 1 → K − 2 − i; k1 − 1 → 8190 + K − i.
-      auto Ys = [&](int idx) -> double2 {
-        const float2 v = (idx & 1) ? yo[idx >> 1] : ye[idx >> 1];
-        return make_double2((double)v.x, (double)v.y);
-      };
-      // lane l < 2·ND walks one (ρ, d) chain and writes the matrix entries it owns
-      double* A = mat;   // row-major N × (N + 2)
-      constexpr int W = N + 2;
-      for (int c = lane; c < 2 * ND; c += 32) {
-        const int rho = c / ND, d = c % ND;
-        if (rho == 1 && d == ND - 1) continue;
-        double sr = dres[Lay::NP + 8 * d + 4 * rho], si = dres[Lay::NP + 8 * d + 4 * rho + 1];
-        double tr_ = dres[Lay::NP + 8 * d + 4 * rho + 2], ti = dres[Lay::NP + 8 * d + 4 * rho + 3];
-        for (int i = -K + rho; i + d <= K; i += 2) {
-          const int r = i + K, q = i + d + K;     // S(r, q) = Σ conj(a_r)·a_q, T(r, q) = Σ a_r·a_q
-          if (wl) {
-            // G = [[Σ ar arᵀ, Σ ar aiᵀ], [Σ ai arᵀ, Σ ai aiᵀ]] from S and T (both orders of (r, q))
-            const double rr = 0.5 * (sr + tr_), ii = 0.5 * (sr - tr_);
-            const double ri = 0.5 * (si + ti), ir = 0.5 * (ti - si);   // Σ ar_r·ai_q, Σ ai_r·ar_q
-            A[r * W + q] = rr;             A[q * W + r] = rr;
-            A[(L + r) * W + (L + q)] = ii; A[(L + q) * W + (L + r)] = ii;
-            A[r * W + (L + q)] = ri;       A[(L + q) * W + r] = ri;
-            A[(L + r) * W + q] = ir;       A[q * W + (L + r)] = ir;
-          } else {
-            // real form of the Hermitian R11: [[Re R, −Im R], [Im R, Re R]], R[r][q] = S, R[q][r] = conj(S)
-            A[r * W + q] = sr;             A[q * W + r] = sr;
-            A[(L + r) * W + (L + q)] = sr; A[(L + q) * W + (L + r)] = sr;
-            A[(L + r) * W + q] = si;       A[(L + q) * W + r] = -si;
-            A[r * W + (L + q)] = -si;      A[q * W + (L + r)] = si;
+          if (grp == 0) {
+            float2 y0 = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int e = 0; e < L; ++e) cmac(y0, wc[e], w[e]);
+            pw = fmaf(y0.x, y0.x, fmaf(y0.y, y0.y, pw));
           }
-          if (i + 2 + d > K) break;
-          const double2 a1 = Ys(K - 2 - i), a2 = Ys(K - 2 - i - d);
-          const double2 b1 = Ys(8190 + K - i), b2 = Ys(8190 + K - i - d);
-          sr += a1.x * a2.x + a1.y * a2.y - (b1.x * b2.x + b1.y * b2.y);
-          si += a1.x * a2.y - a1.y * a2.x - (b1.x * b2.y - b1.y * b2.x);
-          tr_ += a1.x * a2.x - a1.y * a2.y - (b1.x * b2.x - b1.y * b2.y);
-          ti += a1.x * a2.y + a1.y * a2.x - (b1.x * b2.y + b1.y * b2.x);
+        }
+        // red layout: [0, NP) p; [NP + 8·d + {S0re, S0im, T0re, T0im, S1re, S1im, T1re, T1im}]; [IPOW] power
+        warp_partials<8 * G>(acc, red_w, Lay::NP + 8 * d0, lane);
+        if (grp == 0) {
+          pw = warp_sum(pw);
+          if (lane == 0) red_w[Lay::IPOW] = pw;
         }
       }
-      __syncwarp();
-      // ridge and right-hand sides (R27/R10: λ_c = ridge·tr(R)/n_c; real form uses λ_c/2 for WL)
-      double trG = 0.0;
+      __syncthreads();
+      double P0 = 0.0;
 #pragma unroll
-      for (int r = 0; r < N; ++r) trG += A[r * W + r];
-      const double lam = wl ? (double)p.ridge * trG / (double)N          // = λ_c / 2, tr(R) = 2 tr(G)
-                            : (double)p.ridge * 0.5 * trG / (double)L;   // real form doubles tr(R11)
-      if (lane < L) {
-        const int e = lane;
-        const double p1r = dres[4 * e], p1i = dres[4 * e + 1], p2r = dres[4 * e + 2], p2i = dres[4 * e + 3];
-        const double w0r = (double)g * (double)__ldg(&w_cd[e]).x, w0i = (double)g * (double)__ldg(&w_cd[e]).y;
-        if (wl) {
-          // q1 = [Σ ar·dr; Σ ai·dr], q2 = [Σ ar·di; Σ ai·di];  m1₀ = [w0r; −w0i], m2₀ = [w0i; w0r]
-          A[e * W + N] = 0.5 * (p1r + p2r) + lam * w0r;
-          A[(L + e) * W + N] = 0.5 * (p2i - p1i) - lam * w0i;
-          A[e * W + N + 1] = 0.5 * (p1i + p2i) + lam * w0i;
-          A[(L + e) * W + N + 1] = 0.5 * (p1r - p2r) + lam * w0r;
-        } else {
-          A[e * W + N] = p1r + lam * w0r;
-          A[(L + e) * W + N] = p1i + lam * w0i;
-          A[e * W + N + 1] = 0.0;
-          A[(L + e) * W + N + 1] = 0.0;
-        }
-      }
-      __syncwarp();
-      // Gauss–Jordan with one row per lane (SPD ⇒ no pivoting)
-      double row[W];
-#pragma unroll
-      for (int c = 0; c < W; ++c) row[c] = (lane < N) ? A[lane * W + c] : 0.0;
-#pragma unroll
-      for (int c = 0; c < N; ++c) row[c] += (c == lane) ? lam : 0.0;   // ridge (compile-time register index)
-      int fail = 0;
-      gj_step<N, W, 0>(row, lane, fail);
-      fail |= !isfinite(row[N]) || !isfinite(row[N + 1]);
-      fail = __any_sync(0xffffffffu, fail && lane < N) ? 1 : 0;
-      // θ₁ from m1, m2 (lane e holds m1[e], m2[e]; lane L+e holds m1[L+e], m2[L+e])
-      const double m1 = row[N], m2 = row[N + 1];
-      const double m1b = __shfl_down_sync(0xffffffffu, m1, L), m2b = __shfl_down_sync(0xffffffffu, m2, L);
-      if (lane < L) {
-        float2 wv, vv;
-        if (fail) {
-          const float2 w0 = __ldg(&w_cd[lane]);
-          wv = make_float2(g * w0.x, g * w0.y);
-          vv = make_float2(0.f, 0.f);
-        } else if (wl) {
-          wv = make_float2((float)(0.5 * (m1 + m2b)), (float)(0.5 * (m2 - m1b)));
-          vv = make_float2((float)(0.5 * (m1 - m2b)), (float)(0.5 * (m2 + m1b)));
-        } else {
-          wv = make_float2((float)m1, (float)m1b);
-          vv = make_float2(0.f, 0.f);
-        }
-        th[lane] = wv;
-        th[L + lane] = vv;
-      }
-      if (lane == 0) misc[1] = fail;
-    }
-    __syncthreads();
-    bad |= misc[1];
+      for (int w8 = 0; w8 < K3_WARPS; ++w8) P0 += (double)red[w8 * NRED + Lay::IPOW];
+      P0 /= (double)kFrameSym;
+      const bool p0ok = (P0 > 0.0) && isfinite(P0);
+      const float g = p0ok ? (float)(1.0 / sqrt(P0)) : 1.0f;   // AGC (R25)
+      bad |= !p0ok;
 
-    // ---- (4) pass 2: y¹ = Σ_e w_e·a + v_e·conj(a)
-    {
-      float2 tw[L], tv[L];
+      // ---- sweep B: decisions on g·y⁰ and p1[e] = Σ conj(a_j)·d, p2[e] = Σ a_j·d  (a_j = w[e])
+      {
+        float acc[Lay::NP];
 #pragma unroll
-      for (int e = 0; e < L; ++e) { tw[e] = th[e]; tv[e] = th[L + e]; }
-      float acc[32];
-      float gr = 0.f, gi = 0.f, gd = 0.f;
+        for (int i = 0; i < Lay::NP; ++i) acc[i] = 0.f;
 #pragma unroll 2
-      for (int s = 0; s < K3_SPT; ++s) {
-        const int kl = tid + K3_THREADS * s;
-        float2 w[L];
-        load_window(kl, w);
-        float2 o = make_float2(0.f, 0.f);
+        for (int s = 0; s < K3_SPT; ++s) {
+          float2 w[L];
+          load_window(tid + K3_THREADS * s, w);
+          float2 y0 = make_float2(0.f, 0.f);
 #pragma unroll
-        for (int e = 0; e < L; ++e) {
-          cmac(o, tw[e], w[e]);
-          cmac(o, tv[e], cconj(w[e]));
+          for (int e = 0; e < L; ++e) cmac(y0, wc[e], w[e]);
+          const float2 d = sl.point(cscale(y0, g));
+#pragma unroll
+          for (int e = 0; e < L; ++e) {
+            float2 p1 = make_float2(acc[4 * e], acc[4 * e + 1]), p2 = make_float2(acc[4 * e + 2], acc[4 * e + 3]);
+            cmac_conj(p1, w[e], d);
+            cmac(p2, w[e], d);
+            acc[4 * e] = p1.x; acc[4 * e + 1] = p1.y; acc[4 * e + 2] = p2.x; acc[4 * e + 3] = p2.y;
+          }
         }
-        us[kl] = o;
-        // gain unbias γ = Σ y¹·conj(D(y¹)) / Σ|D(y¹)|²
-        const float2 dd = sl.point(o);
-        const float2 c = cmulc(o, dd);
-        gr += c.x; gi += c.y; gd = fmaf(dd.x, dd.x, fmaf(dd.y, dd.y, gd));
+        warp_partials<Lay::NP>(acc, red_w, 0, lane);
+      }
+      __syncthreads();
+      cross_warp_sum(red, dres, NRED, tid);   // fp64, fixed order
+      __syncthreads();
+
+      // ---- solve (warp 0): assemble the real system from S, T, p and Gauss–Jordan it
+      if (warp == 0) {
+        auto Ys = [&](int idx) -> double2 {
+          const float2 v = ys[idx];
+          return make_double2((double)v.x, (double)v.y);
+        };
+        double* A = mat;   // row-major N × (N + 2)
+        constexpr int W = N + 2;
+        // lane c < 2·ND walks one (ρ, d) chain S(i, i+d), T(i, i+d), i = −K+ρ, −K+ρ+2, … ≤ K − d, using the
+        // exact sliding recurrence; edge samples y[2(k0−1) − i] ↔ y_s[K − 2 − i], y[2(k1−1) − i] ↔ y_s[8190 + K − i]
+        for (int c = lane; c < 2 * ND; c += 32) {
+          const int rho = c / ND, d = c % ND;
+          if (rho == 1 && d == ND - 1) continue;
+          double sr = dres[Lay::NP + 8 * d + 4 * rho], si = dres[Lay::NP + 8 * d + 4 * rho + 1];
+          double tr_ = dres[Lay::NP + 8 * d + 4 * rho + 2], ti = dres[Lay::NP + 8 * d + 4 * rho + 3];
+          for (int i = -K + rho; i + d <= K; i += 2) {
+            const int r = i + K, q = i + d + K;     // S(r, q) = Σ conj(a_r)·a_q, T(r, q) = Σ a_r·a_q
+            if (wl) {
+              // G = [[Σ ar arᵀ, Σ ar aiᵀ], [Σ ai arᵀ, Σ ai aiᵀ]] from S and T (both orders of (r, q))
+              const double rr = 0.5 * (sr + tr_), ii = 0.5 * (sr - tr_);
+              const double ri = 0.5 * (si + ti), ir = 0.5 * (ti - si);   // Σ ar_r·ai_q, Σ ai_r·ar_q
+              A[r * W + q] = rr;             A[q * W + r] = rr;
+              A[(L + r) * W + (L + q)] = ii; A[(L + q) * W + (L + r)] = ii;
+              A[r * W + (L + q)] = ri;       A[(L + q) * W + r] = ri;
+              A[(L + r) * W + q] = ir;       A[q * W + (L + r)] = ir;
+            } else {
+              // real form of the Hermitian R11: [[Re R, −Im R], [Im R, Re R]], R[r][q] = S, R[q][r] = conj(S)
+              A[r * W + q] = sr;             A[q * W + r] = sr;
+              A[(L + r) * W + (L + q)] = sr; A[(L + q) * W + (L + r)] = sr;
+              A[(L + r) * W + q] = si;       A[(L + q) * W + r] = -si;
+              A[r * W + (L + q)] = -si;      A[q * W + (L + r)] = si;
+            }
+            if (i + 2 + d > K) break;
+            const double2 a1 = Ys(K - 2 - i), a2 = Ys(K - 2 - i - d);
+            const double2 b1 = Ys(8190 + K - i), b2 = Ys(8190 + K - i - d);
+            sr += a1.x * a2.x + a1.y * a2.y - (b1.x * b2.x + b1.y * b2.y);
+            si += a1.x * a2.y - a1.y * a2.x - (b1.x * b2.y - b1.y * b2.x);
+            tr_ += a1.x * a2.x - a1.y * a2.y - (b1.x * b2.x - b1.y * b2.y);
+            ti += a1.x * a2.y + a1.y * a2.x - (b1.x * b2.y + b1.y * b2.x);
+          }
+        }
+        __syncwarp();
+        // ridge (R10): λ_c = ridge·tr(R)/n_c. WL: real form uses λ_c/2 and tr(R) = 2·tr(G). Linear: tr(M) = 2·tr(R11)
+        double trG = 0.0;
+#pragma unroll
+        for (int r = 0; r < N; ++r) trG += A[r * W + r];
+        const double lam = wl ? (double)p.ridge * trG / (double)N : (double)p.ridge * 0.5 * trG / (double)L;
+        if (lane < L) {
+          const int e = lane;
+          const double p1r = dres[4 * e], p1i = dres[4 * e + 1], p2r = dres[4 * e + 2], p2i = dres[4 * e + 3];
+          const double w0r = (double)g * (double)__ldg(&w_cd[e]).x;
+          const double w0i = (double)g * (double)__ldg(&w_cd[e]).y;
+          if (wl) {
+            // q1 = [Σ ar·dr; Σ ai·dr], q2 = [Σ ar·di; Σ ai·di];  m1₀ = [w0r; −w0i], m2₀ = [w0i; w0r]
+            A[e * W + N] = 0.5 * (p1r + p2r) + lam * w0r;
+            A[(L + e) * W + N] = 0.5 * (p2i - p1i) - lam * w0i;
+            A[e * W + N + 1] = 0.5 * (p1i + p2i) + lam * w0i;
+            A[(L + e) * W + N + 1] = 0.5 * (p1r - p2r) + lam * w0r;
+          } else {
+            A[e * W + N] = p1r + lam * w0r;
+            A[(L + e) * W + N] = p1i + lam * w0i;
+            A[e * W + N + 1] = 0.0;
+            A[(L + e) * W + N + 1] = 0.0;
+          }
+        }
+        __syncwarp();
+        double row[W];
+#pragma unroll
+        for (int c = 0; c < W; ++c) row[c] = (lane < N) ? A[lane * W + c] : 0.0;
+#pragma unroll
+        for (int c = 0; c < N; ++c) row[c] += (c == lane) ? lam : 0.0;   // ridge (compile-time register index)
+        int fail = 0;
+        gj_step<N, W, 0>(row, lane, fail);
+        fail |= !isfinite(row[N]) || !isfinite(row[N + 1]);
+        fail = __any_sync(0xffffffffu, fail && lane < N) ? 1 : 0;
+        // θ₁ from m1, m2 (lane e holds m1[e], m2[e]; lane L+e holds m1[L+e], m2[L+e])
+        const double m1 = row[N], m2 = row[N + 1];
+        const double m1b = __shfl_down_sync(0xffffffffu, m1, L), m2b = __shfl_down_sync(0xffffffffu, m2, L);
+        if (lane < L) {
+          float2 wv, vv;
+          if (fail) {
+            const float2 w0 = __ldg(&w_cd[lane]);
+            wv = make_float2(g * w0.x, g * w0.y);
+            vv = make_float2(0.f, 0.f);
+          } else if (wl) {
+            wv = make_float2((float)(0.5 * (m1 + m2b)), (float)(0.5 * (m2 - m1b)));
+            vv = make_float2((float)(0.5 * (m1 - m2b)), (float)(0.5 * (m2 + m1b)));
+          } else {
+            wv = make_float2((float)m1, (float)m1b);
+            vv = make_float2(0.f, 0.f);
+          }
+          th[lane] = wv;
+          th[L + lane] = vv;
+        }
+        if (lane == 0) misc[1] = fail;
+      }
+      __syncthreads();
+      bad |= misc[1];
+
+      // ---- sweep C: pass 2 y¹ = Σ_e w_e·a + v_e·conj(a) (kept in registers) and the gain-unbias sums
+      float gr = 0.f, gi = 0.f, gd = 0.f;
+      {
+        float2 tw[L], tv[L];
+#pragma unroll
+        for (int e = 0; e < L; ++e) { tw[e] = th[e]; tv[e] = th[L + e]; }
+#pragma unroll
+        for (int s = 0; s < K3_SPT; ++s) {
+          float2 w[L];
+          load_window(tid + K3_THREADS * s, w);
+          float2 o = make_float2(0.f, 0.f);
+#pragma unroll
+          for (int e = 0; e < L; ++e) {
+            cmac(o, tw[e], w[e]);
+            cmac(o, tv[e], cconj(w[e]));
+          }
+          u[s] = o;
+          const float2 dd = sl.point(o);        // γ = Σ y¹·conj(D(y¹)) / Σ|D(y¹)|²  (R27)
+          const float2 c = cmulc(o, dd);
+          gr += c.x; gi += c.y; gd = fmaf(dd.x, dd.x, fmaf(dd.y, dd.y, gd));
+        }
       }
       gr = warp_sum(gr); gi = warp_sum(gi); gd = warp_sum(gd);
       if (lane == 0) { red_w[0] = gr; red_w[1] = gi; red_w[2] = gd; }
       __syncthreads();
-      double Gr = 0, Gi = 0, Gd = 0;
+      {
+        double Gr = 0, Gi = 0, Gd = 0;
 #pragma unroll
-      for (int w8 = 0; w8 < K3_WARPS; ++w8) { Gr += red[w8 * K3_RED]; Gi += red[w8 * K3_RED + 1]; Gd += red[w8 * K3_RED + 2]; }
-      const double ag = sqrt(Gr * Gr + Gi * Gi) / Gd;
-      float sc = 1.0f;
-      if (ag > 0.0 && isfinite(ag)) sc = (float)(1.0 / ag); else bad = 1;
-      __syncthreads();
-      // ---- (5) CPR: c_s = Σ_t u·conj(D(u)) for window s (W = 256 ⇒ one window per s), u = y¹/|γ|
+        for (int w8 = 0; w8 < K3_WARPS; ++w8) { Gr += red[w8 * NRED]; Gi += red[w8 * NRED + 1]; Gd += red[w8 * NRED + 2]; }
+        const double ag = sqrt(Gr * Gr + Gi * Gi) / Gd;
+        float sc = 1.0f;
+        if (ag > 0.0 && isfinite(ag)) sc = (float)(1.0 / ag); else bad = 1;
 #pragma unroll
-      for (int s = 0; s < K3_SPT; ++s) {
-        const int kl = tid + K3_THREADS * s;
-        const float2 uu = cscale(us[kl], sc);
-        us[kl] = uu;
-        const float2 c = cmulc(uu, sl.point(uu));
-        acc[2 * s] = c.x; acc[2 * s + 1] = c.y;
+        for (int s = 0; s < K3_SPT; ++s) u[s] = cscale(u[s], sc);
       }
-      warp_partials<32>(acc, red_w, 0, lane);
+      __syncthreads();
+      // ---- CPR (R12): c_s = Σ_t u·conj(D(u)) for window s (W = 256 ⇒ one window per s), rotation conj(c)/|c|
+      {
+        float acc[32];
+#pragma unroll
+        for (int s = 0; s < K3_SPT; ++s) {
+          const float2 c = cmulc(u[s], sl.point(u[s]));
+          acc[2 * s] = c.x; acc[2 * s + 1] = c.y;
+        }
+        warp_partials<32>(acc, red_w, 0, lane);
+      }
       __syncthreads();
       if (tid < K3_SPT) {
         const int per = p.cpr_window / K3_THREADS;     // s-values per window (1, 2, 4, 8, 16)
@@ -474,65 +490,75 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, const float2* __restr
         for (int q = 0; q < per; ++q)
 #pragma unroll
           for (int w8 = 0; w8 < K3_WARPS; ++w8) {
-            cr += (double)red[w8 * K3_RED + 2 * (w0 + q)];
-            ci += (double)red[w8 * K3_RED + 2 * (w0 + q) + 1];
+            cr += (double)red[w8 * NRED + 2 * (w0 + q)];
+            ci += (double)red[w8 * NRED + 2 * (w0 + q) + 1];
           }
         const double mag = sqrt(cr * cr + ci * ci);
         rot[tid] = (mag > 0.0) ? make_float2((float)(cr / mag), (float)(-ci / mag)) : make_float2(1.f, 0.f);
       }
       __syncthreads();
-    }
-  }
-
-  // ---- (6) decisions, counts, outputs
-  if (ref_tma) mbar_wait(bar, 0);
-  int serr = 0, berr = 0;
-#pragma unroll 4
-  for (int s = 0; s < K3_SPT; ++s) {
-    const int kl = tid + K3_THREADS * s;
-    const float2 zz = dead ? make_float2(0.f, 0.f) : cmul(us[kl], rot[s]);
-    const int lab = sl.label(zz);
-    if (ref) {
-      const int r = ref_tma ? (int)ref_s[kl] : (int)__ldg(&ref[sym0 + kl]);
-      serr += (lab != r);
-      berr += __popc(lab ^ r);
-    }
-    if (dec) dec[sym0 + kl] = (uint8_t)lab;
-    if (zout) zout[sym0 + kl] = zz;
-  }
-  if (ref) {
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      serr += __shfl_xor_sync(0xffffffffu, serr, o);
-      berr += __shfl_xor_sync(0xffffffffu, berr, o);
+      for (int s = 0; s < K3_SPT; ++s) u[s] = cmul(u[s], rot[s]);
+    } else {
+#pragma unroll
+      for (int s = 0; s < K3_SPT; ++s) u[s] = make_float2(0.f, 0.f);
     }
-    if (lane == 0) { misc[8 + warp] = serr; misc[16 + warp] = berr; }
-  }
-  __syncthreads();
-  if (tid == 0) {
+
+    // ---- decisions, counts, outputs
+    int serr = 0, berr = 0;
+#pragma unroll
+    for (int s = 0; s < K3_SPT; ++s) {
+      const int kl = tid + K3_THREADS * s;
+      const int lab = sl.label(u[s]);
+      if (ref) {
+        const int r = ref_tma ? (int)ref_s[kl] : (int)__ldg(&ref[sym0 + kl]);
+        serr += (lab != r);
+        berr += __popc(lab ^ r);
+      }
+      if (dec) dec[sym0 + kl] = (uint8_t)lab;
+      if (zout) zout[sym0 + kl] = u[s];
+    }
     if (ref) {
-      long long se = 0, be = 0;
-      for (int w8 = 0; w8 < K3_WARPS; ++w8) { se += misc[8 + w8]; be += misc[16 + w8]; }
-      if (se) atomicAdd(&counters[5 + bi], (unsigned long long)se);
-      if (be) atomicAdd(&counters[15 + bi], (unsigned long long)be);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        serr += __shfl_xor_sync(0xffffffffu, serr, o);
+        berr += __shfl_xor_sync(0xffffffffu, berr, o);
+      }
+      if (lane == 0) { misc[8 + warp] = serr; misc[16 + warp] = berr; }
     }
-    atomicAdd(&counters[bi], (unsigned long long)kFrameSym);
-    atomicAdd(&counters[10 + bi], (unsigned long long)kFrameSym * (bi + 2));
-    if (ccount) atomicAdd(&counters[20], (unsigned long long)ccount);
-    atomicAdd(&counters[21], 1ull);
-    if (dead) atomicAdd(&counters[22], 1ull);
-    if (!dead && bad) atomicAdd(&counters[23], 1ull);
+    __syncthreads();   // all reads of ys / ref_s / misc for this frame are done
+    if (tid == 0) {
+      const int nf = fl + (int)gridDim.x;
+      if (nf < n_frames) {
+        issue(nf);                                            // from L2 (prefetched one frame ago)
+        if (nf + (int)gridDim.x < n_frames) prefetch(nf + gridDim.x);
+      }
+      if (ref) {
+        long long se = 0, be = 0;
+        for (int w8 = 0; w8 < K3_WARPS; ++w8) { se += misc[8 + w8]; be += misc[16 + w8]; }
+        if (se) atomicAdd(&counters[5 + bi], (unsigned long long)se);
+        if (be) atomicAdd(&counters[15 + bi], (unsigned long long)be);
+      }
+      atomicAdd(&counters[bi], (unsigned long long)kFrameSym);
+      atomicAdd(&counters[10 + bi], (unsigned long long)kFrameSym * (bi + 2));
+      if (ccount) atomicAdd(&counters[20], (unsigned long long)ccount);
+      atomicAdd(&counters[21], 1ull);
+      if (dead) atomicAdd(&counters[22], 1ull);
+      if (!dead && bad) atomicAdd(&counters[23], 1ull);
+    }
   }
 }
 
 template <int K>
 static void launch_k3_t(const float2* y, int64_t frame0, int64_t n_frames, const float2* w_cd, const int* clampcnt,
                         int64_t clamp_frame_off, const uint8_t* ref, uint8_t* dec, float2* z,
-                        unsigned long long* counters, const K3Params& p, cudaStream_t s) {
+                        unsigned long long* counters, const K3Params& p, int num_sms, cudaStream_t s) {
   constexpr int smem = K3Layout<K>::TOTAL;
   cudaFuncSetAttribute(k3_eq_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  k3_eq_kernel<K><<<(unsigned)n_frames, K3_THREADS, smem, s>>>(y, frame0, w_cd, clampcnt, clamp_frame_off, ref, dec,
-                                                               z, counters, p);
+  int64_t grid = (int64_t)num_sms * 2;
+  if (grid > n_frames) grid = n_frames;
+  k3_eq_kernel<K><<<(unsigned)grid, K3_THREADS, smem, s>>>(y, frame0, (int)n_frames, w_cd, clampcnt,
+                                                           clamp_frame_off, ref, dec, z, counters, p);
 }
 
 size_t k3_smem_bytes(int K) {
@@ -550,8 +576,8 @@ size_t k3_smem_bytes(int K) {
 
 void launch_k3(const float2* y, int64_t frame0, int64_t n_frames, int K, const float2* w_cd, const int* clampcnt,
                int64_t clamp_frame_off, const uint8_t* ref, uint8_t* dec, float2* z, unsigned long long* counters,
-               const K3Params& p, cudaStream_t s) {
-#define KK_K3(KV) case KV: launch_k3_t<KV>(y, frame0, n_frames, w_cd, clampcnt, clamp_frame_off, ref, dec, z, counters, p, s); break;
+               const K3Params& p, int num_sms, cudaStream_t s) {
+#define KK_K3(KV) case KV: launch_k3_t<KV>(y, frame0, n_frames, w_cd, clampcnt, clamp_frame_off, ref, dec, z, counters, p, num_sms, s); break;
   switch (K) {
     KK_K3(1) KK_K3(2) KK_K3(3) KK_K3(4) KK_K3(5) KK_K3(6) KK_K3(7)
     default: break;

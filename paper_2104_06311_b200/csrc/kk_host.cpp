@@ -474,7 +474,7 @@ kk_status kk_process_frames(kk_ctx* c, const void* d_adc, int64_t first, int64_t
   p3.cpr_window = cf.cpr_window;
   const int64_t nfr = n / F;
   kk::launch_k3(c->d_y, first / F, nfr, c->K, c->d_wcd, c->d_clamp, (int64_t)F / kk::kHilbertHop /*skip frame −1*/,
-                d_ref, d_dec, cf.keep_intermediate ? c->d_z : nullptr, c->d_counters, p3, s);
+                d_ref, d_dec, cf.keep_intermediate ? c->d_z : nullptr, c->d_counters, p3, c->num_sms, s);
   if (c->timing) {
     cudaEventRecord(tev[3], s);
     c->ev_pending.push_back(tev);

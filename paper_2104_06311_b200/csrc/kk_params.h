@@ -52,6 +52,6 @@ void launch_k2(const float2* E, int64_t E_first, const float2* part, const int* 
 // K3: per-frame widely-linear DD-LS equalizer, CPR, decisions, counters.
 void launch_k3(const float2* y, int64_t frame0, int64_t n_frames, int K, const float2* w_cd, const int* clampcnt,
                int64_t clamp_frame_off, const uint8_t* ref, uint8_t* dec, float2* z, unsigned long long* counters,
-               const K3Params& p, cudaStream_t s);
+               const K3Params& p, int num_sms, cudaStream_t s);
 
 }  // namespace kk
