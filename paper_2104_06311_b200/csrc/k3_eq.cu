@@ -44,7 +44,6 @@ namespace kk {
 constexpr int K3_THREADS = 256;
 constexpr int K3_WARPS = 8;
 constexpr int K3_SPT = kFrameSym / K3_THREADS;   // 16 symbols per thread
-constexpr int K3_RED = 256;                      // max reduced floats per frame (padded)
 
 // runtime-uniform QAM slicer parameters (CTA-uniform: one format per frame, R26)
 struct Slicer {
@@ -101,7 +100,7 @@ __device__ __forceinline__ float warp_transpose_reduce(float (&v)[32], int lane)
   return v[0];
 }
 
-// Write this warp's sums of acc[0..N) to red[warp*K3_RED + base + i].
+// Write this warp's sums of acc[0..N) to red_w[base + i] (red_w = this warp's slice of the reduction buffer).
 template <int N>
 __device__ __forceinline__ void warp_partials(const float (&acc)[N], float* red_w, int base, int lane) {
 #pragma unroll
@@ -114,12 +113,13 @@ __device__ __forceinline__ void warp_partials(const float (&acc)[N], float* red_
   }
 }
 
-// fp64 sum over the 8 warp partials of values [0, n) into dres (call after a __syncthreads).
-__device__ __forceinline__ void cross_warp_sum(const float* red, double* dres, int n, int tid) {
+// fp64 sum over the 8 warp partials (per-warp stride `stride` floats) of values [0, n) into dres
+// (call after a __syncthreads).
+__device__ __forceinline__ void cross_warp_sum(const float* red, double* dres, int n, int stride, int tid) {
   for (int v = tid; v < n; v += K3_THREADS) {
     double s = 0.0;
 #pragma unroll
-    for (int w = 0; w < K3_WARPS; ++w) s += (double)red[w * K3_RED + v];
+    for (int w = 0; w < K3_WARPS; ++w) s += (double)red[w * stride + v];
     dres[v] = s;
   }
 }
@@ -334,7 +334,7 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
         warp_partials<Lay::NP>(acc, red_w, 0, lane);
       }
       __syncthreads();
-      cross_warp_sum(red, dres, NRED, tid);   // fp64, fixed order
+      cross_warp_sum(red, dres, NRED, NRED, tid);   // fp64, fixed order
       __syncthreads();
 
       // ---- solve (warp 0): assemble the real system from S, T, p and Gauss–Jordan it
@@ -405,7 +405,7 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
         __syncwarp();
         double row[W];
 #pragma unroll
-        for (int c = 0; c < W; ++c) row[c] = (lane < N) ? A[lane * W + c] : 0.0;
+        for (int c = 0; c < W; ++c) row[c] = (lane < N) ? A[min(lane, N - 1) * W + c] : 0.0;
 #pragma unroll
         for (int c = 0; c < N; ++c) row[c] += (c == lane) ? lam : 0.0;   // ridge (compile-time register index)
         int fail = 0;
