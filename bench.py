@@ -230,6 +230,7 @@ def main():
 
     import kkgen
     from paper_2104_06311_b200 import Receiver, kkrx, stats_from_words
+    from paper_2104_06311_b200 import shard as SH
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -240,10 +241,11 @@ def main():
     S = a.samples_per_gpu
     chunk = min(a.chunk, S)
     assert S % chunk == 0 and chunk % F == 0
-    first = rank * S                                    # weak scaling: rank r owns [r·S, (r+1)·S)
+    my = SH.plan_weak(S, world)[rank]                   # weak scaling: rank r owns [r·S, (r+1)·S)
+    first = my.first
 
     t0 = time.perf_counter()
-    g = kkgen.generate(lc, first - HALO, first + S + HALO, device=dev, chunk=1 << 24)
+    g = kkgen.generate(lc, my.read_first, my.read_first + my.read_count, device=dev, chunk=1 << 24)
     codes = g["codes"]
     ref = g["labels"][HALO // 4:(HALO + S) // 4]
     del g
@@ -263,8 +265,7 @@ def main():
             rx.process(codes, first + c0, chunk, ref=ref[c0 // 4:(c0 + chunk) // 4],
                        decisions=dec[c0 // 4:(c0 + chunk) // 4], offset=c0, stream=stream)
         rx.stats_device(counters, stream)
-        if world > 1:
-            dist.all_reduce(counters)                   # the only cross-GPU data movement (512 B... 192 B)
+        SH.allreduce_counters(counters)                 # the only cross-GPU data movement (24 × 8 B, NCCL)
 
     for _ in range(a.warmup):
         step()
@@ -287,10 +288,7 @@ def main():
     ms = ev0.elapsed_time(ev1)
     kkrx.kk_enable_timing(rx.ctx, False)
     kt_ms, kt_n = kkrx.kk_kernel_times(rx.ctx, reset=True)
-    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
-    ms_max = float(ms_t.item())
+    ms_max = SH.max_over_ranks(ms, device=dev)
     total_samples = S * world * a.steps
     value = total_samples / (ms_max * 1e-3) / 1e9
     st = stats_from_words(counters.cpu().tolist())
@@ -349,10 +347,8 @@ def main():
             rx.process_host(h_codes, first, En, ref=h_ref, decisions=h_dec)
             _ = rx.stats()                                                   # D2H of the step's result
             t_e.append(time.perf_counter() - t1)
-        te = torch.tensor([sum(t_e)], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2e = {"value": En * world * len(t_e) / float(te.item()) / 1e9, "unit": "GS/s",
+        te = SH.max_over_ranks(sum(t_e), device=dev)
+        e2e = {"value": En * world * len(t_e) / te / 1e9, "unit": "GS/s",
                "h2d_bytes_per_step": int((En + 2 * HALO * n_chunks) * 2 + En // 4),
                "d2h_bytes_per_step": int(En // 4 + 8 * kkrx.KK_STATS_WORDS),
                "samples_per_gpu": En, "api": "kk_process_frames_host (pinned host buffers, 2 streams)"}
