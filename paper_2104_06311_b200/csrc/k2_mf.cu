@@ -34,12 +34,14 @@ __device__ __forceinline__ void stockham_pass(float2* buf, const float2* __restr
   constexpr int NJ = N / R;
   constexpr int PER = NJ / K2_THREADS;
   static_assert(PER >= 1 && NJ % K2_THREADS == 0, "pass shape");
+  static_assert(NJ % 16 == 0 && (Ns == 1 ? R == 16 : Ns % 16 == 0), "padding algebra below");
   float2 v[PER][R];
 #pragma unroll
   for (int it = 0; it < PER; ++it) {
     const int j = tid + it * K2_THREADS;
+    const float2* src = buf + pad16(j);             // pad16(j + r·NJ) = pad16(j) + r·(NJ + NJ/16)
 #pragma unroll
-    for (int r = 0; r < R; ++r) v[it][r] = buf[pad16(j + r * NJ)];
+    for (int r = 0; r < R; ++r) v[it][r] = src[r * (NJ + NJ / 16)];
   }
   __syncthreads();
 #pragma unroll
@@ -55,8 +57,11 @@ __device__ __forceinline__ void stockham_pass(float2* buf, const float2* __restr
     }
     dft_reg<R, DIR>(v[it]);
     const int idxD = (j / Ns) * Ns * R + k;
+    // Ns = 1 (R = 16): pad16(16j + r) = 17j + r;  Ns ≥ 16: pad16(idxD + r·Ns) = pad16(idxD) + r·(Ns + Ns/16)
+    float2* dst = buf + (Ns == 1 ? 17 * j : pad16(idxD));
+    constexpr int stride = (Ns == 1) ? 1 : (Ns + Ns / 16);
 #pragma unroll
-    for (int r = 0; r < R; ++r) buf[pad16(idxD + r * Ns)] = v[it][r];
+    for (int r = 0; r < R; ++r) dst[r * stride] = v[it][r];
   }
   __syncthreads();
 }

@@ -124,26 +124,28 @@ __device__ __forceinline__ void cross_warp_sum(const float* red, double* dres, i
   }
 }
 
-// Gauss–Jordan elimination step KS on an N×N system with (W − N) right-hand sides, one row per lane,
-// unrolled at compile time (keeps `row` in registers). SPD ⇒ no pivoting; non-positive pivot ⇒ fail.
-template <int N, int W, int KS>
-__device__ __forceinline__ void gj_step(double (&row)[W], int lane, int& fail) {
-  if constexpr (KS < N) {
-    const double piv = __shfl_sync(0xffffffffu, row[KS], KS);
+// Gauss–Jordan elimination of an N×N SPD system with two right-hand sides (columns N, N+1), row-major in
+// shared memory with an odd row stride WS (doubles) so a warp's row-strided accesses are conflict-free.
+// Lane i owns row i. Compact loop code on purpose: it runs once per frame on one warp, and a fully
+// unrolled version costs more in cold instruction fetch than in arithmetic. SPD ⇒ no pivoting; a
+// non-positive or non-finite pivot sets `fail`. On return row i, columns N and N+1 hold the solutions.
+__device__ __noinline__ int gj_smem(double* A, int N, int WS, int lane) {
+  int fail = 0;
+  for (int k = 0; k < N; ++k) {
+    const double piv = A[k * WS + k];
     fail |= !(piv > 0.0) || !isfinite(piv);
     const double inv = 1.0 / piv;
-    if (lane == KS) {
-#pragma unroll
-      for (int c = KS; c < W; ++c) row[c] *= inv;
+    __syncwarp();
+    if (lane == k)
+      for (int c = k + 1; c < N + 2; ++c) A[k * WS + c] *= inv;
+    __syncwarp();
+    if (lane < N && lane != k) {
+      const double f = A[lane * WS + k];
+      for (int c = k + 1; c < N + 2; ++c) A[lane * WS + c] = fma(-f, A[k * WS + c], A[lane * WS + c]);
     }
-    const double fct = row[KS];
-#pragma unroll
-    for (int c = KS + 1; c < W; ++c) {
-      const double pc = __shfl_sync(0xffffffffu, row[c], KS);
-      if (lane != KS) row[c] = fma(-fct, pc, row[c]);
-    }
-    gj_step<N, W, KS + 1>(row, lane, fail);
+    __syncwarp();
   }
+  return fail;
 }
 
 template <int K>
@@ -158,13 +160,17 @@ struct K3Layout {
   static constexpr int NRED = ((NP + NR + 1 + 31) / 32) * 32;   // + frame power
   static constexpr int IPOW = NP + NR;             // index of the frame power in the reduction
   static constexpr int YS = 2 * kFrameSym + 2 * K; // float2 loaded per frame (y_s[0 .. 8191 + 2K])
+  static constexpr int WS = N + 3;                 // odd row stride (doubles) of the real system [A | q1 q2]
+  static constexpr int RED_B = K3_WARPS * NRED * 4;
+  static constexpr int MAT_B = N * WS * 8;
   // shared memory (bytes)
-  static constexpr int Y = 0;
+  static constexpr int Y = 0;                      // frame samples; reused for the CPR products after pass 2
   static constexpr int REF = Y + YS * 8;
-  static constexpr int RED = REF + kFrameSym;
-  static constexpr int DRES = RED + K3_WARPS * NRED * 4;
-  static constexpr int MAT = DRES + NRED * 8;      // real system rows (N × (N + 2) doubles)
-  static constexpr int TH = MAT + N * (N + 2) * 8; // θ₁ as float2 [w(L), v(L)]
+  static constexpr int US = REF + kFrameSym;       // y¹ → u → z per symbol (float2 × 4096)
+  static constexpr int RED = US + kFrameSym * 8;   // warp partial sums; the solve's matrix aliases it
+  static constexpr int MAT = RED;
+  static constexpr int DRES = RED + (RED_B > MAT_B ? RED_B : MAT_B);
+  static constexpr int TH = DRES + NRED * 8;       // θ₁ as float2 [w(L), v(L)]
   static constexpr int ROT = TH + 2 * L * 8;       // 16 CPR rotations
   static constexpr int BAR = ROT + 16 * 8;         // mbarrier
   static constexpr int MISC = BAR + 16;
@@ -189,6 +195,7 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
   float2* ys = reinterpret_cast<float2*>(smem + Lay::Y);
   const float4* ys4 = reinterpret_cast<const float4*>(smem + Lay::Y);
   uint8_t* ref_s = smem + Lay::REF;
+  float2* us = reinterpret_cast<float2*>(smem + Lay::US);
   float* red = reinterpret_cast<float*>(smem + Lay::RED);
   double* dres = reinterpret_cast<double*>(smem + Lay::DRES);
   double* mat = reinterpret_cast<double*>(smem + Lay::MAT);
@@ -254,7 +261,6 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
     const int ccount = misc[0];
     const bool dead = (ccount >= kFrameSamp);
 
-    float2 u[K3_SPT];
     int bad = 0;
     if (!dead) {
       // ---- sweep A: lag sums for bases ρ = 0 (i = −K, w[0]) and ρ = 1 (i = −K+1, w[1]) + pass-1 power
@@ -343,8 +349,8 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
           const float2 v = ys[idx];
           return make_double2((double)v.x, (double)v.y);
         };
-        double* A = mat;   // row-major N × (N + 2)
-        constexpr int W = N + 2;
+        double* A = mat;   // row-major N × WS: [G + λI | q1 q2]
+        constexpr int W = Lay::WS;
         // lane c < 2·ND walks one (ρ, d) chain S(i, i+d), T(i, i+d), i = −K+ρ, −K+ρ+2, … ≤ K − d, using the
         // exact sliding recurrence; edge samples y[2(k0−1) − i] ↔ y_s[K − 2 − i], y[2(k1−1) − i] ↔ y_s[8190 + K − i]
         for (int c = lane; c < 2 * ND; c += 32) {
@@ -381,14 +387,13 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
         __syncwarp();
         // ridge (R10): λ_c = ridge·tr(R)/n_c. WL: real form uses λ_c/2 and tr(R) = 2·tr(G). Linear: tr(M) = 2·tr(R11)
         double trG = 0.0;
-#pragma unroll
         for (int r = 0; r < N; ++r) trG += A[r * W + r];
         const double lam = wl ? (double)p.ridge * trG / (double)N : (double)p.ridge * 0.5 * trG / (double)L;
         if (lane < L) {
           const int e = lane;
           const double p1r = dres[4 * e], p1i = dres[4 * e + 1], p2r = dres[4 * e + 2], p2i = dres[4 * e + 3];
-          const double w0r = (double)g * (double)__ldg(&w_cd[e]).x;
-          const double w0i = (double)g * (double)__ldg(&w_cd[e]).y;
+          const float2 w0 = __ldg(&w_cd[e]);
+          const double w0r = (double)g * (double)w0.x, w0i = (double)g * (double)w0.y;
           if (wl) {
             // q1 = [Σ ar·dr; Σ ai·dr], q2 = [Σ ar·di; Σ ai·di];  m1₀ = [w0r; −w0i], m2₀ = [w0i; w0r]
             A[e * W + N] = 0.5 * (p1r + p2r) + lam * w0r;
@@ -402,31 +407,28 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
             A[(L + e) * W + N + 1] = 0.0;
           }
         }
+        if (lane < N) A[lane * W + lane] += lam;
         __syncwarp();
-        double row[W];
-#pragma unroll
-        for (int c = 0; c < W; ++c) row[c] = (lane < N) ? A[min(lane, N - 1) * W + c] : 0.0;
-#pragma unroll
-        for (int c = 0; c < N; ++c) row[c] += (c == lane) ? lam : 0.0;   // ridge (compile-time register index)
-        int fail = 0;
-        gj_step<N, W, 0>(row, lane, fail);
-        fail |= !isfinite(row[N]) || !isfinite(row[N + 1]);
-        fail = __any_sync(0xffffffffu, fail && lane < N) ? 1 : 0;
-        // θ₁ from m1, m2 (lane e holds m1[e], m2[e]; lane L+e holds m1[L+e], m2[L+e])
-        const double m1 = row[N], m2 = row[N + 1];
-        const double m1b = __shfl_down_sync(0xffffffffu, m1, L), m2b = __shfl_down_sync(0xffffffffu, m2, L);
+        int fail = gj_smem(A, N, W, lane);
+        if (lane < N) fail |= !isfinite(A[lane * W + N]) || !isfinite(A[lane * W + N + 1]);
+        fail = __any_sync(0xffffffffu, fail) ? 1 : 0;
+        // θ₁ from m1 = column N, m2 = column N+1 (rows e and L+e)
         if (lane < L) {
           float2 wv, vv;
           if (fail) {
             const float2 w0 = __ldg(&w_cd[lane]);
             wv = make_float2(g * w0.x, g * w0.y);
             vv = make_float2(0.f, 0.f);
-          } else if (wl) {
-            wv = make_float2((float)(0.5 * (m1 + m2b)), (float)(0.5 * (m2 - m1b)));
-            vv = make_float2((float)(0.5 * (m1 - m2b)), (float)(0.5 * (m2 + m1b)));
           } else {
-            wv = make_float2((float)m1, (float)m1b);
-            vv = make_float2(0.f, 0.f);
+            const double m1 = A[lane * W + N], m2 = A[lane * W + N + 1];
+            const double m1b = A[(L + lane) * W + N], m2b = A[(L + lane) * W + N + 1];
+            if (wl) {
+              wv = make_float2((float)(0.5 * (m1 + m2b)), (float)(0.5 * (m2 - m1b)));
+              vv = make_float2((float)(0.5 * (m1 - m2b)), (float)(0.5 * (m2 + m1b)));
+            } else {
+              wv = make_float2((float)m1, (float)m1b);
+              vv = make_float2(0.f, 0.f);
+            }
           }
           th[lane] = wv;
           th[L + lane] = vv;
@@ -436,24 +438,25 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
       __syncthreads();
       bad |= misc[1];
 
-      // ---- sweep C: pass 2 y¹ = Σ_e w_e·a + v_e·conj(a) (kept in registers) and the gain-unbias sums
+      // ---- sweep C: pass 2 y¹ = Σ_e w_e·a + v_e·conj(a) → us, and the gain-unbias sums (R27)
       float gr = 0.f, gi = 0.f, gd = 0.f;
       {
         float2 tw[L], tv[L];
 #pragma unroll
         for (int e = 0; e < L; ++e) { tw[e] = th[e]; tv[e] = th[L + e]; }
-#pragma unroll
+#pragma unroll 2
         for (int s = 0; s < K3_SPT; ++s) {
+          const int kl = tid + K3_THREADS * s;
           float2 w[L];
-          load_window(tid + K3_THREADS * s, w);
+          load_window(kl, w);
           float2 o = make_float2(0.f, 0.f);
 #pragma unroll
           for (int e = 0; e < L; ++e) {
             cmac(o, tw[e], w[e]);
             cmac(o, tv[e], cconj(w[e]));
           }
-          u[s] = o;
-          const float2 dd = sl.point(o);        // γ = Σ y¹·conj(D(y¹)) / Σ|D(y¹)|²  (R27)
+          us[kl] = o;
+          const float2 dd = sl.point(o);        // γ = Σ y¹·conj(D(y¹)) / Σ|D(y¹)|²
           const float2 c = cmulc(o, dd);
           gr += c.x; gi += c.y; gd = fmaf(dd.x, dd.x, fmaf(dd.y, dd.y, gd));
         }
@@ -461,62 +464,66 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
       gr = warp_sum(gr); gi = warp_sum(gi); gd = warp_sum(gd);
       if (lane == 0) { red_w[0] = gr; red_w[1] = gi; red_w[2] = gd; }
       __syncthreads();
+      float sc = 1.0f;
       {
         double Gr = 0, Gi = 0, Gd = 0;
 #pragma unroll
         for (int w8 = 0; w8 < K3_WARPS; ++w8) { Gr += red[w8 * NRED]; Gi += red[w8 * NRED + 1]; Gd += red[w8 * NRED + 2]; }
         const double ag = sqrt(Gr * Gr + Gi * Gi) / Gd;
-        float sc = 1.0f;
         if (ag > 0.0 && isfinite(ag)) sc = (float)(1.0 / ag); else bad = 1;
-#pragma unroll
-        for (int s = 0; s < K3_SPT; ++s) u[s] = cscale(u[s], sc);
+      }
+      // ---- CPR (R12): products c_k = u_k·conj(D(u_k)), u = y¹/|γ|, into the (now dead) frame buffer
+      float2* cb = ys;
+#pragma unroll 2
+      for (int s = 0; s < K3_SPT; ++s) {
+        const int kl = tid + K3_THREADS * s;
+        const float2 uu = cscale(us[kl], sc);
+        us[kl] = uu;
+        cb[kl] = cmulc(uu, sl.point(uu));
       }
       __syncthreads();
-      // ---- CPR (R12): c_s = Σ_t u·conj(D(u)) for window s (W = 256 ⇒ one window per s), rotation conj(c)/|c|
+      // fixed-order sum per 256-symbol block: 16 threads per block, thread j sums entries j, j+16, …
       {
-        float acc[32];
-#pragma unroll
-        for (int s = 0; s < K3_SPT; ++s) {
-          const float2 c = cmulc(u[s], sl.point(u[s]));
-          acc[2 * s] = c.x; acc[2 * s + 1] = c.y;
+        const int blk = tid >> 4, j = tid & 15;
+        float cr = 0.f, ci = 0.f;
+#pragma unroll 4
+        for (int q = 0; q < 16; ++q) {
+          const float2 c = cb[256 * blk + j + 16 * q];
+          cr += c.x; ci += c.y;
         }
-        warp_partials<32>(acc, red_w, 0, lane);
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) {
+          cr += __shfl_xor_sync(0xffffffffu, cr, o);
+          ci += __shfl_xor_sync(0xffffffffu, ci, o);
+        }
+        if (j == 0) { red[2 * blk] = cr; red[2 * blk + 1] = ci; }
       }
       __syncthreads();
-      if (tid < K3_SPT) {
-        const int per = p.cpr_window / K3_THREADS;     // s-values per window (1, 2, 4, 8, 16)
+      if (tid < K3_SPT) {                              // window = (W/256) consecutive blocks
+        const int per = p.cpr_window / K3_THREADS;
         const int w0 = (tid / per) * per;
         double cr = 0.0, ci = 0.0;
-        for (int q = 0; q < per; ++q)
-#pragma unroll
-          for (int w8 = 0; w8 < K3_WARPS; ++w8) {
-            cr += (double)red[w8 * NRED + 2 * (w0 + q)];
-            ci += (double)red[w8 * NRED + 2 * (w0 + q) + 1];
-          }
+        for (int q = 0; q < per; ++q) { cr += (double)red[2 * (w0 + q)]; ci += (double)red[2 * (w0 + q) + 1]; }
         const double mag = sqrt(cr * cr + ci * ci);
         rot[tid] = (mag > 0.0) ? make_float2((float)(cr / mag), (float)(-ci / mag)) : make_float2(1.f, 0.f);
       }
       __syncthreads();
-#pragma unroll
-      for (int s = 0; s < K3_SPT; ++s) u[s] = cmul(u[s], rot[s]);
-    } else {
-#pragma unroll
-      for (int s = 0; s < K3_SPT; ++s) u[s] = make_float2(0.f, 0.f);
     }
 
-    // ---- decisions, counts, outputs
+    // ---- decisions, counts, outputs: z = u·e^{−iϑ_b} (dead frame: z = 0)
     int serr = 0, berr = 0;
-#pragma unroll
+#pragma unroll 2
     for (int s = 0; s < K3_SPT; ++s) {
       const int kl = tid + K3_THREADS * s;
-      const int lab = sl.label(u[s]);
+      const float2 zz = dead ? make_float2(0.f, 0.f) : cmul(us[kl], rot[s]);
+      const int lab = sl.label(zz);
       if (ref) {
         const int r = ref_tma ? (int)ref_s[kl] : (int)__ldg(&ref[sym0 + kl]);
         serr += (lab != r);
         berr += __popc(lab ^ r);
       }
       if (dec) dec[sym0 + kl] = (uint8_t)lab;
-      if (zout) zout[sym0 + kl] = u[s];
+      if (zout) zout[sym0 + kl] = zz;
     }
     if (ref) {
 #pragma unroll
