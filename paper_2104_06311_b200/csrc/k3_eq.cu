@@ -24,8 +24,8 @@
 //    (G + λ/2·I)m_r = q_r + λ/2·m_r0 (r = 1, 2; G = Σ x xᵀ, q_1 = Σ x·Re d, q_2 = Σ x·Im d) with
 //    m_1 = [w_r + v_r; v_i − w_i], m_2 = [w_i + v_i; w_r − v_r]. G and q are read off S, T and p.
 //    Linear-only mode solves the real 2L form [[Re R, −Im R],[Im R, Re R]] of the Hermitian system.
-//    Both are solved in fp64 by one warp with one matrix row per lane (Gauss–Jordan, no pivoting on an
-//    SPD matrix; failure ⇒ fall back to θ₀ and count a bad frame).
+//    Both are solved in fp64 by the whole CTA (Gauss–Jordan on the 2L × (2L + 2) augmented matrix in
+//    shared memory, no pivoting on an SPD matrix; failure ⇒ fall back to θ₀ and count a bad frame).
 //
 // Mapping: persistent CTAs (256 threads, 2 per SM), one frame at a time; thread t owns symbols t + 256·s
 // (s < 16). Each frame's 2-sps samples (64 KiB) and reference labels (4 KiB) arrive by one TMA bulk copy
@@ -122,30 +122,6 @@ __device__ __forceinline__ void cross_warp_sum(const float* red, double* dres, i
     for (int w = 0; w < K3_WARPS; ++w) s += (double)red[w * stride + v];
     dres[v] = s;
   }
-}
-
-// Gauss–Jordan elimination of an N×N SPD system with two right-hand sides (columns N, N+1), row-major in
-// shared memory with an odd row stride WS (doubles) so a warp's row-strided accesses are conflict-free.
-// Lane i owns row i. Compact loop code on purpose: it runs once per frame on one warp, and a fully
-// unrolled version costs more in cold instruction fetch than in arithmetic. SPD ⇒ no pivoting; a
-// non-positive or non-finite pivot sets `fail`. On return row i, columns N and N+1 hold the solutions.
-__device__ __noinline__ int gj_smem(double* A, int N, int WS, int lane) {
-  int fail = 0;
-  for (int k = 0; k < N; ++k) {
-    const double piv = A[k * WS + k];
-    fail |= !(piv > 0.0) || !isfinite(piv);
-    const double inv = 1.0 / piv;
-    __syncwarp();
-    if (lane == k)
-      for (int c = k + 1; c < N + 2; ++c) A[k * WS + c] *= inv;
-    __syncwarp();
-    if (lane < N && lane != k) {
-      const double f = A[lane * WS + k];
-      for (int c = k + 1; c < N + 2; ++c) A[lane * WS + c] = fma(-f, A[k * WS + c], A[lane * WS + c]);
-    }
-    __syncwarp();
-  }
-  return fail;
 }
 
 template <int K>
@@ -408,32 +384,64 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
           }
         }
         if (lane < N) A[lane * W + lane] += lam;
-        __syncwarp();
-        int fail = gj_smem(A, N, W, lane);
-        if (lane < N) fail |= !isfinite(A[lane * W + N]) || !isfinite(A[lane * W + N + 1]);
-        fail = __any_sync(0xffffffffu, fail) ? 1 : 0;
-        // θ₁ from m1 = column N, m2 = column N+1 (rows e and L+e)
-        if (lane < L) {
-          float2 wv, vv;
-          if (fail) {
-            const float2 w0 = __ldg(&w_cd[lane]);
-            wv = make_float2(g * w0.x, g * w0.y);
-            vv = make_float2(0.f, 0.f);
-          } else {
-            const double m1 = A[lane * W + N], m2 = A[lane * W + N + 1];
-            const double m1b = A[(L + lane) * W + N], m2b = A[(L + lane) * W + N + 1];
-            if (wl) {
-              wv = make_float2((float)(0.5 * (m1 + m2b)), (float)(0.5 * (m2 - m1b)));
-              vv = make_float2((float)(0.5 * (m1 - m2b)), (float)(0.5 * (m2 + m1b)));
-            } else {
-              wv = make_float2((float)m1, (float)m1b);
-              vv = make_float2(0.f, 0.f);
+      }
+      __syncthreads();
+      // ---- Gauss–Jordan on [G + λI | q1 q2] by the whole CTA (SPD ⇒ no pivoting): at step k every
+      //      element (i, c), c > k, reads its old value, A[i][k] and A[k][c], then all write together.
+      {
+        constexpr int W = Lay::WS;
+        double* A = mat;
+        int fail = 0;
+        for (int k = 0; k < N; ++k) {
+          const double piv = A[k * W + k];
+          fail |= !(piv > 0.0) || !isfinite(piv);
+          const double inv = 1.0 / piv;
+          const int ncol = N + 1 - k;                 // columns k+1 .. N+1
+          double nv[2];
+          int at[2];
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            const int e = tid + K3_THREADS * q;
+            at[q] = -1;
+            if (e < N * ncol) {
+              const int i = e / ncol, c = k + 1 + e % ncol;
+              const double b = A[k * W + c];
+              nv[q] = (i == k) ? b * inv : fma(-A[i * W + k] * inv, b, A[i * W + c]);
+              at[q] = i * W + c;
             }
           }
-          th[lane] = wv;
-          th[L + lane] = vv;
+          __syncthreads();
+#pragma unroll
+          for (int q = 0; q < 2; ++q)
+            if (at[q] >= 0) A[at[q]] = nv[q];
+          __syncthreads();
         }
-        if (lane == 0) misc[1] = fail;
+        // θ₁ from m1 = column N, m2 = column N+1 (rows e and L+e); fallback θ₀ on failure
+        if (warp == 0) {
+          if (lane < N) fail |= !isfinite(A[lane * W + N]) || !isfinite(A[lane * W + N + 1]);
+          fail = __any_sync(0xffffffffu, fail) ? 1 : 0;
+          if (lane < L) {
+            float2 wv, vv;
+            if (fail) {
+              const float2 w0 = __ldg(&w_cd[lane]);
+              wv = make_float2(g * w0.x, g * w0.y);
+              vv = make_float2(0.f, 0.f);
+            } else {
+              const double m1 = A[lane * W + N], m2 = A[lane * W + N + 1];
+              const double m1b = A[(L + lane) * W + N], m2b = A[(L + lane) * W + N + 1];
+              if (wl) {
+                wv = make_float2((float)(0.5 * (m1 + m2b)), (float)(0.5 * (m2 - m1b)));
+                vv = make_float2((float)(0.5 * (m1 - m2b)), (float)(0.5 * (m2 + m1b)));
+              } else {
+                wv = make_float2((float)m1, (float)m1b);
+                vv = make_float2(0.f, 0.f);
+              }
+            }
+            th[lane] = wv;
+            th[L + lane] = vv;
+          }
+          if (lane == 0) misc[1] = fail;
+        }
       }
       __syncthreads();
       bad |= misc[1];
