@@ -397,10 +397,11 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
           fail |= !(piv > 0.0) || !isfinite(piv);
           const double inv = 1.0 / piv;
           const int ncol = N + 1 - k;                 // columns k+1 .. N+1
-          double nv[2];
-          int at[2];
+          constexpr int PER = (N * (N + 1) + K3_THREADS - 1) / K3_THREADS;   // elements per thread at k = 0
+          double nv[PER];
+          int at[PER];
 #pragma unroll
-          for (int q = 0; q < 2; ++q) {
+          for (int q = 0; q < PER; ++q) {
             const int e = tid + K3_THREADS * q;
             at[q] = -1;
             if (e < N * ncol) {
@@ -412,7 +413,7 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
           }
           __syncthreads();
 #pragma unroll
-          for (int q = 0; q < 2; ++q)
+          for (int q = 0; q < PER; ++q)
             if (at[q] >= 0) A[at[q]] = nv[q];
           __syncthreads();
         }
