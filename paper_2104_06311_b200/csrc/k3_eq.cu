@@ -33,7 +33,8 @@
 // working on its previous frame. A symbol's tap window y_s[2kl .. 2kl + 2K] is K+1 16-byte shared loads
 // (each warp load a contiguous 512-B access, conflict-free) with compile-time offsets (K is a template
 // parameter); every sweep does all of a symbol's MACs from registers. Sweeps: (A) lag sums + frame power,
-// (B) decisions + p, (C) pass 2 — y¹ stays in registers through unbias, CPR and the decisions.
+// (B) decisions + p, (C) pass 2 → y¹ per symbol in shared memory, then unbias, CPR and the decisions in
+// short loops (the kernel's instruction footprint is kept small: it runs once per frame).
 // Reductions: in-warp transpose-reduce (31 shuffles per 32 values), then fp64 over the 8 warps in fixed
 // order (deterministic).
 #include "kk_device.cuh"
