@@ -131,7 +131,7 @@ struct K3Layout {
   static constexpr int ND = 2 * K + 1;             // lags 0..2K for base i = −K (ρ = 0); 0..2K−1 for ρ = 1
   static constexpr int N = 2 * L;                  // real system size
   static constexpr int NP = 4 * L;                 // p floats: p1, p2 complex
-  static constexpr int RG = 5;                     // lags per R sweep (register budget)
+  static constexpr int RG = (K <= 4) ? ND : 5;     // lags per R sweep (register budget)
   static constexpr int NRG = (ND + RG - 1) / RG;   // R sweeps
   static constexpr int NR = 8 * RG * NRG;          // S0,T0,S1,T1 per lag (padded to whole groups)
   static constexpr int NRED = ((NP + NR + 1 + 31) / 32) * 32;   // + frame power
@@ -270,10 +270,11 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
               }
             }
           }
-          if (grp == 0) {
+          if (grp == 0) {                      // pass 1 (kept in us until sweep B) and its power
             float2 y0 = make_float2(0.f, 0.f);
 #pragma unroll
             for (int e = 0; e < L; ++e) cmac(y0, wc[e], w[e]);
+            us[tid + K3_THREADS * s] = y0;
             pw = fmaf(y0.x, y0.x, fmaf(y0.y, y0.y, pw));
           }
         }
@@ -302,10 +303,7 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
         for (int s = 0; s < K3_SPT; ++s) {
           float2 w[L];
           load_window(tid + K3_THREADS * s, w);
-          float2 y0 = make_float2(0.f, 0.f);
-#pragma unroll
-          for (int e = 0; e < L; ++e) cmac(y0, wc[e], w[e]);
-          const float2 d = sl.point(cscale(y0, g));
+          const float2 d = sl.point(cscale(us[tid + K3_THREADS * s], g));
 #pragma unroll
           for (int e = 0; e < L; ++e) {
             float2 p1 = make_float2(acc[4 * e], acc[4 * e + 1]), p2 = make_float2(acc[4 * e + 2], acc[4 * e + 3]);
