@@ -81,6 +81,7 @@ k2_mf_kernel(const float2* __restrict__ E, int64_t E_first, const float2* __rest
   extern __shared__ float2 lo_s[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int i = tid; i < p.lo_den; i += K2_THREADS) lo_s[i] = lo_tab[i];
+  const int step256 = (int)(((int64_t)256 * p.lo_num) % p.lo_den);     // LO index step between r and r+1
 
   // tiles are visited from the END of the range: K1 wrote E front to back, so its most recent (L2-resident)
   // output is consumed first; K3 then walks y front to back, again reading K2's most recent writes first.
@@ -103,51 +104,93 @@ k2_mf_kernel(const float2* __restrict__ E, int64_t E_first, const float2* __rest
       const int64_t s0n = (t - gridDim.x) * kMfHop - kMfLead;
       asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(E + (s0n - E_first)), "r"(kMfN * 8) : "memory");
     }
-    // a5: b = (E − A_f)·LO, one sample per thread per step: 256-B coalesced loads, conflict-free stores
+    // ---- FFT4096 pass 1 (radix 16, Ns = 1) fused with the load: x_i = (E_i − A_f(i))·LO_i, i = j + 256 r
     {
-      const int64_t sA = s0 + tid;
-      int q = (int)(((sA % p.lo_den) + p.lo_den) % p.lo_den);
-      q = (int)(((int64_t)q * p.lo_num) % p.lo_den);
-      const int lo_step1 = (int)(((int64_t)K2_THREADS * p.lo_num) % p.lo_den);
-      const float2* src = E + (s0 - E_first) + tid;
       const float2 A0 = A_s[0], A1 = A_s[1];
       const int isplit = (int)(fsplit - s0);                 // first local sample of frame fa+1
-#pragma unroll 8
-      for (int it = 0; it < kMfN / K2_THREADS; ++it) {
-        const int i = tid + K2_THREADS * it;
-        const float2 e = __ldg(src + it * K2_THREADS);
-        const float2 A = (i < isplit) ? A0 : A1;
-        buf[pad16(i)] = cmul(make_float2(e.x - A.x, e.y - A.y), lo_s[q]);
-        q += lo_step1; q -= (q >= p.lo_den) ? p.lo_den : 0;
+      float2 v[2][16];
+#pragma unroll
+      for (int it = 0; it < 2; ++it) {
+        const int j = tid + K2_THREADS * it;
+        const float2* src = E + (s0 - E_first) + j;
+#pragma unroll
+        for (int r = 0; r < 16; ++r) v[it][r] = __ldg(src + 256 * r);
       }
+#pragma unroll
+      for (int it = 0; it < 2; ++it) {
+        const int j = tid + K2_THREADS * it;
+        const int64_t sj = s0 + j;
+        int q = (int)(((sj % p.lo_den) + p.lo_den) % p.lo_den);
+        q = (int)(((int64_t)q * p.lo_num) % p.lo_den);
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+          const float2 A = (j + 256 * r < isplit) ? A0 : A1;
+          v[it][r] = cmul(make_float2(v[it][r].x - A.x, v[it][r].y - A.y), lo_s[q]);
+          q += step256; q -= (q >= p.lo_den) ? p.lo_den : 0;
+        }
+        dft_reg<16, -1>(v[it]);
+        float2* dst = buf + 17 * j;                          // pad16(16j + r) = 17j + r
+#pragma unroll
+        for (int r = 0; r < 16; ++r) dst[r] = v[it][r];
+      }
+      __syncthreads();
     }
-    __syncthreads();
-    // a6: FFT4096 (radix 16 × 3)
-    stockham_pass<4096, 16, 1, -1>(buf, nullptr, tid);
     stockham_pass<4096, 16, 16, -1>(buf, tw256, tid);
-    stockham_pass<4096, 16, 256, -1>(buf, tw4096, tid);
-    // × H (real) and fold: Y2[q] = Y[q]H[q] + Y[q+2048]H[q+2048]
-#pragma unroll 4
-    for (int it = 0; it < 2048 / K2_THREADS; ++it) {
-      const int qq = tid + it * K2_THREADS;
-      const float2 a = buf[pad16(qq)], b = buf[pad16(qq + 2048)];
-      const float ha = __ldg(&Hs[qq]), hb = __ldg(&Hs[qq + 2048]);
-      buf[pad16(qq)] = make_float2(fmaf(a.x, ha, b.x * hb), fmaf(a.y, ha, b.y * hb));
+    // ---- FFT4096 pass 3 (Ns = 256) fused with × H and the fold: thread j owns Y[j + 256 r], r < 16, so
+    //      Y2[j + 256 r] = Y[j + 256 r]·H[j + 256 r] + Y[j + 256 (r+8)]·H[j + 256 (r+8)], r < 8
+    {
+      float2 v[2][16];
+#pragma unroll
+      for (int it = 0; it < 2; ++it) {
+        const int j = tid + K2_THREADS * it;
+        const float2* src = buf + pad16(j);
+#pragma unroll
+        for (int r = 0; r < 16; ++r) v[it][r] = src[r * (256 + 16)];
+      }
+      __syncthreads();
+#pragma unroll
+      for (int it = 0; it < 2; ++it) {
+        const int j = tid + K2_THREADS * it;
+#pragma unroll
+        for (int r = 1; r < 16; ++r) v[it][r] = cmul(v[it][r], __ldg(&tw4096[r * 256 + j]));
+        dft_reg<16, -1>(v[it]);
+        float2* dst = buf + pad16(j);
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          const float ha = __ldg(&Hs[j + 256 * r]), hb = __ldg(&Hs[j + 256 * (r + 8)]);
+          const float2 a = v[it][r], b = v[it][r + 8];
+          dst[r * (256 + 16)] = make_float2(fmaf(a.x, ha, b.x * hb), fmaf(a.y, ha, b.y * hb));
+        }
+      }
+      __syncthreads();
     }
-    __syncthreads();
-    // IFFT2048 (radix 16, 16, 8)
+    // ---- IFFT2048 (radix 16, 16, 8); the last pass stores the kept outputs straight to y
     stockham_pass<2048, 16, 1, +1>(buf, nullptr, tid);
     stockham_pass<2048, 16, 16, +1>(buf, tw256, tid);
-    stockham_pass<2048, 8, 256, +1>(buf, tw2048, tid);
-    // keep p ∈ [256, 1792) → y[1536t − 256 + p]
-    const int64_t m_base = t * kMfKeep - kMfKeep0;
-#pragma unroll 4
-    for (int it = 0; it < kMfKeep / K2_THREADS; ++it) {
-      const int pp = kMfKeep0 + tid + it * K2_THREADS;
-      const int64_t m = m_base + pp;
-      if (m >= y_first && m < y_first + y_count) y[m - y_first] = buf[pad16(pp)];
+    {
+      const int64_t m_base = t * kMfKeep - kMfKeep0;          // y index of IFFT output p: m_base + p
+      float2 v[2][8];
+#pragma unroll
+      for (int it = 0; it < 2; ++it) {
+        const int j = tid + K2_THREADS * it;
+        const float2* src = buf + pad16(j);
+#pragma unroll
+        for (int r = 0; r < 8; ++r) v[it][r] = src[r * (256 + 16)];
+      }
+#pragma unroll
+      for (int it = 0; it < 2; ++it) {
+        const int j = tid + K2_THREADS * it;
+#pragma unroll
+        for (int r = 1; r < 8; ++r) v[it][r] = cmulc(v[it][r], __ldg(&tw2048[r * 256 + j]));
+        dft_reg<8, +1>(v[it]);
+#pragma unroll
+        for (int r = 1; r < 7; ++r) {                        // p = j + 256 r ∈ [256, 1792) ⇔ 1 ≤ r ≤ 6
+          const int64_t m = m_base + j + 256 * r;
+          if (m >= y_first && m < y_first + y_count) y[m - y_first] = v[it][r];
+        }
+      }
+      __syncthreads();                                        // buf is rewritten by the next tile
     }
-    __syncthreads();
   }
 }
 
