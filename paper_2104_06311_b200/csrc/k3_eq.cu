@@ -74,7 +74,16 @@ struct Slicer {
       else iI = iIb;
     }
   }
+  // decided point. Square/rectangular grids: level = 2·ceil(x/2 + (m−2)/2) − (m−1), clamped — the same
+  // value as the integer path (scaling by ½ commutes with fp32 rounding), without int conversions.
   __device__ __forceinline__ float2 point(float2 z) const {
+    if (!cross) {
+      const float hI = 0.5f * (float)(mI - 2), hQ = 0.5f * (float)(mQ - 2);
+      const float xu = z.x * s, yu = z.y * s;           // as in levels(): same roundings
+      const float lI = fminf(fmaxf(2.f * ceilf(fmaf(0.5f, xu, hI)) - (float)(mI - 1), -(float)(mI - 1)), (float)(mI - 1));
+      const float lQ = fminf(fmaxf(2.f * ceilf(fmaf(0.5f, yu, hQ)) - (float)(mQ - 1), -(float)(mQ - 1)), (float)(mQ - 1));
+      return make_float2(lI * inv_s, lQ * inv_s);
+    }
     int iI, iQ;
     levels(z, iI, iQ);
     return make_float2((float)(2 * iI - (mI - 1)) * inv_s, (float)(2 * iQ - (mQ - 1)) * inv_s);
@@ -385,18 +394,22 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
         if (lane < N) A[lane * W + lane] += lam;
       }
       __syncthreads();
-      // ---- Gauss–Jordan on [G + λI | q1 q2] by the whole CTA (SPD ⇒ no pivoting): at step k every
-      //      element (i, c), c > k, reads its old value, A[i][k] and A[k][c], then all write together.
+      // ---- Gauss–Jordan on [G + λI | q1 q2] by the whole CTA with 2×2 pivot blocks (SPD ⇒ every leading
+      //      2×2 block is SPD, no pivoting; N = 4K + 2 is even): at step k every element (i, c), c ≥ k + 2,
+      //      reads its old value, A[i][k..k+1] and the pivot rows' column c, then all write together —
+      //      N/2 steps, two barriers each.
       {
         constexpr int W = Lay::WS;
         double* A = mat;
         int fail = 0;
-        for (int k = 0; k < N; ++k) {
-          const double piv = A[k * W + k];
-          fail |= !(piv > 0.0) || !isfinite(piv);
-          const double inv = 1.0 / piv;
-          const int ncol = N + 1 - k;                 // columns k+1 .. N+1
-          constexpr int PER = (N * (N + 1) + K3_THREADS - 1) / K3_THREADS;   // elements per thread at k = 0
+        for (int k = 0; k < N; k += 2) {
+          const double pa = A[k * W + k], pb = A[k * W + k + 1];
+          const double pc = A[(k + 1) * W + k], pd = A[(k + 1) * W + k + 1];
+          const double det = pa * pd - pb * pc;
+          fail |= !(pa > 0.0) || !(det > 0.0) || !isfinite(det);
+          const double idet = 1.0 / det;
+          const int ncol = N - k;                     // columns k+2 .. N+1
+          constexpr int PER = (N * N + K3_THREADS - 1) / K3_THREADS;   // elements per thread at k = 0
           double nv[PER];
           int at[PER];
 #pragma unroll
@@ -404,9 +417,14 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
             const int e = tid + K3_THREADS * q;
             at[q] = -1;
             if (e < N * ncol) {
-              const int i = e / ncol, c = k + 1 + e % ncol;
-              const double b = A[k * W + c];
-              nv[q] = (i == k) ? b * inv : fma(-A[i * W + k] * inv, b, A[i * W + c]);
+              const int i = e / ncol, c = k + 2 + e % ncol;
+              const double r0 = A[k * W + c], r1 = A[(k + 1) * W + c];
+              const double R0 = (pd * r0 - pb * r1) * idet, R1 = (pa * r1 - pc * r0) * idet;   // P⁻¹·[r0; r1]
+              double v;
+              if (i == k) v = R0;
+              else if (i == k + 1) v = R1;
+              else v = fma(-A[i * W + k + 1], R1, fma(-A[i * W + k], R0, A[i * W + c]));
+              nv[q] = v;
               at[q] = i * W + c;
             }
           }
