@@ -58,6 +58,13 @@ class OracleConfig:
     clamp_rel: float = 1e-12          # R7
     formats: Sequence[int] = (4,)     # per-segment QAM order (R26)
     segment_frames: int = 1 << 30
+    # paper arrangement: eq_mode "ddlms" folds the CD inverse
+    # into the static filter and equalizes with the 4-tap T/2-spaced widely-linear DDLMS
+    eq_mode: str = "block_ls"         # "block_ls" (north star, default) | "ddlms" (paper)
+    ddlms_mu_warm: float = 1e-3       # step size over the warm-up symbols (SPEC S:377 schedule start)
+    ddlms_mu: float = 2.5e-4          # step size over the kept symbols (SPEC S:377 schedule end)
+    ddlms_block: int = 1024           # symbols kept per DDLMS restart (global grid)
+    ddlms_warmup: int = 1024          # symbols run before each block from the centre-spike state
 
     @property
     def sps(self) -> int:
@@ -177,6 +184,55 @@ def o7_matched_filter(b: np.ndarray, b0: int, m0: int, m1: int, h: np.ndarray) -
     return c[n - b0 + half]
 
 
+def static_filter_taps(cfg: OracleConfig) -> np.ndarray:
+    """Paper arrangement ("frequency-domain static equalization ... multiplication with an
+    offline-optimized filter"): RRC matched filter × CD inverse referenced to the carrier,
+    defined on the 4096-point grid and truncated to the 1025 taps j = −512..512:
+        h_cd[j] = (1/4096)·Σ_k H_rrc[k]·C(ν_k)·e^{2πi·kj/4096},  C(ν) = exp(−i(β₂L/2)(2π(ν + σf_c))²),
+    ν_k the baseband frequency of FFT bin k at 4 GS/s."""
+    h = rrc_taps(cfg)
+    N = 4096
+    half = (len(h) - 1) // 2
+    hc = np.zeros(N)
+    hc[:half + 1] = h[half:]
+    hc[-half:] = h[:half]
+    nu = np.fft.fftfreq(N, d=1.0 / cfg.fs_hz)
+    f_c = cfg.fs_hz * cfg.lo_num / cfg.lo_den
+    C = np.exp(-1j * (beta2L(cfg) / 2) * (2 * np.pi * (nu + cfg.sideband * f_c)) ** 2)
+    full = np.fft.ifft(np.fft.fft(hc) * C)
+    j = np.arange(-half, half + 1)
+    return full[j % N]
+
+
+def o8_ddlms_block(y: np.ndarray, m0: int, n0: int, nwarm: int, nkeep: int, M: int, cfg: OracleConfig):
+    """4-tap T/2-spaced widely-linear DDLMS, restarted per block.
+    Symbols n = n0 .. n0 + nwarm + nkeep − 1 (global); x_n = [u[2n+1], u[2n], u[2n−1], u[2n−2]] with
+    u = g·y, g = (mean_n |y[2n]|²)^(−½) (AGC over the block and its warm-up);
+    out_n = wᵀx_n + vᵀconj(x_n), d_n = D(out_n), e_n = d_n − out_n, w += μ·e·conj(x), v += μ·e·x;
+    w starts as the centre spike on u[2n], v = 0 (and stays 0 when eq_widely_linear is False);
+    μ = ddlms_mu_warm over the warm-up, ddlms_mu after.
+    Returns the outputs of the nkeep kept symbols (before each one's update)."""
+    nn = np.arange(n0, n0 + nwarm + nkeep)
+    centres = y[2 * nn - m0]
+    P = np.mean(np.abs(centres) ** 2)
+    g = 1.0 / math.sqrt(P) if P > 0 else 1.0
+    w = np.array([0, 1, 0, 0], complex)
+    v = np.zeros(4, complex)
+    out = np.zeros(nkeep, complex)
+    for i, n in enumerate(nn):
+        x = g * y[2 * n - m0 + np.array([1, 0, -1, -2])]
+        o = np.dot(w, x) + np.dot(v, np.conj(x))
+        d, _ = nearest(np.array([o]), M)
+        e = d[0] - o
+        mu = cfg.ddlms_mu_warm if i < nwarm else cfg.ddlms_mu
+        if i >= nwarm:
+            out[i - nwarm] = o
+        w = w + mu * e * np.conj(x)
+        if cfg.eq_widely_linear:
+            v = v + mu * e * x
+    return out
+
+
 # ------------------------------------------------------------------------------------------
 # O8–O10: per-frame equalizer, CPR, decisions
 # ------------------------------------------------------------------------------------------
@@ -265,10 +321,13 @@ def receive(codes: np.ndarray, first: int, n: int, cfg: OracleConfig, ref: Optio
     e, A = o5_carrier_removal(E, e0, cfg)
     b = o6_mixer(e, e0, cfg)
     # O7 over the 2-sps range the frames need
+    ddlms = cfg.eq_mode == "ddlms"
     L = tap_count(cfg)
     K = (L - 1) // 2
+    if ddlms:
+        K = 2 * cfg.ddlms_warmup + 2                   # warm-up reaches 2W + 2 samples before the core
     m0, m1 = first // 2 - K, (first + n) // 2 + K
-    h = rrc_taps(cfg)
+    h = static_filter_taps(cfg) if ddlms else rrc_taps(cfg)
     y = o7_matched_filter(b, e0, m0, m1, h)
     # O8–O10 per frame
     w_cd = cd_init_taps(cfg)
@@ -290,6 +349,12 @@ def receive(codes: np.ndarray, first: int, n: int, cfg: OracleConfig, ref: Optio
             zf = np.zeros(Fs, complex)
             _, lab = nearest(np.full(Fs, -1e-9 - 1e-9j), M)   # D(0) with ties to the lower level (R15)
             info = dict(dead=True, bad=False)
+        elif ddlms:
+            B, W = cfg.ddlms_block, cfg.ddlms_warmup
+            kg0 = first // cfg.sps + k0                 # global symbol index of the frame start
+            zf = np.concatenate([o8_ddlms_block(y, m0, kg0 + bb - W, W, B, M, cfg) for bb in range(0, Fs, B)])
+            info = dict(dead=False, bad=False)
+            _, lab = nearest(zf, M)
         else:
             yf = y[2 * k0: 2 * k0 + 2 * Fs - 1 + 2 * K]
             u, info = o8_equalize_frame(yf, K, w_cd, M, cfg)

@@ -424,3 +424,74 @@ def test_dead_frame_counted():
     assert out["counts"]["dead_frames"] == 1
     assert out["counts"]["clamped"] == F
     assert np.all(out["z"][4096:8192] == 0)
+
+
+# ------------------------------------------------------------------ paper arrangement: static CD filter + DDLMS
+def _dd_cfg(**kw):
+    return _cfg(eq_mode="ddlms", **kw)
+
+
+def test_dd_static_filter_zero_km_is_rrc_and_inverts_cd():
+    h0 = R.static_filter_taps(_dd_cfg())
+    assert np.max(np.abs(h0 - R.rrc_taps(_cfg()))) < 1e-14                   # C ≡ 1 at D·L = 0
+    cfg = _dd_cfg(dispersion_ps_per_nm=200000.0)
+    hcd = R.static_filter_taps(cfg)
+    N = 4096
+    Hcd = np.fft.fft(np.roll(np.concatenate([hcd, np.zeros(N - len(hcd))]), -512))
+    Hr = np.fft.fft(np.roll(np.concatenate([R.rrc_taps(_cfg()), np.zeros(N - 1025)]), -512))
+    nu = np.fft.fftfreq(N, d=0.25e-9)
+    chan = np.exp(1j * (R.beta2L(cfg) / 2) * (2 * np.pi * (nu + 0.516e9)) ** 2)   # the generator's CD (R24)
+    band = np.abs(nu) < 0.49e9
+    err = np.abs(Hcd * chan - Hr)[band]
+    assert 20 * np.log10(np.max(err) / np.max(np.abs(Hr))) < -40                 # CD removed in the band
+
+
+def test_dd_mu_zero_is_identity():
+    rng = np.random.default_rng(4)
+    y = rng.standard_normal(6000) + 1j * rng.standard_normal(6000)
+    cfg = _dd_cfg(ddlms_mu_warm=0.0, ddlms_mu=0.0)
+    out = R.o8_ddlms_block(y, 0, 10, 100, 500, 16, cfg)
+    nn = np.arange(110, 610)
+    g = 1 / np.sqrt(np.mean(np.abs(y[2 * np.arange(10, 610)]) ** 2))
+    assert np.max(np.abs(out - g * y[2 * nn])) < 1e-13                          # SPEC S:352 example
+
+
+def test_dd_absorbs_rotation():
+    rng = np.random.default_rng(6)
+    pts = C.points_by_label(4)
+    s = pts[rng.integers(0, 4, 7000)]
+    y = np.zeros(2 * 7000 + 8, complex)
+    y[2 * np.arange(7000)] = s * np.exp(1j * np.deg2rad(20))                     # θ = 20°
+    out = R.o8_ddlms_block(y, 0, 2, 5000, 1900, 4, _dd_cfg())                    # ≤ 5000 symbols to converge
+    d, _ = C.nearest(out, 4)
+    assert 10 * np.log10(np.mean(np.abs(out - d) ** 2)) < -25
+
+
+def test_dd_widely_linear_branch():
+    rng = np.random.default_rng(8)
+    pts = C.points_by_label(16)
+    s = pts[rng.integers(0, 16, 7000)]
+    y = np.zeros(2 * 7000 + 8, complex)
+    y[2 * np.arange(7000)] = s
+    y = y + 0.1 * np.conj(y)                                                       # SPEC S:354 leakage
+    ev = {}
+    for wl in (True, False):
+        out = R.o8_ddlms_block(y, 0, 2, 4000, 2900, 16, _dd_cfg(eq_widely_linear=wl))
+        d, _ = C.nearest(out, 16)
+        ev[wl] = 10 * np.log10(np.mean(np.abs(out - d) ** 2))
+    assert ev[True] < ev[False] - 10, ev
+
+
+@pytest.mark.parametrize("M,dl", [(4, 0.0), (16, 0.0), (64, 32000.0), (16, 200000.0), (32, 112000.0)])
+def test_dd_noiseless_zero_errors(M, dl):
+    out, _, _, _ = _chain(M, dl=dl, cspr=12.0, n=16384, eq_mode="ddlms")
+    assert out["counts"]["bit_err"].sum() == 0
+    assert _evm_db(out["z"], M) < -40
+
+
+def test_dd_awgn_q_vs_theory():
+    out, _, _, _ = _chain(16, dl=32000.0, cspr=16.0, esn0=15.0, noise="analytic", n=1 << 18, seed=19,
+                          eq_mode="ddlms")
+    c = out["counts"]
+    ber = c["bit_err"].sum() / c["bits"].sum()
+    assert abs(T.q_from_ber(ber) - T.q_from_ber(T.ber_awgn(16, 15.0))) <= 0.3
