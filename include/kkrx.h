@@ -50,6 +50,7 @@ typedef enum {
 } kk_status;
 
 enum { KK_IN_INT16 = 0, KK_IN_FLOAT32 = 1 };                  /* input_dtype */
+enum { KK_EQ_BLOCK_LS = 0, KK_EQ_DDLMS = 1 };                 /* eq_mode */
 enum { KK_STAGE_FIELD = 0, KK_STAGE_MF = 1, KK_STAGE_EQ = 2 }; /* kk_get_intermediate stages */
 
 /* Receiver configuration. kk_config_default() fills the paper's values; fields marked [fixed] must
@@ -81,6 +82,16 @@ typedef struct kk_config {
   int64_t max_samples_per_call;  /* sizes the scratch; multiple of 16384                                 */
   int32_t device;                /* CUDA device ordinal the context lives on                             */
   int32_t keep_intermediate;     /* 1: K3 also stores z (EQ stage) for kk_get_intermediate               */
+  /* Equalizer mode. KK_EQ_BLOCK_LS (default, BASELINE north star): RRC static filter + per-frame widely-linear
+   * block-adaptive FIR absorbing CD + CPR. KK_EQ_DDLMS (the paper's arrangement):
+   * static filter = RRC × CD inverse (the "offline-optimized filter"), then the 4-tap T/2-spaced widely-linear
+   * DDLMS, restarted every ddlms_block symbols after ddlms_warmup warm-up symbols (global grid). */
+  int32_t eq_mode;
+  int32_t ddlms_block;           /* 256 … 4096, power of two (kept symbols per restart)                  */
+  int32_t ddlms_warmup;          /* 0 … 3840 warm-up symbols run from the centre-spike state             */
+  int32_t reserved0;
+  double  ddlms_mu_warm;         /* 1e-3 step size during warm-up                           */
+  double  ddlms_mu;              /* 2.5e-4 step size on kept symbols                                     */
 } kk_config;
 
 /* Counters (all uint64, summed over calls until kk_reset_stats; index i = log2(M) − 2 for M = 4..64).
@@ -110,7 +121,7 @@ kk_status kk_init(const kk_config* cfg, kk_ctx** out);
  * one neighbour frame (its carrier estimate A_f and MF support) + half a Hilbert block = 16640. */
 kk_status kk_halo(const kk_ctx* ctx, int64_t* left, int64_t* right);
 
-/* Equalizer taps L actually used (rule or override). */
+/* Equalizer taps L actually used (rule or override; 4 in DDLMS mode). */
 kk_status kk_eq_taps(const kk_ctx* ctx, int32_t* taps);
 
 /* Process the core [first_sample, first_sample + n_samples) of the stream; asynchronous on `stream`.
@@ -144,6 +155,7 @@ kk_status kk_reset_stats(kk_ctx* ctx, kk_stream_t stream);
 /* Describe / copy the last call's intermediate of a stage (device→device, async on stream):
  *   KK_STAGE_FIELD: E (complex64 interleaved) for samples [first − 16384, first + n + 16384)
  *   KK_STAGE_MF   : y (complex64) for 2-sps indices [first/2 − K, (first + n)/2 + K), K = (L−1)/2
+ *                   (DDLMS mode: K = 2·ddlms_warmup + 2)
  *   KK_STAGE_EQ   : z (complex64) for symbols [first/4, (first + n)/4); needs keep_intermediate
  * kk_intermediate_range gives (first global index, count) of the stage. KK_ERR_STATE if no call yet /
  * not kept; KK_ERR_CONFIG if bytes < count·8. */

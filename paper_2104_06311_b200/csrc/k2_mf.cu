@@ -71,11 +71,15 @@ __device__ __forceinline__ int64_t floordiv(int64_t a, int64_t b) {
   return (a % b != 0 && ((a < 0) != (b < 0))) ? q - 1 : q;
 }
 
+// CH = false: real H (RRC matched filter, north star). CH = true: complex H_cd = RRC × CD inverse (the paper's
+// static filter, eq_mode DDLMS).
+template <bool CH>
 __global__ void __launch_bounds__(K2_THREADS, 4)
 k2_mf_kernel(const float2* __restrict__ E, int64_t E_first, const float2* __restrict__ part, int64_t jb0,
              int64_t tile0, int64_t n_tiles, float2* __restrict__ y, int64_t y_first, int64_t y_count,
-             const float* __restrict__ Hs, const float2* __restrict__ lo_tab, const float2* __restrict__ tw256,
-             const float2* __restrict__ tw4096, const float2* __restrict__ tw2048, K2Params p) {
+             const float* __restrict__ Hs, const float2* __restrict__ Hc, const float2* __restrict__ lo_tab,
+             const float2* __restrict__ tw256, const float2* __restrict__ tw4096, const float2* __restrict__ tw2048,
+             K2Params p) {
   __shared__ __align__(16) float2 buf[K2_BUF];
   __shared__ float2 A_s[2];
   extern __shared__ float2 lo_s[];
@@ -157,9 +161,13 @@ k2_mf_kernel(const float2* __restrict__ E, int64_t E_first, const float2* __rest
         float2* dst = buf + pad16(j);
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
-          const float ha = __ldg(&Hs[j + 256 * r]), hb = __ldg(&Hs[j + 256 * (r + 8)]);
           const float2 a = v[it][r], b = v[it][r + 8];
-          dst[r * (256 + 16)] = make_float2(fmaf(a.x, ha, b.x * hb), fmaf(a.y, ha, b.y * hb));
+          if constexpr (CH) {
+            dst[r * (256 + 16)] = cadd(cmul(a, __ldg(&Hc[j + 256 * r])), cmul(b, __ldg(&Hc[j + 256 * (r + 8)])));
+          } else {
+            const float ha = __ldg(&Hs[j + 256 * r]), hb = __ldg(&Hs[j + 256 * (r + 8)]);
+            dst[r * (256 + 16)] = make_float2(fmaf(a.x, ha, b.x * hb), fmaf(a.y, ha, b.y * hb));
+          }
         }
       }
       __syncthreads();
@@ -196,14 +204,18 @@ k2_mf_kernel(const float2* __restrict__ E, int64_t E_first, const float2* __rest
 
 void launch_k2(const float2* E, int64_t E_first, const float2* part, const int* /*clampcnt*/, int64_t jb0,
                int64_t tile0, int64_t n_tiles, float2* y, int64_t y_first, int64_t y_count, const float* Hs,
-               const float2* lo_tab, const float2* tw256, const float2* tw4096, const float2* tw2048,
-               const K2Params& p, int num_sms, cudaStream_t s) {
+               const float2* Hc, const float2* lo_tab, const float2* tw256, const float2* tw4096,
+               const float2* tw2048, const K2Params& p, int num_sms, cudaStream_t s) {
   int per_sm = 4;
   int64_t grid = (int64_t)num_sms * per_sm;
   if (grid > n_tiles) grid = n_tiles;
   const size_t dyn = (size_t)p.lo_den * sizeof(float2);
-  k2_mf_kernel<<<(unsigned)grid, K2_THREADS, dyn, s>>>(E, E_first, part, jb0, tile0, n_tiles, y, y_first, y_count,
-                                                       Hs, lo_tab, tw256, tw4096, tw2048, p);
+  if (Hc)
+    k2_mf_kernel<true><<<(unsigned)grid, K2_THREADS, dyn, s>>>(E, E_first, part, jb0, tile0, n_tiles, y, y_first,
+                                                               y_count, Hs, Hc, lo_tab, tw256, tw4096, tw2048, p);
+  else
+    k2_mf_kernel<false><<<(unsigned)grid, K2_THREADS, dyn, s>>>(E, E_first, part, jb0, tile0, n_tiles, y, y_first,
+                                                                y_count, Hs, Hc, lo_tab, tw256, tw4096, tw2048, p);
 }
 
 }  // namespace kk

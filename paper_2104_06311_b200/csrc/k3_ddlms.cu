@@ -1,0 +1,131 @@
+// k3_ddlms.cu — K3 (paper arrangement, eq_mode = KK_EQ_DDLMS): 4-tap T/2-spaced widely-linear DDLMS.
+//
+// PAPER.md:82 (§2): "the signal is further filtered by a four-tap adaptive time-domain DDLMS widely-linear
+// equalizer. The decisions made by the equalizer are demapped". CD is removed by the static filter in K2
+// (RRC × CD inverse, the "offline-optimized filter"), so the 4 adaptive taps only track residual ISI, gain and
+// phase:
+//   x_n = g·[y[2n+1], y[2n], y[2n−1], y[2n−2]],  g = (mean |y[2n]|²)^(−½) over the block and its warm-up
+//   o_n = wᵀx_n + vᵀconj(x_n),  d_n = D(o_n),  e_n = d_n − o_n,  w += μ e conj(x),  v += μ e x
+//   w₀ = centre spike on y[2n], v₀ = 0; μ = mu_warm over the warm-up, mu over the kept symbols.
+// The paper carries the equalizer state across 2^22-sample buffers in stream order (events serialise the
+// streams). Here the recursion restarts on a global grid of B-symbol blocks, each preceded by W
+// warm-up symbols: blocks are independent, so they run in parallel and any sharding gives the
+// same decisions; the warm-up (≫ the adaptation time constant) makes the kept outputs those of a converged
+// sequential equalizer.
+//
+// Mapping: one thread per block (B = 1024 ⇒ 65,536 threads per 2^26-sample call); the recursion is
+// sequential in registers (4 + 4 complex taps, a 4-sample sliding window refilled with 2 samples per symbol).
+#include "kk_device.cuh"
+#include "kk_params.h"
+
+namespace kk {
+
+constexpr int K3D_THREADS = 64;
+
+__global__ void __launch_bounds__(K3D_THREADS)
+k3_ddlms_kernel(const float2* __restrict__ y, int64_t y_base, int64_t sym_first, int n_blocks, int B, int W,
+                const int* __restrict__ clampcnt, int64_t clamp_frame_off, const uint8_t* __restrict__ ref,
+                uint8_t* __restrict__ dec, float2* __restrict__ zout, unsigned long long* __restrict__ counters,
+                K3DParams p) {
+  const int blk = blockIdx.x * K3D_THREADS + threadIdx.x;
+  if (blk >= n_blocks) return;
+  const int64_t n_keep0 = (int64_t)blk * B;                  // local index of the first kept symbol
+  const int fl = (int)(n_keep0 / kFrameSym);                 // local frame
+  const int64_t f = sym_first / kFrameSym + fl;
+  const int M = (int)p.schedule[(int)(((f / p.segment_frames) % p.n_segments + p.n_segments) % p.n_segments)];
+  const int bi = (M == 4) ? 0 : (M == 8) ? 1 : (M == 16) ? 2 : (M == 32) ? 3 : 4;
+  Slicer sl;
+  sl.init(M);
+  int ccount = 0;
+  for (int q = 0; q < 32; ++q) ccount += __ldg(&clampcnt[clamp_frame_off + (int64_t)fl * 32 + q]);
+  const bool dead = (ccount >= kFrameSamp);
+  // y index of local 2-sps sample m is y_base + m; symbol n ↔ m = 2n
+  const float2* yy = y + y_base;
+  const int64_t n0 = n_keep0 - W;
+  int serr = 0, berr = 0;
+  if (!dead) {
+    // AGC over the block and its warm-up (symbol-centre samples)
+    float pw = 0.f;
+    for (int i = 0; i < W + B; ++i) {
+      const float2 c = __ldg(&yy[2 * (n0 + i)]);
+      pw = fmaf(c.x, c.x, fmaf(c.y, c.y, pw));
+    }
+    const float P = pw / (float)(W + B);
+    const float g = (P > 0.f) ? rsqrtf(P) : 1.0f;
+    float2 w[4] = {make_float2(0.f, 0.f), make_float2(1.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+    float2 v[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+    // window x = [u[2n+1], u[2n], u[2n−1], u[2n−2]]
+    float2 x[4];
+    x[0] = cscale(__ldg(&yy[2 * n0 + 1]), g);
+    x[1] = cscale(__ldg(&yy[2 * n0]), g);
+    x[2] = cscale(__ldg(&yy[2 * n0 - 1]), g);
+    x[3] = cscale(__ldg(&yy[2 * n0 - 2]), g);
+    const bool wl = p.widely_linear != 0;
+    for (int i = 0; i < W + B; ++i) {
+      const int64_t n = n0 + i;
+      // prefetch the next symbol's two new samples
+      const float2 nx0 = __ldg(&yy[2 * n + 3]), nx1 = __ldg(&yy[2 * n + 2]);
+      float2 o = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        cmac(o, w[k], x[k]);
+        cmac(o, v[k], cconj(x[k]));
+      }
+      const float2 d = sl.point(o);
+      const float2 e = csub(d, o);
+      const float mu = (i < W) ? p.mu_warm : p.mu;
+      if (i >= W) {
+        const int64_t kl = n;                                  // local kept symbol index
+        const int lab = sl.label(o);
+        if (ref) {
+          const int r = __ldg(&ref[kl]);
+          serr += (lab != r);
+          berr += __popc(lab ^ r);
+        }
+        if (dec) dec[kl] = (uint8_t)lab;
+        if (zout) zout[kl] = o;
+      }
+      const float2 me = cscale(e, mu);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        cmac(w[k], me, cconj(x[k]));
+        if (wl) cmac(v[k], me, x[k]);
+      }
+      x[3] = x[1]; x[2] = x[0];
+      x[1] = cscale(nx1, g); x[0] = cscale(nx0, g);
+    }
+  } else {
+    const int lab = sl.label(make_float2(0.f, 0.f));
+    for (int i = 0; i < B; ++i) {
+      const int64_t kl = n_keep0 + i;
+      if (ref) {
+        const int r = __ldg(&ref[kl]);
+        serr += (lab != r);
+        berr += __popc(lab ^ r);
+      }
+      if (dec) dec[kl] = (uint8_t)lab;
+      if (zout) zout[kl] = make_float2(0.f, 0.f);
+    }
+  }
+  if (ref) {
+    if (serr) atomicAdd(&counters[5 + bi], (unsigned long long)serr);
+    if (berr) atomicAdd(&counters[15 + bi], (unsigned long long)berr);
+  }
+  atomicAdd(&counters[bi], (unsigned long long)B);
+  atomicAdd(&counters[10 + bi], (unsigned long long)B * (bi + 2));
+  if (n_keep0 % kFrameSym == 0) {                            // once per frame
+    if (ccount) atomicAdd(&counters[20], (unsigned long long)ccount);
+    atomicAdd(&counters[21], 1ull);
+    if (dead) atomicAdd(&counters[22], 1ull);
+  }
+}
+
+void launch_k3_ddlms(const float2* y, int64_t y_base, int64_t sym_first, int64_t n_blocks, int B, int W,
+                     const int* clampcnt, int64_t clamp_frame_off, const uint8_t* ref, uint8_t* dec, float2* z,
+                     unsigned long long* counters, const K3DParams& p, cudaStream_t s) {
+  const unsigned grid = (unsigned)((n_blocks + K3D_THREADS - 1) / K3D_THREADS);
+  k3_ddlms_kernel<<<grid, K3D_THREADS, 0, s>>>(y, y_base, sym_first, (int)n_blocks, B, W, clampcnt, clamp_frame_off,
+                                               ref, dec, z, counters, p);
+}
+
+}  // namespace kk

@@ -161,6 +161,55 @@ __device__ __forceinline__ Decision slice(float2 z) {
   return d;
 }
 
+// runtime-uniform QAM slicer parameters (CTA-uniform: one format per frame, R26)
+struct Slicer {
+  int mI, mQ, hb, cross;
+  float s, inv_s;
+  __device__ __forceinline__ void init(int M) {
+    cross = (M == 32);
+    if (M == 8) { mI = 4; mQ = 2; hb = 1; s = 2.44948974278317810f; }
+    else if (M == 32) { mI = 6; mQ = 6; hb = 0; s = 4.47213595499957940f; }
+    else {
+      mI = mQ = (M == 4) ? 2 : (M == 16) ? 4 : 8;
+      hb = (M == 4) ? 1 : (M == 16) ? 2 : 3;
+      s = (M == 4) ? 1.41421356237309505f : (M == 16) ? 3.16227766016837933f : 6.48074069840786023f;
+    }
+    inv_s = 1.0f / s;
+  }
+  __device__ __forceinline__ void levels(float2 z, int& iI, int& iQ) const {
+    const float xu = z.x * s, yu = z.y * s;
+    iI = pam_index(xu, mI);
+    iQ = pam_index(yu, mQ);
+    if (cross && (iI == 0 || iI == 5) && (iQ == 0 || iQ == 5)) {
+      const float ax = fabsf(xu), ay = fabsf(yu);
+      const int iQa = (iQ == 0) ? 1 : 4, iIb = (iI == 0) ? 1 : 4;
+      if (ax > ay) iQ = iQa;
+      else if (ay > ax) iI = iIb;
+      else if (cross32_label(iI, iQa) < cross32_label(iIb, iQ)) iQ = iQa;
+      else iI = iIb;
+    }
+  }
+  // decided point. Square/rectangular grids: level = 2·ceil(x/2 + (m−2)/2) − (m−1), clamped — the same
+  // value as the integer path (scaling by ½ commutes with fp32 rounding), without int conversions.
+  __device__ __forceinline__ float2 point(float2 z) const {
+    if (!cross) {
+      const float hI = 0.5f * (float)(mI - 2), hQ = 0.5f * (float)(mQ - 2);
+      const float xu = z.x * s, yu = z.y * s;           // as in levels(): same roundings
+      const float lI = fminf(fmaxf(2.f * ceilf(fmaf(0.5f, xu, hI)) - (float)(mI - 1), -(float)(mI - 1)), (float)(mI - 1));
+      const float lQ = fminf(fmaxf(2.f * ceilf(fmaf(0.5f, yu, hQ)) - (float)(mQ - 1), -(float)(mQ - 1)), (float)(mQ - 1));
+      return make_float2(lI * inv_s, lQ * inv_s);
+    }
+    int iI, iQ;
+    levels(z, iI, iQ);
+    return make_float2((float)(2 * iI - (mI - 1)) * inv_s, (float)(2 * iQ - (mQ - 1)) * inv_s);
+  }
+  __device__ __forceinline__ int label(float2 z) const {
+    int iI, iQ;
+    levels(z, iI, iQ);
+    return cross ? cross32_label(iI, iQ) : ((gray(iI) << hb) | gray(iQ));
+  }
+};
+
 // ------------------------------------------------------------------ TMA 1-D bulk copy (cp.async.bulk) + mbarrier
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));

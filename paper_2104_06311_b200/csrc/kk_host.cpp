@@ -33,10 +33,13 @@ struct kk_ctx {
   kk_config cfg;
   int device = 0, num_sms = 148;
   int L = 0, K = 0;
+  bool ddlms = false;   // eq_mode == KK_EQ_DDLMS
+  int Ky = 0;           // 2-sps margin of y around the core: K (block LS) or 2·warmup + 2 (DDLMS)
   std::vector<uint8_t> schedule;
   std::vector<cd> w_cd;
   // device constants
   float* d_H = nullptr;
+  float2* d_Hc = nullptr;   // complex static filter RRC × CD inverse (DDLMS mode)
   float2* d_lo = nullptr;
   float2* d_wcd = nullptr;
   float2 *d_tw1024 = nullptr, *d_tw256 = nullptr, *d_tw4096 = nullptr, *d_tw2048 = nullptr;
@@ -232,6 +235,12 @@ kk_status validate(const kk_config& c, std::string& why) {
     return bad("unsupported QAM order (default_format)");
   }
   if (!(c.lambda_m > 0)) return bad("lambda_m must be > 0");
+  if (c.eq_mode != KK_EQ_BLOCK_LS && c.eq_mode != KK_EQ_DDLMS) return bad("eq_mode");
+  if (c.eq_mode == KK_EQ_DDLMS) {
+    if (c.ddlms_block < 256 || c.ddlms_block > kk::kFrameSym || !is_pow2(c.ddlms_block)) return bad("ddlms_block must be a power of two in [256, 4096]");
+    if (c.ddlms_warmup < 0 || c.ddlms_warmup > 3840) return bad("ddlms_warmup must be in [0, 3840]");
+    if (!(c.ddlms_mu_warm >= 0) || !(c.ddlms_mu >= 0)) return bad("ddlms step sizes must be >= 0");
+  }
   return KK_OK;
 }
 
@@ -258,7 +267,7 @@ void resolve_timing(kk_ctx* c, size_t count) {
 }
 
 void free_all(kk_ctx* c) {
-  void* ptrs[] = {c->d_H, c->d_lo, c->d_wcd, c->d_tw1024, c->d_tw256, c->d_tw4096, c->d_tw2048, c->d_sched,
+  void* ptrs[] = {c->d_H, c->d_Hc, c->d_lo, c->d_wcd, c->d_tw1024, c->d_tw256, c->d_tw4096, c->d_tw2048, c->d_sched,
                   c->d_E, c->d_part, c->d_clamp, c->d_y, c->d_z, c->d_counters,
                   c->d_in[0], c->d_in[1], c->d_ref[0], c->d_ref[1], c->d_dec[0], c->d_dec[1]};
   for (void* p : ptrs) if (p) cudaFree(p);
@@ -309,6 +318,12 @@ void kk_config_default(kk_config* c) {
   c->max_samples_per_call = (int64_t)1 << 24;
   c->device = 0;
   c->keep_intermediate = 0;
+  c->eq_mode = KK_EQ_BLOCK_LS;
+  c->ddlms_block = 1024;
+  c->ddlms_warmup = 1024;
+  c->reserved0 = 0;
+  c->ddlms_mu_warm = 1e-3;
+  c->ddlms_mu = 2.5e-4;
 }
 
 size_t kk_config_sizeof(void) { return sizeof(kk_config); }
@@ -322,7 +337,8 @@ kk_status kk_init(const kk_config* cfg, kk_ctx** out) {
     std::fprintf(stderr, "kk_init: %s\n", why.c_str());
     return KK_ERR_CONFIG;
   }
-  const int L = tap_rule(*cfg);
+  const bool ddlms = cfg->eq_mode == KK_EQ_DDLMS;
+  const int L = ddlms ? 3 : tap_rule(*cfg);   // (DDLMS mode: the block-LS taps are unused)
   if (L < 3 || L > 2 * kk::kMaxK + 1 || (L % 2) == 0) {
     std::fprintf(stderr, "kk_init: tap-count rule gives L=%d outside [3,15]\n", L);
     return KK_ERR_CONFIG;
@@ -330,8 +346,10 @@ kk_status kk_init(const kk_config* cfg, kk_ctx** out) {
   kk_ctx* c = new kk_ctx();
   c->cfg = *cfg;
   c->device = cfg->device;
-  c->L = L;
+  c->L = ddlms ? 4 : L;
   c->K = (L - 1) / 2;
+  c->ddlms = ddlms;
+  c->Ky = ddlms ? 2 * cfg->ddlms_warmup + 2 : c->K;
   if (cfg->format_schedule) {
     c->schedule.assign(cfg->format_schedule, cfg->format_schedule + cfg->n_segments);
   } else {
@@ -364,6 +382,47 @@ kk_status kk_init(const kk_config* cfg, kk_ctx** out) {
     const double a = -2.0 * kPi * (double)cfg->sideband * (double)q / (double)cfg->lo_den;
     lo[q] = make_float2((float)std::cos(a), (float)std::sin(a));
   }
+  // paper arrangement: complex static filter H_cd = DFT4096 of h_cd, h_cd = IDFT4096(H_rrc·C) truncated to
+  // j = −512..512 (the same definition as oracle.receiver.static_filter_taps), ×1/4096 folded in
+  std::vector<float2> Hc;
+  if (ddlms) {
+    const int N = kk::kMfN;
+    std::vector<double> Hr(N);
+    for (int k = 0; k < N; ++k) {
+      double s = h[half];
+      for (int j = 1; j <= half; ++j) s += 2.0 * h[half + j] * std::cos(2.0 * kPi * (double)((int64_t)k * j % N) / N);
+      Hr[k] = s;
+    }
+    std::vector<double> ct(N), st(N);
+    for (int m = 0; m < N; ++m) { ct[m] = std::cos(2.0 * kPi * m / N); st[m] = std::sin(2.0 * kPi * m / N); }
+    const double fc = cfg->fs_hz * (double)cfg->lo_num / (double)cfg->lo_den, b2 = beta2L(*cfg);
+    std::vector<cd> HC(N);
+    for (int k = 0; k < N; ++k) {
+      const double nu = (k < N / 2 ? (double)k : (double)(k - N)) * cfg->fs_hz / N;
+      const double w = 2.0 * kPi * (nu + (double)cfg->sideband * fc);
+      const double ph = -(b2 / 2.0) * w * w;
+      HC[k] = Hr[k] * cd(std::cos(ph), std::sin(ph));
+    }
+    std::vector<cd> hcd(2 * half + 1);
+    for (int j = -half; j <= half; ++j) {
+      cd acc(0, 0);
+      for (int k = 0; k < N; ++k) {
+        const int m = (int)(((int64_t)k * (j + N)) % N);
+        acc += HC[k] * cd(ct[m], st[m]);
+      }
+      hcd[j + half] = acc / (double)N;
+    }
+    Hc.resize(N);
+    for (int k = 0; k < N; ++k) {
+      cd acc(0, 0);
+      for (int j = -half; j <= half; ++j) {
+        const int m = (int)(((int64_t)k * (j + N)) % N);
+        acc += hcd[j + half] * cd(ct[m], -st[m]);
+      }
+      acc /= (double)N;
+      Hc[k] = make_float2((float)acc.real(), (float)acc.imag());
+    }
+  }
   c->w_cd = cd_init_taps(*cfg, L);
   std::vector<float2> wcd(L);
   for (int i = 0; i < L; ++i) wcd[i] = make_float2((float)c->w_cd[i].real(), (float)c->w_cd[i].imag());
@@ -371,6 +430,7 @@ kk_status kk_init(const kk_config* cfg, kk_ctx** out) {
   e = cudaSuccess;
   auto chk = [&](cudaError_t r) { if (e == cudaSuccess) e = r; };
   chk(upload(&c->d_H, H));
+  if (ddlms) chk(upload(&c->d_Hc, Hc));
   chk(upload(&c->d_lo, lo));
   chk(upload(&c->d_wcd, wcd));
   chk(upload(&c->d_tw1024, twiddles(1024, 32, 32)));
@@ -386,7 +446,7 @@ kk_status kk_init(const kk_config* cfg, kk_ctx** out) {
   chk(cudaMalloc((void**)&c->d_E, (size_t)nE * sizeof(float2)));
   chk(cudaMalloc((void**)&c->d_part, (size_t)(nE / kk::kHilbertHop) * sizeof(float2)));
   chk(cudaMalloc((void**)&c->d_clamp, (size_t)(nE / kk::kHilbertHop) * sizeof(int)));
-  chk(cudaMalloc((void**)&c->d_y, (size_t)(n / 2 + 2 * c->K + 2) * sizeof(float2)));
+  chk(cudaMalloc((void**)&c->d_y, (size_t)(n / 2 + 2 * c->Ky + 2) * sizeof(float2)));
   if (cfg->keep_intermediate) chk(cudaMalloc((void**)&c->d_z, (size_t)(n / 4) * sizeof(float2)));
   chk(cudaMalloc((void**)&c->d_counters, 32 * sizeof(unsigned long long)));
   chk(cudaMemset(c->d_counters, 0, 32 * sizeof(unsigned long long)));
@@ -453,15 +513,15 @@ kk_status kk_process_frames(kk_ctx* c, const void* d_adc, int64_t first, int64_t
   kk::launch_k1(adc0, cf.input_dtype == KK_IN_FLOAT32, nblk / 2, c->d_E, c->d_part, c->d_clamp, c->d_tw1024, p1, s);
 
   // K2 over the MF tiles covering y[first/2 − K, (first + n)/2 + K)
-  const int64_t y_first = first / 2 - c->K;
-  const int64_t y_count = n / 2 + 2 * c->K;
+  const int64_t y_first = first / 2 - c->Ky;
+  const int64_t y_count = n / 2 + 2 * c->Ky;
   auto fdiv = [](int64_t a, int64_t b) { int64_t q = a / b; return (a % b != 0 && ((a < 0) != (b < 0))) ? q - 1 : q; };
   const int64_t t_lo = fdiv(y_first, kk::kMfKeep);
   const int64_t t_hi = fdiv(y_first + y_count - 1, kk::kMfKeep);
   if (c->timing) cudaEventRecord(tev[1], s);
   kk::K2Params p2{cf.lo_num, cf.lo_den};
   kk::launch_k2(c->d_E, first - F, c->d_part, c->d_clamp, jb0, t_lo, t_hi - t_lo + 1, c->d_y, y_first, y_count,
-                c->d_H, c->d_lo, c->d_tw256, c->d_tw4096, c->d_tw2048, p2, c->num_sms, s);
+                c->d_H, c->d_Hc, c->d_lo, c->d_tw256, c->d_tw4096, c->d_tw2048, p2, c->num_sms, s);
 
   if (c->timing) cudaEventRecord(tev[2], s);
   // K3 one CTA per frame
@@ -473,8 +533,21 @@ kk_status kk_process_frames(kk_ctx* c, const void* d_adc, int64_t first, int64_t
   p3.widely_linear = cf.eq_widely_linear;
   p3.cpr_window = cf.cpr_window;
   const int64_t nfr = n / F;
-  kk::launch_k3(c->d_y, first / F, nfr, c->K, c->d_wcd, c->d_clamp, (int64_t)F / kk::kHilbertHop /*skip frame −1*/,
-                d_ref, d_dec, cf.keep_intermediate ? c->d_z : nullptr, c->d_counters, p3, c->num_sms, s);
+  if (c->ddlms) {
+    kk::K3DParams pd;
+    pd.schedule = c->d_sched;
+    pd.n_segments = cf.n_segments;
+    pd.segment_frames = cf.segment_frames;
+    pd.mu_warm = (float)cf.ddlms_mu_warm;
+    pd.mu = (float)cf.ddlms_mu;
+    pd.widely_linear = cf.eq_widely_linear;
+    kk::launch_k3_ddlms(c->d_y, c->Ky, first / 4, n / 4 / cf.ddlms_block, cf.ddlms_block, cf.ddlms_warmup,
+                        c->d_clamp, (int64_t)F / kk::kHilbertHop, d_ref, d_dec,
+                        cf.keep_intermediate ? c->d_z : nullptr, c->d_counters, pd, s);
+  } else {
+    kk::launch_k3(c->d_y, first / F, nfr, c->K, c->d_wcd, c->d_clamp, (int64_t)F / kk::kHilbertHop /*skip frame −1*/,
+                  d_ref, d_dec, cf.keep_intermediate ? c->d_z : nullptr, c->d_counters, p3, c->num_sms, s);
+  }
   if (c->timing) {
     cudaEventRecord(tev[3], s);
     c->ev_pending.push_back(tev);
@@ -566,7 +639,7 @@ kk_status kk_intermediate_range(const kk_ctx* c, int stage, int64_t* first_index
   const int64_t f = c->last_first, n = c->last_n;
   switch (stage) {
     case KK_STAGE_FIELD: *first_index = f - kk::kFrameSamp; *count = n + 2 * kk::kFrameSamp; return KK_OK;
-    case KK_STAGE_MF: *first_index = f / 2 - c->K; *count = n / 2 + 2 * c->K; return KK_OK;
+    case KK_STAGE_MF: *first_index = f / 2 - c->Ky; *count = n / 2 + 2 * c->Ky; return KK_OK;
     case KK_STAGE_EQ:
       if (!c->last_z) return KK_ERR_STATE;
       *first_index = f / 4; *count = n / 4; return KK_OK;

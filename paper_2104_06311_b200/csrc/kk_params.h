@@ -41,17 +41,30 @@ struct K3Params {
   int cpr_window;                    // symbols
 };
 
+struct K3DParams {
+  const uint8_t* schedule;
+  int n_segments;
+  int64_t segment_frames;
+  float mu_warm, mu;
+  int widely_linear;
+};
+
 // K1: KK front end + Hilbert + field; one warp per pair of 512-blocks, 8 warps per CTA.
 void launch_k1(const void* adc_cta0, int input_float, int64_t n_pairs, float2* E, float2* part, int* clampcnt,
                const float2* tw1024, const K1Params& p, cudaStream_t s);
 // K2: carrier removal + mixer + RRC MF + decimation by 2 on the global tile grid.
 void launch_k2(const float2* E, int64_t E_first, const float2* part, const int* clampcnt, int64_t jb0,
                int64_t tile0, int64_t n_tiles, float2* y, int64_t y_first, int64_t y_count, const float* Hs,
-               const float2* lo_tab, const float2* tw256, const float2* tw4096, const float2* tw2048,
-               const K2Params& p, int num_sms, cudaStream_t s);
+               const float2* Hc, const float2* lo_tab, const float2* tw256, const float2* tw4096,
+               const float2* tw2048, const K2Params& p, int num_sms, cudaStream_t s);
 // K3: per-frame widely-linear DD-LS equalizer, CPR, decisions, counters.
 void launch_k3(const float2* y, int64_t frame0, int64_t n_frames, int K, const float2* w_cd, const int* clampcnt,
                int64_t clamp_frame_off, const uint8_t* ref, uint8_t* dec, float2* z, unsigned long long* counters,
                const K3Params& p, int num_sms, cudaStream_t s);
+
+// K3 (paper arrangement): 4-tap T/2-spaced widely-linear DDLMS, one thread per restart block.
+void launch_k3_ddlms(const float2* y, int64_t y_base, int64_t sym_first, int64_t n_blocks, int B, int W,
+                     const int* clampcnt, int64_t clamp_frame_off, const uint8_t* ref, uint8_t* dec, float2* z,
+                     unsigned long long* counters, const K3DParams& p, cudaStream_t s);
 
 }  // namespace kk

@@ -17,6 +17,7 @@ LIB_PATH = os.path.join(HERE, "libkkrx.so")
 KK_OK, KK_ERR_CONFIG, KK_ERR_ALIGN, KK_ERR_SHORT, KK_ERR_NULL = 0, -1, -2, -3, -4
 KK_ERR_NOMEM, KK_ERR_CUDA, KK_ERR_DOMAIN, KK_ERR_STATE = -5, -6, -7, -8
 KK_IN_INT16, KK_IN_FLOAT32 = 0, 1
+KK_EQ_BLOCK_LS, KK_EQ_DDLMS = 0, 1
 KK_STAGE_FIELD, KK_STAGE_MF, KK_STAGE_EQ = 0, 1, 2
 KK_STATS_WORDS = 24
 HALO = 16640
@@ -35,6 +36,8 @@ class kk_config(ctypes.Structure):
         ("format_schedule", POINTER(c_uint8)), ("n_segments", c_int32), ("default_format", c_int32),
         ("segment_frames", c_int64), ("max_samples_per_call", c_int64), ("device", c_int32),
         ("keep_intermediate", c_int32),
+        ("eq_mode", c_int32), ("ddlms_block", c_int32), ("ddlms_warmup", c_int32), ("reserved0", c_int32),
+        ("ddlms_mu_warm", c_double), ("ddlms_mu", c_double),
     ]
 
 

@@ -19,7 +19,9 @@ class Receiver:
                  max_samples_per_call: int = 1 << 24, device: int = 0, keep_intermediate: bool = False,
                  eq_taps: int = 0, widely_linear: bool = True, cpr_window: int = 256, eq_ridge: float = 1e-3,
                  input_float: bool = False, sideband: int = 1, lo_num: int = 129, lo_den: int = 1000,
-                 clamp_rel: float = 1e-12, rolloff: float = 0.01, rrc_span_sym: int = 256):
+                 clamp_rel: float = 1e-12, rolloff: float = 0.01, rrc_span_sym: int = 256,
+                 eq_mode: str = "block_ls", ddlms_block: int = 1024, ddlms_warmup: int = 1024,
+                 ddlms_mu_warm: float = 1e-3, ddlms_mu: float = 2.5e-4):
         cfg = kkrx.kk_config_default()
         cfg.adc_scale, cfg.adc_offset, cfg.ref_intensity = adc_scale, adc_offset, ref_intensity
         cfg.dispersion_ps_per_nm = dispersion_ps_per_nm
@@ -33,6 +35,9 @@ class Receiver:
         cfg.input_dtype = kkrx.KK_IN_FLOAT32 if input_float else kkrx.KK_IN_INT16
         cfg.sideband, cfg.lo_num, cfg.lo_den = sideband, lo_num, lo_den
         cfg.clamp_rel, cfg.rolloff, cfg.rrc_span_sym = clamp_rel, rolloff, rrc_span_sym
+        cfg.eq_mode = {"block_ls": kkrx.KK_EQ_BLOCK_LS, "ddlms": kkrx.KK_EQ_DDLMS}[eq_mode]
+        cfg.ddlms_block, cfg.ddlms_warmup = ddlms_block, ddlms_warmup
+        cfg.ddlms_mu_warm, cfg.ddlms_mu = ddlms_mu_warm, ddlms_mu
         fm = list(formats)
         self._sched = (ctypes.c_uint8 * len(fm))(*fm)
         cfg.format_schedule = ctypes.cast(self._sched, ctypes.POINTER(ctypes.c_uint8))

@@ -38,7 +38,9 @@ def receiver_for(case, keep=True, max_samples=None, **kw):
     return Receiver(adc_scale=o.adc_scale, ref_intensity=o.ref_intensity, dispersion_ps_per_nm=case["dl"],
                     formats=case["formats"], segment_frames=case["segment_frames"],
                     max_samples_per_call=max_samples or max(case["n"], F), keep_intermediate=keep,
-                    eq_taps=o.eq_taps, widely_linear=o.eq_widely_linear, cpr_window=o.cpr_window, **kw)
+                    eq_taps=o.eq_taps, widely_linear=o.eq_widely_linear, cpr_window=o.cpr_window,
+                    eq_mode=o.eq_mode, ddlms_block=o.ddlms_block, ddlms_warmup=o.ddlms_warmup,
+                    ddlms_mu_warm=o.ddlms_mu_warm, ddlms_mu=o.ddlms_mu, **kw)
 
 
 def run_gpu(case, keep=True, chunk=None, rx=None):

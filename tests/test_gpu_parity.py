@@ -199,3 +199,26 @@ def test_call_errors():
     with pytest.raises(P.KKError) as e:
         P.kk_intermediate_range(rx.ctx, P.KK_STAGE_EQ)
     assert e.value.status == P.KK_ERR_STATE
+
+
+# ----------------------------------------------------------------------------- paper arrangement (NEXT-1/2)
+@pytest.mark.parametrize("M,dl,cspr,esn0", [(16, 0.0, 12.0, None), (16, 200000.0, 12.0, None),
+                                            (64, 32000.0, 12.0, 26.0), (4, 200000.0, 12.0, 12.0),
+                                            (32, 112000.0, 14.0, 22.0)])
+def test_ddlms_mode_parity(M, dl, cspr, esn0):
+    case = make_case(M=M, dl=dl, cspr=cspr, esn0=esn0, n=1 << 17, seed=600 + M, eq_mode="ddlms")
+    gpu, orc = run_gpu(case), run_oracle(case)
+    _check_all(case, gpu, orc, dec_min=1.0 if esn0 is None else 0.9999)
+    if esn0 is None:
+        assert gpu["stats"]["bit_err"] == [0] * 5 == list(orc["counts"]["bit_err"])
+    assert gpu["stats"]["sym"] == list(orc["counts"]["sym"])
+
+
+def test_ddlms_mode_mixed_formats_and_chunking():
+    case = make_case(formats=(4, 8, 16, 32, 64), segment_frames=1, dl=32000.0, cspr=12.0, esn0=26.0,
+                     n=10 * F, seed=502, eq_mode="ddlms", ddlms_block=512, ddlms_warmup=768)
+    whole = run_gpu(case)
+    chunked = run_gpu(case, chunk=2 * F)
+    orc = run_oracle(case)
+    _check_all(case, whole, orc)
+    assert np.array_equal(whole["dec"], chunked["dec"]) and np.array_equal(whole["z"], chunked["z"])
