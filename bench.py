@@ -49,6 +49,9 @@ def parse():
     ap.add_argument("--cpu-frames", type=int, default=64, help="oracle sample size (frames) for cpu_baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--eq-mode", default="block_ls", choices=["block_ls", "ddlms"],
+                    help="block_ls: north-star per-frame WL least squares + CPR (default); "
+                         "ddlms: the paper's static CD filter + 4-tap WL DDLMS")
     return ap.parse_args()
 
 
@@ -63,17 +66,25 @@ def k3_flops_per_symbol(L: int) -> float:
     return 8.0 * 9 * L + 40.0
 
 
-def kernel_units(chunk: int, L: int):
+def kernel_units(chunk: int, L: int, eq_mode: str = "block_ls", ddlms_block: int = 1024, ddlms_warmup: int = 1024):
     """Algorithmic flops and HBM bytes per launch of each kernel for one call of `chunk` samples."""
     K = (L - 1) // 2
     k1_samples = chunk + 2 * F
     y_first = -K
     n_tiles = (chunk // 2 + 2 * K + 1536 - 1) // 1536 + 1
     frames = chunk // F
+    if eq_mode == "ddlms":
+        # per processed symbol (kept + warm-up): output 8 cMAC + update 8 cMAC = 128 flops + ~20 (slicer, error)
+        sym = chunk // 4 * (ddlms_block + ddlms_warmup) / ddlms_block
+        k3 = dict(flops=148.0 * sym, bytes=(8.0 * (ddlms_block + ddlms_warmup) / ddlms_block * 2 + 2.0) * (chunk // 4))
+        k2_flops = 403456.0 + 2048 * 8.0                  # complex H: 8 more flops per folded bin
+    else:
+        k3 = dict(flops=k3_flops_per_symbol(L) * 4096 * frames, bytes=73728.0 * frames)
+        k2_flops = 403456.0
     return {
         "K1_kk": dict(flops=107.0 * k1_samples, bytes=10.0 * k1_samples),
-        "K2_mf": dict(flops=403456.0 * n_tiles, bytes=36864.0 * n_tiles),
-        "K3_eq": dict(flops=k3_flops_per_symbol(L) * 4096 * frames, bytes=73728.0 * frames),
+        "K2_mf": dict(flops=k2_flops * n_tiles, bytes=36864.0 * n_tiles),
+        "K3_eq": k3,
     }
 
 
@@ -167,9 +178,9 @@ def oracle_sample(runs, ocfg_kw, pool):
     return res, wall
 
 
-def ocfg_kwargs(lc):
+def ocfg_kwargs(lc, eq_mode="block_ls"):
     return dict(dispersion_ps_per_nm=lc.dl_ps_nm, adc_scale=lc.adc_scale, ref_intensity=lc.i_ref,
-                formats=tuple(lc.formats), segment_frames=lc.segment_frames)
+                formats=tuple(lc.formats), segment_frames=lc.segment_frames, eq_mode=eq_mode)
 
 
 # ----------------------------------------------------------------------------------------------- reference arm
@@ -197,7 +208,7 @@ def run_reference(a, rank, world):
     times = []
     pool = make_pool(cores)
     for it in range(a.warmup + a.steps):
-        _, wall = oracle_sample(runs, ocfg_kwargs(lc), pool)
+        _, wall = oracle_sample(runs, ocfg_kwargs(lc, a.eq_mode), pool)
         if it >= a.warmup:
             times.append(wall)
     pool.close()
@@ -253,7 +264,8 @@ def main():
     t_gen = time.perf_counter() - t0
 
     rx = Receiver(adc_scale=lc.adc_scale, ref_intensity=lc.i_ref, dispersion_ps_per_nm=lc.dl_ps_nm,
-                  formats=lc.formats, segment_frames=lc.segment_frames, max_samples_per_call=chunk, device=local)
+                  formats=lc.formats, segment_frames=lc.segment_frames, max_samples_per_call=chunk, device=local,
+                  eq_mode=a.eq_mode)
     L = rx.taps
     dec = torch.empty(S // 4, dtype=torch.uint8, device=dev)
     counters = torch.zeros(kkrx.KK_STATS_WORDS, dtype=torch.int64, device=dev)
@@ -302,7 +314,7 @@ def main():
         peak_fp32 = N_SMS * FP32_LANES_PER_SM * 2 * float(mp.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12
     except Exception:
         pass
-    units = kernel_units(chunk, L)
+    units = kernel_units(chunk, L, a.eq_mode)
     traffic = {}
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
@@ -370,8 +382,8 @@ def main():
             runs.append((c, first + s0, fr_per_run * F, r))
             picks.append(s0 // 4)
         pool = make_pool(cores)
-        oracle_sample(runs[:cores], ocfg_kwargs(lc), pool)            # warm-up pass (first-touch, caches)
-        res, wall = oracle_sample(runs, ocfg_kwargs(lc), pool)
+        oracle_sample(runs[:cores], ocfg_kwargs(lc, a.eq_mode), pool)   # warm-up pass (first-touch, caches)
+        res, wall = oracle_sample(runs, ocfg_kwargs(lc, a.eq_mode), pool)
         pool.close()
         agree, nsym = 0, 0
         be_o = 0
@@ -399,7 +411,7 @@ def main():
             "dtype": "f32", "data": "synthetic (kkgen seeded generator, generated on device)",
             "config": {"workload": f"{a.workload}: continuous mixed 4/8/16/32/64-QAM stream (256-frame segments), "
                                    f"1 GBaud @ 4 GS/s, 1600 km (32000 ps/nm), CSPR 12 dB, Es/N0 26 dB white, int16 ADC",
-                       "samples_per_gpu": S, "chunk_samples": chunk, "eq_taps": L,
+                       "samples_per_gpu": S, "chunk_samples": chunk, "eq_taps": L, "eq_mode": a.eq_mode,
                        "l2": "inputs 8 GiB/GPU per step >> 126 MB L2, no flush needed", "seed": lc.seed},
             "rt_factor": value / 4.0,
             "clocks": clk.summary(),
