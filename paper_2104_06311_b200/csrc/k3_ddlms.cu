@@ -61,38 +61,50 @@ k3_ddlms_kernel(const float2* __restrict__ y, int64_t y_base, int64_t sym_first,
     x[2] = cscale(__ldg(&yy[2 * n0 - 1]), g);
     x[3] = cscale(__ldg(&yy[2 * n0 - 2]), g);
     const bool wl = p.widely_linear != 0;
-    for (int i = 0; i < W + B; ++i) {
-      const int64_t n = n0 + i;
-      // prefetch the next symbol's two new samples
-      const float2 nx0 = __ldg(&yy[2 * n + 3]), nx1 = __ldg(&yy[2 * n + 2]);
-      float2 o = make_float2(0.f, 0.f);
+    // the new samples y[2n+2], y[2n+3] of the next PF symbols are kept in a register ring (loads issued PF
+    // symbols ahead of use, so L2 latency is hidden behind the recursion)
+    constexpr int PF = 8;
+    float4 ring[PF];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        cmac(o, w[k], x[k]);
-        cmac(o, v[k], cconj(x[k]));
-      }
-      const float2 d = sl.point(o);
-      const float2 e = csub(d, o);
-      const float mu = (i < W) ? p.mu_warm : p.mu;
-      if (i >= W) {
-        const int64_t kl = n;                                  // local kept symbol index
-        const int lab = sl.label(o);
-        if (ref) {
-          const int r = __ldg(&ref[kl]);
-          serr += (lab != r);
-          berr += __popc(lab ^ r);
+    for (int q = 0; q < PF; ++q) ring[q] = __ldg(reinterpret_cast<const float4*>(yy + 2 * (n0 + q) + 2));
+    const int total = W + B;                                   // multiple of PF (both multiples of 256)
+    for (int i0 = 0; i0 < total; i0 += PF) {
+#pragma unroll
+      for (int q = 0; q < PF; ++q) {
+        const int i = i0 + q;
+        const int64_t n = n0 + i;
+        const float4 nx = ring[q];                             // (y[2n+2], y[2n+3])
+        if (i + PF < total) ring[q] = __ldg(reinterpret_cast<const float4*>(yy + 2 * (n + PF) + 2));
+        // o = Σ_k w_k x_k + v_k conj(x_k) as two independent partial sums (shorter dependency chain)
+        float2 o0 = make_float2(0.f, 0.f), o1 = make_float2(0.f, 0.f);
+        cmac(o0, w[0], x[0]); cmac(o1, w[1], x[1]);
+        cmac(o0, w[2], x[2]); cmac(o1, w[3], x[3]);
+        cmac(o0, v[0], cconj(x[0])); cmac(o1, v[1], cconj(x[1]));
+        cmac(o0, v[2], cconj(x[2])); cmac(o1, v[3], cconj(x[3]));
+        const float2 o = cadd(o0, o1);
+        const float2 d = sl.point(o);
+        const float2 e = csub(d, o);
+        const float mu = (i < W) ? p.mu_warm : p.mu;
+        if (i >= W) {
+          const int64_t kl = n;                                // local kept symbol index
+          const int lab = sl.label(o);
+          if (ref) {
+            const int r = __ldg(&ref[kl]);
+            serr += (lab != r);
+            berr += __popc(lab ^ r);
+          }
+          if (dec) dec[kl] = (uint8_t)lab;
+          if (zout) zout[kl] = o;
         }
-        if (dec) dec[kl] = (uint8_t)lab;
-        if (zout) zout[kl] = o;
-      }
-      const float2 me = cscale(e, mu);
+        const float2 me = cscale(e, mu);
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        cmac(w[k], me, cconj(x[k]));
-        if (wl) cmac(v[k], me, x[k]);
+        for (int k = 0; k < 4; ++k) {
+          cmac(w[k], me, cconj(x[k]));
+          if (wl) cmac(v[k], me, x[k]);
+        }
+        x[3] = x[1]; x[2] = x[0];
+        x[1] = cscale(make_float2(nx.x, nx.y), g); x[0] = cscale(make_float2(nx.z, nx.w), g);
       }
-      x[3] = x[1]; x[2] = x[0];
-      x[1] = cscale(nx1, g); x[0] = cscale(nx0, g);
     }
   } else {
     const int lab = sl.label(make_float2(0.f, 0.f));
