@@ -52,6 +52,9 @@ def parse():
     ap.add_argument("--eq-mode", default="block_ls", choices=["block_ls", "ddlms"],
                     help="block_ls: north-star per-frame WL least squares + CPR (default); "
                          "ddlms: the paper's static CD filter + 4-tap WL DDLMS")
+    ap.add_argument("--ddlms-block", type=int, default=1024)
+    ap.add_argument("--ddlms-warmup", type=int, default=1024)
+    ap.add_argument("--ddlms-mu-warm", type=float, default=1e-3)
     return ap.parse_args()
 
 
@@ -178,9 +181,12 @@ def oracle_sample(runs, ocfg_kw, pool):
     return res, wall
 
 
-def ocfg_kwargs(lc, eq_mode="block_ls"):
-    return dict(dispersion_ps_per_nm=lc.dl_ps_nm, adc_scale=lc.adc_scale, ref_intensity=lc.i_ref,
-                formats=tuple(lc.formats), segment_frames=lc.segment_frames, eq_mode=eq_mode)
+def ocfg_kwargs(lc, eq_mode="block_ls", a=None):
+    kw = dict(dispersion_ps_per_nm=lc.dl_ps_nm, adc_scale=lc.adc_scale, ref_intensity=lc.i_ref,
+              formats=tuple(lc.formats), segment_frames=lc.segment_frames, eq_mode=eq_mode)
+    if a is not None and eq_mode == "ddlms":
+        kw.update(ddlms_block=a.ddlms_block, ddlms_warmup=a.ddlms_warmup, ddlms_mu_warm=a.ddlms_mu_warm)
+    return kw
 
 
 # ----------------------------------------------------------------------------------------------- reference arm
@@ -208,7 +214,7 @@ def run_reference(a, rank, world):
     times = []
     pool = make_pool(cores)
     for it in range(a.warmup + a.steps):
-        _, wall = oracle_sample(runs, ocfg_kwargs(lc, a.eq_mode), pool)
+        _, wall = oracle_sample(runs, ocfg_kwargs(lc, a.eq_mode, a), pool)
         if it >= a.warmup:
             times.append(wall)
     pool.close()
@@ -265,7 +271,8 @@ def main():
 
     rx = Receiver(adc_scale=lc.adc_scale, ref_intensity=lc.i_ref, dispersion_ps_per_nm=lc.dl_ps_nm,
                   formats=lc.formats, segment_frames=lc.segment_frames, max_samples_per_call=chunk, device=local,
-                  eq_mode=a.eq_mode)
+                  eq_mode=a.eq_mode, ddlms_block=a.ddlms_block, ddlms_warmup=a.ddlms_warmup,
+                  ddlms_mu_warm=a.ddlms_mu_warm)
     L = rx.taps
     dec = torch.empty(S // 4, dtype=torch.uint8, device=dev)
     counters = torch.zeros(kkrx.KK_STATS_WORDS, dtype=torch.int64, device=dev)
@@ -314,7 +321,7 @@ def main():
         peak_fp32 = N_SMS * FP32_LANES_PER_SM * 2 * float(mp.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12
     except Exception:
         pass
-    units = kernel_units(chunk, L, a.eq_mode)
+    units = kernel_units(chunk, L, a.eq_mode, a.ddlms_block, a.ddlms_warmup)
     traffic = {}
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
@@ -382,8 +389,8 @@ def main():
             runs.append((c, first + s0, fr_per_run * F, r))
             picks.append(s0 // 4)
         pool = make_pool(cores)
-        oracle_sample(runs[:cores], ocfg_kwargs(lc, a.eq_mode), pool)   # warm-up pass (first-touch, caches)
-        res, wall = oracle_sample(runs, ocfg_kwargs(lc, a.eq_mode), pool)
+        oracle_sample(runs[:cores], ocfg_kwargs(lc, a.eq_mode, a), pool)   # warm-up pass (first-touch, caches)
+        res, wall = oracle_sample(runs, ocfg_kwargs(lc, a.eq_mode, a), pool)
         pool.close()
         agree, nsym = 0, 0
         be_o = 0
@@ -412,6 +419,8 @@ def main():
             "config": {"workload": f"{a.workload}: continuous mixed 4/8/16/32/64-QAM stream (256-frame segments), "
                                    f"1 GBaud @ 4 GS/s, 1600 km (32000 ps/nm), CSPR 12 dB, Es/N0 26 dB white, int16 ADC",
                        "samples_per_gpu": S, "chunk_samples": chunk, "eq_taps": L, "eq_mode": a.eq_mode,
+                       **({"ddlms_block": a.ddlms_block, "ddlms_warmup": a.ddlms_warmup,
+                           "ddlms_mu_warm": a.ddlms_mu_warm} if a.eq_mode == "ddlms" else {}),
                        "l2": "inputs 8 GiB/GPU per step >> 126 MB L2, no flush needed", "seed": lc.seed},
             "rt_factor": value / 4.0,
             "clocks": clk.summary(),

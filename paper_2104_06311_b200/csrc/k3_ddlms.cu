@@ -28,28 +28,6 @@ k3_ddlms_kernel(const float2* __restrict__ y, int64_t y_base, int64_t sym_first,
                 uint8_t* __restrict__ dec, float2* __restrict__ zout, unsigned long long* __restrict__ counters,
                 K3DParams p) {
   const int blk = blockIdx.x * K3D_THREADS + threadIdx.x;
-  const int lane = threadIdx.x & 31;
-  // ---- AGC powers of the warp's 32 blocks, computed cooperatively with coalesced loads: for block b of the
-  //      warp, lane l sums the symbol-centre samples n0 + l, n0 + l + 32, … then a fixed-order shuffle tree.
-  float my_pw = 0.f;
-  {
-    const int wblk0 = blk - lane;
-    const float2* yy0 = y + y_base;
-    for (int b = 0; b < 32; ++b) {
-      const int bb = wblk0 + b;
-      float s = 0.f;
-      if (bb < n_blocks) {                                     // warp-uniform
-        const int64_t n0b = (int64_t)bb * B - W;
-#pragma unroll 4
-        for (int i = lane; i < W + B; i += 32) {
-          const float2 c = __ldg(&yy0[2 * (n0b + i)]);
-          s = fmaf(c.x, c.x, fmaf(c.y, c.y, s));
-        }
-      }
-      s = warp_sum(s);
-      if (lane == b) my_pw = s;
-    }
-  }
   if (blk >= n_blocks) return;
   const int64_t n_keep0 = (int64_t)blk * B;                  // local index of the first kept symbol
   const int fl = (int)(n_keep0 / kFrameSym);                 // local frame
@@ -67,7 +45,12 @@ k3_ddlms_kernel(const float2* __restrict__ y, int64_t y_base, int64_t sym_first,
   int serr = 0, berr = 0;
   if (!dead) {
     // AGC over the block and its warm-up (symbol-centre samples)
-    const float P = my_pw / (float)(W + B);
+    float pw = 0.f;
+    for (int i = 0; i < W + B; ++i) {
+      const float2 c = __ldg(&yy[2 * (n0 + i)]);
+      pw = fmaf(c.x, c.x, fmaf(c.y, c.y, pw));
+    }
+    const float P = pw / (float)(W + B);
     const float g = (P > 0.f) ? rsqrtf(P) : 1.0f;
     float2 w[4] = {make_float2(0.f, 0.f), make_float2(1.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
     float2 v[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
@@ -84,10 +67,7 @@ k3_ddlms_kernel(const float2* __restrict__ y, int64_t y_base, int64_t sym_first,
     float4 ring[PF];
 #pragma unroll
     for (int q = 0; q < PF; ++q) ring[q] = __ldg(reinterpret_cast<const float4*>(yy + 2 * (n0 + q) + 2));
-    const int total = W + B;                                   // multiple of PF (both multiples of 64)
-    uint4 rpack = make_uint4(0u, 0u, 0u, 0u), dpack = make_uint4(0u, 0u, 0u, 0u);
-    // 16-label packs need 16-B aligned label buffers (kept blocks start at multiples of 256 symbols)
-    const bool vec = ((reinterpret_cast<uintptr_t>(ref) | reinterpret_cast<uintptr_t>(dec)) & 15) == 0;
+    const int total = W + B;                                   // multiple of PF (both multiples of 256)
     for (int i0 = 0; i0 < total; i0 += PF) {
 #pragma unroll
       for (int q = 0; q < PF; ++q) {
@@ -108,32 +88,12 @@ k3_ddlms_kernel(const float2* __restrict__ y, int64_t y_base, int64_t sym_first,
         if (i >= W) {
           const int64_t kl = n;                                // local kept symbol index
           const int lab = sl.label(o);
-          const int j = (i - W) & 15;                          // position in the 16-label pack
           if (ref) {
-            int r;
-            if (vec) {
-              if (j == 0) rpack = __ldg(reinterpret_cast<const uint4*>(ref + kl));
-              const uint32_t word = (j < 4) ? rpack.x : (j < 8) ? rpack.y : (j < 12) ? rpack.z : rpack.w;
-              r = (int)((word >> (8 * (j & 3))) & 0xffu);
-            } else {
-              r = __ldg(&ref[kl]);
-            }
+            const int r = __ldg(&ref[kl]);
             serr += (lab != r);
             berr += __popc(lab ^ r);
           }
-          if (dec) {
-            if (vec) {
-              const uint32_t sh = 8u * (uint32_t)(j & 3);
-              if (j < 4) dpack.x |= (uint32_t)lab << sh; else if (j < 8) dpack.y |= (uint32_t)lab << sh;
-              else if (j < 12) dpack.z |= (uint32_t)lab << sh; else dpack.w |= (uint32_t)lab << sh;
-              if (j == 15) {
-                *reinterpret_cast<uint4*>(dec + kl - 15) = dpack;
-                dpack = make_uint4(0u, 0u, 0u, 0u);
-              }
-            } else {
-              dec[kl] = (uint8_t)lab;
-            }
-          }
+          if (dec) dec[kl] = (uint8_t)lab;
           if (zout) zout[kl] = o;
         }
         const float2 me = cscale(e, mu);
