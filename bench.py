@@ -52,9 +52,9 @@ def parse():
     ap.add_argument("--eq-mode", default="block_ls", choices=["block_ls", "ddlms"],
                     help="block_ls: north-star per-frame WL least squares + CPR (default); "
                          "ddlms: the paper's static CD filter + 4-tap WL DDLMS")
-    ap.add_argument("--ddlms-block", type=int, default=1024)
-    ap.add_argument("--ddlms-warmup", type=int, default=1024)
-    ap.add_argument("--ddlms-mu-warm", type=float, default=1e-3)
+    ap.add_argument("--ddlms-block", type=int, default=256)
+    ap.add_argument("--ddlms-warmup", type=int, default=512)
+    ap.add_argument("--ddlms-mu-warm", type=float, default=2e-3)
     return ap.parse_args()
 
 
@@ -69,7 +69,7 @@ def k3_flops_per_symbol(L: int) -> float:
     return 8.0 * 9 * L + 40.0
 
 
-def kernel_units(chunk: int, L: int, eq_mode: str = "block_ls", ddlms_block: int = 1024, ddlms_warmup: int = 1024):
+def kernel_units(chunk: int, L: int, eq_mode: str = "block_ls", ddlms_block: int = 256, ddlms_warmup: int = 512):
     """Algorithmic flops and HBM bytes per launch of each kernel for one call of `chunk` samples."""
     K = (L - 1) // 2
     k1_samples = chunk + 2 * F

@@ -87,10 +87,10 @@ typedef struct kk_config {
    * static filter = RRC × CD inverse (the "offline-optimized filter"), then the 4-tap T/2-spaced widely-linear
    * DDLMS, restarted every ddlms_block symbols after ddlms_warmup warm-up symbols (global grid). */
   int32_t eq_mode;
-  int32_t ddlms_block;           /* 256 … 4096, power of two (kept symbols per restart)                  */
-  int32_t ddlms_warmup;          /* 0 … 3840, multiple of 64: warm-up symbols run from the centre spike  */
+  int32_t ddlms_block;           /* 256 … 4096, power of two (kept symbols per restart; default 256)     */
+  int32_t ddlms_warmup;          /* 0 … 3840, multiple of 64 (default 512): warm-up from the centre spike */
   int32_t reserved0;
-  double  ddlms_mu_warm;         /* 1e-3 step size during warm-up                           */
+  double  ddlms_mu_warm;         /* 2e-3 step size during warm-up                                        */
   double  ddlms_mu;              /* 2.5e-4 step size on kept symbols                                     */
 } kk_config;
 

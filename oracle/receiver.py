@@ -61,10 +61,10 @@ class OracleConfig:
     # paper arrangement: eq_mode "ddlms" folds the CD inverse
     # into the static filter and equalizes with the 4-tap T/2-spaced widely-linear DDLMS
     eq_mode: str = "block_ls"         # "block_ls" (north star, default) | "ddlms" (paper)
-    ddlms_mu_warm: float = 1e-3       # step size over the warm-up symbols (SPEC S:377 schedule start)
+    ddlms_mu_warm: float = 2e-3       # step size over the warm-up symbols
     ddlms_mu: float = 2.5e-4          # step size over the kept symbols (SPEC S:377 schedule end)
-    ddlms_block: int = 1024           # symbols kept per DDLMS restart (global grid)
-    ddlms_warmup: int = 1024          # symbols run before each block from the centre-spike state
+    ddlms_block: int = 256            # symbols kept per DDLMS restart (global grid)
+    ddlms_warmup: int = 512           # symbols run before each block from the centre-spike state
 
     @property
     def sps(self) -> int:

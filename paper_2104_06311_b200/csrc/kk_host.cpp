@@ -319,10 +319,10 @@ void kk_config_default(kk_config* c) {
   c->device = 0;
   c->keep_intermediate = 0;
   c->eq_mode = KK_EQ_BLOCK_LS;
-  c->ddlms_block = 1024;
-  c->ddlms_warmup = 1024;
+  c->ddlms_block = 256;
+  c->ddlms_warmup = 512;
   c->reserved0 = 0;
-  c->ddlms_mu_warm = 1e-3;
+  c->ddlms_mu_warm = 2e-3;
   c->ddlms_mu = 2.5e-4;
 }
 

@@ -20,8 +20,8 @@ class Receiver:
                  eq_taps: int = 0, widely_linear: bool = True, cpr_window: int = 256, eq_ridge: float = 1e-3,
                  input_float: bool = False, sideband: int = 1, lo_num: int = 129, lo_den: int = 1000,
                  clamp_rel: float = 1e-12, rolloff: float = 0.01, rrc_span_sym: int = 256,
-                 eq_mode: str = "block_ls", ddlms_block: int = 1024, ddlms_warmup: int = 1024,
-                 ddlms_mu_warm: float = 1e-3, ddlms_mu: float = 2.5e-4):
+                 eq_mode: str = "block_ls", ddlms_block: int = 256, ddlms_warmup: int = 512,
+                 ddlms_mu_warm: float = 2e-3, ddlms_mu: float = 2.5e-4):
         cfg = kkrx.kk_config_default()
         cfg.adc_scale, cfg.adc_offset, cfg.ref_intensity = adc_scale, adc_offset, ref_intensity
         cfg.dispersion_ps_per_nm = dispersion_ps_per_nm
