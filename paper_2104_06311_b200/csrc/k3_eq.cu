@@ -107,7 +107,7 @@ struct K3Layout {
   static constexpr int RED = US + kFrameSym * 8;   // warp partial sums; the solve's matrix aliases it
   static constexpr int MAT = RED;
   static constexpr int DRES = RED + (RED_B > MAT_B ? RED_B : MAT_B);
-  static constexpr int TH = DRES + NRED * 8;       // θ₁ as float2 [w(L), v(L)]
+  static constexpr int TH = DRES + (NRED > 128 ? NRED : 128) * 8;   // (dres doubles as the GJ pivot rows)
   static constexpr int ROT = TH + 2 * L * 8;       // 16 CPR rotations
   static constexpr int BAR = ROT + 16 * 8;         // mbarrier
   static constexpr int MISC = BAR + 16;
@@ -346,45 +346,59 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
       }
       __syncthreads();
       // ---- Gauss–Jordan on [G + λI | q1 q2] by the whole CTA with 2×2 pivot blocks (SPD ⇒ every leading
-      //      2×2 block is SPD, no pivoting; N = 4K + 2 is even): at step k every element (i, c), c ≥ k + 2,
-      //      reads its old value, A[i][k..k+1] and the pivot rows' column c, then all write together —
-      //      N/2 steps, two barriers each.
+      //      2×2 block is SPD, no pivoting; N = 4K + 2 is even). The matrix lives in registers: lane = column c,
+      //      warp w owns rows w, w+8, w+16, w+24. Per step the pivot columns arrive by warp shuffles and the two
+      //      pivot rows through a double-buffered shared row pair — one barrier per step, N/2 steps.
       {
         constexpr int W = Lay::WS;
         double* A = mat;
+        double* prow = dres;                          // 2 buffers × 2 rows × 32 columns (dres is consumed)
+        double a[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int i = warp + 8 * q;
+          a[q] = (i < N && lane < N + 2) ? A[i * W + lane] : 0.0;
+        }
         int fail = 0;
-        for (int k = 0; k < N; k += 2) {
-          const double pa = A[k * W + k], pb = A[k * W + k + 1];
-          const double pc = A[(k + 1) * W + k], pd = A[(k + 1) * W + k + 1];
+        for (int k = 0, par = 0; k < N; k += 2, par ^= 1) {
+          // owners of rows k, k+1 publish them (row k is row w = k % 8 of q = k / 8)
+          double* pr = prow + par * 64;
+          const int qk = k >> 3;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            if (q == qk && warp == (k & 7)) pr[lane] = a[q];
+            if (q == ((k + 1) >> 3) && warp == ((k + 1) & 7)) pr[32 + lane] = a[q];
+          }
+          // this warp's rows' pivot-column entries A[i][k], A[i][k+1]
+          double ck[4], ck1[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            ck[q] = __shfl_sync(0xffffffffu, a[q], k);
+            ck1[q] = __shfl_sync(0xffffffffu, a[q], k + 1);
+          }
+          __syncthreads();
+          const double pa = pr[k], pb = pr[k + 1], pc = pr[32 + k], pd = pr[32 + k + 1];
           const double det = pa * pd - pb * pc;
           fail |= !(pa > 0.0) || !(det > 0.0) || !isfinite(det);
           const double idet = 1.0 / det;
-          const int ncol = N - k;                     // columns k+2 .. N+1
-          constexpr int PER = (N * N + K3_THREADS - 1) / K3_THREADS;   // elements per thread at k = 0
-          double nv[PER];
-          int at[PER];
+          const double r0 = pr[lane], r1 = pr[32 + lane];
+          const double R0 = (pd * r0 - pb * r1) * idet, R1 = (pa * r1 - pc * r0) * idet;   // P⁻¹·[r0; r1]
+          if (lane >= k + 2) {                        // columns ≤ k+1 are never read again
 #pragma unroll
-          for (int q = 0; q < PER; ++q) {
-            const int e = tid + K3_THREADS * q;
-            at[q] = -1;
-            if (e < N * ncol) {
-              const int i = e / ncol, c = k + 2 + e % ncol;
-              const double r0 = A[k * W + c], r1 = A[(k + 1) * W + c];
-              const double R0 = (pd * r0 - pb * r1) * idet, R1 = (pa * r1 - pc * r0) * idet;   // P⁻¹·[r0; r1]
-              double v;
-              if (i == k) v = R0;
-              else if (i == k + 1) v = R1;
-              else v = fma(-A[i * W + k + 1], R1, fma(-A[i * W + k], R0, A[i * W + c]));
-              nv[q] = v;
-              at[q] = i * W + c;
+            for (int q = 0; q < 4; ++q) {
+              const int i = warp + 8 * q;
+              a[q] = (i == k) ? R0 : (i == k + 1) ? R1 : fma(-ck1[q], R1, fma(-ck[q], R0, a[q]));
             }
           }
-          __syncthreads();
-#pragma unroll
-          for (int q = 0; q < PER; ++q)
-            if (at[q] >= 0) A[at[q]] = nv[q];
-          __syncthreads();
         }
+        // solution columns N, N+1 back to shared memory (rows < N)
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int i = warp + 8 * q;
+          if (i < N && (lane == N || lane == N + 1)) A[i * W + lane] = a[q];
+        }
+        __syncthreads();
         // θ₁ from m1 = column N, m2 = column N+1 (rows e and L+e); fallback θ₀ on failure
         if (warp == 0) {
           if (lane < N) fail |= !isfinite(A[lane * W + N]) || !isfinite(A[lane * W + N + 1]);
