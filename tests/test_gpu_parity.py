@@ -222,3 +222,12 @@ def test_ddlms_mode_mixed_formats_and_chunking():
     orc = run_oracle(case)
     _check_all(case, whole, orc)
     assert np.array_equal(whole["dec"], chunked["dec"]) and np.array_equal(whole["z"], chunked["z"])
+
+
+@pytest.mark.parametrize("eq_mode", ["block_ls", "ddlms"])
+def test_lower_sideband(eq_mode):
+    """σ = −1: data below the tone — φ and the LO mirror (R2), CD referenced to −f_c."""
+    case = make_case(M=16, dl=112000.0, cspr=12.0, esn0=20.0, n=4 * F, seed=31, sideband=-1, eq_mode=eq_mode)
+    gpu, orc = run_gpu(case), run_oracle(case)
+    _check_all(case, gpu, orc)
+    assert sum(gpu["stats"]["sym_err"]) < 0.05 * sum(gpu["stats"]["sym"])   # it actually demodulates
