@@ -49,7 +49,7 @@ typedef enum {
   KK_ERR_STATE = -8     /* call out of order (e.g. intermediate not kept / no call yet)               */
 } kk_status;
 
-enum { KK_IN_INT16 = 0, KK_IN_FLOAT32 = 1 };                  /* input_dtype */
+enum { KK_IN_INT16 = 0, KK_IN_FLOAT32 = 1, KK_IN_UINT8 = 2 };  /* input_dtype */
 enum { KK_EQ_BLOCK_LS = 0, KK_EQ_DDLMS = 1 };                 /* eq_mode */
 enum { KK_STAGE_FIELD = 0, KK_STAGE_MF = 1, KK_STAGE_EQ = 2 }; /* kk_get_intermediate stages */
 
@@ -71,7 +71,7 @@ typedef struct kk_config {
   double  eq_ridge;              /* 1e-3: λ = ridge·tr(R)/(2L) (R10)                                     */
   double  dispersion_ps_per_nm;  /* accumulated D·L, e.g. 200000 for 10,000 km at 20 ps/nm/km          */
   double  lambda_m;              /* 1550.51e-9                                             */
-  int32_t input_dtype;           /* KK_IN_INT16 (ADC codes) | KK_IN_FLOAT32 (intensities, for tests)    */
+  int32_t input_dtype;           /* KK_IN_INT16 / KK_IN_UINT8 (ADC codes) | KK_IN_FLOAT32 (intensities) */
   float   adc_scale, adc_offset; /* I = adc_scale·(code − adc_offset)                                    */
   float   ref_intensity;         /* I_ref > 0; ε = clamp_rel·I_ref (R7)                                  */
   float   clamp_rel;             /* 1e-12                                                                */
@@ -127,7 +127,7 @@ kk_status kk_eq_taps(const kk_ctx* ctx, int32_t* taps);
 /* Process the core [first_sample, first_sample + n_samples) of the stream; asynchronous on `stream`.
  *   d_adc       device pointer to the CORE start (global sample first_sample); the range
  *               [d_adc − left, d_adc + n_samples + right) must be readable (kk_halo). int16 or float32
- *               per cfg.input_dtype; must be 16-byte aligned.
+ *               int16, uint8 or float32 per cfg.input_dtype; must be 16-byte aligned.
  *   first_sample global index, multiple of 16384 (frame grid), ≥ 0.
  *   n_samples   multiple of 16384, 16384 ≤ n_samples ≤ max_samples_per_call.
  *   d_ref       nullable device uint8[n_samples/4]: transmitted labels; if given, error counters update.
@@ -136,6 +136,14 @@ kk_status kk_eq_taps(const kk_ctx* ctx, int32_t* taps);
  * KK_ERR_CONFIG (n_samples too large), KK_ERR_CUDA (launch failure). */
 kk_status kk_process_frames(kk_ctx* ctx, const void* d_adc, int64_t first_sample, int64_t n_samples,
                             const uint8_t* d_ref, uint8_t* d_decisions, kk_stream_t stream);
+
+/* As kk_process_frames, plus per-frame error counts for binned Q traces ("Q-factors were
+ * estimated from BER in bins of 21 ms"): d_frame_errors (nullable device uint32[2·n/16384])
+ * receives, for local frame f of the call, [2f] = symbol errors and [2f+1] = bit errors (needs d_ref).
+ * The caller bins frames into ≈21 ms (5127-frame) bins and maps BER → Q with kk_q_from_ber. */
+kk_status kk_process_frames_ex(kk_ctx* ctx, const void* d_adc, int64_t first_sample, int64_t n_samples,
+                               const uint8_t* d_ref, uint8_t* d_decisions, uint32_t* d_frame_errors,
+                               kk_stream_t stream);
 
 /* End-to-end variant with HOST buffers (pinned recommended): copies [h_adc − left, h_adc + n + right)
  * host→device, runs kk_process_frames, copies decisions device→host, in chunks of ≤ max_samples_per_call

@@ -158,6 +158,7 @@ class LinkConfig:
     wander_rad: float = 0.0               # optional data-vs-tone phase wander amplitude (CPR fixtures)
     wander_hz: float = 50e3
     sideband: int = +1
+    adc_bits: int = 15                    # 15 → int16 codes 0..32767 (R20); ≤ 8 → uint8 codes (SPEC S:199's 8-bit ADC)
 
     @property
     def px(self) -> float:  # mean |x|^2 of the shaped data at 4 sps with unit-energy taps
@@ -178,8 +179,12 @@ class LinkConfig:
         return (self.amp + 6.0 * math.sqrt(self.px + self.sigma2)) ** 2
 
     @property
+    def adc_max(self) -> int:
+        return (1 << self.adc_bits) - 1
+
+    @property
     def adc_scale(self) -> float:
-        return self.i_clip / 32767.0
+        return self.i_clip / float(self.adc_max)
 
     @property
     def i_ref(self) -> float:  # expected mean intensity
@@ -258,7 +263,7 @@ def generate(cfg: LinkConfig, s0: int, s1: int, device="cpu", chunk: int = 1 << 
     With return_field=True also the noiseless transmitted field E (complex128).
     """
     device = torch.device(device)
-    codes = torch.empty(s1 - s0, dtype=torch.int16, device=device)
+    codes = torch.empty(s1 - s0, dtype=torch.uint8 if cfg.adc_bits <= 8 else torch.int16, device=device)
     fields = []
     if cfg.noise == "analytic" and cfg.sigma2 > 0:
         chunk = max(chunk, s1 - s0)   # analytic noise is a non-local filter: one chunk only
@@ -277,8 +282,8 @@ def generate(cfg: LinkConfig, s0: int, s1: int, device="cpu", chunk: int = 1 << 
                 nz = torch.fft.ifft(torch.where(keep, Nf, torch.zeros_like(Nf)))  # same PSD on f>0
             E = E + math.sqrt(cfg.sigma2) * nz
         inten = E.real * E.real + E.imag * E.imag
-        code = torch.clamp(torch.round(inten * (32767.0 / cfg.i_clip)), 0, 32767)
-        codes[c0 - s0: c1 - s0] = code.to(torch.int16)
+        code = torch.clamp(torch.round(inten * (cfg.adc_max / cfg.i_clip)), 0, cfg.adc_max)
+        codes[c0 - s0: c1 - s0] = code.to(codes.dtype)
     k = torch.arange(s0 // SPS, s1 // SPS, dtype=torch.int64, device=device)
     out = dict(codes=codes, labels=symbol_labels(cfg, k), adc_scale=cfg.adc_scale,
                adc_offset=0.0, i_ref=cfg.i_ref, amp=cfg.amp, px=cfg.px, sigma2=cfg.sigma2)

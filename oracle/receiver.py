@@ -338,6 +338,7 @@ def receive(codes: np.ndarray, first: int, n: int, cfg: OracleConfig, ref: Optio
     counts = dict(sym=np.zeros(5, np.int64), sym_err=np.zeros(5, np.int64), bits=np.zeros(5, np.int64),
                   bit_err=np.zeros(5, np.int64), clamped=int(clamped[H:H + n].sum()), frames=nfr,
                   dead_frames=0, bad_frames=0)
+    frame_err = np.zeros((nfr, 2), np.int64)           # per-frame (symbol, bit) errors (PAPER.md:112 bins)
     infos = []
     for fi in range(nfr):
         f = first // F + fi
@@ -369,11 +370,12 @@ def receive(codes: np.ndarray, first: int, n: int, cfg: OracleConfig, ref: Optio
         counts["bits"][bi] += Fs * (bi + 2)
         if ref is not None:
             r = np.asarray(ref[k0:k0 + Fs]).astype(np.int64)
-            counts["sym_err"][bi] += int(np.sum(lab != r))
-            counts["bit_err"][bi] += int(np.sum(popcount(lab ^ r)))
+            frame_err[fi] = (int(np.sum(lab != r)), int(np.sum(popcount(lab ^ r))))
+            counts["sym_err"][bi] += frame_err[fi, 0]
+            counts["bit_err"][bi] += frame_err[fi, 1]
         if keep:
             infos.append(info)
-    out = dict(z=z, dec=dec, counts=counts, A=A, K=K, L=L)
+    out = dict(z=z, dec=dec, counts=counts, A=A, K=K, L=L, frame_err=frame_err)
     if keep:
         out.update(E=E, E0=e0, y=y, m0=m0, a=a, phi=phi, b=b, frames=infos, w_cd=w_cd, h=h)
     return out

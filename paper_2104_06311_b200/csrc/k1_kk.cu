@@ -64,6 +64,10 @@ k1_kk_kernel(const Tin* __restrict__ adc0, float2* __restrict__ E, float2* __res
       const short* h = reinterpret_cast<const short*>(&raw);
 #pragma unroll
       for (int j = 0; j < 8; ++j) x[j] = fmaf((float)h[j], sc_in, off_in);
+    } else if constexpr (sizeof(Tin) == 1) {
+      const uint2 raw = reinterpret_cast<const uint2*>(stage)[gi];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) x[j] = fmaf((float)(((j < 4 ? raw.x : raw.y) >> (8 * (j & 3))) & 0xffu), sc_in, off_in);
     } else {
       const float4 r0 = reinterpret_cast<const float4*>(stage)[2 * gi];
       const float4 r1 = reinterpret_cast<const float4*>(stage)[2 * gi + 1];
@@ -150,10 +154,14 @@ k1_kk_kernel(const Tin* __restrict__ adc0, float2* __restrict__ E, float2* __res
   if (tid < 2 * K1_WARPS) clampcnt[cta * (2 * K1_WARPS) + tid] = cblk[tid];
 }
 
-void launch_k1(const void* adc_cta0, int input_float, int64_t n_pairs, float2* E, float2* part, int* clampcnt,
+void launch_k1(const void* adc_cta0, int input_dtype, int64_t n_pairs, float2* E, float2* part, int* clampcnt,
                const float2* tw1024, const K1Params& p, cudaStream_t s) {
   const int64_t grid = n_pairs / K1_WARPS;
-  if (input_float) {
+  if (input_dtype == 2) {   // KK_IN_UINT8
+    cudaFuncSetAttribute(k1_kk_kernel<uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K1_SMEM);
+    k1_kk_kernel<uint8_t><<<(unsigned)grid, K1_THREADS, K1_SMEM, s>>>(static_cast<const uint8_t*>(adc_cta0), E,
+                                                                       part, clampcnt, tw1024, p);
+  } else if (input_dtype == 1) {   // KK_IN_FLOAT32
     cudaFuncSetAttribute(k1_kk_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K1_SMEM);
     k1_kk_kernel<float><<<(unsigned)grid, K1_THREADS, K1_SMEM, s>>>(static_cast<const float*>(adc_cta0), E, part,
                                                                      clampcnt, tw1024, p);

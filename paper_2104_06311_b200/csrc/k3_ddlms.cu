@@ -122,6 +122,10 @@ k3_ddlms_kernel(const float2* __restrict__ y, int64_t y_base, int64_t sym_first,
   if (ref) {
     if (serr) atomicAdd(&counters[5 + bi], (unsigned long long)serr);
     if (berr) atomicAdd(&counters[15 + bi], (unsigned long long)berr);
+    if (p.frame_err) {
+      if (serr) atomicAdd(&p.frame_err[2 * fl], (unsigned)serr);
+      if (berr) atomicAdd(&p.frame_err[2 * fl + 1], (unsigned)berr);
+    }
   }
   atomicAdd(&counters[bi], (unsigned long long)B);
   atomicAdd(&counters[10 + bi], (unsigned long long)B * (bi + 2));

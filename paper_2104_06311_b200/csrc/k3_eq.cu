@@ -536,6 +536,7 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
         for (int w8 = 0; w8 < K3_WARPS; ++w8) { se += misc[8 + w8]; be += misc[16 + w8]; }
         if (se) atomicAdd(&counters[5 + bi], (unsigned long long)se);
         if (be) atomicAdd(&counters[15 + bi], (unsigned long long)be);
+        if (p.frame_err) { p.frame_err[2 * fl] = (unsigned)se; p.frame_err[2 * fl + 1] = (unsigned)be; }
       }
       atomicAdd(&counters[bi], (unsigned long long)kFrameSym);
       atomicAdd(&counters[10 + bi], (unsigned long long)kFrameSym * (bi + 2));

@@ -224,7 +224,7 @@ kk_status validate(const kk_config& c, std::string& why) {
   if (c.cpr_window != 256 && c.cpr_window != 512 && c.cpr_window != 1024 && c.cpr_window != 2048 && c.cpr_window != 4096)
     return bad("cpr_window must be one of 256,512,1024,2048,4096");
   if (!(c.eq_ridge >= 0)) return bad("eq_ridge must be >= 0");
-  if (c.input_dtype != KK_IN_INT16 && c.input_dtype != KK_IN_FLOAT32) return bad("input_dtype");
+  if (c.input_dtype != KK_IN_INT16 && c.input_dtype != KK_IN_FLOAT32 && c.input_dtype != KK_IN_UINT8) return bad("input_dtype");
   if (!(c.ref_intensity > 0) || !(c.clamp_rel > 0)) return bad("ref_intensity and clamp_rel must be > 0");
   if (c.max_samples_per_call < kk::kFrameSamp || c.max_samples_per_call % kk::kFrameSamp) return bad("max_samples_per_call must be a positive multiple of 16384");
   auto okM = [](int M) { return M == 4 || M == 8 || M == 16 || M == 32 || M == 64; };
@@ -481,6 +481,11 @@ kk_status kk_eq_taps(const kk_ctx* c, int32_t* taps) {
 
 kk_status kk_process_frames(kk_ctx* c, const void* d_adc, int64_t first, int64_t n, const uint8_t* d_ref,
                             uint8_t* d_dec, kk_stream_t stream) {
+  return kk_process_frames_ex(c, d_adc, first, n, d_ref, d_dec, nullptr, stream);
+}
+
+kk_status kk_process_frames_ex(kk_ctx* c, const void* d_adc, int64_t first, int64_t n, const uint8_t* d_ref,
+                               uint8_t* d_dec, uint32_t* d_ferr, kk_stream_t stream) {
   if (!c || !d_adc) return fail(c, KK_ERR_NULL, "kk_process_frames: NULL ctx or input");
   if (n < kk::kFrameSamp) return fail(c, KK_ERR_SHORT, "kk_process_frames: n_samples < one frame");
   if (first < 0 || first % kk::kFrameSamp || n % kk::kFrameSamp)
@@ -490,7 +495,7 @@ kk_status kk_process_frames(kk_ctx* c, const void* d_adc, int64_t first, int64_t
   DeviceGuard g(c->device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const kk_config& cf = c->cfg;
-  const size_t esz = cf.input_dtype == KK_IN_FLOAT32 ? 4 : 2;
+  const size_t esz = cf.input_dtype == KK_IN_FLOAT32 ? 4 : cf.input_dtype == KK_IN_UINT8 ? 1 : 2;
   const int F = kk::kFrameSamp;
 
   // K1 over blocks [ (first − F)/512, (first + n + F)/512 )
@@ -510,7 +515,7 @@ kk_status kk_process_frames(kk_ctx* c, const void* d_adc, int64_t first, int64_t
     for (auto& e : tev) e = take_event(c);
     cudaEventRecord(tev[0], s);
   }
-  kk::launch_k1(adc0, cf.input_dtype == KK_IN_FLOAT32, nblk / 2, c->d_E, c->d_part, c->d_clamp, c->d_tw1024, p1, s);
+  kk::launch_k1(adc0, cf.input_dtype, nblk / 2, c->d_E, c->d_part, c->d_clamp, c->d_tw1024, p1, s);
 
   // K2 over the MF tiles covering y[first/2 − K, (first + n)/2 + K)
   const int64_t y_first = first / 2 - c->Ky;
@@ -532,6 +537,7 @@ kk_status kk_process_frames(kk_ctx* c, const void* d_adc, int64_t first, int64_t
   p3.ridge = (float)cf.eq_ridge;
   p3.widely_linear = cf.eq_widely_linear;
   p3.cpr_window = cf.cpr_window;
+  p3.frame_err = d_ref ? d_ferr : nullptr;
   const int64_t nfr = n / F;
   if (c->ddlms) {
     kk::K3DParams pd;
@@ -541,6 +547,8 @@ kk_status kk_process_frames(kk_ctx* c, const void* d_adc, int64_t first, int64_t
     pd.mu_warm = (float)cf.ddlms_mu_warm;
     pd.mu = (float)cf.ddlms_mu;
     pd.widely_linear = cf.eq_widely_linear;
+    pd.frame_err = d_ref ? d_ferr : nullptr;
+    if (pd.frame_err) cudaMemsetAsync(pd.frame_err, 0, (size_t)(n / F) * 2 * sizeof(uint32_t), s);
     kk::launch_k3_ddlms(c->d_y, c->Ky, first / 4, n / 4 / cf.ddlms_block, cf.ddlms_block, cf.ddlms_warmup,
                         c->d_clamp, (int64_t)F / kk::kHilbertHop, d_ref, d_dec,
                         cf.keep_intermediate ? c->d_z : nullptr, c->d_counters, pd, s);
@@ -569,7 +577,7 @@ kk_status kk_process_frames_host(kk_ctx* c, const void* h_adc, int64_t first, in
   if (first < 0 || first % kk::kFrameSamp || n % kk::kFrameSamp)
     return fail(c, KK_ERR_ALIGN, "kk_process_frames_host: first_sample/n_samples not multiples of 16384");
   DeviceGuard g(c->device);
-  const size_t esz = c->cfg.input_dtype == KK_IN_FLOAT32 ? 4 : 2;
+  const size_t esz = c->cfg.input_dtype == KK_IN_FLOAT32 ? 4 : c->cfg.input_dtype == KK_IN_UINT8 ? 1 : 2;
   const int64_t H = kk::kHalo;
   cudaError_t e = cudaSuccess;
   auto chk = [&](cudaError_t r) { if (e == cudaSuccess) e = r; };

@@ -39,6 +39,7 @@ struct K3Params {
   float ridge;
   int widely_linear;
   int cpr_window;                    // symbols
+  unsigned* frame_err;               // nullable: [2f] symbol errors, [2f+1] bit errors per local frame
 };
 
 struct K3DParams {
@@ -47,10 +48,11 @@ struct K3DParams {
   int64_t segment_frames;
   float mu_warm, mu;
   int widely_linear;
+  unsigned* frame_err;               // nullable, zeroed by the host before the launch
 };
 
 // K1: KK front end + Hilbert + field; one warp per pair of 512-blocks, 8 warps per CTA.
-void launch_k1(const void* adc_cta0, int input_float, int64_t n_pairs, float2* E, float2* part, int* clampcnt,
+void launch_k1(const void* adc_cta0, int input_dtype, int64_t n_pairs, float2* E, float2* part, int* clampcnt,
                const float2* tw1024, const K1Params& p, cudaStream_t s);
 // K2: carrier removal + mixer + RRC MF + decimation by 2 on the global tile grid.
 void launch_k2(const float2* E, int64_t E_first, const float2* part, const int* clampcnt, int64_t jb0,

@@ -16,7 +16,7 @@ LIB_PATH = os.path.join(HERE, "libkkrx.so")
 
 KK_OK, KK_ERR_CONFIG, KK_ERR_ALIGN, KK_ERR_SHORT, KK_ERR_NULL = 0, -1, -2, -3, -4
 KK_ERR_NOMEM, KK_ERR_CUDA, KK_ERR_DOMAIN, KK_ERR_STATE = -5, -6, -7, -8
-KK_IN_INT16, KK_IN_FLOAT32 = 0, 1
+KK_IN_INT16, KK_IN_FLOAT32, KK_IN_UINT8 = 0, 1, 2
 KK_EQ_BLOCK_LS, KK_EQ_DDLMS = 0, 1
 KK_STAGE_FIELD, KK_STAGE_MF, KK_STAGE_EQ = 0, 1, 2
 KK_STATS_WORDS = 24
@@ -65,6 +65,8 @@ def _load():
         "kk_halo": (c_int, [c_void_p, POINTER(c_int64), POINTER(c_int64)]),
         "kk_eq_taps": (c_int, [c_void_p, POINTER(c_int32)]),
         "kk_process_frames": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_void_p, c_void_p]),
+        "kk_process_frames_ex": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_void_p, c_void_p,
+                                         c_void_p]),
         "kk_process_frames_host": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_void_p]),
         "kk_stats": (c_int, [c_void_p, POINTER(kk_stats_t)]),
         "kk_stats_device": (c_int, [c_void_p, c_void_p, c_void_p]),
@@ -125,6 +127,13 @@ def kk_process_frames(ctx, d_adc: int, first_sample: int, n_samples: int, d_ref:
                       stream: int = 0):
     _check(lib.kk_process_frames(ctx, c_void_p(d_adc), first_sample, n_samples, c_void_p(d_ref or None),
                                  c_void_p(d_decisions or None), c_void_p(stream or None)), "kk_process_frames", ctx)
+
+
+def kk_process_frames_ex(ctx, d_adc: int, first_sample: int, n_samples: int, d_ref: int = 0, d_decisions: int = 0,
+                         d_frame_errors: int = 0, stream: int = 0):
+    _check(lib.kk_process_frames_ex(ctx, c_void_p(d_adc), first_sample, n_samples, c_void_p(d_ref or None),
+                                    c_void_p(d_decisions or None), c_void_p(d_frame_errors or None),
+                                    c_void_p(stream or None)), "kk_process_frames_ex", ctx)
 
 
 def kk_process_frames_host(ctx, h_adc: int, first_sample: int, n_samples: int, h_ref: int = 0, h_decisions: int = 0):

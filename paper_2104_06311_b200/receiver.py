@@ -18,7 +18,7 @@ class Receiver:
                  dispersion_ps_per_nm: float = 0.0, formats: Sequence[int] = (4,), segment_frames: int = 1 << 30,
                  max_samples_per_call: int = 1 << 24, device: int = 0, keep_intermediate: bool = False,
                  eq_taps: int = 0, widely_linear: bool = True, cpr_window: int = 256, eq_ridge: float = 1e-3,
-                 input_float: bool = False, sideband: int = 1, lo_num: int = 129, lo_den: int = 1000,
+                 input_float: bool = False, input_uint8: bool = False, sideband: int = 1, lo_num: int = 129, lo_den: int = 1000,
                  clamp_rel: float = 1e-12, rolloff: float = 0.01, rrc_span_sym: int = 256,
                  eq_mode: str = "block_ls", ddlms_block: int = 256, ddlms_warmup: int = 512,
                  ddlms_mu_warm: float = 2e-3, ddlms_mu: float = 2.5e-4):
@@ -32,7 +32,8 @@ class Receiver:
         cfg.eq_widely_linear = int(widely_linear)
         cfg.cpr_window = cpr_window
         cfg.eq_ridge = eq_ridge
-        cfg.input_dtype = kkrx.KK_IN_FLOAT32 if input_float else kkrx.KK_IN_INT16
+        cfg.input_dtype = (kkrx.KK_IN_FLOAT32 if input_float else kkrx.KK_IN_UINT8 if input_uint8
+                           else kkrx.KK_IN_INT16)
         cfg.sideband, cfg.lo_num, cfg.lo_den = sideband, lo_num, lo_den
         cfg.clamp_rel, cfg.rolloff, cfg.rrc_span_sym = clamp_rel, rolloff, rrc_span_sym
         cfg.eq_mode = {"block_ls": kkrx.KK_EQ_BLOCK_LS, "ddlms": kkrx.KK_EQ_DDLMS}[eq_mode]
@@ -46,19 +47,29 @@ class Receiver:
         cfg.default_format = fm[0]
         self.cfg = cfg
         self.device = torch.device("cuda", device)
-        self.input_float = input_float
+        self.input_dtype = torch.float32 if input_float else torch.uint8 if input_uint8 else torch.int16
         self.ctx = kkrx.kk_init(cfg)
         self.halo = kkrx.kk_halo(self.ctx)[0]
         self.taps = kkrx.kk_eq_taps(self.ctx)
 
     # ------------------------------------------------------------------ processing
     def process(self, adc: torch.Tensor, first_sample: int, n_samples: int, ref: Optional[torch.Tensor] = None,
-                decisions: Optional[torch.Tensor] = None, offset: int = 0, stream: Optional[torch.cuda.Stream] = None):
+                decisions: Optional[torch.Tensor] = None, offset: int = 0, stream: Optional[torch.cuda.Stream] = None,
+                frame_errors: Optional[torch.Tensor] = None):
         """adc: device tensor; element `offset` is global sample first_sample − halo (so the core starts at
-        offset + halo). ref / decisions: device uint8 tensors of n_samples/4 labels (nullable)."""
-        assert adc.is_cuda and adc.dtype == (torch.float32 if self.input_float else torch.int16)
+        offset + halo). ref / decisions: device uint8 tensors of n_samples/4 labels (nullable).
+        frame_errors: optional device int32 tensor of 2·n_samples/16384 (symbol, bit errors per frame)."""
+        assert adc.is_cuda and adc.dtype == self.input_dtype
         core = adc.data_ptr() + (offset + self.halo) * adc.element_size()
         s = (stream or torch.cuda.current_stream(self.device)).cuda_stream
+        if frame_errors is not None:
+            assert frame_errors.is_cuda and frame_errors.dtype == torch.int32
+            assert frame_errors.numel() >= 2 * (n_samples // 16384)
+            kkrx.kk_process_frames_ex(self.ctx, core, first_sample, n_samples,
+                                      ref.data_ptr() if ref is not None else 0,
+                                      decisions.data_ptr() if decisions is not None else 0,
+                                      frame_errors.data_ptr(), s)
+            return
         kkrx.kk_process_frames(self.ctx, core, first_sample, n_samples,
                                ref.data_ptr() if ref is not None else 0,
                                decisions.data_ptr() if decisions is not None else 0, s)

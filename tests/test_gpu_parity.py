@@ -231,3 +231,44 @@ def test_lower_sideband(eq_mode):
     gpu, orc = run_gpu(case), run_oracle(case)
     _check_all(case, gpu, orc)
     assert sum(gpu["stats"]["sym_err"]) < 0.05 * sum(gpu["stats"]["sym"])   # it actually demodulates
+
+
+# ----------------------------------------------------------------------------- 8-bit ADC input, per-frame errors
+def test_uint8_adc_input():
+    case = make_case(M=16, dl=32000.0, cspr=12.0, esn0=18.0, n=4 * F, seed=41)
+    lc = kkgen_linkconfig(case, adc_bits=8)
+    assert case["codes"].dtype == torch.uint8 if False else True
+    import kkgen
+    from oracle import receiver as R
+    g = kkgen.generate(lc, case["first"] - HALO, case["first"] + case["n"] + HALO)
+    assert g["codes"].dtype == torch.uint8
+    case8 = dict(case, codes=g["codes"], ocfg=R.OracleConfig(dispersion_ps_per_nm=case["dl"], adc_scale=lc.adc_scale,
+                                                           ref_intensity=lc.i_ref, formats=case["formats"]))
+    from gpu_case import receiver_for
+    rx = receiver_for(case8, keep=True, input_uint8=True)
+    gpu, orc = run_gpu(case8, rx=rx), run_oracle(case8)
+    _check_all(case8, gpu, orc)
+
+
+def kkgen_linkconfig(case, **kw):
+    import dataclasses
+    return dataclasses.replace(case["lc"], **kw)
+
+
+@pytest.mark.parametrize("eq_mode", ["block_ls", "ddlms"])
+def test_per_frame_errors(eq_mode):
+    case = make_case(M=64, dl=32000.0, cspr=12.0, esn0=22.0, n=6 * F, seed=43, eq_mode=eq_mode)
+    from gpu_case import receiver_for
+    rx = receiver_for(case, keep=False)
+    codes, ref = case["codes"].cuda(), case["ref"].cuda()
+    fe = torch.full((2 * 6,), -1, dtype=torch.int32, device="cuda")
+    rx.process(codes, case["first"], case["n"], ref=ref, frame_errors=fe)
+    st = rx.stats()
+    fe = fe.cpu().numpy().reshape(-1, 2)
+    assert fe[:, 1].sum() == sum(st["bit_err"]) and fe[:, 0].sum() == sum(st["sym_err"])
+    orc = run_oracle(case, keep=False)
+    agree = np.abs(fe - orc["frame_err"]).sum()
+    assert agree <= max(2, 0.002 * orc["frame_err"].sum())
+    from paper_2104_06311_b200 import qtrace
+    bins = qtrace.bin_q(fe[:, 1], [4096 * 6] * 6, frames_per_bin=3)
+    assert len(bins) == 2 and all(b["q_db"] is not None for b in bins)
