@@ -235,24 +235,21 @@ def test_lower_sideband(eq_mode):
 
 # ----------------------------------------------------------------------------- 8-bit ADC input, per-frame errors
 def test_uint8_adc_input():
-    case = make_case(M=16, dl=32000.0, cspr=12.0, esn0=18.0, n=4 * F, seed=41)
-    lc = kkgen_linkconfig(case, adc_bits=8)
-    assert case["codes"].dtype == torch.uint8 if False else True
+    """8-bit ADC codes (SPEC S:199's ADC width; KK_IN_UINT8): same parity bar on the same codes."""
+    import dataclasses
+
     import kkgen
+    from gpu_case import receiver_for
     from oracle import receiver as R
+    case = make_case(M=16, dl=32000.0, cspr=12.0, esn0=18.0, n=4 * F, seed=41)
+    lc = dataclasses.replace(case["lc"], adc_bits=8)
     g = kkgen.generate(lc, case["first"] - HALO, case["first"] + case["n"] + HALO)
     assert g["codes"].dtype == torch.uint8
     case8 = dict(case, codes=g["codes"], ocfg=R.OracleConfig(dispersion_ps_per_nm=case["dl"], adc_scale=lc.adc_scale,
                                                            ref_intensity=lc.i_ref, formats=case["formats"]))
-    from gpu_case import receiver_for
     rx = receiver_for(case8, keep=True, input_uint8=True)
     gpu, orc = run_gpu(case8, rx=rx), run_oracle(case8)
     _check_all(case8, gpu, orc)
-
-
-def kkgen_linkconfig(case, **kw):
-    import dataclasses
-    return dataclasses.replace(case["lc"], **kw)
 
 
 @pytest.mark.parametrize("eq_mode", ["block_ls", "ddlms"])
