@@ -101,8 +101,6 @@ __device__ __forceinline__ float warp_sum(float v) {
 // ------------------------------------------------------------------ QAM slicer
 // Decision regions: per axis, a value exactly on a boundary goes to the lower level; the 32-cross
 // corner cells go to the nearer of the two adjacent points (ties to the lower label).
-struct Decision { float2 pt; int lab; };
-
 __device__ __forceinline__ int gray(int i) { return i ^ (i >> 1); }
 // level index of a PAM slicer with m levels at odd integers −(m−1)..(m−1), x in grid units
 __device__ __forceinline__ int pam_index(float x, int m) {
@@ -123,42 +121,6 @@ __device__ __forceinline__ int cross32_label(int iI, int iQ) {
 #pragma unroll
   for (int q = 1; q < 6; ++q) r = (iQ == q) ? rows[q] : r;
   return (int)((r >> (5 * iI)) & 31ull);
-}
-
-template <int M>
-__device__ __forceinline__ Decision slice(float2 z) {
-  Decision d;
-  if constexpr (M == 4 || M == 16 || M == 64) {
-    constexpr int m = M == 4 ? 2 : (M == 16 ? 4 : 8);
-    constexpr int hb = M == 4 ? 1 : (M == 16 ? 2 : 3);
-    constexpr float s = M == 4 ? 1.41421356237309505f : (M == 16 ? 3.16227766016837933f : 6.48074069840786023f);
-    int iI = pam_index(z.x * s, m), iQ = pam_index(z.y * s, m);
-    d.lab = (gray(iI) << hb) | gray(iQ);
-    d.pt = make_float2((float)(2 * iI - (m - 1)) * (1.0f / s), (float)(2 * iQ - (m - 1)) * (1.0f / s));
-  } else if constexpr (M == 8) {
-    constexpr float s = 2.44948974278317810f;   // √6
-    int iI = pam_index(z.x * s, 4), iQ = pam_index(z.y * s, 2);
-    d.lab = (gray(iI) << 1) | iQ;
-    d.pt = make_float2((float)(2 * iI - 3) * (1.0f / s), (float)(2 * iQ - 1) * (1.0f / s));
-  } else {  // 32-cross
-    constexpr float s = 4.47213595499957940f;   // √20
-    float xu = z.x * s, yu = z.y * s;
-    int iI = pam_index(xu, 6), iQ = pam_index(yu, 6);
-    if ((iI == 0 || iI == 5) && (iQ == 0 || iQ == 5)) {
-      float ax = fabsf(xu), ay = fabsf(yu);
-      int iI_a = iI, iQ_a = (iQ == 0) ? 1 : 4;     // (±5, ±3): keep I, move Q inward
-      int iI_b = (iI == 0) ? 1 : 4, iQ_b = iQ;     // (±3, ±5)
-      if (ax > ay) { iQ = iQ_a; }
-      else if (ay > ax) { iI = iI_b; }
-      else {
-        int la = cross32_label(iI_a, iQ_a), lb = cross32_label(iI_b, iQ_b);
-        if (la < lb) iQ = iQ_a; else iI = iI_b;
-      }
-    }
-    d.lab = cross32_label(iI, iQ);
-    d.pt = make_float2((float)(2 * iI - 5) * (1.0f / s), (float)(2 * iQ - 5) * (1.0f / s));
-  }
-  return d;
 }
 
 // runtime-uniform QAM slicer parameters (CTA-uniform: one format per frame, R26)
