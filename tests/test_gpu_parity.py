@@ -269,3 +269,17 @@ def test_per_frame_errors(eq_mode):
     from paper_2104_06311_b200 import qtrace
     bins = qtrace.bin_q(fe[:, 1], [4096 * 6] * 6, frames_per_bin=3)
     assert len(bins) == 2 and all(b["q_db"] is not None for b in bins)
+
+
+@pytest.mark.parametrize("cspr", [4.0, 8.0, 12.0, 16.0])
+def test_c2_cspr_sweep_q_parity(cspr):
+    """BASELINE configs[1] sweep axis: 16-QAM, 5600 km, OSNR 17 dB, CSPR swept (Q within 0.05 dB)."""
+    import kkgen
+    case = make_case(M=16, dl=112000.0, cspr=cspr, esn0=kkgen.esn0_from_osnr(17.0, cspr), n=1 << 20, seed=201)
+    gpu, orc = run_gpu(case, keep=False), run_oracle(case, keep=False)
+    assert np.mean(gpu["dec"] == orc["dec"]) >= 0.9999
+    bits = sum(gpu["stats"]["bits"])
+    qg = theory.q_from_ber(sum(gpu["stats"]["bit_err"]) / bits)
+    qo = theory.q_from_ber(int(orc["counts"]["bit_err"].sum()) / bits)
+    assert abs(qg - qo) <= 0.05, (qg, qo)
+    assert gpu["stats"]["clamped"] == orc["counts"]["clamped"]

@@ -495,3 +495,15 @@ def test_dd_awgn_q_vs_theory():
     c = out["counts"]
     ber = c["bit_err"].sum() / c["bits"].sum()
     assert abs(T.q_from_ber(ber) - T.q_from_ber(T.ber_awgn(16, 15.0))) <= 0.3
+
+
+def test_p14_q_vs_cspr_has_interior_maximum_at_fixed_osnr():
+    """at fixed OSNR the KK Q-factor is concave in CSPR with an interior optimum (low CSPR: the
+    minimum-phase condition fails; high CSPR: the tone takes the power, "we optimized CSPR")."""
+    qs = []
+    for cspr in (2.0, 7.0, 14.0):
+        esn0 = kkgen.esn0_from_osnr(17.0, cspr)
+        out, _, _, _ = _chain(16, dl=112000.0, cspr=cspr, esn0=esn0, n=1 << 17, seed=29)
+        c = out["counts"]
+        qs.append(T.q_from_ber(c["bit_err"].sum() / c["bits"].sum()))
+    assert qs[1] > qs[0] + 1.0 and qs[1] > qs[2] + 1.0, qs
