@@ -380,7 +380,11 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
           const double pa = pr[k], pb = pr[k + 1], pc = pr[32 + k], pd = pr[32 + k + 1];
           const double det = pa * pd - pb * pc;
           fail |= !(pa > 0.0) || !(det > 0.0) || !isfinite(det);
-          const double idet = 1.0 / det;
+          // 1/det: fp32 seed + two Newton steps (relative error ~1e-28 → full double precision; det is the
+          // determinant of an SPD 2×2 pivot block ≥ λ² ≫ FLT_MIN, so the seed is finite when det is)
+          double idet = (double)__frcp_rn((float)det);
+          idet = idet * fma(-det, idet, 2.0);
+          idet = idet * fma(-det, idet, 2.0);
           const double r0 = pr[lane], r1 = pr[32 + lane];
           const double R0 = (pd * r0 - pb * r1) * idet, R1 = (pa * r1 - pc * r0) * idet;   // P⁻¹·[r0; r1]
           if (lane >= k + 2) {                        // columns ≤ k+1 are never read again
