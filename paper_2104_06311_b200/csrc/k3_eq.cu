@@ -91,7 +91,7 @@ struct K3Layout {
   static constexpr int ND = 2 * K + 1;             // lags 0..2K for base i = −K (ρ = 0); 0..2K−1 for ρ = 1
   static constexpr int N = 2 * L;                  // real system size
   static constexpr int NP = 4 * L;                 // p floats: p1, p2 complex
-  static constexpr int RG = (K <= 4) ? ND : 5;     // lags per R sweep (register budget)
+  static constexpr int RG = (K <= 4) ? ND : 8;     // lags per R sweep (register budget)
   static constexpr int NRG = (ND + RG - 1) / RG;   // R sweeps
   static constexpr int NR = 8 * RG * NRG;          // S0,T0,S1,T1 per lag (padded to whole groups)
   static constexpr int NRED = ((NP + NR + 1 + 31) / 32) * 32;   // + frame power
