@@ -89,7 +89,7 @@ typedef struct kk_config {
   int32_t eq_mode;
   int32_t ddlms_block;           /* 256 … 4096, power of two (kept symbols per restart; default 256)     */
   int32_t ddlms_warmup;          /* 0 … 3840, multiple of 64 (default 512): warm-up from the centre spike */
-  int32_t reserved0;
+  int32_t debug_guard;           /* 1: surround every device scratch buffer with 64 KiB canaries (kk_check_guards) */
   double  ddlms_mu_warm;         /* 2e-3 step size during warm-up                                        */
   double  ddlms_mu;              /* 2.5e-4 step size on kept symbols                                     */
 } kk_config;
@@ -182,6 +182,15 @@ kk_status kk_q_from_ber(double ber, double* q_db);
 
 /* Free everything the context owns (synchronises its device first). NULL is a no-op. */
 void kk_destroy(kk_ctx* ctx);
+
+/* Debug aid (needs debug_guard = 1 at kk_init; a bounds check the library does on itself, since device
+ * sanitizers are not always available): synchronizes the context's device, then checks that the 64 KiB
+ * canary zones (byte 0xA5) before and after every scratch buffer — field E, ΣE partials, clamp counts, y,
+ * z, counters and the host-path staging buffers — are intact. KK_OK if they are (or debug_guard = 0 and
+ * nothing was checked: *n_checked = 0); KK_ERR_STATE if a kernel wrote out of bounds, with kk_last_error
+ * naming the buffer and the first corrupted byte offset. n_checked (may be NULL) receives the number of
+ * buffers checked. */
+kk_status kk_check_guards(kk_ctx* ctx, int32_t* n_checked);
 
 const char* kk_strerror(kk_status status);
 /* Last error message of the context, with (stage, frame) where known; "" if none. */

@@ -64,6 +64,9 @@ struct kk_ctx {
   bool last_z = false;
   cudaStream_t last_stream = nullptr;
   std::string err;
+  // debug_guard: canary-padded allocations {name, base, user bytes}
+  struct GuardRec { const char* name; unsigned char* base; size_t bytes; };
+  std::vector<GuardRec> guards;
   // per-kernel timing (kk_enable_timing)
   bool timing = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -202,6 +205,30 @@ std::vector<float2> twiddles(int N, int R, int Ns) {   // [r][k] = exp(−2πi r
   return t;
 }
 
+constexpr size_t kGuardBytes = 64 * 1024;
+constexpr unsigned char kGuardByte = 0xA5;
+
+// Scratch allocation; with cfg.debug_guard the buffer sits between two kGuardBytes canary zones.
+template <typename T>
+cudaError_t dalloc(kk_ctx* c, const char* name, T** dst, size_t bytes) {
+  if (!c->cfg.debug_guard) return cudaMalloc((void**)dst, bytes);
+  unsigned char* base = nullptr;
+  cudaError_t e = cudaMalloc((void**)&base, bytes + 2 * kGuardBytes);
+  if (e != cudaSuccess) return e;
+  e = cudaMemset(base, kGuardByte, bytes + 2 * kGuardBytes);
+  if (e != cudaSuccess) { cudaFree(base); return e; }
+  c->guards.push_back({name, base, bytes});
+  *dst = reinterpret_cast<T*>(base + kGuardBytes);
+  return cudaSuccess;
+}
+
+void dfree(kk_ctx* c, void* p) {
+  if (!p) return;
+  for (auto& g : c->guards)
+    if (g.base + kGuardBytes == p) { cudaFree(g.base); return; }
+  cudaFree(p);
+}
+
 template <typename T>
 cudaError_t upload(T** dst, const std::vector<T>& v) {
   cudaError_t e = cudaMalloc((void**)dst, v.size() * sizeof(T));
@@ -212,6 +239,7 @@ cudaError_t upload(T** dst, const std::vector<T>& v) {
 kk_status validate(const kk_config& c, std::string& why) {
   auto bad = [&](const char* m) { why = m; return KK_ERR_CONFIG; };
   if (!(c.fs_hz > 0) || !(c.baud_hz > 0) || std::fabs(c.fs_hz / c.baud_hz - 4.0) > 1e-9) return bad("fs/baud must be 4");
+  if (c.debug_guard != 0 && c.debug_guard != 1) return bad("debug_guard must be 0 or 1");
   if (c.lo_den <= 0 || c.lo_den > 4096 || c.lo_num < 0 || c.lo_num >= c.lo_den) return bad("lo_num/lo_den out of range");
   if (c.sideband != 1 && c.sideband != -1) return bad("sideband must be +1 or -1");
   if (!(c.rolloff > 0 && c.rolloff <= 1)) return bad("rolloff must be in (0,1]");
@@ -270,7 +298,8 @@ void free_all(kk_ctx* c) {
   void* ptrs[] = {c->d_H, c->d_Hc, c->d_lo, c->d_wcd, c->d_tw1024, c->d_tw256, c->d_tw4096, c->d_tw2048, c->d_sched,
                   c->d_E, c->d_part, c->d_clamp, c->d_y, c->d_z, c->d_counters,
                   c->d_in[0], c->d_in[1], c->d_ref[0], c->d_ref[1], c->d_dec[0], c->d_dec[1]};
-  for (void* p : ptrs) if (p) cudaFree(p);
+  for (void* p : ptrs) dfree(c, p);
+  c->guards.clear();
   for (auto& r : c->ev_pending) for (auto e : r) cudaEventDestroy(e);
   for (auto e : c->ev_pool) cudaEventDestroy(e);
   c->ev_pending.clear();
@@ -321,7 +350,7 @@ void kk_config_default(kk_config* c) {
   c->eq_mode = KK_EQ_BLOCK_LS;
   c->ddlms_block = 256;
   c->ddlms_warmup = 512;
-  c->reserved0 = 0;
+  c->debug_guard = 0;
   c->ddlms_mu_warm = 2e-3;
   c->ddlms_mu = 2.5e-4;
 }
@@ -443,12 +472,12 @@ kk_status kk_init(const kk_config* cfg, kk_ctx** out) {
   const int64_t n = cfg->max_samples_per_call;
   c->nmax = n;
   const int64_t nE = n + 2 * kk::kFrameSamp;
-  chk(cudaMalloc((void**)&c->d_E, (size_t)nE * sizeof(float2)));
-  chk(cudaMalloc((void**)&c->d_part, (size_t)(nE / kk::kHilbertHop) * sizeof(float2)));
-  chk(cudaMalloc((void**)&c->d_clamp, (size_t)(nE / kk::kHilbertHop) * sizeof(int)));
-  chk(cudaMalloc((void**)&c->d_y, (size_t)(n / 2 + 2 * c->Ky + 2) * sizeof(float2)));
-  if (cfg->keep_intermediate) chk(cudaMalloc((void**)&c->d_z, (size_t)(n / 4) * sizeof(float2)));
-  chk(cudaMalloc((void**)&c->d_counters, 32 * sizeof(unsigned long long)));
+  chk(dalloc(c, "E", &c->d_E, (size_t)nE * sizeof(float2)));
+  chk(dalloc(c, "part", &c->d_part, (size_t)(nE / kk::kHilbertHop) * sizeof(float2)));
+  chk(dalloc(c, "clamp", &c->d_clamp, (size_t)(nE / kk::kHilbertHop) * sizeof(int)));
+  chk(dalloc(c, "y", &c->d_y, (size_t)(n / 2 + 2 * c->Ky + 2) * sizeof(float2)));
+  if (cfg->keep_intermediate) chk(dalloc(c, "z", &c->d_z, (size_t)(n / 4) * sizeof(float2)));
+  chk(dalloc(c, "counters", &c->d_counters, 32 * sizeof(unsigned long long)));
   chk(cudaMemset(c->d_counters, 0, 32 * sizeof(unsigned long long)));
   if (e == cudaSuccess) {
     const size_t k3 = kk::k3_smem_bytes(c->K);
@@ -582,9 +611,9 @@ kk_status kk_process_frames_host(kk_ctx* c, const void* h_adc, int64_t first, in
   cudaError_t e = cudaSuccess;
   auto chk = [&](cudaError_t r) { if (e == cudaSuccess) e = r; };
   for (int i = 0; i < 2; ++i) {
-    if (!c->d_in[i]) chk(cudaMalloc(&c->d_in[i], (size_t)(c->nmax + 2 * H) * esz));
-    if (!c->d_ref[i]) chk(cudaMalloc((void**)&c->d_ref[i], (size_t)(c->nmax / 4)));
-    if (!c->d_dec[i]) chk(cudaMalloc((void**)&c->d_dec[i], (size_t)(c->nmax / 4)));
+    if (!c->d_in[i]) chk(dalloc(c, "host_in", &c->d_in[i], (size_t)(c->nmax + 2 * H) * esz));
+    if (!c->d_ref[i]) chk(dalloc(c, "host_ref", &c->d_ref[i], (size_t)(c->nmax / 4)));
+    if (!c->d_dec[i]) chk(dalloc(c, "host_dec", &c->d_dec[i], (size_t)(c->nmax / 4)));
     if (!c->hs[i]) chk(cudaStreamCreateWithFlags(&c->hs[i], cudaStreamNonBlocking));
     if (!c->ev[i]) chk(cudaEventCreateWithFlags(&c->ev[i], cudaEventDisableTiming));
   }
@@ -708,6 +737,35 @@ void kk_destroy(kk_ctx* c) {
     free_all(c);
   }
   delete c;
+}
+
+kk_status kk_check_guards(kk_ctx* c, int32_t* n_checked) {
+  if (!c) return KK_ERR_NULL;
+  if (n_checked) *n_checked = 0;
+  if (!c->cfg.debug_guard) return KK_OK;
+  DeviceGuard g(c->device);
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) return fail(c, KK_ERR_CUDA, std::string("kk_check_guards: ") + cudaGetErrorString(e));
+  std::vector<unsigned char> h(kGuardBytes);
+  int32_t n = 0;
+  for (const auto& r : c->guards) {
+    for (int side = 0; side < 2; ++side) {
+      const unsigned char* zone = side ? r.base + kGuardBytes + r.bytes : r.base;
+      e = cudaMemcpy(h.data(), zone, kGuardBytes, cudaMemcpyDeviceToHost);
+      if (e != cudaSuccess) return fail(c, KK_ERR_CUDA, std::string("kk_check_guards: ") + cudaGetErrorString(e));
+      for (size_t i = 0; i < kGuardBytes; ++i)
+        if (h[i] != kGuardByte) {
+          // offset of the corrupted byte relative to the buffer start (negative: before it)
+          const long long off = side ? (long long)(r.bytes + i) : (long long)i - (long long)kGuardBytes;
+          return fail(c, KK_ERR_STATE, std::string("kk_check_guards: out-of-bounds write into buffer '") + r.name +
+                                           "' at byte offset " + std::to_string(off) + " (size " +
+                                           std::to_string(r.bytes) + ")");
+        }
+    }
+    ++n;
+  }
+  if (n_checked) *n_checked = n;
+  return KK_OK;
 }
 
 const char* kk_strerror(kk_status s) {

@@ -36,7 +36,7 @@ class kk_config(ctypes.Structure):
         ("format_schedule", POINTER(c_uint8)), ("n_segments", c_int32), ("default_format", c_int32),
         ("segment_frames", c_int64), ("max_samples_per_call", c_int64), ("device", c_int32),
         ("keep_intermediate", c_int32),
-        ("eq_mode", c_int32), ("ddlms_block", c_int32), ("ddlms_warmup", c_int32), ("reserved0", c_int32),
+        ("eq_mode", c_int32), ("ddlms_block", c_int32), ("ddlms_warmup", c_int32), ("debug_guard", c_int32),
         ("ddlms_mu_warm", c_double), ("ddlms_mu", c_double),
     ]
 
@@ -76,6 +76,7 @@ def _load():
         "kk_enable_timing": (c_int, [c_void_p, c_int]),
         "kk_kernel_times": (c_int, [c_void_p, POINTER(c_double), POINTER(c_int64), c_int]),
         "kk_q_from_ber": (c_int, [c_double, POINTER(c_double)]),
+        "kk_check_guards": (c_int, [c_void_p, POINTER(c_int32)]),
         "kk_destroy": (None, [c_void_p]),
         "kk_strerror": (c_char_p, [c_int]),
         "kk_last_error": (c_char_p, [c_void_p]),
@@ -182,6 +183,13 @@ def kk_q_from_ber(ber: float) -> float:
     q = c_double()
     _check(lib.kk_q_from_ber(ber, ctypes.byref(q)), "kk_q_from_ber")
     return q.value
+
+
+def kk_check_guards(ctx) -> int:
+    """Number of canary-guarded buffers checked (0 unless debug_guard); raises KKError on a bounds violation."""
+    n = c_int32()
+    _check(lib.kk_check_guards(ctx, ctypes.byref(n)), "kk_check_guards", ctx)
+    return n.value
 
 
 def kk_destroy(ctx):

@@ -71,7 +71,8 @@ def test_q_from_ber_matches_oracle_theory():
 @pytest.mark.parametrize("field,value", [("cpr_window", 100), ("hilbert_n", 2048), ("fs_hz", 8e9),
                                          ("eq_taps", 4), ("eq_taps", 99), ("default_format", 128),
                                          ("max_samples_per_call", 1000), ("sideband", 0), ("lo_den", 0),
-                                         ("rrc_span_sym", 512), ("ref_intensity", 0.0)])
+                                         ("rrc_span_sym", 512), ("ref_intensity", 0.0),
+                                         ("debug_guard", 2)])
 def test_invalid_configs_rejected_before_any_cuda_call(field, value):
     c = P.kk_config_default()
     setattr(c, field, value)
@@ -86,6 +87,7 @@ def test_strerror_and_null_handling():
     assert P.kkrx.lib.kk_halo(None, None, None) == P.KK_ERR_NULL
     assert P.kkrx.lib.kk_stats(None, None) == P.KK_ERR_NULL
     assert P.kkrx.lib.kk_process_frames(None, None, 0, 16384, None, None, None) == P.KK_ERR_NULL
+    assert P.kkrx.lib.kk_check_guards(None, None) == P.KK_ERR_NULL
     P.kkrx.lib.kk_destroy(None)
 
 
