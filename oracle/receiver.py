@@ -16,6 +16,12 @@ carrier-phase recovery) and the readings R1–R27 of SURVEY.md §8(c) (DESIGN.md
   O10 decisions and error counts                             PAPER.md:82 "decisions ... are demapped"; PAPER.md:112
   O11 Q = 20·log10(√2·erfcinv(2·BER))                        PAPER.md:112; SPEC S:71 (theory.q_from_ber)
 
+  O3u (upsample = 2, SPEC S:277/S:375 upsample_factor — "KK in-principle benefits
+      from digital upsampling before the nonlinear sqrt/log"; DESIGN.md §3 "KK upsampling"): per Hilbert
+      block j, I is interpolated to 8 sps by the half-band filter f over the block's 2048-sample window,
+      O2–O4 run at 8 sps (2048-pt Hilbert, same time span as the 1024-pt one at 4 sps), and E at 4 sps is
+      the half-band decimation of the block's own 8-sps field.
+
 Library primitives used as single steps: numpy.fft (O3), scipy.signal.fftconvolve (O7),
 numpy.linalg.lstsq (CD-init fit), dense Φ̃ᴴΦ̃ and numpy.linalg.cholesky/solve (O8),
 brute-force nearest point (O8–O10).
@@ -65,6 +71,10 @@ class OracleConfig:
     ddlms_mu: float = 2.5e-4          # step size over the kept symbols (SPEC S:377 schedule end)
     ddlms_block: int = 256            # symbols kept per DDLMS restart (global grid)
     ddlms_warmup: int = 512           # symbols run before each block from the centre-spike state
+    # KK upsampling (O3u): 1 = the paper's 4-sps chain; 2 = interpolate I to 8 sps before sqrt/log
+    upsample: int = 1
+    halfband_t: int = 8               # odd half-band taps per side (f[±1], f[±3], …, f[±(2T−1)])
+    halfband_beta: float = 10.0       # Kaiser window β
 
     @property
     def sps(self) -> int:
@@ -159,6 +169,56 @@ def o3_hilbert_ols(a: np.ndarray, g0: int, out0: int, out1: int, cfg: OracleConf
         blk = np.fft.ifft(np.fft.fft(a[s:s + N]) * mult).real
         phi[hop * jb - out0: hop * jb - out0 + hop] = blk[lead:lead + hop]
     return cfg.sideband * phi
+
+
+def halfband_taps(cfg: OracleConfig):
+    """Half-band filter f[k], k = −(2T−1)…2T−1 at 8 sps (DESIGN.md §3 "KK upsampling"): f[0] = ½,
+    f[even ≠ 0] = 0, f[odd k] = ½·sinc(k/2)·kaiser_β(k), the odd taps rescaled to sum to ½ (unit DC gain).
+    Interpolation uses 2f on the odd phase, decimation uses f."""
+    T = cfg.halfband_t
+    k = np.arange(-(2 * T - 1), 2 * T)
+    f = 0.5 * np.sinc(k / 2.0) * np.kaiser(len(k), cfg.halfband_beta)
+    odd = (k % 2) != 0
+    f[~odd] = 0.0
+    f[odd] *= 0.5 / f[odd].sum()
+    f[k == 0] = 0.5
+    return k, f
+
+
+def o3u_field_upsampled(I: np.ndarray, g0: int, out0: int, out1: int, cfg: OracleConfig) -> np.ndarray:
+    """E[n] for global 4-sps n ∈ [out0, out1) with 2× KK upsampling, I over global [g0, g0 + len(I)).
+
+    For 4-sps Hilbert block j (outputs [512j, 512j + 512)) the 8-sps window is P ∈ [1024j − 512, 1024j + 1536):
+      I₂[P] = I[P/2] (P even);  I₂[P] = Σ_{k odd} 2f[k]·I[(P − k)/2] (P odd)          interpolation
+      a₂ = ½·ln max(I₂, ε);  φ₂ = σ·IFFT₂₀₄₈(FFT₂₀₄₈(a₂)·(−i·sgn q))  (q = 0, 1024 → 0)    O2, O3 at 8 sps
+      E₂ = √max(I₂, ε)·e^{iφ₂}                                                       O4 at 8 sps
+      E[n] = Σ_k f[k]·E₂[2n − k]   (E₂ of the block's own window)                     decimation
+    """
+    assert cfg.upsample == 2
+    N, hop = 2 * cfg.hilbert_n, 2 * cfg.hilbert_hop
+    lead = (N - hop) // 2
+    h4 = cfg.hilbert_hop
+    assert out0 % h4 == 0 and out1 % h4 == 0
+    eps = cfg.clamp_rel * cfg.ref_intensity
+    k, f = halfband_taps(cfg)
+    q = np.arange(N)
+    mult = np.where((q > 0) & (q < N // 2), -1j, np.where(q > N // 2, 1j, 0.0))
+    E = np.empty(out1 - out0, complex)
+    odd_taps = [(int(kt), float(ft)) for kt, ft in zip(k, f) if kt % 2 != 0]
+    for jb in range(out0 // h4, out1 // h4):
+        P = np.arange(hop * jb - lead, hop * jb - lead + N)          # 8-sps window positions
+        I2 = np.empty(N)
+        ev = (P % 2) == 0
+        I2[ev] = I[P[ev] // 2 - g0]
+        Po = P[~ev]
+        I2[~ev] = sum(2.0 * ft * I[(Po - kt) // 2 - g0] for kt, ft in odd_taps)
+        Ic = np.maximum(I2, eps)
+        a2 = 0.5 * np.log(Ic)
+        phi2 = cfg.sideband * np.fft.ifft(np.fft.fft(a2) * mult).real
+        E2 = np.sqrt(Ic) * np.exp(1j * phi2)
+        n = np.arange(h4 * jb, h4 * jb + h4)
+        E[n - out0] = 0.5 * E2[2 * n - P[0]] + sum(ft * E2[2 * n - kt - P[0]] for kt, ft in odd_taps)
+    return E
 
 
 def o5_carrier_removal(E: np.ndarray, e0: int, cfg: OracleConfig):
@@ -298,8 +358,13 @@ def o9_cpr(u: np.ndarray, M: int, W: int):
 # the whole chain over a shard
 # ------------------------------------------------------------------------------------------
 def halo(cfg: OracleConfig) -> int:
-    """Samples needed on each side of the core: one neighbour frame + half a Hilbert block."""
-    return cfg.frame_samples + (cfg.hilbert_n - cfg.hilbert_hop) // 2
+    """Samples needed on each side of the core: one neighbour frame + half a Hilbert block (+ 16 for the
+    half-band interpolator's reach when upsample = 2: T ≤ 16 4-sps samples, kept a multiple of 16)."""
+    h = cfg.frame_samples + (cfg.hilbert_n - cfg.hilbert_hop) // 2
+    if cfg.upsample == 2:
+        assert cfg.halfband_t <= 16
+        h += 16
+    return h
 
 
 def receive(codes: np.ndarray, first: int, n: int, cfg: OracleConfig, ref: Optional[np.ndarray] = None,
@@ -315,8 +380,13 @@ def receive(codes: np.ndarray, first: int, n: int, cfg: OracleConfig, ref: Optio
     a, amp, clamped = o2_front_end(I, cfg)
     # O3, O4 over core ± one frame
     e0, e1 = first - F, first + n + F
-    phi = o3_hilbert_ols(a, g0, e0, e1, cfg)
-    E = amp[e0 - g0:e1 - g0] * np.exp(1j * phi)
+    if cfg.upsample == 2:
+        phi = None
+        E = o3u_field_upsampled(I, g0, e0, e1, cfg)
+    else:
+        assert cfg.upsample == 1
+        phi = o3_hilbert_ols(a, g0, e0, e1, cfg)
+        E = amp[e0 - g0:e1 - g0] * np.exp(1j * phi)
     # O5, O6
     e, A = o5_carrier_removal(E, e0, cfg)
     b = o6_mixer(e, e0, cfg)

@@ -507,3 +507,93 @@ def test_p14_q_vs_cspr_has_interior_maximum_at_fixed_osnr():
         c = out["counts"]
         qs.append(T.q_from_ber(c["bit_err"].sum() / c["bits"].sum()))
     assert qs[1] > qs[0] + 1.0 and qs[1] > qs[2] + 1.0, qs
+
+
+# ------------------------------------------------------------------ PU: 2× KK upsampling
+def _hb_response(k, f, nu):
+    return (f[None, :] * np.exp(-2j * np.pi * nu[:, None] * k[None, :])).sum(axis=1)
+
+
+def test_pu_halfband_structure_and_response():
+    """Half-band taps (DESIGN.md §3 "KK upsampling"): f[0] = ½, even taps 0, symmetric, unit DC gain, and the
+    half-band identity H(ν) + H(ν + ½) = 1 (all frequencies, cycles/8-sps sample). Brute-force DTFT: passband
+    [0, 1.021 GHz] flat to 2e-5 (the KK signal band: tone + data edge), stopband [2.979, 4] GHz (the band that
+    folds onto the signal band) below −95 dB."""
+    k, f = R.halfband_taps(_cfg(upsample=2))
+    assert len(k) == 31 and f[k == 0][0] == 0.5
+    assert np.all(f[(k % 2 == 0) & (k != 0)] == 0) and np.allclose(f, f[::-1], atol=0, rtol=0)
+    assert abs(f.sum() - 1.0) < 1e-15
+    nu = np.linspace(0.0, 0.5, 4001)
+    Hh = _hb_response(k, f, nu)
+    assert np.max(np.abs(Hh.imag)) < 1e-15                            # zero phase (symmetric)
+    assert np.max(np.abs(Hh + _hb_response(k, f, nu + 0.5) - 1.0)) < 1e-14
+    pb, sb = nu <= 1.021 / 8, nu >= 2.979 / 8
+    assert np.max(np.abs(Hh[pb] - 1.0)) < 2e-5
+    assert 20 * np.log10(np.max(np.abs(Hh[sb]))) < -95
+
+
+def test_pu_constant_intensity_exact():
+    cfg = _cfg(upsample=2, ref_intensity=1.0)
+    H, F = R.halo(cfg), cfg.frame_samples
+    first, n = 2 * F, F
+    I = np.full(n + 2 * H, 2.25)
+    E = R.o3u_field_upsampled(I, first - H, first - F, first + n + F, cfg)
+    assert np.max(np.abs(E - 1.5)) < 1e-13
+
+
+@pytest.mark.parametrize("cspr_db", [60.0, 80.0])
+def test_pu_high_cspr_limit_within_filter_bound(cspr_db):
+    """As CSPR → ∞ KK becomes exact and E₂ = A + x is band-limited, so the upsampled path reproduces the
+    field up to the half-band passband deviation (≤ 2e-5 per filter, interpolation + decimation) — any
+    index, parity or sign slip in O3u breaks this by orders of magnitude."""
+    rng = np.random.default_rng(3)
+    N = 1024
+    q = np.arange(3, 262)
+    c = rng.standard_normal(len(q)) + 1j * rng.standard_normal(len(q))
+    cfg = _cfg(upsample=2, ref_intensity=1.0)
+    H, F = R.halo(cfg), cfg.frame_samples
+    n, first = F, 2 * F
+    g = np.arange(first - H, first + n + H)
+    x = (c[None, :] * np.exp(2j * np.pi * np.outer(g, q) / N)).sum(axis=1)
+    x /= np.sqrt(np.mean(np.abs(x) ** 2))
+    A = np.sqrt(10 ** (cspr_db / 10))
+    E = A + x
+    Erec = R.o3u_field_upsampled(np.abs(E) ** 2, first - H, first - F, first + n + F, cfg)
+    Et = E[H - F: H + n + F]
+    err = np.linalg.norm(Erec - Et) / np.linalg.norm(Et - A)
+    assert err < 5e-5, err
+
+
+def test_pu_upsampling_reduces_kk_aliasing():
+    """KK benefits from digital upsampling before the nonlinear sqrt/log. Noiseless 16-QAM at
+    CSPR 8 dB (strong aliasing of ln I at 4 sps): the in-band EVM after the whole chain improves by ≥ 10 dB
+    (measured 15.5 dB), with zero errors."""
+    ev = {}
+    for up in (1, 2):
+        out, _, _, _ = _chain(16, cspr=8.0, n=2 * 16384, seed=5, upsample=up)
+        ev[up] = _evm_db(out["z"], 16)
+        if up == 2:
+            assert out["counts"]["bit_err"].sum() == 0
+    assert ev[2] < ev[1] - 10, ev
+
+
+@pytest.mark.parametrize("M,dl,cspr", [(4, 200000.0, 10.0), (64, 32000.0, 12.0), (32, 0.0, 12.0)])
+def test_pu_noiseless_zero_errors(M, dl, cspr):
+    out, _, _, _ = _chain(M, dl=dl, cspr=cspr, n=16384, upsample=2)
+    c = out["counts"]
+    assert c["bit_err"].sum() == 0 and c["bad_frames"] == 0
+    assert _evm_db(out["z"], M) < -40
+
+
+def test_pu_shard_invariance():
+    lc = kkgen.LinkConfig(formats=(16,), dl_ps_nm=32000.0, cspr_db=8.0, esn0_db=18.0, seed=31)
+    cfg = _cfg(dispersion_ps_per_nm=32000.0, adc_scale=lc.adc_scale, ref_intensity=lc.i_ref, formats=(16,),
+               upsample=2)
+    F, H = cfg.frame_samples, R.halo(cfg)
+    first, n = 3 * F, 2 * F
+    g = kkgen.generate(lc, first - H, first + n + H)
+    codes = g["codes"].numpy()
+    whole = R.receive(codes, first, n, cfg, keep=False)
+    parts = [R.receive(codes[s * F: s * F + F + 2 * H], first + s * F, F, cfg, keep=False) for s in range(2)]
+    assert np.array_equal(np.concatenate([p["dec"] for p in parts]), whole["dec"])
+    assert np.max(np.abs(np.concatenate([p["z"] for p in parts]) - whole["z"])) < 1e-9
