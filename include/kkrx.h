@@ -92,6 +92,11 @@ typedef struct kk_config {
   int32_t debug_guard;           /* 1: surround every device scratch buffer with 64 KiB canaries (kk_check_guards) */
   double  ddlms_mu_warm;         /* 2e-3 step size during warm-up                                        */
   double  ddlms_mu;              /* 2.5e-4 step size on kept symbols                                     */
+  /* KK upsampling (SPEC S:277 upsample_factor; DESIGN.md §3 "KK upsampling"):
+   * 1 = the paper's chain (KK at the ADC rate); 2 = interpolate I to 8 sps with a 31-tap half-band filter,
+   * sqrt/log + 2048-point OLS Hilbert at 8 sps, half-band decimation back to 4 sps. Halo grows to 16,656. */
+  int32_t upsample;
+  int32_t reserved1;
 } kk_config;
 
 /* Counters (all uint64, summed over calls until kk_reset_stats; index i = log2(M) − 2 for M = 4..64).

@@ -18,7 +18,7 @@ BUILD = os.path.join(ROOT, "build")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include")]
-SOURCES = ["k1_kk.cu", "k2_mf.cu", "k3_eq.cu", "k3_ddlms.cu", "kk_host.cpp"]
+SOURCES = ["k1_kk.cu", "k1u_kk.cu", "k2_mf.cu", "k3_eq.cu", "k3_ddlms.cu", "kk_host.cpp"]
 
 
 def _newer(target: str, deps) -> bool:

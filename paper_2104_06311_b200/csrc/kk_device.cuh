@@ -48,6 +48,24 @@ __device__ __forceinline__ float2 unit_root(int e) {
   else { c = cos32q(32 - u); s = -cos32q(u - 24); }
   return make_float2(c, s);
 }
+// exp(2πi u/64) for u = 0..63 (K1U's 64-point radix-2 stage); folded to immediates after unroll.
+__device__ __forceinline__ float cos64q(int u) {   // cos(2πu/64), u = 0..16
+  const float q[17] = {1.0f, 0.99518472667219688624f, 0.98078528040323044913f, 0.95694033573220886494f,
+                       0.92387953251128675613f, 0.88192126434835502971f, 0.83146961230254523708f,
+                       0.77301045336273696081f, 0.70710678118654752440f, 0.63439328416364549822f,
+                       0.55557023301960222474f, 0.47139673682599764856f, 0.38268343236508977173f,
+                       0.29028467725446236764f, 0.19509032201612826785f, 0.09801714032956060199f, 0.0f};
+  return q[u];
+}
+__device__ __forceinline__ float2 unit_root64(int u) {
+  u &= 63;
+  float c, s;
+  if (u <= 16) { c = cos64q(u); s = cos64q(16 - u); }
+  else if (u <= 32) { c = -cos64q(32 - u); s = cos64q(u - 16); }
+  else if (u <= 48) { c = -cos64q(u - 32); s = -cos64q(48 - u); }
+  else { c = cos64q(64 - u); s = -cos64q(u - 48); }
+  return make_float2(c, s);
+}
 __host__ __device__ constexpr int ilog2c(int n) { return n <= 1 ? 0 : 1 + ilog2c(n >> 1); }
 // non-recursive so that it folds to a constant after loop unrolling (recursion would block inlining)
 __host__ __device__ __forceinline__ constexpr int bitrevc(int x, int bits) {

@@ -43,6 +43,9 @@ struct kk_ctx {
   float2* d_lo = nullptr;
   float2* d_wcd = nullptr;
   float2 *d_tw1024 = nullptr, *d_tw256 = nullptr, *d_tw4096 = nullptr, *d_tw2048 = nullptr;
+  float2* d_tw2048u = nullptr;   // K1U twiddles W₂₀₄₈^{l·k1}, [k1·32 + l]
+  int64_t halo = 0;              // kk_halo: kHalo, or kHaloUp with upsample = 2
+  double hb_odd[8] = {0};        // odd half-band taps f[1], f[3], …, f[15] (upsample = 2)
   uint8_t* d_sched = nullptr;
   // scratch
   int64_t nmax = 0;
@@ -236,10 +239,35 @@ cudaError_t upload(T** dst, const std::vector<T>& v) {
   return cudaMemcpy(*dst, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice);
 }
 
+// Odd taps of the 31-tap half-band filter (DESIGN.md §3 "KK upsampling"): f[k] = ½·sinc(k/2)·kaiser₁₀(k),
+// k = 2i − 1, rescaled so that Σ_{k odd} f[k] = ½ (unit DC gain). Kaiser: I0(β√(1 − (k/15)²)) / I0(β).
+void halfband_odd(double out[8]) {
+  constexpr double beta = 10.0;
+  auto i0 = [](double x) {
+    double sum = 1.0, term = 1.0;
+    for (int m = 1; m < 200; ++m) {
+      term *= (x / (2.0 * m)) * (x / (2.0 * m));
+      sum += term;
+      if (term < 1e-18 * sum) break;
+    }
+    return sum;
+  };
+  double acc = 0.0;
+  for (int i = 1; i <= 8; ++i) {
+    const double k = 2.0 * i - 1.0;
+    const double w = i0(beta * std::sqrt(1.0 - (k / 15.0) * (k / 15.0))) / i0(beta);
+    const double sinc = std::sin(kPi * k / 2.0) / (kPi * k / 2.0);
+    out[i - 1] = 0.5 * sinc * w;
+    acc += out[i - 1];
+  }
+  for (int i = 0; i < 8; ++i) out[i] *= 0.25 / acc;   // 2·Σ_i f = ½
+}
+
 kk_status validate(const kk_config& c, std::string& why) {
   auto bad = [&](const char* m) { why = m; return KK_ERR_CONFIG; };
   if (!(c.fs_hz > 0) || !(c.baud_hz > 0) || std::fabs(c.fs_hz / c.baud_hz - 4.0) > 1e-9) return bad("fs/baud must be 4");
   if (c.debug_guard != 0 && c.debug_guard != 1) return bad("debug_guard must be 0 or 1");
+  if (c.upsample != 1 && c.upsample != 2) return bad("upsample must be 1 or 2");
   if (c.lo_den <= 0 || c.lo_den > 4096 || c.lo_num < 0 || c.lo_num >= c.lo_den) return bad("lo_num/lo_den out of range");
   if (c.sideband != 1 && c.sideband != -1) return bad("sideband must be +1 or -1");
   if (!(c.rolloff > 0 && c.rolloff <= 1)) return bad("rolloff must be in (0,1]");
@@ -295,7 +323,7 @@ void resolve_timing(kk_ctx* c, size_t count) {
 }
 
 void free_all(kk_ctx* c) {
-  void* ptrs[] = {c->d_H, c->d_Hc, c->d_lo, c->d_wcd, c->d_tw1024, c->d_tw256, c->d_tw4096, c->d_tw2048, c->d_sched,
+  void* ptrs[] = {c->d_H, c->d_Hc, c->d_lo, c->d_wcd, c->d_tw1024, c->d_tw256, c->d_tw4096, c->d_tw2048, c->d_tw2048u, c->d_sched,
                   c->d_E, c->d_part, c->d_clamp, c->d_y, c->d_z, c->d_counters,
                   c->d_in[0], c->d_in[1], c->d_ref[0], c->d_ref[1], c->d_dec[0], c->d_dec[1]};
   for (void* p : ptrs) dfree(c, p);
@@ -353,6 +381,8 @@ void kk_config_default(kk_config* c) {
   c->debug_guard = 0;
   c->ddlms_mu_warm = 2e-3;
   c->ddlms_mu = 2.5e-4;
+  c->upsample = 1;
+  c->reserved1 = 0;
 }
 
 size_t kk_config_sizeof(void) { return sizeof(kk_config); }
@@ -379,6 +409,8 @@ kk_status kk_init(const kk_config* cfg, kk_ctx** out) {
   c->K = (L - 1) / 2;
   c->ddlms = ddlms;
   c->Ky = ddlms ? 2 * cfg->ddlms_warmup + 2 : c->K;
+  c->halo = cfg->upsample == 2 ? kk::kHaloUp : kk::kHalo;
+  if (cfg->upsample == 2) halfband_odd(c->hb_odd);
   if (cfg->format_schedule) {
     c->schedule.assign(cfg->format_schedule, cfg->format_schedule + cfg->n_segments);
   } else {
@@ -466,6 +498,15 @@ kk_status kk_init(const kk_config* cfg, kk_ctx** out) {
   chk(upload(&c->d_tw256, twiddles(256, 16, 16)));
   chk(upload(&c->d_tw4096, twiddles(4096, 16, 256)));
   chk(upload(&c->d_tw2048, twiddles(2048, 8, 256)));
+  if (cfg->upsample == 2) {
+    std::vector<float2> t(2048);
+    for (int k1 = 0; k1 < 64; ++k1)
+      for (int l = 0; l < 32; ++l) {
+        const double a = -2.0 * kPi * (double)(l * k1) / 2048.0;
+        t[(size_t)k1 * 32 + l] = make_float2((float)std::cos(a), (float)std::sin(a));
+      }
+    chk(upload(&c->d_tw2048u, t));
+  }
   chk(upload(&c->d_sched, c->schedule));
 
   // ---- scratch
@@ -497,8 +538,8 @@ kk_status kk_init(const kk_config* cfg, kk_ctx** out) {
 
 kk_status kk_halo(const kk_ctx* c, int64_t* left, int64_t* right) {
   if (!c || !left || !right) return KK_ERR_NULL;
-  *left = kk::kHalo;
-  *right = kk::kHalo;
+  *left = c->halo;
+  *right = c->halo;
   return KK_OK;
 }
 
@@ -538,13 +579,27 @@ kk_status kk_process_frames_ex(kk_ctx* c, const void* d_adc, int64_t first, int6
   p1.half_ln_iref = (float)(0.5 * std::log((double)cf.ref_intensity));
   p1.sideband = (float)cf.sideband;
   const char* adc0 = static_cast<const char*>(d_adc) - (int64_t)kk::kHalo * (int64_t)esz;
+  kk::K1UParams pu;
+  if (cf.upsample == 2) {
+    pu.adc_scale = p1.adc_scale;
+    pu.adc_offset = p1.adc_offset;
+    pu.inv_iref = p1.inv_iref;
+    pu.clamp_rel = p1.clamp_rel;
+    pu.half_ln_iref = p1.half_ln_iref;
+    pu.sideband = p1.sideband;
+    for (int i = 0; i < 8; ++i) { pu.c[i] = (float)c->hb_odd[i]; pu.c2[i] = (float)(2.0 * c->hb_odd[i]); }
+  }
   std::array<cudaEvent_t, 4> tev{};
   if (c->timing) {
     if (c->ev_pending.size() >= 512) resolve_timing(c, 256);
     for (auto& e : tev) e = take_event(c);
     cudaEventRecord(tev[0], s);
   }
-  kk::launch_k1(adc0, cf.input_dtype, nblk / 2, c->d_E, c->d_part, c->d_clamp, c->d_tw1024, p1, s);
+  if (cf.upsample == 2)
+    kk::launch_k1u(static_cast<const char*>(d_adc) - (int64_t)kk::kHaloUp * (int64_t)esz, cf.input_dtype, nblk,
+                   c->d_E, c->d_part, c->d_clamp, c->d_tw2048u, pu, s);
+  else
+    kk::launch_k1(adc0, cf.input_dtype, nblk / 2, c->d_E, c->d_part, c->d_clamp, c->d_tw1024, p1, s);
 
   // K2 over the MF tiles covering y[first/2 − K, (first + n)/2 + K)
   const int64_t y_first = first / 2 - c->Ky;
@@ -607,7 +662,7 @@ kk_status kk_process_frames_host(kk_ctx* c, const void* h_adc, int64_t first, in
     return fail(c, KK_ERR_ALIGN, "kk_process_frames_host: first_sample/n_samples not multiples of 16384");
   DeviceGuard g(c->device);
   const size_t esz = c->cfg.input_dtype == KK_IN_FLOAT32 ? 4 : c->cfg.input_dtype == KK_IN_UINT8 ? 1 : 2;
-  const int64_t H = kk::kHalo;
+  const int64_t H = c->halo;
   cudaError_t e = cudaSuccess;
   auto chk = [&](cudaError_t r) { if (e == cudaSuccess) e = r; };
   for (int i = 0; i < 2; ++i) {

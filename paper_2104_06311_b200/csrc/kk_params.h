@@ -17,6 +17,8 @@ constexpr int kMfLead = 512;         // input of tile t starts at 3072 t − 512
 constexpr int kMfKeep0 = 256;        // IFFT2048 outputs kept: [256, 1792)
 constexpr int kMfKeep = 1536;
 constexpr int kHalo = kFrameSamp + kHilbertLead;   // 16640
+constexpr int kK1uPad = kHilbertLead + 16;   // K1U staging lead: half window + half-band reach (16-B aligned)
+constexpr int kHaloUp = kFrameSamp + kK1uPad;  // 16656 (upsample = 2)
 constexpr int kMaxK = 7;             // L = 2K + 1 ≤ 15 (one real-system row per lane: 2L ≤ 32)
 constexpr int kNumCounters = 24;     // kk_stats_t layout
 
@@ -26,6 +28,16 @@ struct K1Params {
   float clamp_rel;                   // ε / I_ref
   float half_ln_iref;                // ½·ln I_ref
   float sideband;                    // ±1
+};
+
+struct K1UParams {                  // K1 + 2× upsampling (DESIGN.md §3 "KK upsampling")
+  float adc_scale, adc_offset;
+  float inv_iref;
+  float clamp_rel;
+  float half_ln_iref;
+  float sideband;
+  float c[8];                        // odd half-band taps f[1], f[3], …, f[15] (decimation)
+  float c2[8];                       // 2·c (interpolation)
 };
 
 struct K2Params {
@@ -54,6 +66,9 @@ struct K3DParams {
 // K1: KK front end + Hilbert + field; one warp per pair of 512-blocks, 8 warps per CTA.
 void launch_k1(const void* adc_cta0, int input_dtype, int64_t n_pairs, float2* E, float2* part, int* clampcnt,
                const float2* tw1024, const K1Params& p, cudaStream_t s);
+// K1U: K1 with 2× KK upsampling; one warp per pair of 512-blocks, 4 warps per CTA (n_blocks % 8 == 0).
+void launch_k1u(const void* adc_cta0, int input_dtype, int64_t n_blocks, float2* E, float2* part, int* clampcnt,
+                const float2* tw2048u, const K1UParams& p, cudaStream_t s);
 // K2: carrier removal + mixer + RRC MF + decimation by 2 on the global tile grid.
 void launch_k2(const float2* E, int64_t E_first, const float2* part, const int* clampcnt, int64_t jb0,
                int64_t tile0, int64_t n_tiles, float2* y, int64_t y_first, int64_t y_count, const float* Hs,

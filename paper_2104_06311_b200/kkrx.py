@@ -38,6 +38,7 @@ class kk_config(ctypes.Structure):
         ("keep_intermediate", c_int32),
         ("eq_mode", c_int32), ("ddlms_block", c_int32), ("ddlms_warmup", c_int32), ("debug_guard", c_int32),
         ("ddlms_mu_warm", c_double), ("ddlms_mu", c_double),
+        ("upsample", c_int32), ("reserved1", c_int32),
     ]
 
 

@@ -21,7 +21,8 @@ class Receiver:
                  input_float: bool = False, input_uint8: bool = False, sideband: int = 1, lo_num: int = 129, lo_den: int = 1000,
                  clamp_rel: float = 1e-12, rolloff: float = 0.01, rrc_span_sym: int = 256,
                  eq_mode: str = "block_ls", ddlms_block: int = 256, ddlms_warmup: int = 512,
-                 ddlms_mu_warm: float = 2e-3, ddlms_mu: float = 2.5e-4, debug_guard: bool = False):
+                 ddlms_mu_warm: float = 2e-3, ddlms_mu: float = 2.5e-4, debug_guard: bool = False,
+                 upsample: int = 1):
         cfg = kkrx.kk_config_default()
         cfg.adc_scale, cfg.adc_offset, cfg.ref_intensity = adc_scale, adc_offset, ref_intensity
         cfg.dispersion_ps_per_nm = dispersion_ps_per_nm
@@ -40,6 +41,7 @@ class Receiver:
         cfg.ddlms_block, cfg.ddlms_warmup = ddlms_block, ddlms_warmup
         cfg.ddlms_mu_warm, cfg.ddlms_mu = ddlms_mu_warm, ddlms_mu
         cfg.debug_guard = int(debug_guard)
+        cfg.upsample = upsample
         fm = list(formats)
         self._sched = (ctypes.c_uint8 * len(fm))(*fm)
         cfg.format_schedule = ctypes.cast(self._sched, ctypes.POINTER(ctypes.c_uint8))

@@ -19,12 +19,13 @@ def make_case(M=4, dl=0.0, cspr=12.0, esn0=None, n=1 << 16, first=2 * F, seed=7,
     formats = tuple(formats) if formats else (M,)
     lc = kkgen.LinkConfig(formats=formats, segment_frames=segment_frames, dl_ps_nm=dl, cspr_db=cspr,
                           esn0_db=esn0, seed=seed, noise=noise, wander_rad=wander_rad, sideband=sideband)
-    g = kkgen.generate(lc, first - HALO, first + n + HALO)
     ocfg = R.OracleConfig(dispersion_ps_per_nm=dl, adc_scale=lc.adc_scale, ref_intensity=lc.i_ref,
                           formats=formats, segment_frames=segment_frames, sideband=sideband, **ocfg_kw)
-    ref = g["labels"][HALO // 4:(HALO + n) // 4].clone()
+    H = R.halo(ocfg)                      # 16640, or 16656 with upsample = 2 (= kk_halo)
+    g = kkgen.generate(lc, first - H, first + n + H)
+    ref = g["labels"][H // 4:(H + n) // 4].clone()
     return dict(lc=lc, g=g, ocfg=ocfg, first=first, n=n, ref=ref, codes=g["codes"], formats=formats,
-                segment_frames=segment_frames, dl=dl)
+                segment_frames=segment_frames, dl=dl, halo=H)
 
 
 def run_oracle(case, keep=True):
@@ -40,7 +41,8 @@ def receiver_for(case, keep=True, max_samples=None, **kw):
                     max_samples_per_call=max_samples or max(case["n"], F), keep_intermediate=keep,
                     eq_taps=o.eq_taps, widely_linear=o.eq_widely_linear, cpr_window=o.cpr_window,
                     eq_mode=o.eq_mode, ddlms_block=o.ddlms_block, ddlms_warmup=o.ddlms_warmup,
-                    ddlms_mu_warm=o.ddlms_mu_warm, ddlms_mu=o.ddlms_mu, sideband=o.sideband, **kw)
+                    ddlms_mu_warm=o.ddlms_mu_warm, ddlms_mu=o.ddlms_mu, sideband=o.sideband, upsample=o.upsample,
+                    **kw)
 
 
 def run_gpu(case, keep=True, chunk=None, rx=None):

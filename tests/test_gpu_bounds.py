@@ -61,6 +61,9 @@ CASES = [
      dict(input_uint8=True), "uint8"),
     ("blockls_float_lsb", dict(M=64, dl=8000.0, esn0=28.0, sideband=-1), dict(input_float=True), "float"),
     ("ddlms", dict(M=16, dl=112000.0, esn0=18.0, eq_mode="ddlms"), {}, "int16"),
+    ("upsample2", dict(M=16, dl=32000.0, esn0=20.0, cspr=8.0, upsample=2), {}, "int16"),
+    ("upsample2_uint8_lsb", dict(M=64, dl=8000.0, esn0=26.0, sideband=-1, upsample=2), dict(input_uint8=True),
+     "uint8"),
     ("ddlms_warm0_blk4096", dict(M=4, dl=20000.0, esn0=12.0, eq_mode="ddlms", ddlms_block=4096, ddlms_warmup=0),
      {}, "int16"),
 ]
