@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--eq-mode", default="block_ls", choices=["block_ls", "ddlms"],
                     help="block_ls: north-star per-frame WL least squares + CPR (default); "
                          "ddlms: the paper's static CD filter + 4-tap WL DDLMS")
+    ap.add_argument("--upsample", type=int, default=1, choices=[1, 2],
+                    help="2: KK at 8 sps (half-band interpolation/decimation, K1U; DESIGN.md §3)")
     ap.add_argument("--ddlms-block", type=int, default=256)
     ap.add_argument("--ddlms-warmup", type=int, default=512)
     ap.add_argument("--ddlms-mu-warm", type=float, default=2e-3)
@@ -69,7 +71,8 @@ def k3_flops_per_symbol(L: int) -> float:
     return 8.0 * 9 * L + 40.0
 
 
-def kernel_units(chunk: int, L: int, eq_mode: str = "block_ls", ddlms_block: int = 256, ddlms_warmup: int = 512):
+def kernel_units(chunk: int, L: int, eq_mode: str = "block_ls", ddlms_block: int = 256, ddlms_warmup: int = 512,
+                 upsample: int = 1):
     """Algorithmic flops and HBM bytes per launch of each kernel for one call of `chunk` samples."""
     K = (L - 1) // 2
     k1_samples = chunk + 2 * F
@@ -84,8 +87,10 @@ def kernel_units(chunk: int, L: int, eq_mode: str = "block_ls", ddlms_block: int
     else:
         k3 = dict(flops=k3_flops_per_symbol(L) * 4096 * frames, bytes=73728.0 * frames)
         k2_flops = 403456.0
+    # K1U (upsample 2), per output sample: FFT2048 pair 220 + decimation 50 + interpolation 27 + E₂ 13 + logs 7
+    k1_flops = 317.0 if upsample == 2 else 107.0
     return {
-        "K1_kk": dict(flops=107.0 * k1_samples, bytes=10.0 * k1_samples),
+        ("K1u_kk" if upsample == 2 else "K1_kk"): dict(flops=k1_flops * k1_samples, bytes=10.0 * k1_samples),
         "K2_mf": dict(flops=k2_flops * n_tiles, bytes=36864.0 * n_tiles),
         "K3_eq": k3,
     }
@@ -183,10 +188,16 @@ def oracle_sample(runs, ocfg_kw, pool):
 
 def ocfg_kwargs(lc, eq_mode="block_ls", a=None):
     kw = dict(dispersion_ps_per_nm=lc.dl_ps_nm, adc_scale=lc.adc_scale, ref_intensity=lc.i_ref,
-              formats=tuple(lc.formats), segment_frames=lc.segment_frames, eq_mode=eq_mode)
+              formats=tuple(lc.formats), segment_frames=lc.segment_frames, eq_mode=eq_mode,
+              upsample=(a.upsample if a is not None else 1))
     if a is not None and eq_mode == "ddlms":
         kw.update(ddlms_block=a.ddlms_block, ddlms_warmup=a.ddlms_warmup, ddlms_mu_warm=a.ddlms_mu_warm)
     return kw
+
+
+def halo_of(a) -> int:
+    """kk_halo() of the configuration (the oracle's halo() is the same number)."""
+    return 16656 if a.upsample == 2 else 16640
 
 
 # ----------------------------------------------------------------------------------------------- reference arm
@@ -202,6 +213,7 @@ def run_reference(a, rank, world):
     frames_per_run = 4
     n_runs = cores
     S = a.samples_per_gpu
+    HALO = halo_of(a)
     # sample: n_runs runs of 4 frames spread over the rank-0 shard (generated on the CPU)
     runs = []
     stride = max(frames_per_run, (S // F) // n_runs)
@@ -258,13 +270,14 @@ def main():
     S = a.samples_per_gpu
     chunk = min(a.chunk, S)
     assert S % chunk == 0 and chunk % F == 0
-    my = SH.plan_weak(S, world)[rank]                   # weak scaling: rank r owns [r·S, (r+1)·S)
+    HALO = halo_of(a)
+    my = SH.plan_weak(S, world, halo=HALO)[rank]        # weak scaling: rank r owns [r·S, (r+1)·S)
     first = my.first
 
     t0 = time.perf_counter()
     g = kkgen.generate(lc, my.read_first, my.read_first + my.read_count, device=dev, chunk=1 << 24)
     codes = g["codes"]
-    ref = g["labels"][HALO // 4:(HALO + S) // 4]
+    ref = g["labels"][HALO // 4:(HALO + S) // 4].clone()   # own allocation: 16-B aligned (K3 TMA-stages ref)
     del g
     torch.cuda.synchronize()
     t_gen = time.perf_counter() - t0
@@ -272,7 +285,8 @@ def main():
     rx = Receiver(adc_scale=lc.adc_scale, ref_intensity=lc.i_ref, dispersion_ps_per_nm=lc.dl_ps_nm,
                   formats=lc.formats, segment_frames=lc.segment_frames, max_samples_per_call=chunk, device=local,
                   eq_mode=a.eq_mode, ddlms_block=a.ddlms_block, ddlms_warmup=a.ddlms_warmup,
-                  ddlms_mu_warm=a.ddlms_mu_warm)
+                  ddlms_mu_warm=a.ddlms_mu_warm, upsample=a.upsample)
+    assert rx.halo == HALO
     L = rx.taps
     dec = torch.empty(S // 4, dtype=torch.uint8, device=dev)
     counters = torch.zeros(kkrx.KK_STATS_WORDS, dtype=torch.int64, device=dev)
@@ -321,7 +335,7 @@ def main():
         peak_fp32 = N_SMS * FP32_LANES_PER_SM * 2 * float(mp.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12
     except Exception:
         pass
-    units = kernel_units(chunk, L, a.eq_mode, a.ddlms_block, a.ddlms_warmup)
+    units = kernel_units(chunk, L, a.eq_mode, a.ddlms_block, a.ddlms_warmup, a.upsample)
     traffic = {}
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
@@ -330,7 +344,7 @@ def main():
         except Exception:
             traffic = {}
     kernels = {}
-    for i, name in enumerate(("K1_kk", "K2_mf", "K3_eq")):
+    for i, name in enumerate(("K1u_kk" if a.upsample == 2 else "K1_kk", "K2_mf", "K3_eq")):
         avg_ms = kt_ms[i] / max(kt_n[i], 1)
         u = units[name]
         kernels[name] = {
@@ -419,6 +433,7 @@ def main():
             "config": {"workload": f"{a.workload}: continuous mixed 4/8/16/32/64-QAM stream (256-frame segments), "
                                    f"1 GBaud @ 4 GS/s, 1600 km (32000 ps/nm), CSPR 12 dB, Es/N0 26 dB white, int16 ADC",
                        "samples_per_gpu": S, "chunk_samples": chunk, "eq_taps": L, "eq_mode": a.eq_mode,
+                       "kk_upsample": a.upsample,
                        **({"ddlms_block": a.ddlms_block, "ddlms_warmup": a.ddlms_warmup,
                            "ddlms_mu_warm": a.ddlms_mu_warm} if a.eq_mode == "ddlms" else {}),
                        "l2": "inputs 8 GiB/GPU per step >> 126 MB L2, no flush needed", "seed": lc.seed},

@@ -17,8 +17,11 @@
 //   radix-2 stage + 2×DFT32 (= DFT64 over r of x[l + 32r], lane l)  → twiddle W₂₀₄₈^{l·k1}
 //   → transpose (smem, stride 33, even/odd k1 halves) → 2×DFT32 over l → X[k1 + 64k2]
 //   × (−i·sgn q) → the same steps inverted → lane l holds positions l + 32r, l + 1024 + 32r.
-// E₂ for the 1088 needed positions of one block goes to the warp's smem scratch, the decimation reads it
-// back (16 outputs per lane, coalesced 256-B stores), block 0 then block 1.
+// E₂ at the positions the decimation needs goes to the warp's smem scratch split into polyphase arrays
+// (even samples Ev, odd samples Od); each lane makes 4 adjacent outputs per step from one 20-sample Od
+// window (10 conflict-free 16-B loads, 16-B lane stride) and stores them with 16-B coalesced stores.
+// Occupancy: 255 registers (64 complex values per lane) and 90 KB smem → 2 CTAs = 8 warps per SM; the
+// next step is splitting each FFT2048 over two warps (≤ 128 registers) for 16 warps per SM.
 #include "kk_device.cuh"
 #include "kk_params.h"
 
@@ -199,44 +202,59 @@ k1u_kk_kernel(const Tin* __restrict__ adc0, float2* __restrict__ E, float2* __re
     vb[r] = csub(a, t);                             // window position lane + 1024 + 32r
   }
 
-  // ---- E₂ on [480, 1568) of each window → decimation → E, ΣE
+  // ---- E₂ on the window positions the decimation reads → polyphase smem arrays → E, ΣE.
+  // Ev[n] = E₂[2n + 512] (n ∈ [0, 512)), Od[m + 8] = E₂[2m + 513] (m ∈ [−8, 520)); then
+  // E[n] = ½·Ev[n] + Σ_{i=1..8} c_i·(Od[n + 8 − i] + Od[n + 7 + i])   — 16 consecutive Od per output.
   const float sc = p.sideband * (1.0f / 2048.0f);
   const int64_t blk0 = cta * K1U_BLOCKS + 2 * warp;   // 4-sps block index relative to jb0
+  float2* Ev = S;
+  float2* Od = S + 512;
+  auto put = [&](int pos, float ph, const float* wb) {
+    const bool odd = pos & 1;
+    const int idx = odd ? ((pos - 513) >> 1) + 8 : (pos - 512) >> 1;
+    if (odd ? (idx >= 0 && idx < 528) : (idx >= 0 && idx < 512)) {
+      float sn, cs;
+      __sincosf(ph * sc, &sn, &cs);
+      const float m = __expf(wb[pos] + p.half_ln_iref);
+      (odd ? Od : Ev)[idx] = make_float2(m * cs, m * sn);
+    }
+  };
 #pragma unroll
   for (int b = 0; b < 2; ++b) {
     const float* wb = b ? w1 : w0;
 #pragma unroll
-    for (int r = 15; r < 32; ++r) {                 // positions lane + 32r ∈ [480, 1024)
-      const int pos = lane + 32 * r;
-      float sn, cs;
-      __sincosf((b ? va[r].y : va[r].x) * sc, &sn, &cs);
-      const float m = __expf(wb[pos] + p.half_ln_iref);
-      S[pos - K1U_E2_0] = make_float2(m * cs, m * sn);
-    }
+    for (int r = 15; r < 32; ++r) put(lane + 32 * r, b ? va[r].y : va[r].x, wb);          // [480, 1024)
 #pragma unroll
-    for (int r = 0; r < 17; ++r) {                  // positions lane + 1024 + 32r ∈ [1024, 1568)
-      const int pos = lane + 1024 + 32 * r;
-      float sn, cs;
-      __sincosf((b ? vb[r].y : vb[r].x) * sc, &sn, &cs);
-      const float m = __expf(wb[pos] + p.half_ln_iref);
-      S[pos - K1U_E2_0] = make_float2(m * cs, m * sn);
-    }
+    for (int r = 0; r < 17; ++r) put(lane + 1024 + 32 * r, b ? vb[r].y : vb[r].x, wb);   // [1024, 1568)
     __syncwarp();
     float2* Eo = E + (blk0 + b) * kHilbertHop;
     float2 s = make_float2(0.f, 0.f);
-#pragma unroll 4
-    for (int i = 0; i < 16; ++i) {
-      const int n = lane + 32 * i;                  // output n ↔ window position 2n + 512
-      const float2* c = S + (2 * n + 512 - K1U_E2_0);
-      float2 acc = cscale(c[0], 0.5f);
+#pragma unroll 1
+    for (int i = 0; i < 4; ++i) {
+      const int n = 4 * lane + 128 * i;             // 4 adjacent outputs n … n+3 share Od[n … n+18]
+      float2 o[20];
 #pragma unroll
-      for (int t = 1; t <= 8; ++t) {
-        const float2 u = cadd(c[-(2 * t - 1)], c[2 * t - 1]);
-        acc.x = fmaf(p.c[t - 1], u.x, acc.x);
-        acc.y = fmaf(p.c[t - 1], u.y, acc.y);
+      for (int u = 0; u < 10; ++u) {
+        const float4 q = reinterpret_cast<const float4*>(Od + n)[u];
+        o[2 * u] = make_float2(q.x, q.y);
+        o[2 * u + 1] = make_float2(q.z, q.w);
       }
-      Eo[n] = acc;
-      s = cadd(s, acc);
+      const float4 e01 = reinterpret_cast<const float4*>(Ev + n)[0];
+      const float4 e23 = reinterpret_cast<const float4*>(Ev + n)[1];
+      float2 acc[4] = {make_float2(0.5f * e01.x, 0.5f * e01.y), make_float2(0.5f * e01.z, 0.5f * e01.w),
+                       make_float2(0.5f * e23.x, 0.5f * e23.y), make_float2(0.5f * e23.z, 0.5f * e23.w)};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+#pragma unroll
+        for (int t = 1; t <= 8; ++t) {
+          const float2 u = cadd(o[j + 8 - t], o[j + 7 + t]);
+          acc[j].x = fmaf(p.c[t - 1], u.x, acc[j].x);
+          acc[j].y = fmaf(p.c[t - 1], u.y, acc[j].y);
+        }
+      }
+      reinterpret_cast<float4*>(Eo + n)[0] = make_float4(acc[0].x, acc[0].y, acc[1].x, acc[1].y);
+      reinterpret_cast<float4*>(Eo + n)[1] = make_float4(acc[2].x, acc[2].y, acc[3].x, acc[3].y);
+      s = cadd(s, cadd(cadd(acc[0], acc[1]), cadd(acc[2], acc[3])));
     }
     s.x = warp_sum(s.x);
     s.y = warp_sum(s.y);

@@ -13,6 +13,7 @@ from typing import List
 
 FRAME_SAMPLES = 16384
 HALO = 16640            # kk_halo(): one neighbour frame + half a Hilbert block
+HALO_UP = 16656         # kk_halo() with upsample = 2 (+16 for the half-band interpolator)
 
 
 @dataclass(frozen=True)
@@ -20,21 +21,22 @@ class Shard:
     rank: int
     first: int          # global index of the first core sample (multiple of FRAME_SAMPLES)
     n: int              # core samples (multiple of FRAME_SAMPLES)
+    halo: int = HALO    # kk_halo() of the receiver configuration
 
     @property
     def read_first(self) -> int:   # first global sample the rank must hold
-        return self.first - HALO
+        return self.first - self.halo
 
     @property
     def read_count(self) -> int:
-        return self.n + 2 * HALO
+        return self.n + 2 * self.halo
 
     @property
     def frames(self) -> range:
         return range(self.first // FRAME_SAMPLES, (self.first + self.n) // FRAME_SAMPLES)
 
 
-def plan_strong(total_samples: int, world: int, stream_first: int = 0) -> List[Shard]:
+def plan_strong(total_samples: int, world: int, stream_first: int = 0, halo: int = HALO) -> List[Shard]:
     """Split one stream of `total_samples` into `world` contiguous frame ranges (sizes differ by ≤ 1 frame)."""
     assert total_samples % FRAME_SAMPLES == 0 and stream_first % FRAME_SAMPLES == 0 and world >= 1
     nf = total_samples // FRAME_SAMPLES
@@ -42,14 +44,14 @@ def plan_strong(total_samples: int, world: int, stream_first: int = 0) -> List[S
     for r in range(world):
         f0 = (r * nf) // world
         f1 = ((r + 1) * nf) // world
-        out.append(Shard(r, stream_first + f0 * FRAME_SAMPLES, (f1 - f0) * FRAME_SAMPLES))
+        out.append(Shard(r, stream_first + f0 * FRAME_SAMPLES, (f1 - f0) * FRAME_SAMPLES, halo))
     return out
 
 
-def plan_weak(samples_per_rank: int, world: int, stream_first: int = 0) -> List[Shard]:
+def plan_weak(samples_per_rank: int, world: int, stream_first: int = 0, halo: int = HALO) -> List[Shard]:
     """Each rank owns `samples_per_rank` consecutive samples of one global stream (fixed per-GPU work)."""
     assert samples_per_rank % FRAME_SAMPLES == 0 and stream_first % FRAME_SAMPLES == 0
-    return [Shard(r, stream_first + r * samples_per_rank, samples_per_rank) for r in range(world)]
+    return [Shard(r, stream_first + r * samples_per_rank, samples_per_rank, halo) for r in range(world)]
 
 
 def allreduce_counters(counters, group=None):

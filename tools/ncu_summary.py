@@ -57,7 +57,7 @@ def main(report, launches, out_md, traffic_json=None):
             rd = float(r[col["dram__bytes_read.sum"]].replace(",", ""))
             wr = float(r[col["dram__bytes_write.sum"]].replace(",", ""))
             scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(units[col["dram__bytes_read.sum"]], 1)
-            key = "K1_kk" if "k1_" in n else "K2_mf" if "k2_" in n else "K3_eq" if "k3_" in n else n
+            key = "K1u_kk" if "k1u_" in n else "K1_kk" if "k1_" in n else "K2_mf" if "k2_" in n else "K3_eq" if "k3_" in n else n
             traffic[key] = (rd + wr) * scale
         except (KeyError, ValueError):
             pass
