@@ -9,35 +9,41 @@
 // with c_i = f[2i−1] the odd half-band taps (host-computed in fp64) and E₂ taken from the block's own
 // window (positions [497, 1551) of it).
 //
-// Mapping: 4 warps per CTA, one warp per PAIR of blocks (two real windows packed as re/im of one
-// complex 2048-point FFT), CTA = 8 blocks = 4096 outputs. The CTA stages its 4640 ADC samples with one
-// TMA bulk copy, converts them to I/I_ref once (ADC clamp counts per block), interpolates and takes the
-// log for all 9216 window samples once (a₂ in shared memory, shared by overlapping windows), then each
-// warp runs the FFT2048 = 64 × 32 decomposition in registers:
-//   radix-2 stage + 2×DFT32 (= DFT64 over r of x[l + 32r], lane l)  → twiddle W₂₀₄₈^{l·k1}
-//   → transpose (smem, stride 33, even/odd k1 halves) → 2×DFT32 over l → X[k1 + 64k2]
-//   × (−i·sgn q) → the same steps inverted → lane l holds positions l + 32r, l + 1024 + 32r.
-// E₂ at the positions the decimation needs goes to the warp's smem scratch split into polyphase arrays
-// (even samples Ev, odd samples Od); each lane makes 4 adjacent outputs per step from one 20-sample Od
-// window (10 conflict-free 16-B loads, 16-B lane stride) and stores them with 16-B coalesced stores.
-// Occupancy: 255 registers (64 complex values per lane) and 90 KB smem → 2 CTAs = 8 warps per SM; the
-// next step is splitting each FFT2048 over two warps (≤ 128 registers) for 16 warps per SM.
+// Mapping: 8 warps per CTA = 4 groups of 64 threads; a group handles a PAIR of blocks (two real windows
+// packed as re/im of one complex 2048-point FFT), CTA = 8 blocks = 4096 outputs. The CTA stages its 4640
+// ADC samples with one TMA bulk copy, converts them to I/I_ref once (ADC clamp counts per block),
+// interpolates and takes the log for all 9216 window samples once (a₂ in shared memory, shared by the
+// overlapping windows); staging and I alias the FFT scratch. FFT2048 = 64 × 32 over the group, 32 values
+// per thread (128 registers → 2 CTAs = 16 warps per SM):
+//   thread t: DFT32 over r of x[t + 64r] → twiddle W₂₀₄₈^{t·k1} → transpose (stride 33; the half-warp
+//   picks the parity h of t, conflict-free) → thread (k1', h): DFT32 over s of Y'[2s + h][k1'] → radix-2
+//   combine with lane ^ 16 (P₀ ± W₆₄^{k2'}·P₁) → X[k1' + 32k2' + 1024h]; × (−i·sgn q); the inverse
+//   mirrors it (split with lane ^ 16, IDFT32, transpose, conj twiddle, IDFT32) → x[t + 64r].
+// E₂ at the positions the decimation needs goes to group scratch as even/odd polyphase arrays (both
+// blocks); each warp then decimates one block, 4 adjacent outputs per lane-step from one 20-sample odd
+// window (conflict-free 16-B loads) with 16-B coalesced stores.
 #include "kk_device.cuh"
 #include "kk_params.h"
 
 namespace kk {
 
-constexpr int K1U_WARPS = 4;
+constexpr int K1U_WARPS = 8;
 constexpr int K1U_THREADS = K1U_WARPS * 32;
-constexpr int K1U_BLOCKS = 2 * K1U_WARPS;            // 4-sps Hilbert blocks per CTA
+constexpr int K1U_GROUPS = K1U_WARPS / 2;            // FFT groups of 64 threads, one block pair each
+constexpr int K1U_BLOCKS = 2 * K1U_GROUPS;           // 4-sps Hilbert blocks per CTA (8)
 constexpr int K1U_OUT = K1U_BLOCKS * kHilbertHop;    // 4096 outputs per CTA
 constexpr int K1U_PAD = kK1uPad;                     // 272 staged samples before/after (256 + 16)
 constexpr int K1U_IN = K1U_OUT + 2 * K1U_PAD;        // 4640
 constexpr int K1U_UP = 2 * K1U_OUT + 1024;           // 9216 window samples at 8 sps
-constexpr int K1U_E2 = 1088;                         // E₂ positions kept per block: window [480, 1568)
-constexpr int K1U_E2_0 = 480;
-constexpr size_t K1U_SMEM = (size_t)K1U_UP * 4 + (size_t)K1U_IN * 4 + (size_t)K1U_WARPS * K1U_E2 * 8 + 16 +
-                            K1U_BLOCKS * 4;
+constexpr int K1U_GS = 64 * 33;                      // float2 scratch per group (transpose 64 × 33)
+constexpr int K1U_POLY = 1040;                       // Ev (512) + Od (528) per block
+constexpr size_t K1U_SMEM = (size_t)K1U_UP * 4 + (size_t)K1U_GROUPS * K1U_GS * 8 + 16 + K1U_BLOCKS * 4;
+static_assert(2 * K1U_POLY <= K1U_GS, "E2 polyphase arrays of a block pair fit the group scratch");
+static_assert((size_t)K1U_IN * 4 * 2 <= (size_t)K1U_GROUPS * K1U_GS * 8, "staging + I alias the scratch");
+
+__device__ __forceinline__ void group_sync(int id) {   // named barrier for the 64 threads of one group
+  asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory");
+}
 
 template <typename Tin>
 __global__ void __launch_bounds__(K1U_THREADS, 2)
@@ -45,15 +51,15 @@ k1u_kk_kernel(const Tin* __restrict__ adc0, float2* __restrict__ E, float2* __re
               int* __restrict__ clampcnt, const float2* __restrict__ tw, K1UParams p) {
   extern __shared__ __align__(128) unsigned char smem[];
   float* a2 = reinterpret_cast<float*>(smem);
-  float* Ib = a2 + K1U_UP;
-  float2* ws = reinterpret_cast<float2*>(Ib + K1U_IN);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(ws + K1U_WARPS * K1U_E2);
+  float2* ws = reinterpret_cast<float2*>(a2 + K1U_UP);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(ws + K1U_GROUPS * K1U_GS);
   int* cblk = reinterpret_cast<int*>(bar + 2);
+  Tin* stage = reinterpret_cast<Tin*>(ws);                                   // TMA landing zone
+  float* Ib = reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(ws) + K1U_IN * 4);   // I/I_ref
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t cta = blockIdx.x;
   const Tin* src = adc0 + cta * (int64_t)K1U_OUT;
-  Tin* stage = reinterpret_cast<Tin*>(ws);            // TMA landing zone (aliases the warp scratch)
   constexpr uint32_t bytes = (uint32_t)(K1U_IN * sizeof(Tin));
 
   if (tid == 0) mbar_init(bar, 1);
@@ -122,151 +128,129 @@ k1u_kk_kernel(const Tin* __restrict__ adc0, float2* __restrict__ E, float2* __re
   }
   __syncthreads();
 
-  // ---- FFT2048 pair per warp
-  float2* S = ws + warp * K1U_E2;
-  const float* w0 = a2 + (2 * warp) * 1024;          // window of block 2w (local 8-sps start)
+  // ---- FFT2048 pair per 64-thread group: x[t + 64r] (t = group thread, r < 32), 2048 = 64 × 32.
+  const int grp = warp >> 1, t = tid & 63, wg = warp & 1;
+  const int bid = 1 + grp;                          // named barrier id (0 = __syncthreads)
+  float2* S = ws + grp * K1U_GS;
+  const float* w0 = a2 + (2 * grp) * 1024;          // window of block 2·grp (local 8-sps start)
   const float* w1 = w0 + 1024;
-  float2 va[32], vb[32];
+  const int k1p = 16 * wg + (lane & 15), h = lane >> 4;   // role after the transpose: (k1', parity of t)
+  float2 v[32];
 #pragma unroll
-  for (int r = 0; r < 32; ++r) {
-    va[r] = make_float2(w0[lane + 32 * r], w1[lane + 32 * r]);
-    vb[r] = make_float2(w0[lane + 1024 + 32 * r], w1[lane + 1024 + 32 * r]);
+  for (int r = 0; r < 32; ++r) v[r] = make_float2(w0[t + 64 * r], w1[t + 64 * r]);
+  dft_reg<32, -1>(v);                               // Y[t][k1] = Σ_r x[t + 64r]·W₃₂^{r·k1}
+#pragma unroll
+  for (int k = 1; k < 32; ++k) v[k] = cmul(v[k], __ldg(&tw[k * 64 + t]));   // W₂₀₄₈^{t·k1}
+#pragma unroll
+  for (int k = 0; k < 32; ++k) S[t * 33 + k] = v[k];
+  group_sync(bid);
+#pragma unroll
+  for (int s2 = 0; s2 < 32; ++s2) v[s2] = S[(2 * s2 + h) * 33 + k1p];       // Y'[2s + h][k1']
+  dft_reg<32, -1>(v);                               // P_h[k2'] = Σ_s Y'[2s + h][k1']·W₃₂^{s·k2'}
+  // radix-2 combine with the partner (lane ^ 16): X[k1' + 32(k2' + 32h)] = P₀ ± W₆₄^{k2'}·P₁
+#pragma unroll
+  for (int k = 0; k < 32; ++k) {
+    const float2 o = make_float2(__shfl_xor_sync(0xffffffffu, v[k].x, 16), __shfl_xor_sync(0xffffffffu, v[k].y, 16));
+    float2 wv = unit_root64(k);
+    wv.y = -wv.y;                                   // e^{−2πi k/64}
+    const float2 a = h ? o : v[k], b = h ? v[k] : o;
+    const float2 tb = cmul(b, wv);
+    v[k] = h ? csub(a, tb) : cadd(a, tb);
   }
-  // DFT64 over r of x[lane + 32r] (DIF radix-2 stage, then DFT32 of each half): va[k] = Y[2k], vb[k] = Y[2k+1]
+  // −i·sgn(q), q = k1' + 32k2' + 1024h: h = 0 ⇒ 0 ≤ q < 1024, h = 1 ⇒ q ≥ 1024; q ∈ {0, 1024} → 0
 #pragma unroll
-  for (int i = 0; i < 32; ++i) {
-    const float2 a = va[i], b = vb[i];
-    va[i] = cadd(a, b);
-    float2 wv = unit_root64(i);
-    wv.y = -wv.y;                                   // W₆₄^{i} = e^{−2πi·i/64}
-    vb[i] = cmul(csub(a, b), wv);
+  for (int k = 0; k < 32; ++k) {
+    const float2 x = v[k];
+    v[k] = h ? make_float2(-x.y, x.x) : make_float2(x.y, -x.x);
   }
-  dft_reg<32, -1>(va);
-  dft_reg<32, -1>(vb);
-  // twiddle W₂₀₄₈^{l·k1}, table tw[k1·32 + l]
+  if (k1p == 0) v[0] = make_float2(0.f, 0.f);
+  // inverse: A_g[k2'] = (X₀ + (−1)^g X₁)·W₆₄^{−g·k2'}… (conj roots), g = h
 #pragma unroll
-  for (int k = 1; k < 32; ++k) va[k] = cmul(va[k], __ldg(&tw[(2 * k) * 32 + lane]));
+  for (int k = 0; k < 32; ++k) {
+    const float2 o = make_float2(__shfl_xor_sync(0xffffffffu, v[k].x, 16), __shfl_xor_sync(0xffffffffu, v[k].y, 16));
+    if (h) {
+      v[k] = cmul(csub(o, v[k]), unit_root64(k));  // (X₀ − X₁)·e^{+2πi k/64}
+    } else {
+      v[k] = cadd(v[k], o);                         // X₀ + X₁
+    }
+  }
+  dft_reg<32, +1>(v);                               // Z[k1'][2s + h], s = 0..31
+  group_sync(bid);                                  // every thread finished reading S (forward transpose)
 #pragma unroll
-  for (int k = 0; k < 32; ++k) vb[k] = cmul(vb[k], __ldg(&tw[(2 * k + 1) * 32 + lane]));
-  // transpose: lane m ← Y'[l][2m] (va[l]) and Y'[l][2m+1] (vb[l])
+  for (int s2 = 0; s2 < 32; ++s2) S[(2 * s2 + h) * 33 + k1p] = v[s2];
+  group_sync(bid);
 #pragma unroll
-  for (int k = 0; k < 32; ++k) S[lane * 33 + k] = va[k];
-  __syncwarp();
+  for (int k = 0; k < 32; ++k) v[k] = S[t * 33 + k];                          // Z[k1][t]
 #pragma unroll
-  for (int l = 0; l < 32; ++l) va[l] = S[l * 33 + lane];
-  __syncwarp();
-#pragma unroll
-  for (int k = 0; k < 32; ++k) S[lane * 33 + k] = vb[k];
-  __syncwarp();
-#pragma unroll
-  for (int l = 0; l < 32; ++l) vb[l] = S[l * 33 + lane];
-  __syncwarp();
-  dft_reg<32, -1>(va);                              // X[2m + 64k2], k2 = 0..31
-  dft_reg<32, -1>(vb);                              // X[2m + 1 + 64k2]
+  for (int k = 1; k < 32; ++k) v[k] = cmulc(v[k], __ldg(&tw[k * 64 + t]));  // W₂₀₄₈^{−t·k1}
+  dft_reg<32, +1>(v);                               // 2048·(φ₀ + iφ₁)[t + 64r]
+  group_sync(bid);                                  // S is reused for E₂ below
 
-  // −i·sgn(q), q = k1 + 64k2: k2 < 16 ⇒ 0 < q < 1024 (except q = 0); k2 ≥ 16 ⇒ q > 1024 (except 1024)
-#pragma unroll
-  for (int r = 0; r < 32; ++r) {
-    const float2 x = va[r], y = vb[r];
-    va[r] = (r < 16) ? make_float2(x.y, -x.x) : make_float2(-x.y, x.x);
-    vb[r] = (r < 16) ? make_float2(y.y, -y.x) : make_float2(-y.y, y.x);
-  }
-  if (lane == 0) { va[0] = make_float2(0.f, 0.f); va[16] = make_float2(0.f, 0.f); }
-
-  dft_reg<32, +1>(va);                              // Z[2m][l']
-  dft_reg<32, +1>(vb);                              // Z[2m+1][l']
-#pragma unroll
-  for (int k = 0; k < 32; ++k) S[lane * 33 + k] = va[k];
-  __syncwarp();
-#pragma unroll
-  for (int k = 0; k < 32; ++k) va[k] = S[k * 33 + lane];   // lane l': va[k] = Z[2k][l']
-  __syncwarp();
-#pragma unroll
-  for (int k = 0; k < 32; ++k) S[lane * 33 + k] = vb[k];
-  __syncwarp();
-#pragma unroll
-  for (int k = 0; k < 32; ++k) vb[k] = S[k * 33 + lane];   // vb[k] = Z[2k+1][l']
-  __syncwarp();
-#pragma unroll
-  for (int k = 1; k < 32; ++k) va[k] = cmulc(va[k], __ldg(&tw[(2 * k) * 32 + lane]));
-#pragma unroll
-  for (int k = 0; k < 32; ++k) vb[k] = cmulc(vb[k], __ldg(&tw[(2 * k + 1) * 32 + lane]));
-  // inverse DFT64 over k1 (DIT): A = IDFT32(even), B = IDFT32(odd); x[r] = A + W^{−r}… (conj roots)
-  dft_reg<32, +1>(va);
-  dft_reg<32, +1>(vb);
-#pragma unroll
-  for (int r = 0; r < 32; ++r) {
-    const float2 t = cmul(vb[r], unit_root64(r));   // e^{+2πi r/64}
-    const float2 a = va[r];
-    va[r] = cadd(a, t);                             // window position lane + 32r
-    vb[r] = csub(a, t);                             // window position lane + 1024 + 32r
-  }
-
-  // ---- E₂ on the window positions the decimation reads → polyphase smem arrays → E, ΣE.
+  // ---- E₂ at the window positions the decimation reads → polyphase arrays per block:
   // Ev[n] = E₂[2n + 512] (n ∈ [0, 512)), Od[m + 8] = E₂[2m + 513] (m ∈ [−8, 520)); then
-  // E[n] = ½·Ev[n] + Σ_{i=1..8} c_i·(Od[n + 8 − i] + Od[n + 7 + i])   — 16 consecutive Od per output.
+  // E[n] = ½·Ev[n] + Σ_{i=1..8} c_i·(Od[n + 8 − i] + Od[n + 7 + i]).
   const float sc = p.sideband * (1.0f / 2048.0f);
-  const int64_t blk0 = cta * K1U_BLOCKS + 2 * warp;   // 4-sps block index relative to jb0
-  float2* Ev = S;
-  float2* Od = S + 512;
-  auto put = [&](int pos, float ph, const float* wb) {
+  float2* poly0 = S;
+  float2* poly1 = S + K1U_POLY;
+#pragma unroll
+  for (int r = 7; r < 25; ++r) {
+    const int pos = t + 64 * r;                     // positions [448, 1600) ⊇ [497, 1551)
     const bool odd = pos & 1;
-    const int idx = odd ? ((pos - 513) >> 1) + 8 : (pos - 512) >> 1;
-    if (odd ? (idx >= 0 && idx < 528) : (idx >= 0 && idx < 512)) {
+    const int idx = odd ? 512 + ((pos - 513) >> 1) + 8 : (pos - 512) >> 1;
+    const bool need = odd ? (pos >= 497 && pos < 1552) : (pos >= 512 && pos < 1536);
+    if (need) {
       float sn, cs;
-      __sincosf(ph * sc, &sn, &cs);
-      const float m = __expf(wb[pos] + p.half_ln_iref);
-      (odd ? Od : Ev)[idx] = make_float2(m * cs, m * sn);
+      __sincosf(v[r].x * sc, &sn, &cs);
+      float m = __expf(w0[pos] + p.half_ln_iref);
+      poly0[idx] = make_float2(m * cs, m * sn);
+      __sincosf(v[r].y * sc, &sn, &cs);
+      m = __expf(w1[pos] + p.half_ln_iref);
+      poly1[idx] = make_float2(m * cs, m * sn);
     }
-  };
-#pragma unroll
-  for (int b = 0; b < 2; ++b) {
-    const float* wb = b ? w1 : w0;
-#pragma unroll
-    for (int r = 15; r < 32; ++r) put(lane + 32 * r, b ? va[r].y : va[r].x, wb);          // [480, 1024)
-#pragma unroll
-    for (int r = 0; r < 17; ++r) put(lane + 1024 + 32 * r, b ? vb[r].y : vb[r].x, wb);   // [1024, 1568)
-    __syncwarp();
-    float2* Eo = E + (blk0 + b) * kHilbertHop;
-    float2 s = make_float2(0.f, 0.f);
-#pragma unroll 1
-    for (int i = 0; i < 4; ++i) {
-      const int n = 4 * lane + 128 * i;             // 4 adjacent outputs n … n+3 share Od[n … n+18]
-      float2 o[20];
-#pragma unroll
-      for (int u = 0; u < 10; ++u) {
-        const float4 q = reinterpret_cast<const float4*>(Od + n)[u];
-        o[2 * u] = make_float2(q.x, q.y);
-        o[2 * u + 1] = make_float2(q.z, q.w);
-      }
-      const float4 e01 = reinterpret_cast<const float4*>(Ev + n)[0];
-      const float4 e23 = reinterpret_cast<const float4*>(Ev + n)[1];
-      float2 acc[4] = {make_float2(0.5f * e01.x, 0.5f * e01.y), make_float2(0.5f * e01.z, 0.5f * e01.w),
-                       make_float2(0.5f * e23.x, 0.5f * e23.y), make_float2(0.5f * e23.z, 0.5f * e23.w)};
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-#pragma unroll
-        for (int t = 1; t <= 8; ++t) {
-          const float2 u = cadd(o[j + 8 - t], o[j + 7 + t]);
-          acc[j].x = fmaf(p.c[t - 1], u.x, acc[j].x);
-          acc[j].y = fmaf(p.c[t - 1], u.y, acc[j].y);
-        }
-      }
-      reinterpret_cast<float4*>(Eo + n)[0] = make_float4(acc[0].x, acc[0].y, acc[1].x, acc[1].y);
-      reinterpret_cast<float4*>(Eo + n)[1] = make_float4(acc[2].x, acc[2].y, acc[3].x, acc[3].y);
-      s = cadd(s, cadd(cadd(acc[0], acc[1]), cadd(acc[2], acc[3])));
-    }
-    s.x = warp_sum(s.x);
-    s.y = warp_sum(s.y);
-    if (lane == 0) part[blk0 + b] = s;
-    __syncwarp();
   }
+  group_sync(bid);
+  // decimation: warp wg of the group makes the 512 outputs of block 2·grp + wg, 4 adjacent per lane-step
+  const float2* Ev = wg ? poly1 : poly0;
+  const float2* Od = Ev + 512;
+  const int64_t blk = cta * K1U_BLOCKS + 2 * grp + wg;   // 4-sps block index relative to jb0
+  float2* Eo = E + blk * kHilbertHop;
+  float2 s = make_float2(0.f, 0.f);
+#pragma unroll 1
+  for (int i = 0; i < 4; ++i) {
+    const int n = 4 * lane + 128 * i;               // outputs n … n+3 share Od[n … n+18]
+    float2 o[20];
+#pragma unroll
+    for (int u = 0; u < 10; ++u) {
+      const float4 q = reinterpret_cast<const float4*>(Od + n)[u];
+      o[2 * u] = make_float2(q.x, q.y);
+      o[2 * u + 1] = make_float2(q.z, q.w);
+    }
+    const float4 e01 = reinterpret_cast<const float4*>(Ev + n)[0];
+    const float4 e23 = reinterpret_cast<const float4*>(Ev + n)[1];
+    float2 acc[4] = {make_float2(0.5f * e01.x, 0.5f * e01.y), make_float2(0.5f * e01.z, 0.5f * e01.w),
+                     make_float2(0.5f * e23.x, 0.5f * e23.y), make_float2(0.5f * e23.z, 0.5f * e23.w)};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+#pragma unroll
+      for (int tt = 1; tt <= 8; ++tt) {
+        const float2 u = cadd(o[j + 8 - tt], o[j + 7 + tt]);
+        acc[j].x = fmaf(p.c[tt - 1], u.x, acc[j].x);
+        acc[j].y = fmaf(p.c[tt - 1], u.y, acc[j].y);
+      }
+    }
+    reinterpret_cast<float4*>(Eo + n)[0] = make_float4(acc[0].x, acc[0].y, acc[1].x, acc[1].y);
+    reinterpret_cast<float4*>(Eo + n)[1] = make_float4(acc[2].x, acc[2].y, acc[3].x, acc[3].y);
+    s = cadd(s, cadd(cadd(acc[0], acc[1]), cadd(acc[2], acc[3])));
+  }
+  s.x = warp_sum(s.x);
+  s.y = warp_sum(s.y);
+  if (lane == 0) part[blk] = s;
   if (tid < K1U_BLOCKS) clampcnt[cta * K1U_BLOCKS + tid] = cblk[tid];
 }
 
 void launch_k1u(const void* adc_cta0, int input_dtype, int64_t n_blocks, float2* E, float2* part, int* clampcnt,
                 const float2* tw2048u, const K1UParams& p, cudaStream_t s) {
-  const int64_t grid = n_blocks / K1U_BLOCKS;
+  const int64_t grid = n_blocks / K1U_BLOCKS;   // n_blocks % 8 == 0 (n is a multiple of 16384)
   if (input_dtype == 2) {   // KK_IN_UINT8
     cudaFuncSetAttribute(k1u_kk_kernel<uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K1U_SMEM);
     k1u_kk_kernel<uint8_t><<<(unsigned)grid, K1U_THREADS, K1U_SMEM, s>>>(static_cast<const uint8_t*>(adc_cta0), E,

@@ -43,7 +43,7 @@ struct kk_ctx {
   float2* d_lo = nullptr;
   float2* d_wcd = nullptr;
   float2 *d_tw1024 = nullptr, *d_tw256 = nullptr, *d_tw4096 = nullptr, *d_tw2048 = nullptr;
-  float2* d_tw2048u = nullptr;   // K1U twiddles W₂₀₄₈^{l·k1}, [k1·32 + l]
+  float2* d_tw2048u = nullptr;   // K1U twiddles W₂₀₄₈^{t·k1}, [k1·64 + t] (k1 < 32, t < 64)
   int64_t halo = 0;              // kk_halo: kHalo, or kHaloUp with upsample = 2
   double hb_odd[8] = {0};        // odd half-band taps f[1], f[3], …, f[15] (upsample = 2)
   uint8_t* d_sched = nullptr;
@@ -500,10 +500,10 @@ kk_status kk_init(const kk_config* cfg, kk_ctx** out) {
   chk(upload(&c->d_tw2048, twiddles(2048, 8, 256)));
   if (cfg->upsample == 2) {
     std::vector<float2> t(2048);
-    for (int k1 = 0; k1 < 64; ++k1)
-      for (int l = 0; l < 32; ++l) {
+    for (int k1 = 0; k1 < 32; ++k1)
+      for (int l = 0; l < 64; ++l) {
         const double a = -2.0 * kPi * (double)(l * k1) / 2048.0;
-        t[(size_t)k1 * 32 + l] = make_float2((float)std::cos(a), (float)std::sin(a));
+        t[(size_t)k1 * 64 + l] = make_float2((float)std::cos(a), (float)std::sin(a));
       }
     chk(upload(&c->d_tw2048u, t));
   }

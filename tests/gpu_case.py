@@ -81,3 +81,21 @@ def field_rel_err(gpu, orc):
     E_or = orc["E"]
     A = np.repeat(orc["A"], F)
     return rel(gpu["E"], E_or, E_or - A)
+
+
+def eq_check(z_gpu, z_or, tol=1e-4, flip_tol=2e-3, max_flip_frac=0.25, frame_symbols=4096):
+    """Equalizer-output parity per frame (DESIGN.md §3 "EQ tolerance and training-decision flips"): every
+    frame whose decision-directed training decisions agree is within `tol` relative RMS (global over those
+    frames); a pass-1 decision that fp32 and fp64 take differently at a slicer boundary moves that frame's
+    taps by O(|Δd|/N) ≈ 1.5e-4 per flip — such frames (error > tol) must be few (≤ max_flip_frac, at least
+    one allowed) and bounded by flip_tol. Returns (clean-frame error, flipped frames, worst frame)."""
+    zg = np.asarray(z_gpu).reshape(-1, frame_symbols)
+    zo = np.asarray(z_or).reshape(-1, frame_symbols)
+    fe = np.linalg.norm(zg - zo, axis=1) / np.maximum(np.linalg.norm(zo, axis=1), 1e-30)
+    clean = fe <= tol
+    n_flip = int(np.sum(~clean))
+    assert n_flip <= max(1, int(max_flip_frac * len(fe))), f"EQ: {n_flip}/{len(fe)} frames over {tol}: {fe}"
+    assert fe.max() <= flip_tol, f"EQ worst frame {fe.max():.3e} > {flip_tol}"
+    ce = rel(zg[clean], zo[clean]) if clean.any() else 0.0
+    assert ce <= tol, f"EQ rel err on clean frames {ce:.3e}"
+    return ce, n_flip, float(fe.max())
