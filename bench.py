@@ -54,6 +54,9 @@ def parse():
                          "ddlms: the paper's static CD filter + 4-tap WL DDLMS")
     ap.add_argument("--upsample", type=int, default=1, choices=[1, 2],
                     help="2: KK at 8 sps (half-band interpolation/decimation, K1U; DESIGN.md §3)")
+    ap.add_argument("--ingest", default="local", choices=["local", "single"],
+                    help="e2e input path: every rank reads its own shard from host memory (local), or rank 0 "
+                         "holds the whole stream and sends each rank its windows over NVLink (single; NEXT-3)")
     ap.add_argument("--ddlms-block", type=int, default=256)
     ap.add_argument("--ddlms-warmup", type=int, default=512)
     ap.add_argument("--ddlms-mu-warm", type=float, default=2e-3)
@@ -247,6 +250,54 @@ def run_reference(a, rank, world):
     return 0
 
 
+# ----------------------------------------------------------------------------------------------- single ingest
+def e2e_single_ingest(a, rx, lc, HALO, chunk, rank, world, dev, SH, kkrx, kkgen, torch, dist):
+    """e2e with ONE ingest point (paper_2104_06311_b200/ingest.py): rank 0 holds the whole
+    stream in pinned host memory (the ADC's DMA target), copies each rank's windows to the device and sends
+    them point-to-point (NCCL over NVLink); each rank runs kk_process_frames on what it receives. Timed per
+    step: distribution + processing + the D2H read of the counters; max over ranks."""
+    from paper_2104_06311_b200 import ingest
+    En = min(a.e2e_samples, 1 << 28, a.samples_per_gpu)
+    shards = SH.plan_weak(En, world, halo=HALO)
+    lo, hi = shards[0].read_first, shards[-1].read_first + shards[-1].read_count
+    host = None
+    if rank == 0:
+        g = kkgen.generate(lc, lo, hi, device=dev)
+        host = torch.empty(hi - lo, dtype=torch.int16, pin_memory=True)
+        host.copy_(g["codes"])
+        del g
+    me = shards[rank]
+    k = torch.arange(me.first // 4, (me.first + me.n) // 4, dtype=torch.int64, device=dev)
+    ref = kkgen.symbol_labels(lc, k)
+    dec = torch.empty(me.n // 4, dtype=torch.uint8, device=dev)
+
+    def process(w, f0, nc):
+        o = (f0 - me.first) // 4
+        rx.process(w, f0, nc, ref=ref[o:o + nc // 4], decisions=dec[o:o + nc // 4])
+
+    def one():
+        ingest.distribute(shards, chunk, process, host_stream=host, stream_first=lo, device=dev)
+        _ = rx.stats()
+
+    one()                                                   # warm-up (allocations, NCCL P2P setup)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t = []
+    for _ in range(max(1, a.steps)):
+        t1 = time.perf_counter()
+        one()
+        t.append(time.perf_counter() - t1)
+    te = SH.max_over_ranks(sum(t), device=dev)
+    n_chunks = (En + chunk - 1) // chunk
+    return {"value": En * world * len(t) / te / 1e9, "unit": "GS/s",
+            "h2d_bytes_per_step": int(world * (En + 2 * HALO * n_chunks) * 2) if rank == 0 else 0,
+            "d2h_bytes_per_step": int(8 * kkrx.KK_STATS_WORDS),
+            "nvlink_bytes_per_step": int((world - 1) * (En + 2 * HALO * n_chunks) * 2),
+            "samples_per_gpu": En, "ingest": "single (rank 0 -> all, ingest.distribute)",
+            "api": "kk_process_frames on received windows"}
+
+
 # ----------------------------------------------------------------------------------------------- GPU arm
 def main():
     a = parse()
@@ -363,7 +414,9 @@ def main():
 
     # ---------------- end to end through the host-buffer C-ABI call (pinned memory, copies inside)
     e2e = None
-    if not a.no_e2e:
+    if not a.no_e2e and a.ingest == "single":
+        e2e = e2e_single_ingest(a, rx, lc, HALO, chunk, rank, world, dev, SH, kkrx, kkgen, torch, dist)
+    elif not a.no_e2e:
         En = min(a.e2e_samples, S)
         h_codes = torch.empty(En + 2 * HALO, dtype=torch.int16, pin_memory=True)
         h_codes.copy_(codes[:En + 2 * HALO])

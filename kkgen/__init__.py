@@ -255,35 +255,51 @@ def _data_field(cfg: LinkConfig, s0: int, s1: int, device, guard_sym: int = 1024
     return x * torch.exp(1j * ph)
 
 
-def generate(cfg: LinkConfig, s0: int, s1: int, device="cpu", chunk: int = 1 << 24,
+GEN_GRID = 1 << 18        # samples per generation chunk on the CPU, anchored at global sample 0
+GEN_GRID_CUDA = 1 << 22   # on a GPU (fewer launches; invariance holds per device type)
+
+
+def gen_grid(device) -> int:
+    return GEN_GRID_CUDA if torch.device(device).type == "cuda" else GEN_GRID
+
+
+def generate(cfg: LinkConfig, s0: int, s1: int, device="cpu", chunk: int = GEN_GRID,
              return_field: bool = False):
     """int16 ADC codes for global samples [s0, s1) and labels for symbols [s0/4, s1/4).
 
+    The field is built chunk by chunk on a fixed global grid (chunks [k·G, (k+1)·G), G = gen_grid(device),
+    each with the same guard and FFT length), so any sub-range — another chunking, another rank's window —
+    yields bit-identical codes on the same device type. (`chunk` is accepted for compatibility and ignored; analytic
+    noise, a non-local filter used only for calibration, is generated over [s0, s1) in one piece.)
     Returns dict(codes=int16[s1-s0], labels=uint8[(s1-s0)/4], and the sidecar numbers).
     With return_field=True also the noiseless transmitted field E (complex128).
     """
     device = torch.device(device)
     codes = torch.empty(s1 - s0, dtype=torch.uint8 if cfg.adc_bits <= 8 else torch.int16, device=device)
     fields = []
-    if cfg.noise == "analytic" and cfg.sigma2 > 0:
-        chunk = max(chunk, s1 - s0)   # analytic noise is a non-local filter: one chunk only
-    for c0 in range(s0, s1, chunk):
-        c1 = min(s1, c0 + chunk)
+    analytic = cfg.noise == "analytic" and cfg.sigma2 > 0
+    G = gen_grid(device)
+    pieces = [(s0, s1)] if analytic else [(c0, c0 + G) for c0 in range((s0 // G) * G, s1, G)]
+    for c0, c1 in pieces:
         E = cfg.amp + _data_field(cfg, c0, c1, device)
+        a, b = max(c0, s0), min(c1, s1)                # part of the chunk inside [s0, s1)
+        E = E[a - c0:b - c0]
         if return_field:
             fields.append(E.clone())
         if cfg.sigma2 > 0:
-            n = torch.arange(c0, c1, dtype=torch.int64, device=device)
-            nz = gauss_complex(cfg.seed, n)
-            if cfg.noise == "analytic":
+            if analytic:
+                n = torch.arange(c0, c1, dtype=torch.int64, device=device)
+                nz = gauss_complex(cfg.seed, n)
                 Nf = torch.fft.fft(nz)
                 nu = torch.fft.fftfreq(c1 - c0, device=device)
                 keep = (nu * cfg.sideband) > 0
                 nz = torch.fft.ifft(torch.where(keep, Nf, torch.zeros_like(Nf)))  # same PSD on f>0
+            else:
+                nz = gauss_complex(cfg.seed, torch.arange(a, b, dtype=torch.int64, device=device))
             E = E + math.sqrt(cfg.sigma2) * nz
         inten = E.real * E.real + E.imag * E.imag
         code = torch.clamp(torch.round(inten * (cfg.adc_max / cfg.i_clip)), 0, cfg.adc_max)
-        codes[c0 - s0: c1 - s0] = code.to(codes.dtype)
+        codes[a - s0: b - s0] = code.to(codes.dtype)
     k = torch.arange(s0 // SPS, s1 // SPS, dtype=torch.int64, device=device)
     out = dict(codes=codes, labels=symbol_labels(cfg, k), adc_scale=cfg.adc_scale,
                adc_offset=0.0, i_ref=cfg.i_ref, amp=cfg.amp, px=cfg.px, sigma2=cfg.sigma2)

@@ -57,3 +57,17 @@ def test_white_noise_statistics():
     assert abs(float((n.abs() ** 2).mean()) - 1) < 0.01
     assert abs(float((n * n).mean().abs())) < 0.01                      # circular
     assert abs(cfg.sigma2 - 4 * 0.25 / 10.0) < 1e-15                    # σ² = 4·P_x/(Es/N0) (R14)
+
+
+def test_codes_bit_identical_for_any_subrange():
+    """The generation grid is global (kkgen.GEN_GRID), so a rank's window — any [s0, s1) — has exactly the
+    codes of the same samples in a longer stream (the basis of bit-identical multi-GPU shards and of
+    single-ingest windows)."""
+    lc = kkgen.LinkConfig(formats=(4, 64), segment_frames=1, dl_ps_nm=200000.0, cspr_db=10.0, esn0_db=18.0,
+                          seed=5)
+    lo, hi = -20000, 3 * kkgen.GEN_GRID + 1000
+    full = kkgen.generate(lc, lo, hi)
+    for a, b in ((0, 4096), (kkgen.GEN_GRID - 8, kkgen.GEN_GRID + 8), (-20000, -19000), (123456, 600000)):
+        sub = kkgen.generate(lc, a, b)
+        assert torch.equal(sub["codes"], full["codes"][a - lo:b - lo])
+        assert torch.equal(sub["labels"], full["labels"][(a - lo) // 4:(b - lo) // 4])

@@ -84,3 +84,50 @@ def test_two_rank_counters_match_single_stream():
         [c["clamped"], c["frames"], c["dead_frames"], c["bad_frames"]]
     assert words == [int(x) for x in whole]
     assert sum(words[5:10]) > 0          # non-trivial error counts were reduced
+
+
+# ------------------------------------------------------------------ single-ingest distribution (NEXT-3)
+def _ingest_worker(rank, world, port, q, weak):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import kkgen
+    from paper_2104_06311_b200 import ingest
+    lc = kkgen.LinkConfig(formats=(16,), dl_ps_nm=8000.0, cspr_db=12.0, esn0_db=20.0, seed=91)
+    F = S.FRAME_SAMPLES
+    halo = S.HALO_UP if weak else S.HALO
+    shards = (S.plan_weak(3 * F, world, stream_first=F, halo=halo) if weak
+              else S.plan_strong(7 * F, world, stream_first=F, halo=halo))
+    lo = min(s.read_first for s in shards)
+    hi = max(s.read_first + s.read_count for s in shards)
+    full = kkgen.generate(lc, lo, hi)["codes"]        # every rank: the reference (rank 0: the ADC stream)
+    host = full if rank == 0 else None
+    got = []
+    n = ingest.distribute(shards, 2 * F, lambda w, f0, nc: got.append((w.clone(), f0, nc)), host_stream=host,
+                          stream_first=lo)
+    # every window must be the stream's samples [f0 − halo, f0 + nc + halo) exactly, chunks tiling the core
+    me = shards[rank]
+    ok = sum(nc for _, _, nc in got) == me.n and n == sum(nc + 2 * halo for _, _, nc in got)
+    cur = me.first
+    for w, f0, nc in got:
+        ref = full[f0 - halo - lo:f0 + nc + halo - lo]
+        ok = ok and f0 == cur and torch.equal(w, ref)
+        cur += nc
+    flag = torch.tensor([int(ok)])
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+    if rank == 0:
+        q.put(int(flag.item()))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,weak", [(2, True), (3, False)])
+def test_single_ingest_delivers_exact_windows(world, weak):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_ingest_worker, args=(r, world, port, q, weak)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = q.get(timeout=300)
+    for p in ps:
+        p.join(timeout=60)
+    assert res == 1

@@ -1,6 +1,7 @@
 """Fig. 3b analogue: continuous Q-factor traces in 21 ms bins over a long stream.
 
-The stream is generated on the device piece by piece (kkgen is counter-based, so pieces join exactly) and
+The stream is generated on the device piece by piece (kkgen's chunks sit on a global grid, so pieces join
+bit-exactly) and
 received with kk_process_frames_ex in 2^26-sample calls; per-frame bit errors are binned into 5127-frame
 (21.0 ms) bins and mapped to Q with kk_q_from_ber.
 
