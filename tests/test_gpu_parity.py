@@ -282,3 +282,15 @@ def test_c2_cspr_sweep_q_parity(cspr):
     qo = theory.q_from_ber(int(orc["counts"]["bit_err"].sum()) / bits)
     assert abs(qg - qo) <= 0.05, (qg, qo)
     assert gpu["stats"]["clamped"] == orc["counts"]["clamped"]
+
+
+# ----------------------------------------------------------------------------- minimum-phase violated
+@pytest.mark.parametrize("M,cspr,esn0,up", [(16, 0.0, 18.0, 1), (4, 1.0, 12.0, 1), (16, 2.0, 18.0, 2),
+                                            (64, 4.0, 26.0, 1)])
+def test_very_low_cspr_parity(M, cspr, esn0, up):
+    """CSPR 0–4 dB: the minimum-phase condition fails (SER 7–44 %) and intensities touch zero (clamped
+    samples); the fp32 path must still track the fp64 oracle (measured: field 3e-7 … 1.6e-6, decisions 100 %)."""
+    case = make_case(M=M, dl=32000.0, cspr=cspr, esn0=esn0, n=1 << 17, seed=141, upsample=up)
+    gpu, orc = run_gpu(case), run_oracle(case)
+    _check_all(case, gpu, orc)
+    assert gpu["stats"]["clamped"] == orc["counts"]["clamped"]
