@@ -74,30 +74,60 @@ __host__ __device__ __forceinline__ constexpr int bitrevc(int x, int bits) {
   return r;
 }
 
+// x · W_R^{e} for DIR = −1 (W = e^{−2πi/R}), x · conj(W_R^{e}) for DIR = +1; e is a compile-time constant after
+// unrolling, so the trivial angles (0, ±i, −1) fold to moves/negations.
+template <int R, int DIR>
+__device__ __forceinline__ float2 twiddle(float2 x, int e) {
+  e &= R - 1;
+  if (e == 0) return x;
+  if (2 * e == R) return make_float2(-x.x, -x.y);
+  if (4 * e == R) return DIR < 0 ? make_float2(x.y, -x.x) : make_float2(-x.y, x.x);
+  if (4 * e == 3 * R) return DIR < 0 ? make_float2(-x.y, x.x) : make_float2(x.y, -x.x);
+  float2 w = unit_root<R>(e);
+  if (DIR < 0) w.y = -w.y;
+  return cmul(x, w);
+}
+
 // In-register DFT of length R (power of two ≤ 32), natural order in and out, unnormalised.
 // DIR = −1: X[k] = Σ x[n] e^{−2πi nk/R} (forward);  DIR = +1: inverse (no 1/R).
+// Decimation in frequency, two radix-2 stages fused into one radix-4 butterfly where possible: for
+// a = v[s+j], b = v[s+j+q], c = v[s+j+2q], d = v[s+j+3q] (q = R/2^{st+2}, j < q, u = 2^st):
+//   v[s+j]    = (a + c) + (b + d)
+//   v[s+j+q]  = ((a + c) − (b + d))·W^{2ju}
+//   v[s+j+2q] = ((a − c) ∓ i(b − d))·W^{ju}
+//   v[s+j+3q] = ((a − c) ± i(b − d))·W^{3ju}
+// — exactly the two radix-2 stages (same output positions, so the final bit reversal is unchanged) with the
+// (j + q) twiddle W^{ju}·(∓i) folded into the butterfly: 3 twiddle multiplies per group instead of 4.
 template <int R, int DIR>
 __device__ __forceinline__ void dft_reg(float2 (&v)[R]) {
   constexpr int LOGR = ilog2c(R);
 #pragma unroll
-  for (int st = 0; st < LOGR; ++st) {
-    const int half = R >> (st + 1);
+  for (int st = 0; st < LOGR; st += 2) {
+    if (st + 1 < LOGR) {
+      const int q = R >> (st + 2);
 #pragma unroll
-    for (int i = 0; i < R / 2; ++i) {
-      const int j = i & (half - 1);                  // position inside the butterfly group
-      const int start = (i - j) * 2;                 // group start
-      float2 a = v[start + j], b = v[start + j + half];
-      v[start + j] = cadd(a, b);
-      float2 d = csub(a, b);
-      const int e = j << st;                         // twiddle W_R^{e}, e < R/2
-      if (e == 0) {
-        v[start + j + half] = d;
-      } else if (4 * e == R) {                       // ±i
-        v[start + j + half] = DIR < 0 ? make_float2(d.y, -d.x) : make_float2(-d.y, d.x);
-      } else {
-        float2 w = unit_root<R>(e);
-        if (DIR < 0) w.y = -w.y;
-        v[start + j + half] = cmul(d, w);
+      for (int i = 0; i < R / 4; ++i) {
+        const int j = i & (q - 1);
+        const int s = (i - j) * 4;
+        const float2 a = v[s + j], b = v[s + j + q], c = v[s + j + 2 * q], d = v[s + j + 3 * q];
+        const float2 apc = cadd(a, c), amc = csub(a, c), bpd = cadd(b, d), bmd = csub(b, d);
+        // ∓i·(b − d): forward −i, inverse +i
+        const float2 ibmd = DIR < 0 ? make_float2(bmd.y, -bmd.x) : make_float2(-bmd.y, bmd.x);
+        const int u = 1 << st;
+        v[s + j] = cadd(apc, bpd);
+        v[s + j + q] = twiddle<R, DIR>(csub(apc, bpd), 2 * j * u);
+        v[s + j + 2 * q] = twiddle<R, DIR>(cadd(amc, ibmd), j * u);
+        v[s + j + 3 * q] = twiddle<R, DIR>(csub(amc, ibmd), 3 * j * u);
+      }
+    } else {
+      const int half = R >> (st + 1);
+#pragma unroll
+      for (int i = 0; i < R / 2; ++i) {
+        const int j = i & (half - 1);
+        const int s = (i - j) * 2;
+        const float2 a = v[s + j], b = v[s + j + half];
+        v[s + j] = cadd(a, b);
+        v[s + j + half] = twiddle<R, DIR>(csub(a, b), j << st);
       }
     }
   }
