@@ -82,10 +82,16 @@ k2_mf_kernel(const float2* __restrict__ E, int64_t E_first, const float2* __rest
              K2Params p) {
   __shared__ __align__(16) float2 buf[K2_BUF];
   __shared__ float2 A_s[2];
+  __shared__ int qb_s;
   extern __shared__ float2 lo_s[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int i = tid; i < p.lo_den; i += K2_THREADS) lo_s[i] = lo_tab[i];
   const int step256 = (int)(((int64_t)256 * p.lo_num) % p.lo_den);     // LO index step between r and r+1
+  // LO index of local sample j of a tile: (lo_num·(s0 + j)) mod lo_den = (qb + offj) mod lo_den with the
+  // tile base qb = (lo_num·s0) mod lo_den and the per-thread constant offj = (lo_num·j) mod lo_den
+  int offj[2];
+#pragma unroll
+  for (int it = 0; it < 2; ++it) offj[it] = (int)(((int64_t)(tid + K2_THREADS * it) * p.lo_num) % p.lo_den);
 
   // tiles are visited from the END of the range: K1 wrote E front to back, so its most recent (L2-resident)
   // output is consumed first; K3 then walks y front to back, again reading K2's most recent writes first.
@@ -94,13 +100,26 @@ k2_mf_kernel(const float2* __restrict__ E, int64_t E_first, const float2* __rest
     const int64_t s0 = t * kMfHop - kMfLead;                 // global sample of x[0]
     const int64_t fa = floordiv(s0, kFrameSamp);
     const int64_t fsplit = (fa + 1) * kFrameSamp;            // first sample of frame fa+1
-    // carrier estimates A_fa, A_fa+1 from K1's per-512-block sums (fixed order → deterministic)
+    // ---- FFT4096 pass 1 (radix 16, Ns = 1) fused with the load: x_i = (E_i − A_f(i))·LO_i, i = j + 256 r.
+    //      The E loads are issued first so their latency overlaps the carrier estimate below.
+    float2 v[2][16];
+#pragma unroll
+    for (int it = 0; it < 2; ++it) {
+      const int j = tid + K2_THREADS * it;
+      const float2* src = E + (s0 - E_first) + j;
+#pragma unroll
+      for (int r = 0; r < 16; ++r) v[it][r] = __ldg(src + 256 * r);
+    }
+    // carrier estimates A_fa, A_fa+1 from K1's per-512-block sums (fixed order → deterministic); tile LO base
     if (warp < 2) {
       const int64_t f = fa + warp;
-      float2 v = make_float2(0.f, 0.f);
-      if (warp == 0 || s0 + kMfN > fsplit) v = part[f * 32 - jb0 + lane];
-      v.x = warp_sum(v.x); v.y = warp_sum(v.y);
-      if (lane == 0) A_s[warp] = make_float2(v.x * (1.0f / kFrameSamp), v.y * (1.0f / kFrameSamp));
+      float2 a = make_float2(0.f, 0.f);
+      if (warp == 0 || s0 + kMfN > fsplit) a = part[f * 32 - jb0 + lane];
+      a.x = warp_sum(a.x); a.y = warp_sum(a.y);
+      if (lane == 0) A_s[warp] = make_float2(a.x * (1.0f / kFrameSamp), a.y * (1.0f / kFrameSamp));
+    } else if (tid == 64) {
+      const int sm = (int)(((s0 % p.lo_den) + p.lo_den) % p.lo_den);
+      qb_s = (sm * p.lo_num) % p.lo_den;                    // < 4096², 32-bit
     }
     __syncthreads();
     // next tile's input (32 KiB of E) → L2 while this tile computes
@@ -108,24 +127,15 @@ k2_mf_kernel(const float2* __restrict__ E, int64_t E_first, const float2* __rest
       const int64_t s0n = (t - gridDim.x) * kMfHop - kMfLead;
       asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(E + (s0n - E_first)), "r"(kMfN * 8) : "memory");
     }
-    // ---- FFT4096 pass 1 (radix 16, Ns = 1) fused with the load: x_i = (E_i − A_f(i))·LO_i, i = j + 256 r
     {
       const float2 A0 = A_s[0], A1 = A_s[1];
+      const int qb = qb_s;
       const int isplit = (int)(fsplit - s0);                 // first local sample of frame fa+1
-      float2 v[2][16];
 #pragma unroll
       for (int it = 0; it < 2; ++it) {
         const int j = tid + K2_THREADS * it;
-        const float2* src = E + (s0 - E_first) + j;
-#pragma unroll
-        for (int r = 0; r < 16; ++r) v[it][r] = __ldg(src + 256 * r);
-      }
-#pragma unroll
-      for (int it = 0; it < 2; ++it) {
-        const int j = tid + K2_THREADS * it;
-        const int64_t sj = s0 + j;
-        int q = (int)(((sj % p.lo_den) + p.lo_den) % p.lo_den);
-        q = (int)(((int64_t)q * p.lo_num) % p.lo_den);
+        int q = qb + offj[it];
+        q -= (q >= p.lo_den) ? p.lo_den : 0;
 #pragma unroll
         for (int r = 0; r < 16; ++r) {
           const float2 A = (j + 256 * r < isplit) ? A0 : A1;

@@ -180,21 +180,24 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
 
   int it = 0;
   for (int fl = blockIdx.x; fl < n_frames; fl += gridDim.x, ++it) {
-    const int64_t f = frame0 + fl;
-    const int M = (int)p.schedule[(int)(((f / p.segment_frames) % p.n_segments + p.n_segments) % p.n_segments)];
-    const int bi = (M == 4) ? 0 : (M == 8) ? 1 : (M == 16) ? 2 : (M == 32) ? 3 : 4;
-    Slicer sl;
-    sl.init(M);
     const int64_t sym0 = (int64_t)fl * kFrameSym;
-    // frame clamp count (K1 per-block counts) → dead-frame rule
+    // frame clamp count (K1 per-block counts) → dead-frame rule; the frame's QAM order (R26) — one 64-bit
+    // division per frame by one thread, broadcast through shared memory
     if (warp == 0) {
       int c = __ldg(&clampcnt[clamp_frame_off + (int64_t)fl * 32 + lane]);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
       if (lane == 0) misc[0] = c;
+    } else if (tid == 32) {
+      const int64_t f = frame0 + fl;
+      misc[2] = (int)p.schedule[(int)(((f / p.segment_frames) % p.n_segments + p.n_segments) % p.n_segments)];
     }
     mbar_wait(bar, it & 1);
     __syncthreads();
+    const int M = misc[2];
+    const int bi = (M == 4) ? 0 : (M == 8) ? 1 : (M == 16) ? 2 : (M == 32) ? 3 : 4;
+    Slicer sl;
+    sl.init(M);
     const int ccount = misc[0];
     const bool dead = (ccount >= kFrameSamp);
 
