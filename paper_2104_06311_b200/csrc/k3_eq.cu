@@ -147,12 +147,17 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
   const bool ref_tma = ref && ((reinterpret_cast<uintptr_t>(ref) & 15) == 0);
   constexpr uint32_t YBYTES = Lay::YS * 8;
 
-  auto issue = [&](int fl) {   // thread 0: TMA the frame (and its labels) into shared memory
+  // thread 0: TMA the frame samples (and, separately, its labels) into shared memory. One arrival with the
+  // total byte count; the two copies may be issued at different times (the phase completes when both land).
+  auto issue_y = [&](int fl) {
     const uint32_t bytes = YBYTES + (ref_tma ? (uint32_t)kFrameSym : 0u);
     mbar_arrive_expect_tx(bar, bytes);
     tma_bulk_g2s(ys, y + (int64_t)fl * (2 * kFrameSym), YBYTES, bar);
+  };
+  auto issue_ref = [&](int fl) {
     if (ref_tma) tma_bulk_g2s(ref_s, ref + (int64_t)fl * kFrameSym, kFrameSym, bar);
   };
+  auto issue = [&](int fl) { issue_y(fl); issue_ref(fl); };
   auto prefetch = [&](int fl) {
     prefetch_l2(y + (int64_t)fl * (2 * kFrameSym), YBYTES);
     if (ref_tma) prefetch_l2(ref + (int64_t)fl * kFrameSym, kFrameSym);
@@ -180,6 +185,7 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
 
   int it = 0;
   for (int fl = blockIdx.x; fl < n_frames; fl += gridDim.x, ++it) {
+    bool early = false;                                // thread 0: next frame's samples already requested
     const int64_t sym0 = (int64_t)fl * kFrameSym;
     // frame clamp count (K1 per-block counts) → dead-frame rule; the frame's QAM order (R26) — one 64-bit
     // division per frame by one thread, broadcast through shared memory
@@ -497,13 +503,20 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
         if (j == 0) { red[2 * blk] = cr; red[2 * blk + 1] = ci; }
       }
       __syncthreads();
-      if (tid < K3_SPT) {                              // window = (W/256) consecutive blocks
+      // the frame buffer (ys, reused for the CPR products) is dead now: start the next frame's sample copy
+      // so that it overlaps the decisions (its labels follow at the end of the frame, after ref_s is read)
+      if (tid == 0) {
+        const int nf = fl + (int)gridDim.x;
+        if (nf < n_frames) { issue_y(nf); early = true; }
+      }
+      if (tid < K3_SPT) {                              // window = (W/256) consecutive blocks, fixed order
         const int per = p.cpr_window / K3_THREADS;
         const int w0 = (tid / per) * per;
-        double cr = 0.0, ci = 0.0;
-        for (int q = 0; q < per; ++q) { cr += (double)red[2 * (w0 + q)]; ci += (double)red[2 * (w0 + q) + 1]; }
-        const double mag = sqrt(cr * cr + ci * ci);
-        rot[tid] = (mag > 0.0) ? make_float2((float)(cr / mag), (float)(-ci / mag)) : make_float2(1.f, 0.f);
+        float cr = 0.f, ci = 0.f;
+        for (int q = 0; q < per; ++q) { cr += red[2 * (w0 + q)]; ci += red[2 * (w0 + q) + 1]; }
+        const float m2 = cr * cr + ci * ci;            // rotation conj(c)/|c|; none if c = 0
+        const float rs = (m2 > 0.f && isfinite(m2)) ? rsqrtf(m2) : 0.f;
+        rot[tid] = (rs > 0.f) ? make_float2(cr * rs, -ci * rs) : make_float2(1.f, 0.f);
       }
       __syncthreads();
     }
@@ -535,7 +548,7 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
     if (tid == 0) {
       const int nf = fl + (int)gridDim.x;
       if (nf < n_frames) {
-        issue(nf);                                            // from L2 (prefetched one frame ago)
+        if (early) issue_ref(nf); else issue(nf);             // from L2 (prefetched one frame ago)
         if (nf + (int)gridDim.x < n_frames) prefetch(nf + gridDim.x);
       }
       if (ref) {
