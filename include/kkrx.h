@@ -88,7 +88,7 @@ typedef struct kk_config {
    * DDLMS, restarted every ddlms_block symbols after ddlms_warmup warm-up symbols (global grid). */
   int32_t eq_mode;
   int32_t ddlms_block;           /* 256 … 4096, power of two (kept symbols per restart; default 256)     */
-  int32_t ddlms_warmup;          /* 0 … 3840, multiple of 64 (default 512): warm-up from the centre spike */
+  int32_t ddlms_warmup;          /* 0 … 3136, multiple of 64 (default 512): warm-up from the centre spike */
   int32_t debug_guard;           /* 1: surround every device scratch buffer with 64 KiB canaries (kk_check_guards) */
   double  ddlms_mu_warm;         /* 2e-3 step size during warm-up                                        */
   double  ddlms_mu;              /* 2.5e-4 step size on kept symbols                                     */

@@ -294,7 +294,11 @@ kk_status validate(const kk_config& c, std::string& why) {
   if (c.eq_mode != KK_EQ_BLOCK_LS && c.eq_mode != KK_EQ_DDLMS) return bad("eq_mode");
   if (c.eq_mode == KK_EQ_DDLMS) {
     if (c.ddlms_block < 256 || c.ddlms_block > kk::kFrameSym || !is_pow2(c.ddlms_block)) return bad("ddlms_block must be a power of two in [256, 4096]");
-    if (c.ddlms_warmup < 0 || c.ddlms_warmup > 3840 || c.ddlms_warmup % 64) return bad("ddlms_warmup must be a multiple of 64 in [0, 3840]");
+    // K2's outermost tiles must read E inside core ± one frame: with Ky = 2·W + 2 (2-sps margin),
+    // 2·Ky + 2·kMfKeep − 2 + kMfLead ≤ kFrameSamp (both ends) ⇒ W ≤ 3136 on the 4096/3072 grid
+    if (c.ddlms_warmup < 0 || c.ddlms_warmup % 64 ||
+        2 * (2 * c.ddlms_warmup + 2) + 2 * kk::kMfKeep - 2 + kk::kMfLead > kk::kFrameSamp)
+      return bad("ddlms_warmup must be a multiple of 64 in [0, 3136]");
     if (!(c.ddlms_mu_warm >= 0) || !(c.ddlms_mu >= 0)) return bad("ddlms step sizes must be >= 0");
   }
   return KK_OK;

@@ -81,6 +81,18 @@ def test_invalid_configs_rejected_before_any_cuda_call(field, value):
     assert e.value.status == P.KK_ERR_CONFIG
 
 
+@pytest.mark.parametrize("warmup", [3200, 100, -64])
+def test_ddlms_warmup_bound(warmup):
+    """K2's outermost tiles must stay inside E (core ± one frame): 2·(2W + 2) + 2·1536 − 2 + 512 ≤ 16384
+    ⇒ W ≤ 3136 (multiple of 64)."""
+    c = P.kk_config_default()
+    c.eq_mode = P.KK_EQ_DDLMS
+    c.ddlms_warmup = warmup
+    with pytest.raises(P.KKError) as e:
+        P.kk_init(c)
+    assert e.value.status == P.KK_ERR_CONFIG
+
+
 def test_strerror_and_null_handling():
     for s in range(-8, 1):
         assert isinstance(P.kk_strerror(s), str) and P.kk_strerror(s)

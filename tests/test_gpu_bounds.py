@@ -64,6 +64,8 @@ CASES = [
     ("upsample2", dict(M=16, dl=32000.0, esn0=20.0, cspr=8.0, upsample=2), {}, "int16"),
     ("upsample2_uint8_lsb", dict(M=64, dl=8000.0, esn0=26.0, sideband=-1, upsample=2), dict(input_uint8=True),
      "uint8"),
+    ("ddlms_max_warmup", dict(M=16, dl=50000.0, esn0=18.0, eq_mode="ddlms", ddlms_block=256, ddlms_warmup=3136),
+     {}, "int16"),
     ("ddlms_warm0_blk4096", dict(M=4, dl=20000.0, esn0=12.0, eq_mode="ddlms", ddlms_block=4096, ddlms_warmup=0),
      {}, "int16"),
 ]
