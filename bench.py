@@ -57,6 +57,8 @@ def parse():
     ap.add_argument("--ingest", default="local", choices=["local", "single"],
                     help="e2e input path: every rank reads its own shard from host memory (local), or rank 0 "
                          "holds the whole stream and sends each rank its windows over NVLink (single; NEXT-3)")
+    ap.add_argument("--mf-n", type=int, default=4096, choices=[4096, 8192],
+                    help="K2 overlap-save grid: FFT4096/hop 3072 or FFT8192/hop 7168 (same exact convolution)")
     ap.add_argument("--ddlms-block", type=int, default=256)
     ap.add_argument("--ddlms-warmup", type=int, default=512)
     ap.add_argument("--ddlms-mu-warm", type=float, default=2e-3)
@@ -74,27 +76,35 @@ def k3_flops_per_symbol(L: int) -> float:
     return 8.0 * 9 * L + 40.0
 
 
+def k2_tile_flops(n: int) -> float:
+    """One MF tile: FFT_n + IFFT_{n/2} (5·N·log2 N each) + ×H and fold (6 per folded bin) + mixer (8 per input
+    sample): 403,456 for n = 4096 (3072 new samples), 868,352 for n = 8192 (7168 new samples)."""
+    import math
+    return 5.0 * n * math.log2(n) + 5.0 * (n // 2) * math.log2(n // 2) + 6.0 * (n // 2) + 8.0 * n
+
+
 def kernel_units(chunk: int, L: int, eq_mode: str = "block_ls", ddlms_block: int = 256, ddlms_warmup: int = 512,
-                 upsample: int = 1):
+                 upsample: int = 1, mf_n: int = 4096):
     """Algorithmic flops and HBM bytes per launch of each kernel for one call of `chunk` samples."""
     K = (L - 1) // 2
     k1_samples = chunk + 2 * F
     y_first = -K
-    n_tiles = (chunk // 2 + 2 * K + 1536 - 1) // 1536 + 1
+    keep = mf_n // 2 - 512
+    n_tiles = (chunk // 2 + 2 * K + keep - 1) // keep + 1
     frames = chunk // F
     if eq_mode == "ddlms":
         # per processed symbol (kept + warm-up): output 8 cMAC + update 8 cMAC = 128 flops + ~20 (slicer, error)
         sym = chunk // 4 * (ddlms_block + ddlms_warmup) / ddlms_block
         k3 = dict(flops=148.0 * sym, bytes=(8.0 * (ddlms_block + ddlms_warmup) / ddlms_block * 2 + 2.0) * (chunk // 4))
-        k2_flops = 403456.0 + 2048 * 8.0                  # complex H: 8 more flops per folded bin
+        k2_flops = k2_tile_flops(mf_n) + (mf_n // 2) * 8.0   # complex H: 8 more flops per folded bin
     else:
         k3 = dict(flops=k3_flops_per_symbol(L) * 4096 * frames, bytes=73728.0 * frames)
-        k2_flops = 403456.0
+        k2_flops = k2_tile_flops(mf_n)
     # K1U (upsample 2), per output sample: FFT2048 pair 220 + decimation 50 + interpolation 27 + E₂ 13 + logs 7
     k1_flops = 317.0 if upsample == 2 else 107.0
     return {
         ("K1u_kk" if upsample == 2 else "K1_kk"): dict(flops=k1_flops * k1_samples, bytes=10.0 * k1_samples),
-        "K2_mf": dict(flops=k2_flops * n_tiles, bytes=36864.0 * n_tiles),
+        "K2_mf": dict(flops=k2_flops * n_tiles, bytes=(8.0 * mf_n + 8.0 * keep) * n_tiles),
         "K3_eq": k3,
     }
 
@@ -336,7 +346,7 @@ def main():
     rx = Receiver(adc_scale=lc.adc_scale, ref_intensity=lc.i_ref, dispersion_ps_per_nm=lc.dl_ps_nm,
                   formats=lc.formats, segment_frames=lc.segment_frames, max_samples_per_call=chunk, device=local,
                   eq_mode=a.eq_mode, ddlms_block=a.ddlms_block, ddlms_warmup=a.ddlms_warmup,
-                  ddlms_mu_warm=a.ddlms_mu_warm, upsample=a.upsample)
+                  ddlms_mu_warm=a.ddlms_mu_warm, upsample=a.upsample, mf_fft_n=a.mf_n)
     assert rx.halo == HALO
     L = rx.taps
     dec = torch.empty(S // 4, dtype=torch.uint8, device=dev)
@@ -386,7 +396,7 @@ def main():
         peak_fp32 = N_SMS * FP32_LANES_PER_SM * 2 * float(mp.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12
     except Exception:
         pass
-    units = kernel_units(chunk, L, a.eq_mode, a.ddlms_block, a.ddlms_warmup, a.upsample)
+    units = kernel_units(chunk, L, a.eq_mode, a.ddlms_block, a.ddlms_warmup, a.upsample, a.mf_n)
     traffic = {}
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
@@ -486,7 +496,7 @@ def main():
             "config": {"workload": f"{a.workload}: continuous mixed 4/8/16/32/64-QAM stream (256-frame segments), "
                                    f"1 GBaud @ 4 GS/s, 1600 km (32000 ps/nm), CSPR 12 dB, Es/N0 26 dB white, int16 ADC",
                        "samples_per_gpu": S, "chunk_samples": chunk, "eq_taps": L, "eq_mode": a.eq_mode,
-                       "kk_upsample": a.upsample,
+                       "kk_upsample": a.upsample, "mf_grid": f"FFT{a.mf_n}/hop {a.mf_n - 1024}",
                        **({"ddlms_block": a.ddlms_block, "ddlms_warmup": a.ddlms_warmup,
                            "ddlms_mu_warm": a.ddlms_mu_warm} if a.eq_mode == "ddlms" else {}),
                        "l2": "inputs 8 GiB/GPU per step >> 126 MB L2, no flush needed", "seed": lc.seed},

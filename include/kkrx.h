@@ -63,7 +63,8 @@ typedef struct kk_config {
   int32_t rrc_span_sym;          /* 256 → 1025 taps (R4); span·4 ≤ mf_fft_n − mf_hop                    */
   double  rolloff;               /* 0.01 ("1% roll-off")                                     */
   int32_t hilbert_n, hilbert_hop;/* 1024, 512 [fixed] ("1024-point 100% overlap-save"; R1)  */
-  int32_t mf_fft_n, mf_hop;      /* 4096, 3072 [fixed] (FFT4096 → fold → IFFT2048; R6)                 */
+  int32_t mf_fft_n, mf_hop;      /* 4096, 3072 (default: FFT4096 → fold → IFFT2048; R6) or 8192, 7168 (same exact
+                                  * convolution on a larger overlap-save grid; DDLMS warm-up ≤ 2112)      */
   int32_t frame_symbols;         /* 4096 [fixed] (R23)                                                   */
   int32_t eq_taps;               /* 0 = tap-count rule of SURVEY §8(a); else odd L in [3, 15]           */
   int32_t eq_widely_linear;      /* 1 = widely linear ("widely-linear"), 0 = linear only    */

@@ -42,7 +42,8 @@ struct kk_ctx {
   float2* d_Hc = nullptr;   // complex static filter RRC × CD inverse (DDLMS mode)
   float2* d_lo = nullptr;
   float2* d_wcd = nullptr;
-  float2 *d_tw1024 = nullptr, *d_tw256 = nullptr, *d_tw4096 = nullptr, *d_tw2048 = nullptr;
+  float2 *d_tw1024 = nullptr, *d_tw256 = nullptr, *d_twN = nullptr, *d_twI = nullptr;
+  int mfN = 4096, mfKeep = 1536;   // MF overlap-save grid: FFT size, kept 2-sps outputs per tile
   float2* d_tw2048u = nullptr;   // K1U twiddles W₂₀₄₈^{t·k1}, [k1·64 + t] (k1 < 32, t < 64)
   int64_t halo = 0;              // kk_halo: kHalo, or kHaloUp with upsample = 2
   double hb_odd[8] = {0};        // odd half-band taps f[1], f[3], …, f[15] (upsample = 2)
@@ -273,7 +274,8 @@ kk_status validate(const kk_config& c, std::string& why) {
   if (!(c.rolloff > 0 && c.rolloff <= 1)) return bad("rolloff must be in (0,1]");
   if (!is_pow2(c.hilbert_n) || c.hilbert_hop < 1 || c.hilbert_hop > c.hilbert_n) return bad("hilbert_n must be pow2, hop in [1,n]");
   if (c.hilbert_n != kk::kHilbertN || c.hilbert_hop != kk::kHilbertHop) return bad("kernels are built for hilbert 1024/512");
-  if (c.mf_fft_n != kk::kMfN || c.mf_hop != kk::kMfHop) return bad("kernels are built for MF 4096/3072");
+  if (!((c.mf_fft_n == 4096 && c.mf_hop == 3072) || (c.mf_fft_n == 8192 && c.mf_hop == 7168)))
+    return bad("kernels are built for MF 4096/3072 and 8192/7168");
   if (c.rrc_span_sym < 8 || c.rrc_span_sym * 4 > c.mf_fft_n - c.mf_hop) return bad("rrc span: taps-1 must fit the MF overlap");
   if (c.frame_symbols != kk::kFrameSym) return bad("kernels are built for 4096-symbol frames");
   if (c.eq_taps != 0 && (c.eq_taps < 3 || c.eq_taps > 2 * kk::kMaxK + 1 || (c.eq_taps % 2) == 0)) return bad("eq_taps must be 0 or odd in [3,15]");
@@ -294,11 +296,13 @@ kk_status validate(const kk_config& c, std::string& why) {
   if (c.eq_mode != KK_EQ_BLOCK_LS && c.eq_mode != KK_EQ_DDLMS) return bad("eq_mode");
   if (c.eq_mode == KK_EQ_DDLMS) {
     if (c.ddlms_block < 256 || c.ddlms_block > kk::kFrameSym || !is_pow2(c.ddlms_block)) return bad("ddlms_block must be a power of two in [256, 4096]");
-    // K2's outermost tiles must read E inside core ± one frame: with Ky = 2·W + 2 (2-sps margin),
-    // 2·Ky + 2·kMfKeep − 2 + kMfLead ≤ kFrameSamp (both ends) ⇒ W ≤ 3136 on the 4096/3072 grid
+    // K2's outermost tiles must read E inside core ± one frame: with Ky = 2·W + 2 (2-sps margin) and
+    // keep = mf_fft_n/2 − 512, 2·Ky + 2·keep − 2 + 512 ≤ kFrameSamp (both ends)
+    // ⇒ W ≤ 3136 on the 4096/3072 grid, W ≤ 2112 on the 8192/7168 grid
+    const int keep = c.mf_fft_n / 2 - 512;
     if (c.ddlms_warmup < 0 || c.ddlms_warmup % 64 ||
-        2 * (2 * c.ddlms_warmup + 2) + 2 * kk::kMfKeep - 2 + kk::kMfLead > kk::kFrameSamp)
-      return bad("ddlms_warmup must be a multiple of 64 in [0, 3136]");
+        2 * (2 * c.ddlms_warmup + 2) + 2 * keep - 2 + 512 > kk::kFrameSamp)
+      return bad("ddlms_warmup must be a multiple of 64 in [0, 3136] (MF 4096) or [0, 2112] (MF 8192)");
     if (!(c.ddlms_mu_warm >= 0) || !(c.ddlms_mu >= 0)) return bad("ddlms step sizes must be >= 0");
   }
   return KK_OK;
@@ -327,7 +331,7 @@ void resolve_timing(kk_ctx* c, size_t count) {
 }
 
 void free_all(kk_ctx* c) {
-  void* ptrs[] = {c->d_H, c->d_Hc, c->d_lo, c->d_wcd, c->d_tw1024, c->d_tw256, c->d_tw4096, c->d_tw2048, c->d_tw2048u, c->d_sched,
+  void* ptrs[] = {c->d_H, c->d_Hc, c->d_lo, c->d_wcd, c->d_tw1024, c->d_tw256, c->d_twN, c->d_twI, c->d_tw2048u, c->d_sched,
                   c->d_E, c->d_part, c->d_clamp, c->d_y, c->d_z, c->d_counters,
                   c->d_in[0], c->d_in[1], c->d_ref[0], c->d_ref[1], c->d_dec[0], c->d_dec[1]};
   for (void* p : ptrs) dfree(c, p);
@@ -413,6 +417,8 @@ kk_status kk_init(const kk_config* cfg, kk_ctx** out) {
   c->K = (L - 1) / 2;
   c->ddlms = ddlms;
   c->Ky = ddlms ? 2 * cfg->ddlms_warmup + 2 : c->K;
+  c->mfN = cfg->mf_fft_n;
+  c->mfKeep = cfg->mf_fft_n / 2 - 512;
   c->halo = cfg->upsample == 2 ? kk::kHaloUp : kk::kHalo;
   if (cfg->upsample == 2) halfband_odd(c->hb_odd);
   if (cfg->format_schedule) {
@@ -436,22 +442,24 @@ kk_status kk_init(const kk_config* cfg, kk_ctx** out) {
   // ---- fp64 constants
   const std::vector<double> h = rrc_taps(cfg->rolloff, cfg->rrc_span_sym, 4);
   const int half = (int)(h.size() - 1) / 2;
-  std::vector<float> H(kk::kMfN);
-  for (int k = 0; k < kk::kMfN; ++k) {
+  const int NM = cfg->mf_fft_n;                 // MF grid (4096 or 8192)
+  std::vector<float> H(NM);
+  for (int k = 0; k < NM; ++k) {
     double s = h[half];
-    for (int j = 1; j <= half; ++j) s += 2.0 * h[half + j] * std::cos(2.0 * kPi * (double)((int64_t)k * j % kk::kMfN) / kk::kMfN);
-    H[k] = (float)(s / kk::kMfN);
+    for (int j = 1; j <= half; ++j) s += 2.0 * h[half + j] * std::cos(2.0 * kPi * (double)((int64_t)k * j % NM) / NM);
+    H[k] = (float)(s / NM);
   }
   std::vector<float2> lo(cfg->lo_den);
   for (int q = 0; q < cfg->lo_den; ++q) {
     const double a = -2.0 * kPi * (double)cfg->sideband * (double)q / (double)cfg->lo_den;
     lo[q] = make_float2((float)std::cos(a), (float)std::sin(a));
   }
-  // paper arrangement: complex static filter H_cd = DFT4096 of h_cd, h_cd = IDFT4096(H_rrc·C) truncated to
-  // j = −512..512 (the same definition as oracle.receiver.static_filter_taps), ×1/4096 folded in
+  // paper arrangement: complex static filter H_cd = DFT_NM of h_cd, h_cd = IDFT4096(H_rrc·C) truncated to
+  // j = −512..512 (the same definition as oracle.receiver.static_filter_taps: the taps live on the 4096 grid
+  // whatever the MF grid), ×1/NM folded in
   std::vector<float2> Hc;
   if (ddlms) {
-    const int N = kk::kMfN;
+    const int N = 4096;
     std::vector<double> Hr(N);
     for (int k = 0; k < N; ++k) {
       double s = h[half];
@@ -477,14 +485,14 @@ kk_status kk_init(const kk_config* cfg, kk_ctx** out) {
       }
       hcd[j + half] = acc / (double)N;
     }
-    Hc.resize(N);
-    for (int k = 0; k < N; ++k) {
+    Hc.resize(NM);
+    for (int k = 0; k < NM; ++k) {
       cd acc(0, 0);
       for (int j = -half; j <= half; ++j) {
-        const int m = (int)(((int64_t)k * (j + N)) % N);
-        acc += hcd[j + half] * cd(ct[m], -st[m]);
+        const double a = -2.0 * kPi * (double)(((int64_t)k * (j + NM)) % NM) / (double)NM;
+        acc += hcd[j + half] * cd(std::cos(a), std::sin(a));
       }
-      acc /= (double)N;
+      acc /= (double)NM;
       Hc[k] = make_float2((float)acc.real(), (float)acc.imag());
     }
   }
@@ -500,8 +508,9 @@ kk_status kk_init(const kk_config* cfg, kk_ctx** out) {
   chk(upload(&c->d_wcd, wcd));
   chk(upload(&c->d_tw1024, twiddles(1024, 32, 32)));
   chk(upload(&c->d_tw256, twiddles(256, 16, 16)));
-  chk(upload(&c->d_tw4096, twiddles(4096, 16, 256)));
-  chk(upload(&c->d_tw2048, twiddles(2048, 8, 256)));
+  // K2 last-pass twiddles: forward W_NM^{r·k} (radix NM/256), inverse W_{NM/2}^{r·k} (radix NM/512), k < 256
+  chk(upload(&c->d_twN, twiddles(c->mfN, c->mfN / 256, 256)));
+  chk(upload(&c->d_twI, twiddles(c->mfN / 2, c->mfN / 512, 256)));
   if (cfg->upsample == 2) {
     std::vector<float2> t(2048);
     for (int k1 = 0; k1 < 32; ++k1)
@@ -609,12 +618,12 @@ kk_status kk_process_frames_ex(kk_ctx* c, const void* d_adc, int64_t first, int6
   const int64_t y_first = first / 2 - c->Ky;
   const int64_t y_count = n / 2 + 2 * c->Ky;
   auto fdiv = [](int64_t a, int64_t b) { int64_t q = a / b; return (a % b != 0 && ((a < 0) != (b < 0))) ? q - 1 : q; };
-  const int64_t t_lo = fdiv(y_first, kk::kMfKeep);
-  const int64_t t_hi = fdiv(y_first + y_count - 1, kk::kMfKeep);
+  const int64_t t_lo = fdiv(y_first, c->mfKeep);
+  const int64_t t_hi = fdiv(y_first + y_count - 1, c->mfKeep);
   if (c->timing) cudaEventRecord(tev[1], s);
   kk::K2Params p2{cf.lo_num, cf.lo_den};
-  kk::launch_k2(c->d_E, first - F, c->d_part, c->d_clamp, jb0, t_lo, t_hi - t_lo + 1, c->d_y, y_first, y_count,
-                c->d_H, c->d_Hc, c->d_lo, c->d_tw256, c->d_tw4096, c->d_tw2048, p2, c->num_sms, s);
+  kk::launch_k2(c->mfN, c->d_E, first - F, c->d_part, c->d_clamp, jb0, t_lo, t_hi - t_lo + 1, c->d_y, y_first,
+                y_count, c->d_H, c->d_Hc, c->d_lo, c->d_tw256, c->d_twN, c->d_twI, p2, c->num_sms, s);
 
   if (c->timing) cudaEventRecord(tev[2], s);
   // K3 one CTA per frame

@@ -69,11 +69,13 @@ void launch_k1(const void* adc_cta0, int input_dtype, int64_t n_pairs, float2* E
 // K1U: K1 with 2× KK upsampling; one warp per pair of 512-blocks, 4 warps per CTA (n_blocks % 8 == 0).
 void launch_k1u(const void* adc_cta0, int input_dtype, int64_t n_blocks, float2* E, float2* part, int* clampcnt,
                 const float2* tw2048u, const K1UParams& p, cudaStream_t s);
-// K2: carrier removal + mixer + RRC MF + decimation by 2 on the global tile grid.
-void launch_k2(const float2* E, int64_t E_first, const float2* part, const int* clampcnt, int64_t jb0,
+// K2: carrier removal + mixer + RRC MF + decimation by 2 on the global tile grid (nf = 4096 or 8192:
+// FFT size; hop nf − 1024, nf/2 − 512 kept 2-sps outputs per tile). twN: W_nf^{r·k} [r][k < 256];
+// twI: W_{nf/2}^{r·k} [r][k < 256].
+void launch_k2(int nf, const float2* E, int64_t E_first, const float2* part, const int* clampcnt, int64_t jb0,
                int64_t tile0, int64_t n_tiles, float2* y, int64_t y_first, int64_t y_count, const float* Hs,
-               const float2* Hc, const float2* lo_tab, const float2* tw256, const float2* tw4096,
-               const float2* tw2048, const K2Params& p, int num_sms, cudaStream_t s);
+               const float2* Hc, const float2* lo_tab, const float2* tw256, const float2* twN,
+               const float2* twI, const K2Params& p, int num_sms, cudaStream_t s);
 // K3: per-frame widely-linear DD-LS equalizer, CPR, decisions, counters.
 void launch_k3(const float2* y, int64_t frame0, int64_t n_frames, int K, const float2* w_cd, const int* clampcnt,
                int64_t clamp_frame_off, const uint8_t* ref, uint8_t* dec, float2* z, unsigned long long* counters,

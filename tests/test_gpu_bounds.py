@@ -66,6 +66,9 @@ CASES = [
      "uint8"),
     ("ddlms_max_warmup", dict(M=16, dl=50000.0, esn0=18.0, eq_mode="ddlms", ddlms_block=256, ddlms_warmup=3136),
      {}, "int16"),
+    ("mf8192_blockls", dict(M=64, dl=200000.0, esn0=24.0), dict(mf_fft_n=8192), "int16"),
+    ("mf8192_ddlms_max_warmup", dict(M=16, dl=50000.0, esn0=18.0, eq_mode="ddlms", ddlms_warmup=2112),
+     dict(mf_fft_n=8192), "int16"),
     ("ddlms_warm0_blk4096", dict(M=4, dl=20000.0, esn0=12.0, eq_mode="ddlms", ddlms_block=4096, ddlms_warmup=0),
      {}, "int16"),
 ]

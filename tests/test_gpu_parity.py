@@ -294,3 +294,17 @@ def test_very_low_cspr_parity(M, cspr, esn0, up):
     gpu, orc = run_gpu(case), run_oracle(case)
     _check_all(case, gpu, orc)
     assert gpu["stats"]["clamped"] == orc["counts"]["clamped"]
+
+
+# ----------------------------------------------------------------------------- MF grid 8192/7168
+@pytest.mark.parametrize("kw", [dict(M=16, dl=112000.0, esn0=17.0), dict(M=64, dl=32000.0, esn0=26.0, upsample=2),
+                                dict(M=16, dl=112000.0, esn0=18.0, eq_mode="ddlms"),
+                                dict(formats=(4, 8, 16, 32, 64), segment_frames=1, dl=32000.0, esn0=24.0, sideband=-1)])
+def test_mf8192_grid_parity(kw):
+    """The FFT8192/hop-7168 overlap-save grid computes the same exact linear convolution as the 4096/3072 one
+    (K2 template): MF output, equalizer output and decisions against the grid-independent oracle."""
+    case = make_case(n=5 * F, first=3 * F, seed=151, **kw)
+    from gpu_case import receiver_for
+    rx = receiver_for(case, keep=True, mf_fft_n=8192)
+    gpu, orc = run_gpu(case, rx=rx), run_oracle(case)
+    _check_all(case, gpu, orc)
