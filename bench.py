@@ -9,7 +9,7 @@ Workload (BASELINE.json configs[4], "C5"): a continuous mixed 4→8→16→32→
 nominal Es/N0 26 dB white noise, int16 ADC codes — generated on the device from the seeded generator
 (kkgen). Each rank owns 2^32 samples (8 GiB of int16) of the global stream, a contiguous frame range with
 its 16,640-sample halos: per-GPU work is fixed as N grows ("weak" scaling). One step = the whole hot path
-(K1 KK → K2 MF → K3 EQ/CPR/decisions, in 2^26-sample calls through the C ABI) over the rank's 2^32
+(K1 KK → K2 MF → K3 EQ/CPR/decisions, in 2^28-sample calls through the C ABI) over the rank's 2^32
 samples, plus the NCCL allreduce of the 24 error counters — the only cross-GPU traffic. Inputs (8 GiB) are
 far larger than the 126 MB L2, so no L2 flush is needed between steps.
 
@@ -44,7 +44,8 @@ def parse():
     ap.add_argument("--impl", default="kkrx", choices=["kkrx", "reference"])
     ap.add_argument("--workload", default="C5")
     ap.add_argument("--samples-per-gpu", type=int, default=1 << 32)
-    ap.add_argument("--chunk", type=int, default=1 << 26)
+    ap.add_argument("--chunk", type=int, default=1 << 28,
+                    help="samples per kk_process_frames call (2^28: launch gaps and tail waves amortised)")
     ap.add_argument("--e2e-samples", type=int, default=1 << 30)
     ap.add_argument("--cpu-frames", type=int, default=64, help="oracle sample size (frames) for cpu_baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -401,7 +402,9 @@ def main():
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
         try:
-            traffic = json.load(open(tp)).get("bytes_per_launch", {})
+            tj = json.load(open(tp))
+            scale = chunk / float(tj.get("chunk_samples", chunk))      # per-launch bytes scale with the call size
+            traffic = {k: v * scale for k, v in tj.get("bytes_per_launch", {}).items()}
         except Exception:
             traffic = {}
     kernels = {}

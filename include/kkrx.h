@@ -153,7 +153,7 @@ kk_status kk_process_frames_ex(kk_ctx* ctx, const void* d_adc, int64_t first_sam
                                kk_stream_t stream);
 
 /* End-to-end variant with HOST buffers (pinned recommended): copies [h_adc − left, h_adc + n + right)
- * host→device, runs kk_process_frames, copies decisions device→host, in chunks of ≤ max_samples_per_call
+ * host→device, runs kk_process_frames, copies decisions device→host, in chunks of ≤ min(max_samples_per_call, 2^26)
  * with two internal streams so the copies of chunk i+1 overlap the kernels of chunk i. Blocks until done.
  * h_ref / h_decisions nullable host uint8[n_samples/4]. Same constraints/errors as kk_process_frames,
  * except n_samples may exceed max_samples_per_call (it must be a multiple of 16384). */

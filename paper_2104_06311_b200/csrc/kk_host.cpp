@@ -676,12 +676,15 @@ kk_status kk_process_frames_host(kk_ctx* c, const void* h_adc, int64_t first, in
   DeviceGuard g(c->device);
   const size_t esz = c->cfg.input_dtype == KK_IN_FLOAT32 ? 4 : c->cfg.input_dtype == KK_IN_UINT8 ? 1 : 2;
   const int64_t H = c->halo;
+  // staging granularity: ≤ 2^26 samples per transfer so that copies and kernels of consecutive sub-calls
+  // overlap on the two streams even when the context was sized for much larger device calls
+  const int64_t hc = std::min<int64_t>(c->nmax, (int64_t)1 << 26);
   cudaError_t e = cudaSuccess;
   auto chk = [&](cudaError_t r) { if (e == cudaSuccess) e = r; };
   for (int i = 0; i < 2; ++i) {
-    if (!c->d_in[i]) chk(dalloc(c, "host_in", &c->d_in[i], (size_t)(c->nmax + 2 * H) * esz));
-    if (!c->d_ref[i]) chk(dalloc(c, "host_ref", &c->d_ref[i], (size_t)(c->nmax / 4)));
-    if (!c->d_dec[i]) chk(dalloc(c, "host_dec", &c->d_dec[i], (size_t)(c->nmax / 4)));
+    if (!c->d_in[i]) chk(dalloc(c, "host_in", &c->d_in[i], (size_t)(hc + 2 * H) * esz));
+    if (!c->d_ref[i]) chk(dalloc(c, "host_ref", &c->d_ref[i], (size_t)(hc / 4)));
+    if (!c->d_dec[i]) chk(dalloc(c, "host_dec", &c->d_dec[i], (size_t)(hc / 4)));
     if (!c->hs[i]) chk(cudaStreamCreateWithFlags(&c->hs[i], cudaStreamNonBlocking));
     if (!c->ev[i]) chk(cudaEventCreateWithFlags(&c->ev[i], cudaEventDisableTiming));
   }
@@ -690,7 +693,7 @@ kk_status kk_process_frames_host(kk_ctx* c, const void* h_adc, int64_t first, in
   int64_t done = 0;
   int k = 0;
   while (done < n && e == cudaSuccess) {
-    const int64_t nc = std::min<int64_t>(c->nmax, n - done);
+    const int64_t nc = std::min<int64_t>(hc, n - done);
     const int b = k & 1;
     cudaStream_t s = c->hs[b];
     chk(cudaMemcpyAsync(c->d_in[b], src + (done - H) * (int64_t)esz, (size_t)(nc + 2 * H) * esz, cudaMemcpyHostToDevice, s));
