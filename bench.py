@@ -261,6 +261,42 @@ def run_reference(a, rank, world):
     return 0
 
 
+# ----------------------------------------------------------------------------------------------- 8-bit ADC e2e
+def e2e_uint8(a, lc, HALO, chunk, first, En, world, dev, SH, kkrx, kkgen, torch, dist, Receiver):
+    """Same end-to-end measurement with an 8-bit ADC stream of the same link (SPEC S:199's AdcConfig default;
+    the paper does not state the ADC resolution): half the host→device bytes of the int16 headline."""
+    import dataclasses
+    lc8 = dataclasses.replace(lc, adc_bits=8)
+    g = kkgen.generate(lc8, first - HALO, first + En + HALO, device=dev)
+    h_codes = torch.empty(En + 2 * HALO, dtype=torch.uint8, pin_memory=True)
+    h_codes.copy_(g["codes"])
+    h_ref = torch.empty(En // 4, dtype=torch.uint8, pin_memory=True)
+    h_ref.copy_(g["labels"][HALO // 4:(HALO + En) // 4])
+    del g
+    h_dec = torch.empty(En // 4, dtype=torch.uint8, pin_memory=True)
+    rx8 = Receiver(adc_scale=lc8.adc_scale, ref_intensity=lc8.i_ref, dispersion_ps_per_nm=lc8.dl_ps_nm,
+                   formats=lc8.formats, segment_frames=lc8.segment_frames, max_samples_per_call=chunk, device=dev.index,
+                   input_uint8=True, upsample=a.upsample, mf_fft_n=a.mf_n)
+    rx8.process_host(h_codes, first, En, ref=h_ref, decisions=h_dec)          # warm-up
+    if world > 1:
+        dist.barrier()
+    rx8.reset_stats()
+    t_e = []
+    for _ in range(max(1, a.steps)):
+        t1 = time.perf_counter()
+        rx8.process_host(h_codes, first, En, ref=h_ref, decisions=h_dec)
+        st = rx8.stats()
+        t_e.append(time.perf_counter() - t1)
+    rx8.close()
+    te = SH.max_over_ranks(sum(t_e), device=dev)
+    n_chunks = (En + (1 << 26) - 1) // (1 << 26)
+    be = {f"{M}QAM": st["bit_err"][i] / st["bits"][i] for i, M in enumerate((4, 8, 16, 32, 64)) if st["bits"][i]}
+    return {"value": En * world * len(t_e) / te / 1e9, "unit": "GS/s",
+            "h2d_bytes_per_step": int((En + 2 * HALO * n_chunks) * 1 + En // 4),
+            "d2h_bytes_per_step": int(En // 4 + 8 * kkrx.KK_STATS_WORDS), "samples_per_gpu": En,
+            "adc": "uint8 (adc_bits 8, same link)", "ber": be}
+
+
 # ----------------------------------------------------------------------------------------------- single ingest
 def e2e_single_ingest(a, rx, lc, HALO, chunk, rank, world, dev, SH, kkrx, kkgen, torch, dist):
     """e2e with ONE ingest point (paper_2104_06311_b200/ingest.py): rank 0 holds the whole
@@ -427,6 +463,7 @@ def main():
 
     # ---------------- end to end through the host-buffer C-ABI call (pinned memory, copies inside)
     e2e = None
+    e2e_u8 = None
     if not a.no_e2e and a.ingest == "single":
         e2e = e2e_single_ingest(a, rx, lc, HALO, chunk, rank, world, dev, SH, kkrx, kkgen, torch, dist)
     elif not a.no_e2e:
@@ -436,7 +473,7 @@ def main():
         h_ref = torch.empty(En // 4, dtype=torch.uint8, pin_memory=True)
         h_ref.copy_(ref[:En // 4])
         h_dec = torch.empty(En // 4, dtype=torch.uint8, pin_memory=True)
-        n_chunks = En // chunk
+        n_chunks = (En + min(chunk, 1 << 26) - 1) // min(chunk, 1 << 26)    # host path stages ≤ 2^26 per sub-call
         rx.process_host(h_codes, first, En, ref=h_ref, decisions=h_dec)       # warm-up (allocates staging)
         if world > 1:
             dist.barrier()
@@ -452,6 +489,7 @@ def main():
                "d2h_bytes_per_step": int(En // 4 + 8 * kkrx.KK_STATS_WORDS),
                "samples_per_gpu": En, "api": "kk_process_frames_host (pinned host buffers, 2 streams)"}
         del h_codes, h_ref, h_dec
+        e2e_u8 = e2e_uint8(a, lc, HALO, chunk, first, En, world, dev, SH, kkrx, kkgen, torch, dist, Receiver)
 
     # ---------------- oracle beside it (rank 0, N = 1 only): timing + sampled-frame parity
     cpu = None
@@ -506,6 +544,7 @@ def main():
             "rt_factor": value / 4.0,
             "clocks": clk.summary(),
             "e2e": e2e,
+            "e2e_uint8": e2e_u8,
             "gpu_launches": 3 * calls_per_step * a.steps,
             "roofline": roofline,
             "kernels": kernels,
