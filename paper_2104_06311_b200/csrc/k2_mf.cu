@@ -204,6 +204,7 @@ k2_mf_kernel(const float2* __restrict__ E, int64_t E_first, const float2* __rest
 #pragma unroll
         for (int r = 0; r < RI3; ++r) v3[it][r] = src[r * (256 + 16)];
       }
+      float pw[PER3][RI3];                                    // DDLMS mode: |y|² of the symbol-centre outputs
 #pragma unroll
       for (int it = 0; it < PER3; ++it) {
         const int j = tid + T * it;
@@ -214,6 +215,29 @@ k2_mf_kernel(const float2* __restrict__ E, int64_t E_first, const float2* __rest
         for (int r = 1; r < RI3 - 1; ++r) {                  // p = j + 256 r ∈ [256, NI − 256) ⇔ 1 ≤ r ≤ RI3 − 2
           const int64_t m = m_base + j + 256 * r;
           if (m >= y_first && m < y_first + y_count) y[m - y_first] = v3[it][r];
+          if constexpr (CH) pw[it][r] = (j & 1) ? 0.f : fmaf(v3[it][r].x, v3[it][r].x, v3[it][r].y * v3[it][r].y);
+        }
+      }
+      if constexpr (CH) {
+        // per-64-symbol (128-sample) segment power for K3′'s AGC: output p = j + 256 r lies in tile segment
+        // 2(r − 1) + (j ≥ 128); warp sums, then the 4 (T = 128) or 4 (T = 256, per half) warp partials of a
+        // segment in fixed order → deterministic. Segment g (global) = m / 128.
+        constexpr int NSEG = KEEP / 128;
+        float* red = reinterpret_cast<float*>(lo_s + p.lo_den);   // NSEG × 4 floats past the LO table
+#pragma unroll
+        for (int it = 0; it < PER3; ++it) {
+          const int j = tid + T * it;
+#pragma unroll
+          for (int r = 1; r < RI3 - 1; ++r) {
+            const float s = warp_sum(pw[it][r]);
+            const int seg = 2 * (r - 1) + (j >= 128 ? 1 : 0);
+            if (lane == 0) red[seg * 4 + ((j & 127) >> 5)] = s;
+          }
+        }
+        __syncthreads();
+        if (tid < NSEG) {
+          const float s = ((red[tid * 4] + red[tid * 4 + 1]) + red[tid * 4 + 2]) + red[tid * 4 + 3];
+          p.seg_pow[t * (KEEP / 128) + tid - p.seg_first] = s;
         }
       }
       __syncthreads();                                        // buf is rewritten by the next tile
@@ -229,7 +253,8 @@ static void launch_k2_t(const float2* E, int64_t E_first, const float2* part, in
   constexpr int T = NF / 32;
   int64_t grid = (int64_t)num_sms * (16384 / NF);
   if (grid > n_tiles) grid = n_tiles;
-  const size_t dyn = (size_t)(NF + NF / 16) * sizeof(float2) + (size_t)p.lo_den * sizeof(float2);
+  const size_t dyn = (size_t)(NF + NF / 16) * sizeof(float2) + (size_t)p.lo_den * sizeof(float2) +
+                     (CH ? (size_t)(NF / 2 - 512) / 128 * 4 * sizeof(float) : 0);
   cudaFuncSetAttribute(k2_mf_kernel<NF, CH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
   k2_mf_kernel<NF, CH><<<(unsigned)grid, T, dyn, s>>>(E, E_first, part, jb0, tile0, n_tiles, y, y_first, y_count,
                                                       Hs, Hc, lo_tab, tw256, twN, twI, p);

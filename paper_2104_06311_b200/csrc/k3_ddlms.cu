@@ -5,6 +5,7 @@
 // (RRC × CD inverse, the "offline-optimized filter"), so the 4 adaptive taps only track residual ISI, gain and
 // phase:
 //   x_n = g·[y[2n+1], y[2n], y[2n−1], y[2n−2]],  g = (mean |y[2n]|²)^(−½) over the block and its warm-up
+//   (the power comes from K2's per-64-symbol segment sums)
 //   o_n = wᵀx_n + vᵀconj(x_n),  d_n = D(o_n),  e_n = d_n − o_n,  w += μ e conj(x),  v += μ e x
 //   w₀ = centre spike on y[2n], v₀ = 0; μ = mu_warm over the warm-up, mu over the kept symbols.
 // The paper carries the equalizer state across 2^22-sample buffers in stream order (events serialise the
@@ -44,12 +45,12 @@ k3_ddlms_kernel(const float2* __restrict__ y, int64_t y_base, int64_t sym_first,
   const int64_t n0 = n_keep0 - W;
   int serr = 0, berr = 0;
   if (!dead) {
-    // AGC over the block and its warm-up (symbol-centre samples)
+    // AGC over the block and its warm-up (symbol-centre samples): K2 summed |y[2n]|² per 64-symbol segment
+    // (global grid), so the block's power is (W + B)/64 segment sums — no second pass over y
+    const int64_t g0 = (sym_first + n0) >> 6;                  // first segment (floor; W, B multiples of 64)
+    const float* sp = p.seg_pow + (g0 - p.seg_first);
     float pw = 0.f;
-    for (int i = 0; i < W + B; ++i) {
-      const float2 c = __ldg(&yy[2 * (n0 + i)]);
-      pw = fmaf(c.x, c.x, fmaf(c.y, c.y, pw));
-    }
+    for (int q = 0; q < (W + B) / 64; ++q) pw += __ldg(&sp[q]);
     const float P = pw / (float)(W + B);
     const float g = (P > 0.f) ? rsqrtf(P) : 1.0f;
     float2 w[4] = {make_float2(0.f, 0.f), make_float2(1.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
@@ -67,8 +68,19 @@ k3_ddlms_kernel(const float2* __restrict__ y, int64_t y_base, int64_t sym_first,
     float4 ring[PF];
 #pragma unroll
     for (int q = 0; q < PF; ++q) ring[q] = __ldg(reinterpret_cast<const float4*>(yy + 2 * (n0 + q) + 2));
-    const int total = W + B;                                   // multiple of PF (both multiples of 256)
+    const int total = W + B;                                   // multiple of PF (W multiple of 64, B of 256)
+    // labels: 8 per chunk as one 8-byte word (kept chunks start at multiples of 8 symbols), the reference word
+    // loaded one chunk ahead; byte accesses when a pointer is not 8-byte aligned
+    const bool ref8 = ref && ((reinterpret_cast<uintptr_t>(ref) & 7) == 0);
+    const bool dec8 = dec && ((reinterpret_cast<uintptr_t>(dec) & 7) == 0);
+    uint2 rnext = make_uint2(0u, 0u);
+    if (ref8 && W == 0) rnext = __ldg(reinterpret_cast<const uint2*>(ref + n_keep0));
     for (int i0 = 0; i0 < total; i0 += PF) {
+      const bool kept = i0 >= W;
+      const uint2 rcur = rnext;
+      if (ref8 && i0 + PF >= W && i0 + PF < total)
+        rnext = __ldg(reinterpret_cast<const uint2*>(ref + (n0 + i0 + PF)));
+      uint32_t dlo = 0u, dhi = 0u;
 #pragma unroll
       for (int q = 0; q < PF; ++q) {
         const int i = i0 + q;
@@ -84,16 +96,17 @@ k3_ddlms_kernel(const float2* __restrict__ y, int64_t y_base, int64_t sym_first,
         const float2 o = cadd(o0, o1);
         const float2 d = sl.point(o);
         const float2 e = csub(d, o);
-        const float mu = (i < W) ? p.mu_warm : p.mu;
-        if (i >= W) {
+        const float mu = kept ? p.mu : p.mu_warm;
+        if (kept) {
           const int64_t kl = n;                                // local kept symbol index
           const int lab = sl.label(o);
           if (ref) {
-            const int r = __ldg(&ref[kl]);
+            const int r = ref8 ? (int)(((q < 4 ? rcur.x : rcur.y) >> (8 * (q & 3))) & 0xffu) : (int)__ldg(&ref[kl]);
             serr += (lab != r);
             berr += __popc(lab ^ r);
           }
-          if (dec) dec[kl] = (uint8_t)lab;
+          if (q < 4) dlo |= (uint32_t)lab << (8 * q); else dhi |= (uint32_t)lab << (8 * (q - 4));
+          if (dec && !dec8) dec[kl] = (uint8_t)lab;
           if (zout) zout[kl] = o;
         }
         const float2 me = cscale(e, mu);
@@ -105,6 +118,7 @@ k3_ddlms_kernel(const float2* __restrict__ y, int64_t y_base, int64_t sym_first,
         x[3] = x[1]; x[2] = x[0];
         x[1] = cscale(make_float2(nx.x, nx.y), g); x[0] = cscale(make_float2(nx.z, nx.w), g);
       }
+      if (kept && dec8) *reinterpret_cast<uint2*>(dec + (n0 + i0)) = make_uint2(dlo, dhi);
     }
   } else {
     const int lab = sl.label(make_float2(0.f, 0.f));

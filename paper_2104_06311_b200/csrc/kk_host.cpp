@@ -55,6 +55,7 @@ struct kk_ctx {
   int* d_clamp = nullptr;
   float2* d_y = nullptr;
   float2* d_z = nullptr;
+  float* d_segpow = nullptr;     // DDLMS mode: K2's per-64-symbol power sums (K3′ AGC)
   unsigned long long* d_counters = nullptr;
   // host-buffer path staging (lazy)
   void* d_in[2] = {nullptr, nullptr};
@@ -332,7 +333,7 @@ void resolve_timing(kk_ctx* c, size_t count) {
 
 void free_all(kk_ctx* c) {
   void* ptrs[] = {c->d_H, c->d_Hc, c->d_lo, c->d_wcd, c->d_tw1024, c->d_tw256, c->d_twN, c->d_twI, c->d_tw2048u, c->d_sched,
-                  c->d_E, c->d_part, c->d_clamp, c->d_y, c->d_z, c->d_counters,
+                  c->d_E, c->d_part, c->d_clamp, c->d_y, c->d_z, c->d_segpow, c->d_counters,
                   c->d_in[0], c->d_in[1], c->d_ref[0], c->d_ref[1], c->d_dec[0], c->d_dec[1]};
   for (void* p : ptrs) dfree(c, p);
   c->guards.clear();
@@ -531,6 +532,7 @@ kk_status kk_init(const kk_config* cfg, kk_ctx** out) {
   chk(dalloc(c, "clamp", &c->d_clamp, (size_t)(nE / kk::kHilbertHop) * sizeof(int)));
   chk(dalloc(c, "y", &c->d_y, (size_t)(n / 2 + 2 * c->Ky + 2) * sizeof(float2)));
   if (cfg->keep_intermediate) chk(dalloc(c, "z", &c->d_z, (size_t)(n / 4) * sizeof(float2)));
+  if (ddlms) chk(dalloc(c, "segpow", &c->d_segpow, (size_t)((n / 2 + 2 * c->Ky) / 128 + 2 * (c->mfKeep / 128) + 64) * sizeof(float)));
   chk(dalloc(c, "counters", &c->d_counters, 32 * sizeof(unsigned long long)));
   chk(cudaMemset(c->d_counters, 0, 32 * sizeof(unsigned long long)));
   if (e == cudaSuccess) {
@@ -621,7 +623,7 @@ kk_status kk_process_frames_ex(kk_ctx* c, const void* d_adc, int64_t first, int6
   const int64_t t_lo = fdiv(y_first, c->mfKeep);
   const int64_t t_hi = fdiv(y_first + y_count - 1, c->mfKeep);
   if (c->timing) cudaEventRecord(tev[1], s);
-  kk::K2Params p2{cf.lo_num, cf.lo_den};
+  kk::K2Params p2{cf.lo_num, cf.lo_den, c->d_segpow, t_lo * (c->mfKeep / 128)};
   kk::launch_k2(c->mfN, c->d_E, first - F, c->d_part, c->d_clamp, jb0, t_lo, t_hi - t_lo + 1, c->d_y, y_first,
                 y_count, c->d_H, c->d_Hc, c->d_lo, c->d_tw256, c->d_twN, c->d_twI, p2, c->num_sms, s);
 
@@ -638,6 +640,8 @@ kk_status kk_process_frames_ex(kk_ctx* c, const void* d_adc, int64_t first, int6
   const int64_t nfr = n / F;
   if (c->ddlms) {
     kk::K3DParams pd;
+    pd.seg_pow = c->d_segpow;
+    pd.seg_first = p2.seg_first;
     pd.schedule = c->d_sched;
     pd.n_segments = cf.n_segments;
     pd.segment_frames = cf.segment_frames;

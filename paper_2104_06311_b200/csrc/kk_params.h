@@ -42,6 +42,8 @@ struct K1UParams {                  // K1 + 2× upsampling (DESIGN.md §3 "KK up
 
 struct K2Params {
   int lo_num, lo_den;
+  float* seg_pow;                    // DDLMS mode (CH): Σ|y[2n]|² per 64-symbol segment (global y/128 grid)
+  int64_t seg_first;                 // global segment index of seg_pow[0]
 };
 
 struct K3Params {
@@ -55,6 +57,8 @@ struct K3Params {
 };
 
 struct K3DParams {
+  const float* seg_pow;              // from K2: Σ|y[2n]|² per 64-symbol segment
+  int64_t seg_first;                 // global segment index of seg_pow[0]
   const uint8_t* schedule;
   int n_segments;
   int64_t segment_frames;
