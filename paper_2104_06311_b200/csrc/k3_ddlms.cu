@@ -73,13 +73,16 @@ k3_ddlms_kernel(const float2* __restrict__ y, int64_t y_base, int64_t sym_first,
     // loaded one chunk ahead; byte accesses when a pointer is not 8-byte aligned
     const bool ref8 = ref && ((reinterpret_cast<uintptr_t>(ref) & 7) == 0);
     const bool dec8 = dec && ((reinterpret_cast<uintptr_t>(dec) & 7) == 0);
-    uint2 rnext = make_uint2(0u, 0u);
-    if (ref8 && W == 0) rnext = __ldg(reinterpret_cast<const uint2*>(ref + n_keep0));
+    // reference words two chunks ahead of use (ra: this chunk, rb: the next one)
+    auto rword = [&](int i) { return __ldg(reinterpret_cast<const uint2*>(ref + (n0 + i))); };
+    uint2 ra = make_uint2(0u, 0u), rb = make_uint2(0u, 0u);
+    if (ref8 && 0 >= W) ra = rword(0);
+    if (ref8 && PF >= W && PF < total) rb = rword(PF);
     for (int i0 = 0; i0 < total; i0 += PF) {
       const bool kept = i0 >= W;
-      const uint2 rcur = rnext;
-      if (ref8 && i0 + PF >= W && i0 + PF < total)
-        rnext = __ldg(reinterpret_cast<const uint2*>(ref + (n0 + i0 + PF)));
+      const uint2 rcur = ra;
+      ra = rb;
+      if (ref8 && i0 + 2 * PF >= W && i0 + 2 * PF < total) rb = rword(i0 + 2 * PF);
       uint32_t dlo = 0u, dhi = 0u;
 #pragma unroll
       for (int q = 0; q < PF; ++q) {
@@ -94,12 +97,12 @@ k3_ddlms_kernel(const float2* __restrict__ y, int64_t y_base, int64_t sym_first,
         cmac(o0, v[0], cconj(x[0])); cmac(o1, v[1], cconj(x[1]));
         cmac(o0, v[2], cconj(x[2])); cmac(o1, v[3], cconj(x[3]));
         const float2 o = cadd(o0, o1);
-        const float2 d = sl.point(o);
+        int lab = 0;
+        const float2 d = kept ? sl.decide(o, lab) : sl.point(o);   // kept: point and label from one slicing
         const float2 e = csub(d, o);
         const float mu = kept ? p.mu : p.mu_warm;
         if (kept) {
           const int64_t kl = n;                                // local kept symbol index
-          const int lab = sl.label(o);
           if (ref) {
             const int r = ref8 ? (int)(((q < 4 ? rcur.x : rcur.y) >> (8 * (q & 3))) & 0xffu) : (int)__ldg(&ref[kl]);
             serr += (lab != r);

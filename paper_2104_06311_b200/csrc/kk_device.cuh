@@ -218,6 +218,13 @@ struct Slicer {
     levels(z, iI, iQ);
     return cross ? cross32_label(iI, iQ) : ((gray(iI) << hb) | gray(iQ));
   }
+  // point and label of one decision from a single level computation (same values as point() / label())
+  __device__ __forceinline__ float2 decide(float2 z, int& lab) const {
+    int iI, iQ;
+    levels(z, iI, iQ);
+    lab = cross ? cross32_label(iI, iQ) : ((gray(iI) << hb) | gray(iQ));
+    return make_float2((float)(2 * iI - (mI - 1)) * inv_s, (float)(2 * iQ - (mQ - 1)) * inv_s);
+  }
 };
 
 // ------------------------------------------------------------------ TMA 1-D bulk copy (cp.async.bulk) + mbarrier
