@@ -308,3 +308,16 @@ def test_mf8192_grid_parity(kw):
     rx = receiver_for(case, keep=True, mf_fft_n=8192)
     gpu, orc = run_gpu(case, rx=rx), run_oracle(case)
     _check_all(case, gpu, orc)
+
+
+# ----------------------------------------------------------------------------- far into the stream
+@pytest.mark.parametrize("kw", [dict(M=16, dl=112000.0, esn0=17.0),
+                                dict(formats=(4, 8, 16, 32, 64), segment_frames=3, dl=32000.0, esn0=24.0,
+                                     eq_mode="ddlms"),
+                                dict(M=64, dl=32000.0, esn0=26.0, upsample=2)])
+def test_global_index_2_40(kw):
+    """first_sample = 2^40 (≈ 4.6 min of stream): the LO index (129·n mod 1000), frame and segment numbers,
+    the format schedule and the generator's hash all run on 64-bit global positions."""
+    case = make_case(n=3 * F, first=1 << 40, seed=161, **kw)
+    gpu, orc = run_gpu(case), run_oracle(case)
+    _check_all(case, gpu, orc)
