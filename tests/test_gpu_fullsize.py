@@ -1,4 +1,5 @@
-"""GPU parity at BASELINE.json's full sizes, in the launch configuration bench.py times (2^26-sample calls),
+"""GPU parity at BASELINE.json's full sizes, in the launch configuration bench.py times (calls of
+min(2^28, S) samples),
 checked on frames sampled across the stream (the oracle recomputes each sampled run of frames from the same
 int16 codes with its halo), plus properties that hold at any size (counts add up, chunking invariance).
 
@@ -22,7 +23,7 @@ from oracle import theory  # noqa: E402
 from paper_2104_06311_b200 import Receiver  # noqa: E402
 
 F, H = 16384, 16640
-CHUNK = 1 << 26
+CHUNK = 1 << 28          # bench.py --chunk default
 
 
 def _run_stream(lc, S, first=0, chunk=CHUNK):
@@ -98,12 +99,13 @@ def test_c4_full_size_sampled():
 
 
 def test_c5_bench_shard_sampled():
-    """The bench workload exactly: 2^32 samples of the mixed-format stream on one GPU in 2^26-sample calls;
-    sampled frames include every format and both ends of the shard and of several calls."""
+    """The bench workload exactly: 2^32 samples of the mixed-format stream on one GPU in 2^28-sample calls;
+    sampled frames include every format, format switches, both ends of the shard and runs straddling call
+    boundaries (16384 frames per call)."""
     lc = kkgen.WORKLOADS["C5"]["cfg"]
     S = 1 << 32
     nf = S // F
-    picks = [0, 255, 256 + 255, 4095, 4096 + 511, 1023 + 128, 1024 + 256 * 3, nf // 2, nf - 2]
+    picks = [0, 255, 256 + 255, 1023 + 128, 1024 + 256 * 3, 16383, 16384 + 255, 2 * 16384 - 1, nf // 2, nf - 2]
     st, bg, bo, n = _check_sampled(lc, S, picks=picks, nfr=2)
     assert all(v > 0 for v in st["sym"])    # every format of the schedule was received
     assert st["bit_err"][4] > 0          # 64-QAM at 26 dB has errors
