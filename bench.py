@@ -72,9 +72,10 @@ def env_rank():
 
 # ----------------------------------------------------------------------------------------------- per-unit work
 def k3_flops_per_symbol(L: int) -> float:
-    """pass 1 (L cMAC) + structured R (4L) + p (2L) + WL pass 2 (2L) = 9L complex MACs (8 flops) + ~40
-    (four slicers, unbias, CPR rotation)."""
-    return 8.0 * 9 * L + 40.0
+    """Real-form arithmetic of the widely-linear block-LS step: pass 1 (L complex MACs = 8L) +
+    lag sums (2L − 1 (ρ, d) pairs × 4 FMA, the shared real products of conj(a)·b and a·b) + cross-correlations
+    (L × 4 FMA for p1 and p2) + WL pass 2 (L × 4 FMA) = 40L − 8 flops, + ~40 (four slicers, unbias, CPR)."""
+    return 40.0 * L + 32.0
 
 
 def k2_tile_flops(n: int) -> float:

@@ -227,15 +227,19 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
           for (int gg = 0; gg < G; ++gg) {
             const int d = d0 + gg;
             if (d < ND) {
-              float2 s0 = make_float2(acc[8 * gg], acc[8 * gg + 1]), t0 = make_float2(acc[8 * gg + 2], acc[8 * gg + 3]);
-              cmac_conj(s0, w[0], w[d]);
-              cmac(t0, w[0], w[d]);
-              acc[8 * gg] = s0.x; acc[8 * gg + 1] = s0.y; acc[8 * gg + 2] = t0.x; acc[8 * gg + 3] = t0.y;
+              // conj(a)·b and a·b share the four real products: accumulate Σ ar·br, Σ ai·bi, Σ ar·bi, Σ ai·br
+              // (4 FMA for both); S = (A1 + A2, A3 − A4), T = (A1 − A2, A3 + A4) after the fp64 reduction
+              const float2 a0 = w[0], b0 = w[d];
+              acc[8 * gg] = fmaf(a0.x, b0.x, acc[8 * gg]);
+              acc[8 * gg + 1] = fmaf(a0.y, b0.y, acc[8 * gg + 1]);
+              acc[8 * gg + 2] = fmaf(a0.x, b0.y, acc[8 * gg + 2]);
+              acc[8 * gg + 3] = fmaf(a0.y, b0.x, acc[8 * gg + 3]);
               if (d < ND - 1) {
-                float2 s1 = make_float2(acc[8 * gg + 4], acc[8 * gg + 5]), t1 = make_float2(acc[8 * gg + 6], acc[8 * gg + 7]);
-                cmac_conj(s1, w[1], w[1 + d]);
-                cmac(t1, w[1], w[1 + d]);
-                acc[8 * gg + 4] = s1.x; acc[8 * gg + 5] = s1.y; acc[8 * gg + 6] = t1.x; acc[8 * gg + 7] = t1.y;
+                const float2 a1 = w[1], b1 = w[1 + d];
+                acc[8 * gg + 4] = fmaf(a1.x, b1.x, acc[8 * gg + 4]);
+                acc[8 * gg + 5] = fmaf(a1.y, b1.y, acc[8 * gg + 5]);
+                acc[8 * gg + 6] = fmaf(a1.x, b1.y, acc[8 * gg + 6]);
+                acc[8 * gg + 7] = fmaf(a1.y, b1.x, acc[8 * gg + 7]);
               }
             }
           }
@@ -247,7 +251,8 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
             pw = fmaf(y0.x, y0.x, fmaf(y0.y, y0.y, pw));
           }
         }
-        // red layout: [0, NP) p; [NP + 8·d + {S0re, S0im, T0re, T0im, S1re, S1im, T1re, T1im}]; [IPOW] power
+        // red layout: [0, NP) Σ ar·dr, Σ ai·di, Σ ar·di, Σ ai·dr per tap; [NP + 8·d + {A1, A2, A3, A4} (ρ = 0),
+        // + 4 + {…} (ρ = 1)]; [IPOW] power
         warp_partials<8 * G>(acc, red_w, Lay::NP + 8 * d0, lane);
         if (grp == 0) {
           pw = warp_sum(pw);
@@ -274,11 +279,11 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
           load_window(tid + K3_THREADS * s, w);
           const float2 d = sl.point(cscale(us[tid + K3_THREADS * s], g));
 #pragma unroll
-          for (int e = 0; e < L; ++e) {
-            float2 p1 = make_float2(acc[4 * e], acc[4 * e + 1]), p2 = make_float2(acc[4 * e + 2], acc[4 * e + 3]);
-            cmac_conj(p1, w[e], d);
-            cmac(p2, w[e], d);
-            acc[4 * e] = p1.x; acc[4 * e + 1] = p1.y; acc[4 * e + 2] = p2.x; acc[4 * e + 3] = p2.y;
+          for (int e = 0; e < L; ++e) {       // Σ ar·dr, Σ ai·di, Σ ar·di, Σ ai·dr → p1 = Σ conj(a)·d, p2 = Σ a·d
+            acc[4 * e] = fmaf(w[e].x, d.x, acc[4 * e]);
+            acc[4 * e + 1] = fmaf(w[e].y, d.y, acc[4 * e + 1]);
+            acc[4 * e + 2] = fmaf(w[e].x, d.y, acc[4 * e + 2]);
+            acc[4 * e + 3] = fmaf(w[e].y, d.x, acc[4 * e + 3]);
           }
         }
         warp_partials<Lay::NP>(acc, red_w, 0, lane);
@@ -300,8 +305,9 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
         for (int c = lane; c < 2 * ND; c += 32) {
           const int rho = c / ND, d = c % ND;
           if (rho == 1 && d == ND - 1) continue;
-          double sr = dres[Lay::NP + 8 * d + 4 * rho], si = dres[Lay::NP + 8 * d + 4 * rho + 1];
-          double tr_ = dres[Lay::NP + 8 * d + 4 * rho + 2], ti = dres[Lay::NP + 8 * d + 4 * rho + 3];
+          const double A1 = dres[Lay::NP + 8 * d + 4 * rho], A2 = dres[Lay::NP + 8 * d + 4 * rho + 1];
+          const double A3 = dres[Lay::NP + 8 * d + 4 * rho + 2], A4 = dres[Lay::NP + 8 * d + 4 * rho + 3];
+          double sr = A1 + A2, si = A3 - A4, tr_ = A1 - A2, ti = A3 + A4;   // S = Σ conj(a)·b, T = Σ a·b
           for (int i = -K + rho; i + d <= K; i += 2) {
             const int r = i + K, q = i + d + K;     // S(r, q) = Σ conj(a_r)·a_q, T(r, q) = Σ a_r·a_q
             if (wl) {
@@ -335,7 +341,8 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
         const double lam = wl ? (double)p.ridge * trG / (double)N : (double)p.ridge * 0.5 * trG / (double)L;
         if (lane < L) {
           const int e = lane;
-          const double p1r = dres[4 * e], p1i = dres[4 * e + 1], p2r = dres[4 * e + 2], p2i = dres[4 * e + 3];
+          const double B1 = dres[4 * e], B2 = dres[4 * e + 1], B3 = dres[4 * e + 2], B4 = dres[4 * e + 3];
+          const double p1r = B1 + B2, p1i = B3 - B4, p2r = B1 - B2, p2i = B3 + B4;   // p1 = Σ conj(a)·d, p2 = Σ a·d
           const float2 w0 = __ldg(&w_cd[e]);
           const double w0r = (double)g * (double)w0.x, w0i = (double)g * (double)w0.y;
           if (wl) {
@@ -445,9 +452,14 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
       // ---- sweep C: pass 2 y¹ = Σ_e w_e·a + v_e·conj(a) → us, and the gain-unbias sums (R27)
       float gr = 0.f, gi = 0.f, gd = 0.f;
       {
-        float2 tw[L], tv[L];
+        // w·a + v·conj(a) = (ar·(wr + vr) + ai·(vi − wi), ar·(wi + vi) + ai·(wr − vr)): 4 FMA per tap
+        float2 cr[L], ci[L];                   // cr = (wr + vr, wi + vi), ci = (vi − wi, wr − vr)
 #pragma unroll
-        for (int e = 0; e < L; ++e) { tw[e] = th[e]; tv[e] = th[L + e]; }
+        for (int e = 0; e < L; ++e) {
+          const float2 tw = th[e], tv = th[L + e];
+          cr[e] = make_float2(tw.x + tv.x, tw.y + tv.y);
+          ci[e] = make_float2(tv.y - tw.y, tw.x - tv.x);
+        }
 #pragma unroll 2
         for (int s = 0; s < K3_SPT; ++s) {
           const int kl = tid + K3_THREADS * s;
@@ -456,8 +468,10 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
           float2 o = make_float2(0.f, 0.f);
 #pragma unroll
           for (int e = 0; e < L; ++e) {
-            cmac(o, tw[e], w[e]);
-            cmac(o, tv[e], cconj(w[e]));
+            o.x = fmaf(w[e].x, cr[e].x, o.x);
+            o.x = fmaf(w[e].y, ci[e].x, o.x);
+            o.y = fmaf(w[e].x, cr[e].y, o.y);
+            o.y = fmaf(w[e].y, ci[e].y, o.y);
           }
           us[kl] = o;
           const float2 dd = sl.point(o);        // γ = Σ y¹·conj(D(y¹)) / Σ|D(y¹)|²
