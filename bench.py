@@ -95,9 +95,10 @@ def kernel_units(chunk: int, L: int, eq_mode: str = "block_ls", ddlms_block: int
     n_tiles = (chunk // 2 + 2 * K + keep - 1) // keep + 1
     frames = chunk // F
     if eq_mode == "ddlms":
-        # per processed symbol (kept + warm-up): output 8 cMAC + update 8 cMAC = 128 flops + ~20 (slicer, error)
+        # per processed symbol (kept + warm-up), real-form WL (DESIGN.md §5 K3′): output 4 taps × 4 FMA +
+        # update 4 taps × 4 FMA = 64 flops + ~20 (slicer, error)
         sym = chunk // 4 * (ddlms_block + ddlms_warmup) / ddlms_block
-        k3 = dict(flops=148.0 * sym, bytes=(8.0 * (ddlms_block + ddlms_warmup) / ddlms_block * 2 + 2.0) * (chunk // 4))
+        k3 = dict(flops=84.0 * sym, bytes=(8.0 * (ddlms_block + ddlms_warmup) / ddlms_block * 2 + 2.0) * (chunk // 4))
         k2_flops = k2_tile_flops(mf_n) + (mf_n // 2) * 8.0   # complex H: 8 more flops per folded bin
     else:
         k3 = dict(flops=k3_flops_per_symbol(L) * 4096 * frames, bytes=73728.0 * frames)

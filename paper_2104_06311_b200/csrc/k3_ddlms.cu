@@ -23,6 +23,10 @@ namespace kk {
 
 constexpr int K3D_THREADS = 64;
 
+// WL = true: the widely-linear recursion in real form — per tap c = (wr + vr, vi − wi, wi + vi, wr − vr), so
+// o = (Σ xr·c1 + xi·c2, Σ xr·c3 + xi·c4) and w += μe·conj(x), v += μe·x become c += 2μe ⊗ (xr, xi)
+// (4 FMA per tap for each instead of 8). WL = false: linear taps only (v ≡ 0), complex form.
+template <bool WL>
 __global__ void __launch_bounds__(K3D_THREADS)
 k3_ddlms_kernel(const float2* __restrict__ y, int64_t y_base, int64_t sym_first, int n_blocks, int B, int W,
                 const int* __restrict__ clampcnt, int64_t clamp_frame_off, const uint8_t* __restrict__ ref,
@@ -55,13 +59,15 @@ k3_ddlms_kernel(const float2* __restrict__ y, int64_t y_base, int64_t sym_first,
     const float g = (P > 0.f) ? rsqrtf(P) : 1.0f;
     float2 w[4] = {make_float2(0.f, 0.f), make_float2(1.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
     float2 v[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+    // real form (WL): cr = (c1, c3) = (wr + vr, wi + vi), ci = (c2, c4) = (vi − wi, wr − vr); centre spike w1 = 1
+    float2 cr[4] = {make_float2(0.f, 0.f), make_float2(1.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+    float2 ci[4] = {make_float2(0.f, 0.f), make_float2(0.f, 1.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
     // window x = [u[2n+1], u[2n], u[2n−1], u[2n−2]]
     float2 x[4];
     x[0] = cscale(__ldg(&yy[2 * n0 + 1]), g);
     x[1] = cscale(__ldg(&yy[2 * n0]), g);
     x[2] = cscale(__ldg(&yy[2 * n0 - 1]), g);
     x[3] = cscale(__ldg(&yy[2 * n0 - 2]), g);
-    const bool wl = p.widely_linear != 0;
     // the new samples y[2n+2], y[2n+3] of the next PF symbols are kept in a register ring (loads issued PF
     // symbols ahead of use, so L2 latency is hidden behind the recursion)
     constexpr int PF = 8;
@@ -92,10 +98,18 @@ k3_ddlms_kernel(const float2* __restrict__ y, int64_t y_base, int64_t sym_first,
         if (i + PF < total) ring[q] = __ldg(reinterpret_cast<const float4*>(yy + 2 * (n + PF) + 2));
         // o = Σ_k w_k x_k + v_k conj(x_k) as two independent partial sums (shorter dependency chain)
         float2 o0 = make_float2(0.f, 0.f), o1 = make_float2(0.f, 0.f);
-        cmac(o0, w[0], x[0]); cmac(o1, w[1], x[1]);
-        cmac(o0, w[2], x[2]); cmac(o1, w[3], x[3]);
-        cmac(o0, v[0], cconj(x[0])); cmac(o1, v[1], cconj(x[1]));
-        cmac(o0, v[2], cconj(x[2])); cmac(o1, v[3], cconj(x[3]));
+        if constexpr (WL) {
+#pragma unroll
+          for (int k = 0; k < 4; k += 2) {
+            o0.x = fmaf(x[k].x, cr[k].x, o0.x);         o0.x = fmaf(x[k].y, ci[k].x, o0.x);
+            o0.y = fmaf(x[k].x, cr[k].y, o0.y);         o0.y = fmaf(x[k].y, ci[k].y, o0.y);
+            o1.x = fmaf(x[k + 1].x, cr[k + 1].x, o1.x); o1.x = fmaf(x[k + 1].y, ci[k + 1].x, o1.x);
+            o1.y = fmaf(x[k + 1].x, cr[k + 1].y, o1.y); o1.y = fmaf(x[k + 1].y, ci[k + 1].y, o1.y);
+          }
+        } else {
+          cmac(o0, w[0], x[0]); cmac(o1, w[1], x[1]);
+          cmac(o0, w[2], x[2]); cmac(o1, w[3], x[3]);
+        }
         const float2 o = cadd(o0, o1);
         int lab = 0;
         const float2 d = kept ? sl.decide(o, lab) : sl.point(o);   // kept: point and label from one slicing
@@ -112,11 +126,19 @@ k3_ddlms_kernel(const float2* __restrict__ y, int64_t y_base, int64_t sym_first,
           if (dec && !dec8) dec[kl] = (uint8_t)lab;
           if (zout) zout[kl] = o;
         }
-        const float2 me = cscale(e, mu);
+        if constexpr (WL) {
+          const float2 m2 = cscale(e, 2.f * mu);             // c += 2μe ⊗ (xr, xi)
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          cmac(w[k], me, cconj(x[k]));
-          if (wl) cmac(v[k], me, x[k]);
+          for (int k = 0; k < 4; ++k) {
+            cr[k].x = fmaf(m2.x, x[k].x, cr[k].x);
+            ci[k].x = fmaf(m2.x, x[k].y, ci[k].x);
+            cr[k].y = fmaf(m2.y, x[k].x, cr[k].y);
+            ci[k].y = fmaf(m2.y, x[k].y, ci[k].y);
+          }
+        } else {
+          const float2 me = cscale(e, mu);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) cmac(w[k], me, cconj(x[k]));
         }
         x[3] = x[1]; x[2] = x[0];
         x[1] = cscale(make_float2(nx.x, nx.y), g); x[0] = cscale(make_float2(nx.z, nx.w), g);
@@ -157,8 +179,12 @@ void launch_k3_ddlms(const float2* y, int64_t y_base, int64_t sym_first, int64_t
                      const int* clampcnt, int64_t clamp_frame_off, const uint8_t* ref, uint8_t* dec, float2* z,
                      unsigned long long* counters, const K3DParams& p, cudaStream_t s) {
   const unsigned grid = (unsigned)((n_blocks + K3D_THREADS - 1) / K3D_THREADS);
-  k3_ddlms_kernel<<<grid, K3D_THREADS, 0, s>>>(y, y_base, sym_first, (int)n_blocks, B, W, clampcnt, clamp_frame_off,
-                                               ref, dec, z, counters, p);
+  if (p.widely_linear)
+    k3_ddlms_kernel<true><<<grid, K3D_THREADS, 0, s>>>(y, y_base, sym_first, (int)n_blocks, B, W, clampcnt,
+                                                       clamp_frame_off, ref, dec, z, counters, p);
+  else
+    k3_ddlms_kernel<false><<<grid, K3D_THREADS, 0, s>>>(y, y_base, sym_first, (int)n_blocks, B, W, clampcnt,
+                                                        clamp_frame_off, ref, dec, z, counters, p);
 }
 
 }  // namespace kk
