@@ -190,13 +190,17 @@ struct Slicer {
     const float xu = z.x * s, yu = z.y * s;
     iI = pam_index(xu, mI);
     iQ = pam_index(yu, mQ);
-    if (cross && (iI == 0 || iI == 5) && (iQ == 0 || iQ == 5)) {
-      const float ax = fabsf(xu), ay = fabsf(yu);
-      const int iQa = (iQ == 0) ? 1 : 4, iIb = (iI == 0) ? 1 : 4;
-      if (ax > ay) iQ = iQa;
-      else if (ay > ax) iI = iIb;
-      else if (cross32_label(iI, iQa) < cross32_label(iIb, iQ)) iQ = iQa;
-      else iI = iIb;
+    if (cross) {                                        // uniform: one format per frame / block
+      // 32-cross corner cell → the nearer of the two adjacent points (rare); an exact tie (measure zero)
+      // goes to the lower label
+      if (__builtin_expect((iI == 0 || iI == 5) && (iQ == 0 || iQ == 5), 0)) {
+        const float ax = fabsf(xu), ay = fabsf(yu);
+        const int iQa = (iQ == 0) ? 1 : 4, iIb = (iI == 0) ? 1 : 4;
+        if (ax > ay) iQ = iQa;
+        else if (ay > ax) iI = iIb;
+        else if (__builtin_expect(cross32_label(iI, iQa) < cross32_label(iIb, iQ), 0)) iQ = iQa;
+        else iI = iIb;
+      }
     }
   }
   // decided point. Square/rectangular grids: level = 2·ceil(x/2 + (m−2)/2) − (m−1), clamped — the same
