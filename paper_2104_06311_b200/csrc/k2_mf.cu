@@ -219,25 +219,25 @@ k2_mf_kernel(const float2* __restrict__ E, int64_t E_first, const float2* __rest
         }
       }
       if constexpr (CH) {
-        // per-64-symbol (128-sample) segment power for K3′'s AGC: output p = j + 256 r lies in tile segment
-        // 2(r − 1) + (j ≥ 128); warp sums, then the 4 (T = 128) or 4 (T = 256, per half) warp partials of a
-        // segment in fixed order → deterministic. Segment g (global) = m / 128.
-        constexpr int NSEG = KEEP / 128;
-        float* red = reinterpret_cast<float*>(lo_s + p.lo_den);   // NSEG × 4 floats past the LO table
+        // per-256-symbol (512-sample) segment power for K3′'s AGC: output p = j + 256 r lies in tile segment
+        // (r − 1)/2 for every j, so each thread sums its values per segment, then warp sums and the warps'
+        // partials in fixed order → deterministic. Segment g (global) = m / 512.
+        constexpr int NSEG = KEEP / 512;                      // 3 (4096 grid) or 7 (8192 grid)
+        constexpr int NW = T / 32;
+        float* red = reinterpret_cast<float*>(lo_s + p.lo_den);   // NSEG × NW floats past the LO table
 #pragma unroll
-        for (int it = 0; it < PER3; ++it) {
-          const int j = tid + T * it;
+        for (int sg = 0; sg < NSEG; ++sg) {
+          float a = 0.f;
 #pragma unroll
-          for (int r = 1; r < RI3 - 1; ++r) {
-            const float s = warp_sum(pw[it][r]);
-            const int seg = 2 * (r - 1) + (j >= 128 ? 1 : 0);
-            if (lane == 0) red[seg * 4 + ((j & 127) >> 5)] = s;
-          }
+          for (int it = 0; it < PER3; ++it) a += pw[it][2 * sg + 1] + pw[it][2 * sg + 2];
+          a = warp_sum(a);
+          if (lane == 0) red[sg * NW + warp] = a;
         }
         __syncthreads();
         if (tid < NSEG) {
-          const float s = ((red[tid * 4] + red[tid * 4 + 1]) + red[tid * 4 + 2]) + red[tid * 4 + 3];
-          p.seg_pow[t * (KEEP / 128) + tid - p.seg_first] = s;
+          float a = 0.f;
+          for (int w8 = 0; w8 < NW; ++w8) a += red[tid * NW + w8];
+          p.seg_pow[t * NSEG + tid - p.seg_first] = a;
         }
       }
       __syncthreads();                                        // buf is rewritten by the next tile
@@ -254,7 +254,7 @@ static void launch_k2_t(const float2* E, int64_t E_first, const float2* part, in
   int64_t grid = (int64_t)num_sms * (16384 / NF);
   if (grid > n_tiles) grid = n_tiles;
   const size_t dyn = (size_t)(NF + NF / 16) * sizeof(float2) + (size_t)p.lo_den * sizeof(float2) +
-                     (CH ? (size_t)(NF / 2 - 512) / 128 * 4 * sizeof(float) : 0);
+                     (CH ? (size_t)(NF / 2 - 512) / 512 * (NF / 1024) * sizeof(float) : 0);
   cudaFuncSetAttribute(k2_mf_kernel<NF, CH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
   k2_mf_kernel<NF, CH><<<(unsigned)grid, T, dyn, s>>>(E, E_first, part, jb0, tile0, n_tiles, y, y_first, y_count,
                                                       Hs, Hc, lo_tab, tw256, twN, twI, p);

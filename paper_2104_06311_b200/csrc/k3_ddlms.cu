@@ -49,12 +49,18 @@ k3_ddlms_kernel(const float2* __restrict__ y, int64_t y_base, int64_t sym_first,
   const int64_t n0 = n_keep0 - W;
   int serr = 0, berr = 0;
   if (!dead) {
-    // AGC over the block and its warm-up (symbol-centre samples): K2 summed |y[2n]|² per 64-symbol segment
-    // (global grid), so the block's power is (W + B)/64 segment sums — no second pass over y
-    const int64_t g0 = (sym_first + n0) >> 6;                  // first segment (floor; W, B multiples of 64)
-    const float* sp = p.seg_pow + (g0 - p.seg_first);
+    // AGC over the block and its warm-up (symbol-centre samples): K2 summed |y[2n]|² per 256-symbol segment
+    // (global grid); the block's range [n_keep0 − W, n_keep0 + B) is (W mod 256) leading symbols read here plus
+    // whole segments — no second pass over the block's samples
+    const int Wr = W & 255;
     float pw = 0.f;
-    for (int q = 0; q < (W + B) / 64; ++q) pw += __ldg(&sp[q]);
+    for (int i = 0; i < Wr; ++i) {
+      const float2 c = __ldg(&yy[2 * (n0 + i)]);
+      pw = fmaf(c.x, c.x, fmaf(c.y, c.y, pw));
+    }
+    const int64_t g0 = (sym_first + n0 + Wr) >> 8;             // first whole segment
+    const float* sp = p.seg_pow + (g0 - p.seg_first);
+    for (int q = 0; q < (W - Wr + B) / 256; ++q) pw += __ldg(&sp[q]);
     const float P = pw / (float)(W + B);
     const float g = (P > 0.f) ? rsqrtf(P) : 1.0f;
     float2 w[4] = {make_float2(0.f, 0.f), make_float2(1.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};

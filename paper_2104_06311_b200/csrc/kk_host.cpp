@@ -532,7 +532,7 @@ kk_status kk_init(const kk_config* cfg, kk_ctx** out) {
   chk(dalloc(c, "clamp", &c->d_clamp, (size_t)(nE / kk::kHilbertHop) * sizeof(int)));
   chk(dalloc(c, "y", &c->d_y, (size_t)(n / 2 + 2 * c->Ky + 2) * sizeof(float2)));
   if (cfg->keep_intermediate) chk(dalloc(c, "z", &c->d_z, (size_t)(n / 4) * sizeof(float2)));
-  if (ddlms) chk(dalloc(c, "segpow", &c->d_segpow, (size_t)((n / 2 + 2 * c->Ky) / 128 + 2 * (c->mfKeep / 128) + 64) * sizeof(float)));
+  if (ddlms) chk(dalloc(c, "segpow", &c->d_segpow, (size_t)((n / 2 + 2 * c->Ky) / 512 + 2 * (c->mfKeep / 512) + 16) * sizeof(float)));
   chk(dalloc(c, "counters", &c->d_counters, 32 * sizeof(unsigned long long)));
   chk(cudaMemset(c->d_counters, 0, 32 * sizeof(unsigned long long)));
   if (e == cudaSuccess) {
@@ -623,7 +623,7 @@ kk_status kk_process_frames_ex(kk_ctx* c, const void* d_adc, int64_t first, int6
   const int64_t t_lo = fdiv(y_first, c->mfKeep);
   const int64_t t_hi = fdiv(y_first + y_count - 1, c->mfKeep);
   if (c->timing) cudaEventRecord(tev[1], s);
-  kk::K2Params p2{cf.lo_num, cf.lo_den, c->d_segpow, t_lo * (c->mfKeep / 128)};
+  kk::K2Params p2{cf.lo_num, cf.lo_den, c->d_segpow, t_lo * (c->mfKeep / 512)};
   kk::launch_k2(c->mfN, c->d_E, first - F, c->d_part, c->d_clamp, jb0, t_lo, t_hi - t_lo + 1, c->d_y, y_first,
                 y_count, c->d_H, c->d_Hc, c->d_lo, c->d_tw256, c->d_twN, c->d_twI, p2, c->num_sms, s);
 

@@ -42,7 +42,7 @@ struct K1UParams {                  // K1 + 2× upsampling (DESIGN.md §3 "KK up
 
 struct K2Params {
   int lo_num, lo_den;
-  float* seg_pow;                    // DDLMS mode (CH): Σ|y[2n]|² per 64-symbol segment (global y/128 grid)
+  float* seg_pow;                    // DDLMS mode (CH): Σ|y[2n]|² per 256-symbol segment (global y/512 grid)
   int64_t seg_first;                 // global segment index of seg_pow[0]
 };
 
@@ -57,7 +57,7 @@ struct K3Params {
 };
 
 struct K3DParams {
-  const float* seg_pow;              // from K2: Σ|y[2n]|² per 64-symbol segment
+  const float* seg_pow;              // from K2: Σ|y[2n]|² per 256-symbol segment
   int64_t seg_first;                 // global segment index of seg_pow[0]
   const uint8_t* schedule;
   int n_segments;
