@@ -23,11 +23,6 @@ __device__ __forceinline__ void cmac(float2& acc, float2 a, float2 b) {
   acc.x = fmaf(a.x, b.x, acc.x); acc.x = fmaf(-a.y, b.y, acc.x);
   acc.y = fmaf(a.x, b.y, acc.y); acc.y = fmaf(a.y, b.x, acc.y);
 }
-// acc += conj(a) * b
-__device__ __forceinline__ void cmac_conj(float2& acc, float2 a, float2 b) {
-  acc.x = fmaf(a.x, b.x, acc.x); acc.x = fmaf(a.y, b.y, acc.x);
-  acc.y = fmaf(a.x, b.y, acc.y); acc.y = fmaf(-a.y, b.x, acc.y);
-}
 
 // ------------------------------------------------------------------ register DFT
 // cos(2πk/32) for k = 0..8 (quarter wave); other angles by symmetry. Folded to immediates after unroll.
