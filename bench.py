@@ -60,6 +60,9 @@ def parse():
                          "holds the whole stream and sends each rank its windows over NVLink (single; NEXT-3)")
     ap.add_argument("--mf-n", type=int, default=4096, choices=[4096, 8192],
                     help="K2 overlap-save grid: FFT4096/hop 3072 or FFT8192/hop 7168 (same exact convolution)")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process group for N > 1 (gloo only for functional smoke runs of the multi-rank path on "
+                         "fewer GPUs than ranks; never for timing)")
     ap.add_argument("--ddlms-block", type=int, default=256)
     ap.add_argument("--ddlms-warmup", type=int, default=512)
     ap.add_argument("--ddlms-mu-warm", type=float, default=2e-3)
@@ -361,10 +364,14 @@ def main():
     from paper_2104_06311_b200 import Receiver, kkrx, stats_from_words
     from paper_2104_06311_b200 import shard as SH
 
+    local = local % max(torch.cuda.device_count(), 1)    # = LOCAL_RANK on a node with one GPU per rank
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if a.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
     wl = kkgen.WORKLOADS[a.workload]
     lc = wl["cfg"]
     S = a.samples_per_gpu

@@ -84,6 +84,9 @@ def _distribute_cuda(shards, chunk, process, host_stream, stream_first, src, dev
     me = shards[rank]
     halo = me.halo
     n_max = max(s.n for s in shards)
+    # gloo cannot move CUDA tensors point-to-point: stage through host memory (functional smoke runs of the
+    # multi-rank path on fewer GPUs than ranks only — NCCL is the transport on a real multi-GPU node)
+    via_host = dist.is_initialized() and dist.get_backend(group) == "gloo"
     cs = torch.cuda.current_stream(dev)
     xs = torch.cuda.Stream(device=dev)
     bufs = [torch.empty(chunk + 2 * halo, dtype=dtype, device=dev) for _ in range(2)]
@@ -115,13 +118,21 @@ def _distribute_cuda(shards, chunk, process, host_stream, stream_first, src, dev
                     if stage_work[si] is not None:
                         stage_work[si].wait()            # xs waits for the send that last used this buffer
                     st = stage[si]
+                    if via_host:
+                        dist.send(view.contiguous(), dst=r, group=group)
+                        continue
                     st[:b - a].copy_(view, non_blocking=True)
                     stage_work[si] = dist.isend(st[:b - a], dst=r, group=group)
                     si ^= 1
             elif c0 < me.n:
                 a, b = window_bounds(me, c0, min(chunk, me.n - c0))
-                work = dist.irecv(buf[:b - a], src=src, group=group)
-                work.wait()                              # xs waits for the transfer
+                if via_host:
+                    hb = torch.empty(b - a, dtype=dtype)
+                    dist.recv(hb, src=src, group=group)
+                    buf[:b - a].copy_(hb)
+                else:
+                    work = dist.irecv(buf[:b - a], src=src, group=group)
+                    work.wait()                          # xs waits for the transfer
             ready.record(xs)
         if c0 < me.n:
             nc = min(chunk, me.n - c0)
