@@ -256,7 +256,7 @@ def _data_field(cfg: LinkConfig, s0: int, s1: int, device, guard_sym: int = 1024
 
 
 GEN_GRID = 1 << 18        # samples per generation chunk on the CPU, anchored at global sample 0
-GEN_GRID_CUDA = 1 << 22   # on a GPU (fewer launches; invariance holds per device type)
+GEN_GRID_CUDA = 1 << 24   # on a GPU (fewer launches; invariance holds per device type)
 
 
 def gen_grid(device) -> int:

@@ -72,7 +72,7 @@ def main():
     ap.add_argument("--dl", type=float, default=152000.0)          # 7600 km at 20 ps/nm/km
     ap.add_argument("--cspr", type=float, default=12.0)
     ap.add_argument("--piece", type=int, default=1 << 30)
-    ap.add_argument("--chunk", type=int, default=1 << 26)
+    ap.add_argument("--chunk", type=int, default=1 << 28)
     ap.add_argument("--out", default="")
     a = ap.parse_args()
     res = [run(m, e, a.dl, a.seconds, a.cspr, a.piece, a.chunk, seed=700 + m) for m, e in zip(a.formats, a.esn0)]
