@@ -62,9 +62,27 @@ def main():
     ap.add_argument("--powers", type=float, nargs="+", default=[-16, -14, -12, -10, -8, -6, -4, -2, 0])
     ap.add_argument("--csprs", type=float, nargs="+", default=[6.0, 8.0, 10.0])
     ap.add_argument("--out", default="")
+    ap.add_argument("--fig", default="2bc", choices=["2bc", "2a"])
     a = ap.parse_args()
     dev = torch.device("cuda", 0)
     t0 = time.time()
+    if a.fig == "2a":
+        # Q vs distance per format, launch power and CSPR optimised per point ("For each point, the
+        # launch power of the test channel ... and its CSPR were optimized")
+        dist = {4: (20, 40, 60, 80, 100), 8: (16, 36, 56, 76, 96), 16: (16, 28, 40, 56, 72), 32: (8, 16, 24, 36, 48),
+                64: (4, 8, 12, 16, 24)}
+        fig2a = []
+        for M, spans_list in dist.items():
+            for spans in spans_list:
+                pts = [best_over_cspr(M, spans, p, a.csprs, dev)[0] for p in a.powers]
+                opt = min(pts, key=_key)
+                fig2a.append(dict(M=M, km=spans * 100, p_opt_dbm=opt["p_dbm"], cspr_db=opt["cspr_db"],
+                                  q_db=opt["q_db"], ber=opt["ber"], snr_evm_db=opt["snr_evm_db"]))
+                print("2a", fig2a[-1], flush=True)
+        if a.out:
+            json.dump(dict(fig2a=fig2a, block_samples=ssfm.BLOCK, link=vars(ssfm.FiberLink()),
+                           seconds=time.time() - t0), open(a.out, "w"), indent=1)
+        return
     fig2b = []
     for M, spans in LIMITS.items():
         for p in a.powers:
