@@ -106,11 +106,9 @@ k3_ddlms_kernel(const float2* __restrict__ y, int64_t y_base, int64_t sym_first,
         float2 o0 = make_float2(0.f, 0.f), o1 = make_float2(0.f, 0.f);
         if constexpr (WL) {
 #pragma unroll
-          for (int k = 0; k < 4; k += 2) {
-            o0.x = fmaf(x[k].x, cr[k].x, o0.x);         o0.x = fmaf(x[k].y, ci[k].x, o0.x);
-            o0.y = fmaf(x[k].x, cr[k].y, o0.y);         o0.y = fmaf(x[k].y, ci[k].y, o0.y);
-            o1.x = fmaf(x[k + 1].x, cr[k + 1].x, o1.x); o1.x = fmaf(x[k + 1].y, ci[k + 1].x, o1.x);
-            o1.y = fmaf(x[k + 1].x, cr[k + 1].y, o1.y); o1.y = fmaf(x[k + 1].y, ci[k + 1].y, o1.y);
+          for (int k = 0; k < 4; k += 2) {              // o += xr·(c1, c3) + xi·(c2, c4), packed
+            ffma2s(o0, x[k].x, cr[k]);         ffma2s(o0, x[k].y, ci[k]);
+            ffma2s(o1, x[k + 1].x, cr[k + 1]); ffma2s(o1, x[k + 1].y, ci[k + 1]);
           }
         } else {
           cmac(o0, w[0], x[0]); cmac(o1, w[1], x[1]);
@@ -135,11 +133,9 @@ k3_ddlms_kernel(const float2* __restrict__ y, int64_t y_base, int64_t sym_first,
         if constexpr (WL) {
           const float2 m2 = cscale(e, 2.f * mu);             // c += 2μe ⊗ (xr, xi)
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            cr[k].x = fmaf(m2.x, x[k].x, cr[k].x);
-            ci[k].x = fmaf(m2.x, x[k].y, ci[k].x);
-            cr[k].y = fmaf(m2.y, x[k].x, cr[k].y);
-            ci[k].y = fmaf(m2.y, x[k].y, ci[k].y);
+          for (int k = 0; k < 4; ++k) {                 // (c1, c3) += xr·m2, (c2, c4) += xi·m2, packed
+            ffma2s(cr[k], x[k].x, m2);
+            ffma2s(ci[k], x[k].y, m2);
           }
         } else {
           const float2 me = cscale(e, mu);

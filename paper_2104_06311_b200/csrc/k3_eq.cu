@@ -229,30 +229,28 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
             if (d < ND) {
               // conj(a)·b and a·b share the four real products: accumulate Σ ar·br, Σ ai·bi, Σ ar·bi, Σ ai·br
               // (4 FMA for both); S = (A1 + A2, A3 − A4), T = (A1 − A2, A3 + A4) after the fp64 reduction
-              const float2 a0 = w[0], b0 = w[d];
-              acc[8 * gg] = fmaf(a0.x, b0.x, acc[8 * gg]);
-              acc[8 * gg + 1] = fmaf(a0.y, b0.y, acc[8 * gg + 1]);
-              acc[8 * gg + 2] = fmaf(a0.x, b0.y, acc[8 * gg + 2]);
-              acc[8 * gg + 3] = fmaf(a0.y, b0.x, acc[8 * gg + 3]);
+              // packed: (A1, A3) += ar·(br, bi), (A4, A2) += ai·(br, bi)  — 2 FFMA2
+              ffma2s(acc[8 * gg], acc[8 * gg + 1], w[0].x, w[d]);
+              ffma2s(acc[8 * gg + 2], acc[8 * gg + 3], w[0].y, w[d]);
               if (d < ND - 1) {
-                const float2 a1 = w[1], b1 = w[1 + d];
-                acc[8 * gg + 4] = fmaf(a1.x, b1.x, acc[8 * gg + 4]);
-                acc[8 * gg + 5] = fmaf(a1.y, b1.y, acc[8 * gg + 5]);
-                acc[8 * gg + 6] = fmaf(a1.x, b1.y, acc[8 * gg + 6]);
-                acc[8 * gg + 7] = fmaf(a1.y, b1.x, acc[8 * gg + 7]);
+                ffma2s(acc[8 * gg + 4], acc[8 * gg + 5], w[1].x, w[1 + d]);
+                ffma2s(acc[8 * gg + 6], acc[8 * gg + 7], w[1].y, w[1 + d]);
               }
             }
           }
           if (grp == 0) {                      // pass 1 (kept in us until sweep B) and its power
             float2 y0 = make_float2(0.f, 0.f);
 #pragma unroll
-            for (int e = 0; e < L; ++e) cmac(y0, wc[e], w[e]);
+            for (int e = 0; e < L; ++e) {        // w_cd·a = ar·(wr, wi) + ai·(−wi, wr)
+              ffma2s(y0, w[e].x, wc[e]);
+              ffma2s(y0, w[e].y, make_float2(-wc[e].y, wc[e].x));
+            }
             us[tid + K3_THREADS * s] = y0;
             pw = fmaf(y0.x, y0.x, fmaf(y0.y, y0.y, pw));
           }
         }
-        // red layout: [0, NP) Σ ar·dr, Σ ai·di, Σ ar·di, Σ ai·dr per tap; [NP + 8·d + {A1, A2, A3, A4} (ρ = 0),
-        // + 4 + {…} (ρ = 1)]; [IPOW] power
+        // red layout: [0, NP) {B1, B3, B4, B2} per tap; [NP + 8·d + {A1, A3, A4, A2} (ρ = 0), + 4 + {…} (ρ = 1)];
+        // [IPOW] power  (A1 = Σ ar·br, A2 = Σ ai·bi, A3 = Σ ar·bi, A4 = Σ ai·br; B likewise with d)
         warp_partials<8 * G>(acc, red_w, Lay::NP + 8 * d0, lane);
         if (grp == 0) {
           pw = warp_sum(pw);
@@ -279,11 +277,9 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
           load_window(tid + K3_THREADS * s, w);
           const float2 d = sl.point(cscale(us[tid + K3_THREADS * s], g));
 #pragma unroll
-          for (int e = 0; e < L; ++e) {       // Σ ar·dr, Σ ai·di, Σ ar·di, Σ ai·dr → p1 = Σ conj(a)·d, p2 = Σ a·d
-            acc[4 * e] = fmaf(w[e].x, d.x, acc[4 * e]);
-            acc[4 * e + 1] = fmaf(w[e].y, d.y, acc[4 * e + 1]);
-            acc[4 * e + 2] = fmaf(w[e].x, d.y, acc[4 * e + 2]);
-            acc[4 * e + 3] = fmaf(w[e].y, d.x, acc[4 * e + 3]);
+          for (int e = 0; e < L; ++e) {       // (B1, B3) += ar·(dr, di), (B4, B2) += ai·(dr, di): p1, p2 later
+            ffma2s(acc[4 * e], acc[4 * e + 1], w[e].x, d);
+            ffma2s(acc[4 * e + 2], acc[4 * e + 3], w[e].y, d);
           }
         }
         warp_partials<Lay::NP>(acc, red_w, 0, lane);
@@ -305,8 +301,8 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
         for (int c = lane; c < 2 * ND; c += 32) {
           const int rho = c / ND, d = c % ND;
           if (rho == 1 && d == ND - 1) continue;
-          const double A1 = dres[Lay::NP + 8 * d + 4 * rho], A2 = dres[Lay::NP + 8 * d + 4 * rho + 1];
-          const double A3 = dres[Lay::NP + 8 * d + 4 * rho + 2], A4 = dres[Lay::NP + 8 * d + 4 * rho + 3];
+          const double A1 = dres[Lay::NP + 8 * d + 4 * rho], A3 = dres[Lay::NP + 8 * d + 4 * rho + 1];
+          const double A4 = dres[Lay::NP + 8 * d + 4 * rho + 2], A2 = dres[Lay::NP + 8 * d + 4 * rho + 3];
           double sr = A1 + A2, si = A3 - A4, tr_ = A1 - A2, ti = A3 + A4;   // S = Σ conj(a)·b, T = Σ a·b
           for (int i = -K + rho; i + d <= K; i += 2) {
             const int r = i + K, q = i + d + K;     // S(r, q) = Σ conj(a_r)·a_q, T(r, q) = Σ a_r·a_q
@@ -341,7 +337,7 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
         const double lam = wl ? (double)p.ridge * trG / (double)N : (double)p.ridge * 0.5 * trG / (double)L;
         if (lane < L) {
           const int e = lane;
-          const double B1 = dres[4 * e], B2 = dres[4 * e + 1], B3 = dres[4 * e + 2], B4 = dres[4 * e + 3];
+          const double B1 = dres[4 * e], B3 = dres[4 * e + 1], B4 = dres[4 * e + 2], B2 = dres[4 * e + 3];
           const double p1r = B1 + B2, p1i = B3 - B4, p2r = B1 - B2, p2i = B3 + B4;   // p1 = Σ conj(a)·d, p2 = Σ a·d
           const float2 w0 = __ldg(&w_cd[e]);
           const double w0r = (double)g * (double)w0.x, w0i = (double)g * (double)w0.y;
@@ -467,11 +463,9 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
           load_window(kl, w);
           float2 o = make_float2(0.f, 0.f);
 #pragma unroll
-          for (int e = 0; e < L; ++e) {
-            o.x = fmaf(w[e].x, cr[e].x, o.x);
-            o.x = fmaf(w[e].y, ci[e].x, o.x);
-            o.y = fmaf(w[e].x, cr[e].y, o.y);
-            o.y = fmaf(w[e].y, ci[e].y, o.y);
+          for (int e = 0; e < L; ++e) {         // o += ar·(c1, c3) + ai·(c2, c4)
+            ffma2s(o, w[e].x, cr[e]);
+            ffma2s(o, w[e].y, ci[e]);
           }
           us[kl] = o;
           const float2 dd = sl.point(o);        // γ = Σ y¹·conj(D(y¹)) / Σ|D(y¹)|²

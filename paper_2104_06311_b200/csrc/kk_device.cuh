@@ -24,6 +24,14 @@ __device__ __forceinline__ float2 csub(float2 a, float2 b) {
       : "=f"(r.x), "=f"(r.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
   return r;
 }
+// (x, y) += s·(b.x, b.y) as one packed FP32x2 FMA (FFMA2 with a scalar-broadcast operand; each lane is the
+// scalar fmaf, so results are bit-identical to two FFMAs)
+__device__ __forceinline__ void ffma2s(float& x, float& y, float s, float2 b) {
+  asm("{\n\t.reg .b64 pa, pb, pc;\n\tmov.b64 pa, {%2, %2};\n\tmov.b64 pb, {%3, %4};\n\tmov.b64 pc, {%0, %1};\n\t"
+      "fma.rn.f32x2 pc, pa, pb, pc;\n\tmov.b64 {%0, %1}, pc;\n\t}"
+      : "+f"(x), "+f"(y) : "f"(s), "f"(b.x), "f"(b.y));
+}
+__device__ __forceinline__ void ffma2s(float2& acc, float s, float2 b) { ffma2s(acc.x, acc.y, s, b); }
 __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
   return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
 }
