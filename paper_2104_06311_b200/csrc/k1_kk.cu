@@ -142,7 +142,7 @@ k1_kk_kernel(const Tin* __restrict__ adc0, float2* __restrict__ E, float2* __res
     __sincosf(v[r].x * sc, &sn0, &cs0);
     __sincosf(v[r].y * sc, &sn1, &cs1);
     const float m0 = __expf(ab0[pos] + p.half_ln_iref), m1 = __expf(ab1[pos] + p.half_ln_iref);
-    const float2 e0 = make_float2(m0 * cs0, m0 * sn0), e1 = make_float2(m1 * cs1, m1 * sn1);
+    const float2 e0 = cscale(make_float2(cs0, sn0), m0), e1 = cscale(make_float2(cs1, sn1), m1);
     E0[pos] = e0;
     E1[pos] = e1;
     s0 = cadd(s0, e0);

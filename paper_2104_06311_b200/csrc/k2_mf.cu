@@ -148,7 +148,7 @@ k2_mf_kernel(const float2* __restrict__ E, int64_t E_first, const float2* __rest
 #pragma unroll
         for (int r = 0; r < 16; ++r) {
           const float2 A = (j + NJ1 * r < isplit) ? A0 : A1;
-          v[it][r] = cmul(make_float2(v[it][r].x - A.x, v[it][r].y - A.y), lo_s[q]);
+          v[it][r] = cmul(csub(v[it][r], A), lo_s[q]);
           q += stepJ; q -= (q >= p.lo_den) ? p.lo_den : 0;
         }
         dft_reg<16, -1>(v[it]);
@@ -185,7 +185,9 @@ k2_mf_kernel(const float2* __restrict__ E, int64_t E_first, const float2* __rest
             dst[r * (256 + 16)] = cadd(cmul(a, __ldg(&Hc[j + 256 * r])), cmul(b, __ldg(&Hc[j + 256 * (r + R3 / 2)])));
           } else {
             const float ha = __ldg(&Hs[j + 256 * r]), hb = __ldg(&Hs[j + 256 * (r + R3 / 2)]);
-            dst[r * (256 + 16)] = make_float2(fmaf(a.x, ha, b.x * hb), fmaf(a.y, ha, b.y * hb));
+            float2 yv = cscale(b, hb);                         // packed: b·hb, then + a·ha (same roundings)
+            ffma2s(yv, ha, a);
+            dst[r * (256 + 16)] = yv;
           }
         }
       }
