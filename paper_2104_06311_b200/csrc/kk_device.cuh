@@ -174,11 +174,6 @@ __device__ __forceinline__ float warp_sum(float v) {
 // Decision regions: per axis, a value exactly on a boundary goes to the lower level; the 32-cross
 // corner cells go to the nearer of the two adjacent points (ties to the lower label).
 __device__ __forceinline__ int gray(int i) { return i ^ (i >> 1); }
-// level index of a PAM slicer with m levels at odd integers −(m−1)..(m−1), x in grid units
-__device__ __forceinline__ int pam_index(float x, int m) {
-  int i = (int)ceilf(0.5f * (x + (float)(m - 2)));
-  return min(max(i, 0), m - 1);
-}
 // 32-cross label of grid cell (iI, iQ) (level index 0 = −5); corners unused.
 // rows iQ = 0..5 (Q = −5..+5), 5 bits per column iI = 0..5.
 __device__ __forceinline__ int cross32_label(int iI, int iQ) {
@@ -196,9 +191,21 @@ __device__ __forceinline__ int cross32_label(int iI, int iQ) {
 }
 
 // runtime-uniform QAM slicer parameters (CTA-uniform: one format per frame, R26)
+//
+// Per axis with m levels at the odd integers −(m−1)..(m−1) (grid units x·s): the decided level is 2r − 1 with
+// r = ceil(x·s/2) clamped to [−(m−2)/2, m/2] — a value exactly on a boundary (x·s/2 an integer) goes to the lower
+// level. r is formed on the FMA pipe: t = kSliceMagic + x·(s/2) rounded toward +∞ (one FFMA2.RP for both axes;
+// kSliceMagic = 1.5·2²³ has ulp 1, so t − kSliceMagic = ceil(x·s/2) exactly for |x·s/2| < 2²²), clamped in the
+// biased domain; the level index r + (m−2)/2 is then an integer subtraction on the bits of t, and the decided
+// point (2r − 1)/s one FADD2 + one FFMA2 (the same value as the former FRND.CEIL / F2I path, which rounded x·s
+// first; both are exact ceil semantics, they can differ only within one fp32 ulp of a boundary). A NaN input
+// clamps to the lowest level on both paths.
+constexpr float kSliceMagic = 12582912.0f;   // 1.5·2^23
 struct Slicer {
   int mI, mQ, hb, cross;
   float s, inv_s;
+  float sh, loI, hiI, loQ, hiQ;   // s/2; clamp bounds of t per axis
+  int offI, offQ;                 // level index = bits(t) − off
   __device__ __forceinline__ void init(int M) {
     cross = (M == 32);
     if (M == 8) { mI = 4; mQ = 2; hb = 1; s = 2.44948974278317810f; }
@@ -209,16 +216,38 @@ struct Slicer {
       s = (M == 4) ? 1.41421356237309505f : (M == 16) ? 3.16227766016837933f : 6.48074069840786023f;
     }
     inv_s = 1.0f / s;
+    sh = 0.5f * s;
+    loI = kSliceMagic - (float)((mI - 2) / 2); hiI = kSliceMagic + (float)(mI / 2);
+    loQ = kSliceMagic - (float)((mQ - 2) / 2); hiQ = kSliceMagic + (float)(mQ / 2);
+    offI = __float_as_int(kSliceMagic) - (mI - 2) / 2;
+    offQ = __float_as_int(kSliceMagic) - (mQ - 2) / 2;
+  }
+  // biased, clamped per-axis ceil: t = kSliceMagic + clamp(ceil(z·s/2))
+  __device__ __forceinline__ float2 tq(float2 z) const {
+    float tx, ty;
+    asm("{\n\t.reg .b64 pa, pb, pc;\n\tmov.b64 pa, {%2, %3};\n\tmov.b64 pb, {%4, %4};\n\tmov.b64 pc, {%5, %5};\n\t"
+        "fma.rp.f32x2 pa, pa, pb, pc;\n\tmov.b64 {%0, %1}, pa;\n\t}"
+        : "=f"(tx), "=f"(ty) : "f"(z.x), "f"(z.y), "f"(sh), "f"(kSliceMagic));
+    return make_float2(fminf(fmaxf(tx, loI), hiI), fminf(fmaxf(ty, loQ), hiQ));
+  }
+  // point (2r − 1)/s from t: (t − kSliceMagic)·(2/s) − 1/s, each lane one exact subtraction + one rounding
+  __device__ __forceinline__ float2 point_t(float2 t) const {
+    float px, py;
+    asm("{\n\t.reg .b64 pa, pb, pc;\n\tmov.b64 pa, {%2, %3};\n\tmov.b64 pb, {%4, %4};\n\t"
+        "sub.rn.f32x2 pa, pa, pb;\n\tmov.b64 pb, {%5, %5};\n\tmov.b64 pc, {%6, %6};\n\t"
+        "fma.rn.f32x2 pa, pa, pb, pc;\n\tmov.b64 {%0, %1}, pa;\n\t}"
+        : "=f"(px), "=f"(py) : "f"(t.x), "f"(t.y), "f"(kSliceMagic), "f"(2.0f * inv_s), "f"(-inv_s));
+    return make_float2(px, py);
   }
   __device__ __forceinline__ void levels(float2 z, int& iI, int& iQ) const {
-    const float xu = z.x * s, yu = z.y * s;
-    iI = pam_index(xu, mI);
-    iQ = pam_index(yu, mQ);
+    const float2 t = tq(z);
+    iI = __float_as_int(t.x) - offI;
+    iQ = __float_as_int(t.y) - offQ;
     if (cross) {                                        // uniform: one format per frame / block
       // 32-cross corner cell → the nearer of the two adjacent points (rare); an exact tie (measure zero)
       // goes to the lower label
       if (__builtin_expect((iI == 0 || iI == 5) && (iQ == 0 || iQ == 5), 0)) {
-        const float ax = fabsf(xu), ay = fabsf(yu);
+        const float ax = fabsf(z.x * s), ay = fabsf(z.y * s);
         const int iQa = (iQ == 0) ? 1 : 4, iIb = (iI == 0) ? 1 : 4;
         if (ax > ay) iQ = iQa;
         else if (ay > ax) iI = iIb;
@@ -227,31 +256,35 @@ struct Slicer {
       }
     }
   }
-  // decided point. Square/rectangular grids: level = 2·ceil(x/2 + (m−2)/2) − (m−1), clamped — the same
-  // value as the integer path (scaling by ½ commutes with fp32 rounding), without int conversions.
+  __device__ __forceinline__ float2 point_i(int iI, int iQ) const {
+    return make_float2((float)(2 * iI - (mI - 1)) * inv_s, (float)(2 * iQ - (mQ - 1)) * inv_s);
+  }
+  // decided point
   __device__ __forceinline__ float2 point(float2 z) const {
-    if (!cross) {
-      const float hI = 0.5f * (float)(mI - 2), hQ = 0.5f * (float)(mQ - 2);
-      const float xu = z.x * s, yu = z.y * s;           // as in levels(): same roundings
-      const float lI = fminf(fmaxf(2.f * ceilf(fmaf(0.5f, xu, hI)) - (float)(mI - 1), -(float)(mI - 1)), (float)(mI - 1));
-      const float lQ = fminf(fmaxf(2.f * ceilf(fmaf(0.5f, yu, hQ)) - (float)(mQ - 1), -(float)(mQ - 1)), (float)(mQ - 1));
-      return make_float2(lI * inv_s, lQ * inv_s);
-    }
+    if (!cross) return point_t(tq(z));
     int iI, iQ;
     levels(z, iI, iQ);
-    return make_float2((float)(2 * iI - (mI - 1)) * inv_s, (float)(2 * iQ - (mQ - 1)) * inv_s);
+    return point_i(iI, iQ);
+  }
+  __device__ __forceinline__ int label_i(int iI, int iQ) const {
+    return cross ? cross32_label(iI, iQ) : ((gray(iI) << hb) | gray(iQ));
   }
   __device__ __forceinline__ int label(float2 z) const {
     int iI, iQ;
     levels(z, iI, iQ);
-    return cross ? cross32_label(iI, iQ) : ((gray(iI) << hb) | gray(iQ));
+    return label_i(iI, iQ);
   }
-  // point and label of one decision from a single level computation (same values as point() / label())
+  // point and label of one decision from a single slicing (same values as point() / label())
   __device__ __forceinline__ float2 decide(float2 z, int& lab) const {
+    if (!cross) {
+      const float2 t = tq(z);
+      lab = (gray(__float_as_int(t.x) - offI) << hb) | gray(__float_as_int(t.y) - offQ);
+      return point_t(t);
+    }
     int iI, iQ;
     levels(z, iI, iQ);
-    lab = cross ? cross32_label(iI, iQ) : ((gray(iI) << hb) | gray(iQ));
-    return make_float2((float)(2 * iI - (mI - 1)) * inv_s, (float)(2 * iQ - (mQ - 1)) * inv_s);
+    lab = cross32_label(iI, iQ);
+    return point_i(iI, iQ);
   }
 };
 
