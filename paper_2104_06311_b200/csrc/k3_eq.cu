@@ -24,7 +24,7 @@
 //    (G + λ/2·I)m_r = q_r + λ/2·m_r0 (r = 1, 2; G = Σ x xᵀ, q_1 = Σ x·Re d, q_2 = Σ x·Im d) with
 //    m_1 = [w_r + v_r; v_i − w_i], m_2 = [w_i + v_i; w_r − v_r]. G and q are read off S, T and p.
 //    Linear-only mode solves the real 2L form [[Re R, −Im R],[Im R, Re R]] of the Hermitian system.
-//    Both are solved in fp64 by the whole CTA (Gauss–Jordan on the 2L × (2L + 2) augmented matrix in
+//    Both are solved in fp64 by one warp (Gauss–Jordan on the 2L × (2L + 2) augmented matrix in
 //    shared memory, no pivoting on an SPD matrix; failure ⇒ fall back to θ₀ and count a bad frame).
 //
 // Mapping: persistent CTAs (256 threads, 2 per SM), one frame at a time; thread t owns symbols t + 256·s
@@ -45,6 +45,7 @@ namespace kk {
 constexpr int K3_THREADS = 256;
 constexpr int K3_WARPS = 8;
 constexpr int K3_SPT = kFrameSym / K3_THREADS;   // 16 symbols per thread
+constexpr int kGJWarpN = 18;                     // largest real system solved by one warp (2N fp64 registers/lane)
 
 // In-warp transpose-reduce of 32 floats: afterwards lane l holds the warp sum of element l.
 __device__ __forceinline__ float warp_transpose_reduce(float (&v)[32], int lane) {
@@ -288,7 +289,8 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
       cross_warp_sum(red, dres, NRED, NRED, tid);   // fp64, fixed order
       __syncthreads();
 
-      // ---- solve (warp 0): assemble the real system from S, T, p and Gauss–Jordan it
+      // ---- solve: warp 0 assembles the real system from S, T, p; Gauss–Jordan by warp 0 (N ≤ kGJWarpN) or the CTA
+      int fail = 0;
       if (warp == 0) {
         auto Ys = [&](int idx) -> double2 {
           const float2 v = ys[idx];
@@ -355,13 +357,59 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
           }
         }
         if (lane < N) A[lane * W + lane] += lam;
+        if constexpr (N <= kGJWarpN) {
+        __syncwarp();
+        // ---- Gauss–Jordan on [G + λI | q1 q2] by warp 0 with 2×2 pivot blocks (SPD ⇒ every leading 2×2 block
+        //      is SPD, no pivoting; N = 4K + 2 is even). Lane c holds column c in registers (a[i] = A[i][c]); per
+        //      step the two pivot lanes publish their columns as (A[i][k], A[i][k+1]) pairs in a double-buffered
+        //      shared strip (dres is consumed) that every lane reads with broadcast 16-B loads — no CTA barriers
+        //      and no shuffles (warp 0 runs this alone: shuffles in that branch would compile to collectives).
+        double a[N];
+#pragma unroll
+        for (int i = 0; i < N; ++i) a[i] = (lane < N + 2) ? A[i * W + lane] : 0.0;
+#pragma unroll
+        for (int k = 0; k < N; k += 2) {
+          double* col = dres + ((k >> 1) & 1) * (2 * N);
+          if (lane == k || lane == k + 1) {
+#pragma unroll
+            for (int i = 0; i < N; ++i) col[2 * i + (lane - k)] = a[i];
+          }
+          __syncwarp();
+          const double2 pk = reinterpret_cast<const double2*>(col)[k];       // (A[k][k], A[k][k+1])
+          const double2 pk1 = reinterpret_cast<const double2*>(col)[k + 1];  // (A[k+1][k], A[k+1][k+1])
+          const double pa = pk.x, pb = pk.y, pc = pk1.x, pd = pk1.y;
+          const double det = pa * pd - pb * pc;
+          fail |= !(pa > 0.0) || !(det > 0.0) || !isfinite(det);
+          // 1/det: fp32 seed + two Newton steps (relative error ~1e-28 → full double precision; det is the
+          // determinant of an SPD 2×2 pivot block ≥ λ² ≫ FLT_MIN, so the seed is finite when det is)
+          double idet = (double)__frcp_rn((float)det);
+          idet = idet * fma(-det, idet, 2.0);
+          idet = idet * fma(-det, idet, 2.0);
+          const double r0 = a[k], r1 = a[k + 1];
+          const double R0 = (pd * r0 - pb * r1) * idet, R1 = (pa * r1 - pc * r0) * idet;   // P⁻¹·[r0; r1]
+#pragma unroll
+          for (int i = 0; i < N; ++i) {
+            if (i == k || i == k + 1) continue;
+            const double2 c = reinterpret_cast<const double2*>(col)[i];      // (A[i][k], A[i][k+1])
+            a[i] = fma(-c.y, R1, fma(-c.x, R0, a[i]));
+          }
+          a[k] = R0;
+          a[k + 1] = R1;
+        }
+        // solution columns N, N+1 back to shared memory (rows < N)
+        if (lane == N || lane == N + 1) {
+#pragma unroll
+          for (int i = 0; i < N; ++i) A[i * W + lane] = a[i];
+        }
+        __syncwarp();
+        }
       }
-      __syncthreads();
       // ---- Gauss–Jordan on [G + λI | q1 q2] by the whole CTA with 2×2 pivot blocks (SPD ⇒ every leading
       //      2×2 block is SPD, no pivoting; N = 4K + 2 is even). The matrix lives in registers: lane = column c,
       //      warp w owns rows w, w+8, w+16, w+24. Per step the pivot columns arrive by warp shuffles and the two
       //      pivot rows through a double-buffered shared row pair — one barrier per step, N/2 steps.
-      {
+      if constexpr (N > kGJWarpN) {
+        __syncthreads();
         constexpr int W = Lay::WS;
         double* A = mat;
         double* prow = dres;                          // 2 buffers × 2 rows × 32 columns (dres is consumed)
@@ -371,7 +419,6 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
           const int i = warp + 8 * q;
           a[q] = (i < N && lane < N + 2) ? A[i * W + lane] : 0.0;
         }
-        int fail = 0;
         for (int k = 0, par = 0; k < N; k += 2, par ^= 1) {
           // owners of rows k, k+1 publish them (row k is row w = k % 8 of q = k / 8)
           double* pr = prow + par * 64;
@@ -415,8 +462,12 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
           if (i < N && (lane == N || lane == N + 1)) A[i * W + lane] = a[q];
         }
         __syncthreads();
-        // θ₁ from m1 = column N, m2 = column N+1 (rows e and L+e); fallback θ₀ on failure
-        if (warp == 0) {
+      }
+      // θ₁ from m1 = column N, m2 = column N+1 (rows e and L+e); fallback θ₀ on failure
+      if (warp == 0) {
+        __syncwarp();
+        constexpr int W = Lay::WS;
+        const double* A = mat;
           if (lane < N) fail |= !isfinite(A[lane * W + N]) || !isfinite(A[lane * W + N + 1]);
           fail = __any_sync(0xffffffffu, fail) ? 1 : 0;
           if (lane < L) {
@@ -441,7 +492,6 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
           }
           if (lane == 0) misc[1] = fail;
         }
-      }
       __syncthreads();
       bad |= misc[1];
 
