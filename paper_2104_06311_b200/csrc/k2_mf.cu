@@ -28,6 +28,24 @@ namespace kk {
 
 __device__ __forceinline__ int pad16(int i) { return i + (i >> 4); }
 
+__host__ __device__ constexpr int hibit16(int r) { return r >= 8 ? 8 : r >= 4 ? 4 : r >= 2 ? 2 : 1; }
+
+// v[r] ·= w^r (DIR < 0) or ·= conj(w)^r (DIR > 0) for r = 1..R−1, R ≤ 16, with tw[r·stride] = w^r. Only the
+// entries r = 1, 2, 4, 8 are loaded; every other power is the product of two loaded/formed ones (≤ 3 roundings
+// deep). K2 is bound by L1/shared-memory wavefronts, so 11 of 15 twiddle loads move to the FMA pipe (2 packed
+// instructions per product).
+template <int R, int DIR>
+__device__ __forceinline__ void apply_twiddles(float2 (&v)[R], const float2* __restrict__ tw, int stride) {
+  float2 w[R];
+#pragma unroll
+  for (int r = 1; r < R; r <<= 1) w[r] = __ldg(tw + r * stride);
+#pragma unroll
+  for (int r = 3; r < R; ++r)
+    if (r != hibit16(r)) w[r] = cmul(w[hibit16(r)], w[r - hibit16(r)]);
+#pragma unroll
+  for (int r = 1; r < R; ++r) v[r] = DIR < 0 ? cmul(v[r], w[r]) : cmulc(v[r], w[r]);
+}
+
 // One radix-R Stockham pass over an N-point array in shared memory (in place, barrier-separated).
 // tw: table of W_{Ns·R}^{r·k} laid out [r][k] (k < Ns), conjugated when DIR = +1.
 template <int N, int R, int Ns, int DIR, int T>
@@ -49,13 +67,7 @@ __device__ __forceinline__ void stockham_pass(float2* buf, const float2* __restr
   for (int it = 0; it < PER; ++it) {
     const int j = tid + it * T;
     const int k = j & (Ns - 1);
-    if (Ns > 1) {
-#pragma unroll
-      for (int r = 1; r < R; ++r) {
-        const float2 w = __ldg(&tw[r * Ns + k]);
-        v[it][r] = DIR < 0 ? cmul(v[it][r], w) : cmulc(v[it][r], w);
-      }
-    }
+    if (Ns > 1) apply_twiddles<R, DIR>(v[it], tw + k, Ns);
     dft_reg<R, DIR>(v[it]);
     const int idxD = (j / Ns) * Ns * R + k;
     // Ns = 1 (R = 16): pad16(16j + r) = 17j + r;  Ns ≥ 16: pad16(idxD + r·Ns) = pad16(idxD) + r·(Ns + Ns/16)
@@ -90,17 +102,21 @@ k2_mf_kernel(const float2* __restrict__ E, int64_t E_first, const float2* __rest
   constexpr int PER3 = 256 / T;              // last-pass DFTs per thread (2 / 1)
   extern __shared__ __align__(16) float2 k2_smem[];
   float2* buf = k2_smem;                                   // NF + NF/16 (padded tile)
-  float2* lo_s = k2_smem + NF + NF / 16;                   // lo_den
   __shared__ float2 A_s[2];
-  __shared__ int qb_s;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int i = tid; i < p.lo_den; i += T) lo_s[i] = lo_tab[i];
-  const int stepJ = (int)(((int64_t)NJ1 * p.lo_num) % p.lo_den);     // LO index step between r and r+1
-  // LO index of local sample j of a tile: (lo_num·(s0 + j)) mod lo_den = (qb + offj) mod lo_den with the
-  // tile base qb = (lo_num·s0) mod lo_den and the per-thread constant offj = (lo_num·j) mod lo_den
-  int offj[2];
+  // LO of local sample i = j + NJ1·r of a tile starting at global sample s0 (R9, exponents add mod lo_den):
+  //   LO[(lo_num·(s0 + i)) mod lo_den] = φ_t · λ_j · ρ^r,  φ_t = LO[qb_t], qb_t = (lo_num·s0) mod lo_den,
+  //   λ_j = LO[(lo_num·j) mod lo_den] (per thread, loaded once), ρ^r = LO[(r·NJ1·lo_num) mod lo_den] (p.rho)
+  // — no per-sample table lookups or index arithmetic; qb_t advances by a fixed dq between a CTA's tiles.
+  float2 lam[2];
 #pragma unroll
-  for (int it = 0; it < 2; ++it) offj[it] = (int)(((int64_t)(tid + T * it) * p.lo_num) % p.lo_den);
+  for (int it = 0; it < 2; ++it) lam[it] = __ldg(&lo_tab[(int)(((int64_t)(tid + T * it) * p.lo_num) % p.lo_den)]);
+  int qb;
+  {
+    const int64_t s0f = (tile0 + (n_tiles - 1 - (int64_t)blockIdx.x)) * HOP - LEAD;
+    qb = (int)((((s0f % p.lo_den) + p.lo_den) % p.lo_den) * p.lo_num % p.lo_den);
+  }
+  const int dq = (int)(((p.lo_den - ((int64_t)gridDim.x * HOP) % p.lo_den) % p.lo_den) * p.lo_num % p.lo_den);
 
   // tiles are visited from the END of the range: K1 wrote E front to back, so its most recent (L2-resident)
   // output is consumed first; K3 then walks y front to back, again reading K2's most recent writes first.
@@ -119,16 +135,15 @@ k2_mf_kernel(const float2* __restrict__ E, int64_t E_first, const float2* __rest
 #pragma unroll
       for (int r = 0; r < 16; ++r) v[it][r] = __ldg(src + NJ1 * r);
     }
-    // carrier estimates A_fa, A_fa+1 from K1's per-512-block sums (fixed order → deterministic); tile LO base
+    const float2 phi = __ldg(&lo_tab[qb]);
+    qb += dq; qb -= (qb >= p.lo_den) ? p.lo_den : 0;
+    // carrier estimates A_fa, A_fa+1 from K1's per-512-block sums (fixed order → deterministic)
     if (warp < 2) {
       const int64_t f = fa + warp;
       float2 a = make_float2(0.f, 0.f);
       if (warp == 0 || s0 + NF > fsplit) a = part[f * 32 - jb0 + lane];
       a.x = warp_sum(a.x); a.y = warp_sum(a.y);
       if (lane == 0) A_s[warp] = make_float2(a.x * (1.0f / kFrameSamp), a.y * (1.0f / kFrameSamp));
-    } else if (tid == 64) {
-      const int sm = (int)(((s0 % p.lo_den) + p.lo_den) % p.lo_den);
-      qb_s = (sm * p.lo_num) % p.lo_den;                    // < 4096², 32-bit
     }
     __syncthreads();
     // next tile's input (NF·8 bytes of E) → L2 while this tile computes
@@ -138,18 +153,20 @@ k2_mf_kernel(const float2* __restrict__ E, int64_t E_first, const float2* __rest
     }
     {
       const float2 A0 = A_s[0], A1 = A_s[1];
-      const int qb = qb_s;
       const int isplit = (int)(fsplit - s0);                 // first local sample of frame fa+1
 #pragma unroll
       for (int it = 0; it < 2; ++it) {
         const int j = tid + T * it;
-        int q = qb + offj[it];
-        q -= (q >= p.lo_den) ? p.lo_den : 0;
+        const float2 c = cmul(phi, lam[it]);                 // LO of sample j (r = 0)
+        if (isplit >= NF) {                                  // tile inside one frame (uniform branch)
 #pragma unroll
-        for (int r = 0; r < 16; ++r) {
-          const float2 A = (j + NJ1 * r < isplit) ? A0 : A1;
-          v[it][r] = cmul(csub(v[it][r], A), lo_s[q]);
-          q += stepJ; q -= (q >= p.lo_den) ? p.lo_den : 0;
+          for (int r = 0; r < 16; ++r) v[it][r] = cmul(csub(v[it][r], A0), r == 0 ? c : cmul(c, p.rho[r]));
+        } else {
+#pragma unroll
+          for (int r = 0; r < 16; ++r) {
+            const float2 A = (j + NJ1 * r < isplit) ? A0 : A1;
+            v[it][r] = cmul(csub(v[it][r], A), r == 0 ? c : cmul(c, p.rho[r]));
+          }
         }
         dft_reg<16, -1>(v[it]);
         float2* dst = buf + 17 * j;                          // pad16(16j + r) = 17j + r
@@ -174,8 +191,7 @@ k2_mf_kernel(const float2* __restrict__ E, int64_t E_first, const float2* __rest
 #pragma unroll
       for (int it = 0; it < PER3; ++it) {
         const int j = tid + T * it;
-#pragma unroll
-        for (int r = 1; r < R3; ++r) v3[it][r] = cmul(v3[it][r], __ldg(&twN[r * 256 + j]));
+        apply_twiddles<R3, -1>(v3[it], twN + j, 256);
         dft_reg<R3, -1>(v3[it]);
         float2* dst = buf + pad16(j);
 #pragma unroll
@@ -210,13 +226,13 @@ k2_mf_kernel(const float2* __restrict__ E, int64_t E_first, const float2* __rest
 #pragma unroll
       for (int it = 0; it < PER3; ++it) {
         const int j = tid + T * it;
-#pragma unroll
-        for (int r = 1; r < RI3; ++r) v3[it][r] = cmulc(v3[it][r], __ldg(&twI[r * 256 + j]));
+        apply_twiddles<RI3, +1>(v3[it], twI + j, 256);
         dft_reg<RI3, +1>(v3[it]);
+        const bool inside = (m_base + 256 >= y_first) && (m_base + NI - 256 <= y_first + y_count);   // tile-uniform
 #pragma unroll
         for (int r = 1; r < RI3 - 1; ++r) {                  // p = j + 256 r ∈ [256, NI − 256) ⇔ 1 ≤ r ≤ RI3 − 2
           const int64_t m = m_base + j + 256 * r;
-          if (m >= y_first && m < y_first + y_count) y[m - y_first] = v3[it][r];
+          if (inside || (m >= y_first && m < y_first + y_count)) y[m - y_first] = v3[it][r];
           if constexpr (CH) pw[it][r] = (j & 1) ? 0.f : fmaf(v3[it][r].x, v3[it][r].x, v3[it][r].y * v3[it][r].y);
         }
       }
@@ -226,7 +242,7 @@ k2_mf_kernel(const float2* __restrict__ E, int64_t E_first, const float2* __rest
         // partials in fixed order → deterministic. Segment g (global) = m / 512.
         constexpr int NSEG = KEEP / 512;                      // 3 (4096 grid) or 7 (8192 grid)
         constexpr int NW = T / 32;
-        float* red = reinterpret_cast<float*>(lo_s + p.lo_den);   // NSEG × NW floats past the LO table
+        float* red = reinterpret_cast<float*>(buf + NF + NF / 16);   // NSEG × NW floats past the tile
 #pragma unroll
         for (int sg = 0; sg < NSEG; ++sg) {
           float a = 0.f;
@@ -255,7 +271,7 @@ static void launch_k2_t(const float2* E, int64_t E_first, const float2* part, in
   constexpr int T = NF / 32;
   int64_t grid = (int64_t)num_sms * (16384 / NF);
   if (grid > n_tiles) grid = n_tiles;
-  const size_t dyn = (size_t)(NF + NF / 16) * sizeof(float2) + (size_t)p.lo_den * sizeof(float2) +
+  const size_t dyn = (size_t)(NF + NF / 16) * sizeof(float2) +
                      (CH ? (size_t)(NF / 2 - 512) / 512 * (NF / 1024) * sizeof(float) : 0);
   cudaFuncSetAttribute(k2_mf_kernel<NF, CH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
   k2_mf_kernel<NF, CH><<<(unsigned)grid, T, dyn, s>>>(E, E_first, part, jb0, tile0, n_tiles, y, y_first, y_count,

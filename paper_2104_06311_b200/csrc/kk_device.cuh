@@ -32,11 +32,26 @@ __device__ __forceinline__ void ffma2s(float& x, float& y, float s, float2 b) {
       : "+f"(x), "+f"(y) : "f"(s), "f"(b.x), "f"(b.y));
 }
 __device__ __forceinline__ void ffma2s(float2& acc, float s, float2 b) { ffma2s(acc.x, acc.y, s, b); }
+// complex multiply as two packed FP32x2 instructions: a·b = b.x·a + b.y·(i·a), i·a = (−a.y, a.x). ptxas folds the
+// swapped, half-negated operand into FFMA2's operand modifiers (R.F32x2.LO_HI.NP) and b.x, b.y into scalar
+// broadcasts, so the product is FMUL2 + FFMA2 (scalar form: 2 FMUL + 2 FFMA). Per lane: re = fma(−a.y, b.y,
+// a.x·b.x), im = fma(a.x, b.y, a.y·b.x) — the same accuracy as the scalar form (one product rounded, one fused).
 __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
-  return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+  float2 r;
+  asm("{\n\t.reg .b64 pa, ps, pc, pn, pr;\n\tmov.b64 pa, {%2, %3};\n\tmov.b64 ps, {%3, %2};\n\t"
+      "mov.b64 pc, {%4, %4};\n\tmov.b64 pn, {%5, %6};\n\t"
+      "mul.rn.f32x2 pr, pa, pc;\n\tfma.rn.f32x2 pr, ps, pn, pr;\n\tmov.b64 {%0, %1}, pr;\n\t}"
+      : "=f"(r.x), "=f"(r.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(-b.y), "f"(b.y));
+  return r;
 }
-__device__ __forceinline__ float2 cmulc(float2 a, float2 b) {  // a * conj(b)
-  return make_float2(fmaf(a.x, b.x, a.y * b.y), fmaf(a.y, b.x, -a.x * b.y));
+// a·conj(b) = b.x·a − b.y·(i·a): re = fma(a.y, b.y, a.x·b.x), im = fma(−a.x, b.y, a.y·b.x)
+__device__ __forceinline__ float2 cmulc(float2 a, float2 b) {
+  float2 r;
+  asm("{\n\t.reg .b64 pa, ps, pc, pn, pr;\n\tmov.b64 pa, {%2, %3};\n\tmov.b64 ps, {%3, %2};\n\t"
+      "mov.b64 pc, {%4, %4};\n\tmov.b64 pn, {%5, %6};\n\t"
+      "mul.rn.f32x2 pr, pa, pc;\n\tfma.rn.f32x2 pr, ps, pn, pr;\n\tmov.b64 {%0, %1}, pr;\n\t}"
+      : "=f"(r.x), "=f"(r.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(-b.y));
+  return r;
 }
 __device__ __forceinline__ float2 cconj(float2 a) { return make_float2(a.x, -a.y); }
 // a·s as one packed FP32x2 multiply with a scalar-broadcast operand (FMUL2; bit-identical to two FMULs)

@@ -623,7 +623,21 @@ kk_status kk_process_frames_ex(kk_ctx* c, const void* d_adc, int64_t first, int6
   const int64_t t_lo = fdiv(y_first, c->mfKeep);
   const int64_t t_hi = fdiv(y_first + y_count - 1, c->mfKeep);
   if (c->timing) cudaEventRecord(tev[1], s);
-  kk::K2Params p2{cf.lo_num, cf.lo_den, c->d_segpow, t_lo * (c->mfKeep / 512)};
+  kk::K2Params p2{};
+  p2.lo_num = cf.lo_num;
+  p2.lo_den = cf.lo_den;
+  p2.seg_pow = c->d_segpow;
+  p2.seg_first = t_lo * (c->mfKeep / 512);
+  {
+    // ρ^r = LO[(r·stepJ) mod lo_den], stepJ = (NF/16)·lo_num: the LO advance between a pass-1 thread's samples
+    // (the same fp64 formula as the LO table, so ρ^r equals the table entry)
+    const int64_t stepJ = ((int64_t)(c->mfN / 16) * cf.lo_num) % cf.lo_den;
+    for (int r = 0; r < 16; ++r) {
+      const int64_t q = ((int64_t)r * stepJ) % cf.lo_den;
+      const double a = -2.0 * kPi * (double)cf.sideband * (double)q / (double)cf.lo_den;
+      p2.rho[r] = make_float2((float)std::cos(a), (float)std::sin(a));
+    }
+  }
   kk::launch_k2(c->mfN, c->d_E, first - F, c->d_part, c->d_clamp, jb0, t_lo, t_hi - t_lo + 1, c->d_y, y_first,
                 y_count, c->d_H, c->d_Hc, c->d_lo, c->d_tw256, c->d_twN, c->d_twI, p2, c->num_sms, s);
 

@@ -42,6 +42,7 @@ struct K1UParams {                  // K1 + 2× upsampling (DESIGN.md §3 "KK up
 
 struct K2Params {
   int lo_num, lo_den;
+  float2 rho[16];                    // LO step between a pass-1 thread's samples r and 0: LO[(r·(NF/16)·lo_num) mod lo_den]
   float* seg_pow;                    // DDLMS mode (CH): Σ|y[2n]|² per 256-symbol segment (global y/512 grid)
   int64_t seg_first;                 // global segment index of seg_pow[0]
 };
