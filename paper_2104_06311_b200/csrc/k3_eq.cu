@@ -110,7 +110,8 @@ struct K3Layout {
   static constexpr int DRES = RED + (RED_B > MAT_B ? RED_B : MAT_B);
   static constexpr int TH = DRES + (NRED > 128 ? NRED : 128) * 8;   // (dres doubles as the GJ pivot rows)
   static constexpr int ROT = TH + 2 * L * 8;       // 16 CPR rotations
-  static constexpr int BAR = ROT + 16 * 8;         // mbarrier
+  static constexpr int CC = ROT + 16 * 8;          // the frame's 32 per-block clamp counts (TMA, with the samples)
+  static constexpr int BAR = CC + 32 * 4;          // mbarrier
   static constexpr int MISC = BAR + 16;
   static constexpr int TOTAL = MISC + 64 * 4;
   static_assert(N <= 32, "one matrix row per lane");
@@ -120,6 +121,12 @@ struct K3Layout {
 __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
+
+#ifdef KK_PHASE_TIMING   // debug: per-phase SM clocks of CTA 0 (tools/k3_phases.py), printed at kernel exit
+#define KK_PT(i) do { if (tid == 0 && blockIdx.x == 0) { const long long c_ = clock64(); pt_[i] += c_ - pt_last_; pt_last_ = c_; } } while (0)
+#else
+#define KK_PT(i) do { } while (0)
+#endif
 
 template <int K>
 __global__ void __launch_bounds__(K3_THREADS, 2)
@@ -140,6 +147,7 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
   float2* th = reinterpret_cast<float2*>(smem + Lay::TH);
   float2* rot = reinterpret_cast<float2*>(smem + Lay::ROT);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + Lay::BAR);
+  const int* cc_s = reinterpret_cast<const int*>(smem + Lay::CC);
   int* misc = reinterpret_cast<int*>(smem + Lay::MISC);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -151,9 +159,10 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
   // thread 0: TMA the frame samples (and, separately, its labels) into shared memory. One arrival with the
   // total byte count; the two copies may be issued at different times (the phase completes when both land).
   auto issue_y = [&](int fl) {
-    const uint32_t bytes = YBYTES + (ref_tma ? (uint32_t)kFrameSym : 0u);
+    const uint32_t bytes = YBYTES + 128u + (ref_tma ? (uint32_t)kFrameSym : 0u);
     mbar_arrive_expect_tx(bar, bytes);
     tma_bulk_g2s(ys, y + (int64_t)fl * (2 * kFrameSym), YBYTES, bar);
+    tma_bulk_g2s(smem + Lay::CC, clampcnt + clamp_frame_off + (int64_t)fl * 32, 128u, bar);
   };
   auto issue_ref = [&](int fl) {
     if (ref_tma) tma_bulk_g2s(ref_s, ref + (int64_t)fl * kFrameSym, kFrameSym, bar);
@@ -162,6 +171,9 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
   auto prefetch = [&](int fl) {
     prefetch_l2(y + (int64_t)fl * (2 * kFrameSym), YBYTES);
     if (ref_tma) prefetch_l2(ref + (int64_t)fl * kFrameSym, kFrameSym);
+  };
+  auto frame_order = [&](int64_t f) -> int {     // QAM order of global frame f (R26)
+    return (int)p.schedule[(int)(((f / p.segment_frames) % p.n_segments + p.n_segments) % p.n_segments)];
   };
   if (tid == 0) mbar_init(bar, 1);
   __syncthreads();
@@ -184,28 +196,30 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
     }
   };
 
+#ifdef KK_PHASE_TIMING
+  long long pt_[13] = {}, pt_last_ = clock64();
+#endif
   int it = 0;
   for (int fl = blockIdx.x; fl < n_frames; fl += gridDim.x, ++it) {
     bool early = false;                                // thread 0: next frame's samples already requested
     const int64_t sym0 = (int64_t)fl * kFrameSym;
-    // frame clamp count (K1 per-block counts) → dead-frame rule; the frame's QAM order (R26) — one 64-bit
-    // division per frame by one thread, broadcast through shared memory
-    if (warp == 0) {
-      int c = __ldg(&clampcnt[clamp_frame_off + (int64_t)fl * 32 + lane]);
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-      if (lane == 0) misc[0] = c;
-    } else if (tid == 32) {
-      const int64_t f = frame0 + fl;
-      misc[2] = (int)p.schedule[(int)(((f / p.segment_frames) % p.n_segments + p.n_segments) % p.n_segments)];
-    }
+    // the frame's QAM order (R26): one 64-bit division per frame by one thread, broadcast through shared memory;
+    // computed here for the CTA's first frame, later ones during the previous frame and published at its end
+    if (it == 0 && tid == 32) misc[2] = frame_order(frame0 + fl);
     mbar_wait(bar, it & 1);
     __syncthreads();
+    KK_PT(0);
     const int M = misc[2];
     const int bi = (M == 4) ? 0 : (M == 8) ? 1 : (M == 16) ? 2 : (M == 32) ? 3 : 4;
     Slicer sl;
     sl.init(M);
-    const int ccount = misc[0];
+    // frame clamp count (K1's 32 per-block counts, landed with the samples) → dead-frame rule; every warp sums
+    // them itself (fixed order), so no extra barrier
+    int ccount = cc_s[lane];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ccount += __shfl_xor_sync(0xffffffffu, ccount, o);
+    const int fn = fl + (int)gridDim.x;
+    const int m_next = (tid == 32 && fn < n_frames) ? frame_order(frame0 + fn) : 0;
     const bool dead = (ccount >= kFrameSamp);
 
     int bad = 0;
@@ -259,6 +273,7 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
         }
       }
       __syncthreads();
+      KK_PT(1);
       double P0 = 0.0;
 #pragma unroll
       for (int w8 = 0; w8 < K3_WARPS; ++w8) P0 += (double)red[w8 * NRED + Lay::IPOW];
@@ -286,27 +301,49 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
         warp_partials<Lay::NP>(acc, red_w, 0, lane);
       }
       __syncthreads();
+      KK_PT(2);
       cross_warp_sum(red, dres, NRED, NRED, tid);   // fp64, fixed order
       __syncthreads();
+      KK_PT(3);
 
       // ---- solve: warp 0 assembles the real system from S, T, p; Gauss–Jordan by warp 0 (N ≤ kGJWarpN) or the CTA
       int fail = 0;
       if (warp == 0) {
-        auto Ys = [&](int idx) -> double2 {
-          const float2 v = ys[idx];
-          return make_double2((double)v.x, (double)v.y);
-        };
         double* A = mat;   // row-major N × WS: [G + λI | q1 q2]
         constexpr int W = Lay::WS;
         // lane c < 2·ND walks one (ρ, d) chain S(i, i+d), T(i, i+d), i = −K+ρ, −K+ρ+2, … ≤ K − d, using the
-        // exact sliding recurrence; edge samples y[2(k0−1) − i] ↔ y_s[K − 2 − i], y[2(k1−1) − i] ↔ y_s[8190 + K − i]
-        for (int c = lane; c < 2 * ND; c += 32) {
-          const int rho = c / ND, d = c % ND;
-          if (rho == 1 && d == ND - 1) continue;
+        // exact sliding recurrence; edge samples y[2(k0−1) − i] ↔ y_s[K − 2 − i], y[2(k1−1) − i] ↔ y_s[8190 + K − i].
+        // The recurrence increments are formed first (all edge loads issued before any store to A, which the
+        // compiler cannot reorder across), then the chain is a running sum. The d = 0 chains also return the
+        // diagonal's contribution to tr(G) (WL: rr + ii = Re S; linear: 2·Re S) for the ridge.
+        double* trp = reinterpret_cast<double*>(th);  // 2 partial traces (th is written only after the solve)
+        if (lane < 2 * ND - 1) {
+          const int rho = lane / ND, d = lane % ND;
+          const int npts = (2 * K - d - rho) / 2 + 1;  // chain points (i = −K + ρ + 2m, m < npts)
+          // edge samples of step m (i → i + 2) are loaded one step ahead, before the step's stores to A
+          float2 a1 = make_float2(0.f, 0.f), a2 = a1, b1 = a1, b2 = a1;
+          auto load_edges = [&](int m) {
+            const int i = -K + rho + 2 * m;
+            a1 = ys[K - 2 - i]; a2 = ys[K - 2 - i - d]; b1 = ys[8190 + K - i]; b2 = ys[8190 + K - i - d];
+          };
+          if (npts > 1) load_edges(0);
           const double A1 = dres[Lay::NP + 8 * d + 4 * rho], A3 = dres[Lay::NP + 8 * d + 4 * rho + 1];
           const double A4 = dres[Lay::NP + 8 * d + 4 * rho + 2], A2 = dres[Lay::NP + 8 * d + 4 * rho + 3];
           double sr = A1 + A2, si = A3 - A4, tr_ = A1 - A2, ti = A3 + A4;   // S = Σ conj(a)·b, T = Σ a·b
-          for (int i = -K + rho; i + d <= K; i += 2) {
+          double tsum = 0.0;
+#pragma unroll
+          for (int m = 0; m <= K; ++m) {
+            if (m >= npts) break;
+            // fp32 edge increments: O(|y|²) terms added to fp64 sums of 4096 such terms
+            float i0 = 0.f, i1 = 0.f, i2 = 0.f, i3 = 0.f;
+            if (m + 1 < npts) {
+              i0 = fmaf(a1.x, a2.x, a1.y * a2.y) - fmaf(b1.x, b2.x, b1.y * b2.y);
+              i1 = fmaf(a1.x, a2.y, -a1.y * a2.x) - fmaf(b1.x, b2.y, -b1.y * b2.x);
+              i2 = fmaf(a1.x, a2.x, -a1.y * a2.y) - fmaf(b1.x, b2.x, -b1.y * b2.y);
+              i3 = fmaf(a1.x, a2.y, a1.y * a2.x) - fmaf(b1.x, b2.y, b1.y * b2.x);
+              if (m + 2 < npts) load_edges(m + 1);
+            }
+            const int i = -K + rho + 2 * m;
             const int r = i + K, q = i + d + K;     // S(r, q) = Σ conj(a_r)·a_q, T(r, q) = Σ a_r·a_q
             if (wl) {
               // G = [[Σ ar arᵀ, Σ ar aiᵀ], [Σ ai arᵀ, Σ ai aiᵀ]] from S and T (both orders of (r, q))
@@ -316,26 +353,24 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
               A[(L + r) * W + (L + q)] = ii; A[(L + q) * W + (L + r)] = ii;
               A[r * W + (L + q)] = ri;       A[(L + q) * W + r] = ri;
               A[(L + r) * W + q] = ir;       A[q * W + (L + r)] = ir;
+              tsum += rr + ii;
             } else {
               // real form of the Hermitian R11: [[Re R, −Im R], [Im R, Re R]], R[r][q] = S, R[q][r] = conj(S)
               A[r * W + q] = sr;             A[q * W + r] = sr;
               A[(L + r) * W + (L + q)] = sr; A[(L + q) * W + (L + r)] = sr;
               A[(L + r) * W + q] = si;       A[(L + q) * W + r] = -si;
               A[r * W + (L + q)] = -si;      A[q * W + (L + r)] = si;
+              tsum += sr + sr;
             }
-            if (i + 2 + d > K) break;
-            const double2 a1 = Ys(K - 2 - i), a2 = Ys(K - 2 - i - d);
-            const double2 b1 = Ys(8190 + K - i), b2 = Ys(8190 + K - i - d);
-            sr += a1.x * a2.x + a1.y * a2.y - (b1.x * b2.x + b1.y * b2.y);
-            si += a1.x * a2.y - a1.y * a2.x - (b1.x * b2.y - b1.y * b2.x);
-            tr_ += a1.x * a2.x - a1.y * a2.y - (b1.x * b2.x - b1.y * b2.y);
-            ti += a1.x * a2.y + a1.y * a2.x - (b1.x * b2.y + b1.y * b2.x);
+            sr += (double)i0; si += (double)i1; tr_ += (double)i2; ti += (double)i3;
           }
+          if (d == 0) trp[rho] = tsum;
         }
         __syncwarp();
+        KK_PT(8);
         // ridge (R10): λ_c = ridge·tr(R)/n_c. WL: real form uses λ_c/2 and tr(R) = 2·tr(G). Linear: tr(M) = 2·tr(R11)
-        double trG = 0.0;
-        for (int r = 0; r < N; ++r) trG += A[r * W + r];
+        const double trG = trp[0] + trp[1];
+        KK_PT(9);
         const double lam = wl ? (double)p.ridge * trG / (double)N : (double)p.ridge * 0.5 * trG / (double)L;
         if (lane < L) {
           const int e = lane;
@@ -359,11 +394,18 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
         if (lane < N) A[lane * W + lane] += lam;
         if constexpr (N <= kGJWarpN) {
         __syncwarp();
+        KK_PT(10);
         // ---- Gauss–Jordan on [G + λI | q1 q2] by warp 0 with 2×2 pivot blocks (SPD ⇒ every leading 2×2 block
         //      is SPD, no pivoting; N = 4K + 2 is even). Lane c holds column c in registers (a[i] = A[i][c]); per
         //      step the two pivot lanes publish their columns as (A[i][k], A[i][k+1]) pairs in a double-buffered
         //      shared strip (dres is consumed) that every lane reads with broadcast 16-B loads — no CTA barriers
         //      and no shuffles (warp 0 runs this alone: shuffles in that branch would compile to collectives).
+        //      Division-free form: the pivot rows become s·adj(P)·[row k; row k+1] and every other row
+        //      row_i ← s·det(P)·row_i − A[i][k]·u0 − A[i][k+1]·u1, with s a power of two (≈ 1/pa², exact scaling
+        //      that keeps the rows bounded). The matrix ends as diag(D) with D = s·det·(later factors) per pivot
+        //      block, so x_i = rhs_i / D_i — one reciprocal per row at the end instead of one per step on the
+        //      serial path (each step's chain is ~5 dependent fp64 operations instead of ~11 + a conversion round
+        //      trip through MUFU.RCP).
         double a[N];
 #pragma unroll
         for (int i = 0; i < N; ++i) a[i] = (lane < N + 2) ? A[i * W + lane] : 0.0;
@@ -380,21 +422,39 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
           const double pa = pk.x, pb = pk.y, pc = pk1.x, pd = pk1.y;
           const double det = pa * pd - pb * pc;
           fail |= !(pa > 0.0) || !(det > 0.0) || !isfinite(det);
-          // 1/det: fp32 seed + two Newton steps (relative error ~1e-28 → full double precision; det is the
-          // determinant of an SPD 2×2 pivot block ≥ λ² ≫ FLT_MIN, so the seed is finite when det is)
-          double idet = (double)__frcp_rn((float)det);
-          idet = idet * fma(-det, idet, 2.0);
-          idet = idet * fma(-det, idet, 2.0);
-          const double r0 = a[k], r1 = a[k + 1];
-          const double R0 = (pd * r0 - pb * r1) * idet, R1 = (pa * r1 - pc * r0) * idet;   // P⁻¹·[r0; r1]
+          // s = 2^(−2e), e = unbiased exponent of pa (clamped so that s stays a normal double)
+          const int e = min(max((int)((__double_as_longlong(pa) >> 52) & 0x7ff) - 1023, -500), 500);
+          const double sc = __longlong_as_double((long long)(1023 - 2 * e) << 52);
+          const double r0 = a[k] * sc, r1 = a[k + 1] * sc;
+          const double u0 = pd * r0 - pb * r1, u1 = pa * r1 - pc * r0;        // s·adj(P)·[r0; r1]
+          const double ds = det * sc;
 #pragma unroll
           for (int i = 0; i < N; ++i) {
             if (i == k || i == k + 1) continue;
             const double2 c = reinterpret_cast<const double2*>(col)[i];      // (A[i][k], A[i][k+1])
-            a[i] = fma(-c.y, R1, fma(-c.x, R0, a[i]));
+            a[i] = fma(-c.y, u1, fma(-c.x, u0, a[i] * ds));
           }
-          a[k] = R0;
-          a[k + 1] = R1;
+          a[k] = u0;
+          a[k + 1] = u1;
+        }
+        {
+          // lane c < N owns D_c = a[c]: 1/D_c (fp32 seed + two Newton steps, full double precision) → strip
+          double* rD = dres + 4 * N;
+          if (lane < N) {
+            double dg = 0.0;
+#pragma unroll
+            for (int i = 0; i < N; ++i) dg = (i == lane) ? a[i] : dg;
+            double rc = (double)__frcp_rn((float)dg);
+            rc = rc * fma(-dg, rc, 2.0);
+            rc = rc * fma(-dg, rc, 2.0);
+            fail |= !(dg > 0.0) || !isfinite(rc) || !((float)dg > 0.f);
+            rD[lane] = rc;
+          }
+          __syncwarp();
+          if (lane == N || lane == N + 1) {
+#pragma unroll
+            for (int i = 0; i < N; ++i) a[i] *= rD[i];
+          }
         }
         // solution columns N, N+1 back to shared memory (rows < N)
         if (lane == N || lane == N + 1) {
@@ -402,6 +462,7 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
           for (int i = 0; i < N; ++i) A[i * W + lane] = a[i];
         }
         __syncwarp();
+        KK_PT(11);
         }
       }
       // ---- Gauss–Jordan on [G + λI | q1 q2] by the whole CTA with 2×2 pivot blocks (SPD ⇒ every leading
@@ -491,8 +552,10 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
             th[L + lane] = vv;
           }
           if (lane == 0) misc[1] = fail;
+          KK_PT(12);
         }
       __syncthreads();
+      KK_PT(4);
       bad |= misc[1];
 
       // ---- sweep C: pass 2 y¹ = Σ_e w_e·a + v_e·conj(a) → us, and the gain-unbias sums (R27)
@@ -526,6 +589,7 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
       gr = warp_sum(gr); gi = warp_sum(gi); gd = warp_sum(gd);
       if (lane == 0) { red_w[0] = gr; red_w[1] = gi; red_w[2] = gd; }
       __syncthreads();
+      KK_PT(5);
       float sc = 1.0f;
       {
         double Gr = 0, Gi = 0, Gd = 0;
@@ -577,6 +641,7 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
         rot[tid] = (rs > 0.f) ? make_float2(cr * rs, -ci * rs) : make_float2(1.f, 0.f);
       }
       __syncthreads();
+      KK_PT(6);
     }
 
     // ---- decisions, counts, outputs: z = u·e^{−iϑ_b} (dead frame: z = 0)
@@ -602,7 +667,9 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
       }
       if (lane == 0) { misc[8 + warp] = serr; misc[16 + warp] = berr; }
     }
+    if (tid == 32) misc[2] = m_next;                   // publish the next frame's QAM order
     __syncthreads();   // all reads of ys / ref_s / misc for this frame are done
+    KK_PT(7);
     if (tid == 0) {
       const int nf = fl + (int)gridDim.x;
       if (nf < n_frames) {
@@ -624,6 +691,11 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
       if (!dead && bad) atomicAdd(&counters[23], 1ull);
     }
   }
+#ifdef KK_PHASE_TIMING
+  if (tid == 0 && blockIdx.x == 0)
+    printf("K3PHASES K=%d frames=%d wait %lld sweepA %lld sweepB %lld xwarp %lld solve %lld sweepC %lld cpr %lld decide %lld | chains %lld trG %lld rhs %lld gj %lld theta %lld\n",
+           K, it, pt_[0], pt_[1], pt_[2], pt_[3], pt_[4], pt_[5], pt_[6], pt_[7], pt_[8], pt_[9], pt_[10], pt_[11], pt_[12]);
+#endif
 }
 
 template <int K>
