@@ -159,12 +159,14 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
   // thread 0: TMA the frame samples (and, separately, its labels) into shared memory. One arrival with the
   // total byte count; the two copies may be issued at different times (the phase completes when both land).
   auto issue_y = [&](int fl) {
+    fence_proxy_async_smem();                     // the frame buffer was written by generic stores (CPR products)
     const uint32_t bytes = YBYTES + 128u + (ref_tma ? (uint32_t)kFrameSym : 0u);
     mbar_arrive_expect_tx(bar, bytes);
     tma_bulk_g2s(ys, y + (int64_t)fl * (2 * kFrameSym), YBYTES, bar);
     tma_bulk_g2s(smem + Lay::CC, clampcnt + clamp_frame_off + (int64_t)fl * 32, 128u, bar);
   };
   auto issue_ref = [&](int fl) {
+    if (ref_tma) fence_proxy_async_smem();
     if (ref_tma) tma_bulk_g2s(ref_s, ref + (int64_t)fl * kFrameSym, kFrameSym, bar);
   };
   auto issue = [&](int fl) { issue_y(fl); issue_ref(fl); };
