@@ -602,7 +602,7 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
       }
       // ---- CPR (R12): products c_k = u_k·conj(D(u_k)), u = y¹/|γ|, into the (now dead) frame buffer
       float2* cb = ys;
-#pragma unroll 2
+#pragma unroll 4
       for (int s = 0; s < K3_SPT; ++s) {
         const int kl = tid + K3_THREADS * s;
         const float2 uu = cscale(us[kl], sc);
@@ -648,7 +648,7 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
 
     // ---- decisions, counts, outputs: z = u·e^{−iϑ_b} (dead frame: z = 0)
     int serr = 0, berr = 0;
-#pragma unroll 2
+#pragma unroll 4
     for (int s = 0; s < K3_SPT; ++s) {
       const int kl = tid + K3_THREADS * s;
       const float2 zz = dead ? make_float2(0.f, 0.f) : cmul(us[kl], rot[s]);
