@@ -28,26 +28,6 @@ constexpr int K1_SAMPLES = K1_WARPS * 1024 + 512;   // staged input samples per 
 constexpr int K1_TR = 32 * 33;                      // float2 per warp transpose tile
 constexpr size_t K1_SMEM = (size_t)K1_SAMPLES * 4 + (size_t)K1_WARPS * K1_TR * 8 + 16 + 2 * K1_WARPS * 4;
 
-// v[r] ·= w^r (DIR < 0) or conj(w)^r (DIR > 0), r = 1..31, tw[32·r] = w^r = W_1024^{r·j}: loads w^1..w^3 and
-// w^{4a} (10 of the 31 table entries — the twiddle loads are a quarter of K1's L1 wavefronts) and forms
-// w^{4a+b} = w^{4a}·w^b (one product, so every twiddle is at most two roundings from exact)
-template <int DIR>
-__device__ __forceinline__ void twiddle32(float2 (&v)[32], const float2* __restrict__ tw) {
-  const float2 w1 = __ldg(tw + 32), w2 = __ldg(tw + 64), w3 = __ldg(tw + 96);
-#pragma unroll
-  for (int a = 0; a < 8; ++a) {
-    const float2 base = a ? __ldg(tw + 128 * a) : make_float2(1.f, 0.f);
-#pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      const int r = 4 * a + b;
-      if (r == 0) continue;
-      const float2 wb = (b == 1) ? w1 : (b == 2) ? w2 : w3;
-      const float2 w = (b == 0) ? base : (a == 0) ? wb : cmul(base, wb);
-      v[r] = DIR < 0 ? cmul(v[r], w) : cmulc(v[r], w);
-    }
-  }
-}
-
 template <typename Tin>
 __global__ void __launch_bounds__(K1_THREADS, 2)
 k1_kk_kernel(const Tin* __restrict__ adc0, float2* __restrict__ E, float2* __restrict__ part,
@@ -127,7 +107,7 @@ k1_kk_kernel(const Tin* __restrict__ adc0, float2* __restrict__ E, float2* __res
 #pragma unroll
   for (int r = 0; r < 32; ++r) v[r] = S[r * 33 + lane];
   __syncwarp();
-  twiddle32<-1>(v, tw + lane);                // × W_1024^{r·j}
+  twiddle32<-1, 32>(v, tw + lane);                // × W_1024^{r·j}
   dft_reg<32, -1>(v);                       // pass 2 (Ns = 32): lane j holds X[j + 32 r]
 
   // −i·sgn(q), q = j + 32 r: r < 16 ⇒ 0 < q < 512 (except q = 0); r ≥ 16 ⇒ q > 512 (except q = 512)
@@ -144,7 +124,7 @@ k1_kk_kernel(const Tin* __restrict__ adc0, float2* __restrict__ E, float2* __res
   __syncwarp();
 #pragma unroll
   for (int r = 0; r < 32; ++r) v[r] = S[r * 33 + lane];
-  twiddle32<+1>(v, tw + lane);                // × W_1024^{−r·j}
+  twiddle32<+1, 32>(v, tw + lane);                // × W_1024^{−r·j}
   dft_reg<32, +1>(v);                       // lane j holds 1024·(φ₀ + iφ₁)[j + 32 r]
 
   // ---- a4: E = √I_ref·e^{a}·e^{iσφ} on the central 512 samples; per-block ΣE

@@ -139,8 +139,7 @@ k1u_kk_kernel(const Tin* __restrict__ adc0, float2* __restrict__ E, float2* __re
 #pragma unroll
   for (int r = 0; r < 32; ++r) v[r] = make_float2(w0[t + 64 * r], w1[t + 64 * r]);
   dft_reg<32, -1>(v);                               // Y[t][k1] = Σ_r x[t + 64r]·W₃₂^{r·k1}
-#pragma unroll
-  for (int k = 1; k < 32; ++k) v[k] = cmul(v[k], __ldg(&tw[k * 64 + t]));   // W₂₀₄₈^{t·k1}
+  twiddle32<-1, 64>(v, tw + t);               // × W₂₀₄₈^{t·k1}
 #pragma unroll
   for (int k = 0; k < 32; ++k) S[t * 33 + k] = v[k];
   group_sync(bid);
@@ -181,8 +180,7 @@ k1u_kk_kernel(const Tin* __restrict__ adc0, float2* __restrict__ E, float2* __re
   group_sync(bid);
 #pragma unroll
   for (int k = 0; k < 32; ++k) v[k] = S[t * 33 + k];                          // Z[k1][t]
-#pragma unroll
-  for (int k = 1; k < 32; ++k) v[k] = cmulc(v[k], __ldg(&tw[k * 64 + t]));  // W₂₀₄₈^{−t·k1}
+  twiddle32<+1, 64>(v, tw + t);               // × W₂₀₄₈^{−t·k1}
   dft_reg<32, +1>(v);                               // 2048·(φ₀ + iφ₁)[t + 64r]
   group_sync(bid);                                  // S is reused for E₂ below
 

@@ -178,6 +178,26 @@ __device__ __forceinline__ void dft_reg(float2 (&v)[R]) {
   for (int i = 0; i < R; ++i) v[i] = t[i];
 }
 
+// v[r] ·= w^r (DIR < 0) or conj(w)^r (DIR > 0), r = 1..31, tw[S·r] = w^r (K1: W_1024^{r·j}, S = 32; K1U:
+// W_2048^{r·t}, S = 64): loads w^1..w^3 and w^{4a} (10 of the 31 table entries — the twiddle loads were a quarter
+// of K1's L1 wavefronts) and forms w^{4a+b} = w^{4a}·w^b (one product: every twiddle ≤ two roundings from exact)
+template <int DIR, int S>
+__device__ __forceinline__ void twiddle32(float2 (&v)[32], const float2* __restrict__ tw) {
+  const float2 w1 = __ldg(tw + S), w2 = __ldg(tw + 2 * S), w3 = __ldg(tw + 3 * S);
+#pragma unroll
+  for (int a = 0; a < 8; ++a) {
+    const float2 base = a ? __ldg(tw + 4 * S * a) : make_float2(1.f, 0.f);
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int r = 4 * a + b;
+      if (r == 0) continue;
+      const float2 wb = (b == 1) ? w1 : (b == 2) ? w2 : w3;
+      const float2 w = (b == 0) ? base : (a == 0) ? wb : cmul(base, wb);
+      v[r] = DIR < 0 ? cmul(v[r], w) : cmulc(v[r], w);
+    }
+  }
+}
+
 // ------------------------------------------------------------------ reductions
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
