@@ -5,6 +5,7 @@ usage: python tools/ncu_summary.py REPORT.ncu-rep LAUNCHES.csv OUT.md [TRAFFIC.j
 import csv
 import io
 import json
+import os
 import subprocess
 import sys
 from collections import defaultdict
@@ -85,7 +86,7 @@ def main(report, launches, out_md, traffic_json=None):
                      f"{sum(cnt.values()) - sum(cnt[k] for k in ours)} | {other / 1e3:.1f} | — |")
     open(out_md, "w").write("\n".join(lines) + "\n")
     if traffic_json:
-        json.dump({"source": report, "chunk_samples": 1 << 26, "bytes_per_launch": traffic}, open(traffic_json, "w"),
+        json.dump({"source": report, "chunk_samples": int(os.environ.get("KK_NCU_CHUNK", 1 << 28)), "bytes_per_launch": traffic}, open(traffic_json, "w"),
                   indent=1)
     print("\n".join(lines))
 

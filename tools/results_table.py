@@ -26,7 +26,7 @@ FOOT = """
 C1–C3 are smaller than one 2^28 call, so they are launch/occupancy-bound (C1: 4 frames); throughput is judged
 on C4/C5. C4 runs L = 15 taps (10,000 km), hence the slower K3. In the DDLMS row K3 is the sequential 4-tap
 equalizer (one thread per 256-symbol block) and K2 carries the complex static filter and the AGC segment sums;
-in the upsampling row K1 is K1U. End to end from pinned host memory (C5): `profiles/r01_bench_final_candidate.json`.
+in the upsampling row K1 is K1U. End to end from pinned host memory (C5): the `e2e` / `e2e_uint8` keys of `profiles/r01_configs/C5.json`.
 """
 
 
