@@ -62,16 +62,43 @@ __device__ __forceinline__ float warp_transpose_reduce(float (&v)[32], int lane)
   return v[0];
 }
 
+__host__ __device__ constexpr int pow2_ceil(int n) { return n <= 1 ? 1 : 2 * pow2_ceil((n + 1) / 2); }
+
 // Write this warp's sums of acc[0..N) to red_w[base + i] (red_w = this warp's slice of the reduction buffer).
+// Whole groups of 32 values: in-warp transpose-reduce. A remainder of R < 32 values (padded to P = 2^⌈log2 R⌉):
+// plain butterflies over the lane bits ≥ P (every lane keeps all P values), then the transpose-reduce over the
+// low log2 P bits — about half the instructions of a zero-padded 32-value transpose for R = 4 or 8.
 template <int N>
 __device__ __forceinline__ void warp_partials(const float (&acc)[N], float* red_w, int base, int lane) {
+  constexpr int NF = N / 32, R = N % 32, P = pow2_ceil(R);
 #pragma unroll
-  for (int b = 0; b < (N + 31) / 32; ++b) {
+  for (int b = 0; b < NF; ++b) {
     float t[32];
 #pragma unroll
-    for (int i = 0; i < 32; ++i) t[i] = (b * 32 + i < N) ? acc[b * 32 + i] : 0.f;
+    for (int i = 0; i < 32; ++i) t[i] = acc[b * 32 + i];
     const float r = warp_transpose_reduce(t, lane);
-    if (b * 32 + lane < N) red_w[base + b * 32 + lane] = r;
+    red_w[base + b * 32 + lane] = r;
+  }
+  if constexpr (R > 0) {
+    float t[P];
+#pragma unroll
+    for (int i = 0; i < P; ++i) t[i] = (i < R) ? acc[NF * 32 + i] : 0.f;
+#pragma unroll
+    for (int off = 16; off >= P; off >>= 1) {
+#pragma unroll
+      for (int i = 0; i < P; ++i) t[i] += __shfl_xor_sync(0xffffffffu, t[i], off);
+    }
+#pragma unroll
+    for (int off = P / 2; off >= 1; off >>= 1) {
+      const bool up = (lane & off) != 0;
+#pragma unroll
+      for (int i = 0; i < off; ++i) {
+        const float send = up ? t[i] : t[i + off];
+        const float keep = up ? t[i + off] : t[i];
+        t[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+      }
+    }
+    if (lane < R) red_w[base + NF * 32 + lane] = t[0];   // lane l (< P) holds element l
   }
 }
 
