@@ -675,18 +675,32 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
 
     // ---- decisions, counts, outputs: z = u·e^{−iϑ_b} (dead frame: z = 0)
     int serr = 0, berr = 0;
+    if (!dead && !sl.cross && ref_tma && dec && !zout) {
+      // the common case as its own loop (square/rectangular slicer, labels from shared memory, no z output):
+      // no per-symbol tests of runtime-uniform flags
 #pragma unroll 4
-    for (int s = 0; s < K3_SPT; ++s) {
-      const int kl = tid + K3_THREADS * s;
-      const float2 zz = dead ? make_float2(0.f, 0.f) : cmul(us[kl], rot[s]);
-      const int lab = sl.label(zz);
-      if (ref) {
-        const int r = ref_tma ? (int)ref_s[kl] : (int)__ldg(&ref[sym0 + kl]);
+      for (int s = 0; s < K3_SPT; ++s) {
+        const int kl = tid + K3_THREADS * s;
+        const int lab = sl.label_sq(cmul(us[kl], rot[s]));
+        const int r = (int)ref_s[kl];
         serr += (lab != r);
         berr += __popc(lab ^ r);
+        dec[sym0 + kl] = (uint8_t)lab;
       }
-      if (dec) dec[sym0 + kl] = (uint8_t)lab;
-      if (zout) zout[sym0 + kl] = zz;
+    } else {
+#pragma unroll 4
+      for (int s = 0; s < K3_SPT; ++s) {
+        const int kl = tid + K3_THREADS * s;
+        const float2 zz = dead ? make_float2(0.f, 0.f) : cmul(us[kl], rot[s]);
+        const int lab = sl.label(zz);
+        if (ref) {
+          const int r = ref_tma ? (int)ref_s[kl] : (int)__ldg(&ref[sym0 + kl]);
+          serr += (lab != r);
+          berr += __popc(lab ^ r);
+        }
+        if (dec) dec[sym0 + kl] = (uint8_t)lab;
+        if (zout) zout[sym0 + kl] = zz;
+      }
     }
     if (ref) {
 #pragma unroll

@@ -304,6 +304,11 @@ struct Slicer {
   __device__ __forceinline__ int label_i(int iI, int iQ) const {
     return cross ? cross32_label(iI, iQ) : ((gray(iI) << hb) | gray(iQ));
   }
+  // square / rectangular grids only (no 32-cross corner logic): gray(iI) << hb | gray(iQ)
+  __device__ __forceinline__ int label_sq(float2 z) const {
+    const float2 t = tq(z);
+    return (gray(__float_as_int(t.x) - offI) << hb) | gray(__float_as_int(t.y) - offQ);
+  }
   __device__ __forceinline__ int label(float2 z) const {
     int iI, iQ;
     levels(z, iI, iQ);
