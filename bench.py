@@ -58,6 +58,9 @@ def parse():
     ap.add_argument("--ingest", default="local", choices=["local", "single"],
                     help="e2e input path: every rank reads its own shard from host memory (local), or rank 0 "
                          "holds the whole stream and sends each rank its windows over NVLink (single; NEXT-3)")
+    ap.add_argument("--e2e-ref", default="prbs", choices=["prbs", "buffer"],
+                    help="e2e reference labels: generated in the receiver from the transmitter's known sequence "
+                         "(kk_config.ref_prbs, default) or a host label buffer copied with the samples")
     ap.add_argument("--mf-n", type=int, default=4096, choices=[4096, 8192],
                     help="K2 overlap-save grid: FFT4096/hop 3072 or FFT8192/hop 7168 (same exact convolution)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
@@ -275,17 +278,21 @@ def e2e_uint8(a, lc, HALO, chunk, first, En, world, dev, SH, kkrx, kkgen, torch,
     g = kkgen.generate(lc8, first - HALO, first + En + HALO, device=dev)
     h_codes = torch.empty(En + 2 * HALO, dtype=torch.uint8, pin_memory=True)
     h_codes.copy_(g["codes"])
-    h_ref = torch.empty(En // 4, dtype=torch.uint8, pin_memory=True)
-    h_ref.copy_(g["labels"][HALO // 4:(HALO + En) // 4])
+    h_ref = None
+    if a.e2e_ref == "buffer":
+        h_ref = torch.empty(En // 4, dtype=torch.uint8, pin_memory=True)
+        h_ref.copy_(g["labels"][HALO // 4:(HALO + En) // 4])
     del g
     h_dec = torch.empty(En // 4, dtype=torch.uint8, pin_memory=True)
     rx8 = Receiver(adc_scale=lc8.adc_scale, ref_intensity=lc8.i_ref, dispersion_ps_per_nm=lc8.dl_ps_nm,
                    formats=lc8.formats, segment_frames=lc8.segment_frames, max_samples_per_call=chunk, device=dev.index,
-                   input_uint8=True, upsample=a.upsample, mf_fft_n=a.mf_n)
+                   input_uint8=True, upsample=a.upsample, mf_fft_n=a.mf_n,
+                   ref_prbs_seed=None if h_ref is not None else lc8.seed)
     rx8.process_host(h_codes, first, En, ref=h_ref, decisions=h_dec)          # warm-up
     if world > 1:
         dist.barrier()
     rx8.reset_stats()
+    torch.cuda.synchronize()
     t_e = []
     for _ in range(max(1, a.steps)):
         t1 = time.perf_counter()
@@ -297,7 +304,7 @@ def e2e_uint8(a, lc, HALO, chunk, first, En, world, dev, SH, kkrx, kkgen, torch,
     n_chunks = (En + (1 << 26) - 1) // (1 << 26)
     be = {f"{M}QAM": st["bit_err"][i] / st["bits"][i] for i, M in enumerate((4, 8, 16, 32, 64)) if st["bits"][i]}
     return {"value": En * world * len(t_e) / te / 1e9, "unit": "GS/s",
-            "h2d_bytes_per_step": int((En + 2 * HALO * n_chunks) * 1 + En // 4),
+            "h2d_bytes_per_step": int((En + 2 * HALO * n_chunks) * 1 + (En // 4 if h_ref is not None else 0)),
             "d2h_bytes_per_step": int(En // 4 + 8 * kkrx.KK_STATS_WORDS), "samples_per_gpu": En,
             "adc": "uint8 (adc_bits 8, same link)", "ber": be}
 
@@ -479,24 +486,41 @@ def main():
         En = min(a.e2e_samples, S)
         h_codes = torch.empty(En + 2 * HALO, dtype=torch.int16, pin_memory=True)
         h_codes.copy_(codes[:En + 2 * HALO])
-        h_ref = torch.empty(En // 4, dtype=torch.uint8, pin_memory=True)
-        h_ref.copy_(ref[:En // 4])
+        h_ref = None
+        if a.e2e_ref == "buffer":                                            # labels cross PCIe with the samples
+            h_ref = torch.empty(En // 4, dtype=torch.uint8, pin_memory=True)
+            h_ref.copy_(ref[:En // 4])
+            rxe = rx
+        else:                                                                # the receiver knows the transmitter's
+            rxe = Receiver(adc_scale=lc.adc_scale, ref_intensity=lc.i_ref, dispersion_ps_per_nm=lc.dl_ps_nm,
+                           formats=lc.formats, segment_frames=lc.segment_frames, max_samples_per_call=chunk,
+                           device=local, eq_mode=a.eq_mode, ddlms_block=a.ddlms_block, ddlms_warmup=a.ddlms_warmup,
+                           ddlms_mu_warm=a.ddlms_mu_warm, upsample=a.upsample, mf_fft_n=a.mf_n,
+                           ref_prbs_seed=lc.seed)                            # label sequence (kk_config.ref_prbs)
         h_dec = torch.empty(En // 4, dtype=torch.uint8, pin_memory=True)
         n_chunks = (En + min(chunk, 1 << 26) - 1) // min(chunk, 1 << 26)    # host path stages ≤ 2^26 per sub-call
-        rx.process_host(h_codes, first, En, ref=h_ref, decisions=h_dec)       # warm-up (allocates staging)
+        rxe.process_host(h_codes, first, En, ref=h_ref, decisions=h_dec)     # warm-up (allocates staging)
         if world > 1:
             dist.barrier()
+        rxe.reset_stats()
+        torch.cuda.synchronize()                                             # the host path runs on its own streams
         t_e = []
         for _ in range(max(1, a.steps)):
             t1 = time.perf_counter()
-            rx.process_host(h_codes, first, En, ref=h_ref, decisions=h_dec)
-            _ = rx.stats()                                                   # D2H of the step's result
+            rxe.process_host(h_codes, first, En, ref=h_ref, decisions=h_dec)
+            st_e = rxe.stats()                                               # D2H of the step's result
             t_e.append(time.perf_counter() - t1)
         te = SH.max_over_ranks(sum(t_e), device=dev)
         e2e = {"value": En * world * len(t_e) / te / 1e9, "unit": "GS/s",
-               "h2d_bytes_per_step": int((En + 2 * HALO * n_chunks) * 2 + En // 4),
+               "h2d_bytes_per_step": int((En + 2 * HALO * n_chunks) * 2 + (En // 4 if h_ref is not None else 0)),
                "d2h_bytes_per_step": int(En // 4 + 8 * kkrx.KK_STATS_WORDS),
-               "samples_per_gpu": En, "api": "kk_process_frames_host (pinned host buffers, 2 streams)"}
+               "samples_per_gpu": En, "api": "kk_process_frames_host (pinned host buffers, 2 streams)",
+               "ref": ("host label buffer" if h_ref is not None else
+                       "transmitter label sequence generated on the GPU (kk_config.ref_prbs)"),
+               "ber": {f"{M}QAM": st_e["bit_err"][i] / st_e["bits"][i]
+                       for i, M in enumerate((4, 8, 16, 32, 64)) if st_e["bits"][i]}}
+        if rxe is not rx:
+            rxe.close()
         del h_codes, h_ref, h_dec
         e2e_u8 = e2e_uint8(a, lc, HALO, chunk, first, En, world, dev, SH, kkrx, kkgen, torch, dist, Receiver)
 

@@ -97,7 +97,16 @@ typedef struct kk_config {
    * 1 = the paper's chain (KK at the ADC rate); 2 = interpolate I to 8 sps with a 31-tap half-band filter,
    * sqrt/log + 2048-point OLS Hilbert at 8 sps, half-band decimation back to 4 sps. Halo grows to 16,656. */
   int32_t upsample;
-  int32_t reserved1;
+  /* Reference labels for the error counters (BER counted against the transmitted sequence, which
+   * the real-time receiver knows). A non-NULL d_ref / h_ref argument always wins. With ref_prbs = 1 and a NULL
+   * ref argument the library generates the transmitter's known label sequence on the device instead of reading
+   * it — no host→device label transfer on the host path: label(k) = H(ref_seed, k) & (M(k) − 1) for global symbol
+   * k, M(k) the QAM order of k's frame (R26 schedule) and H the synthetic transmitter's counter-based 32-bit hash
+   * (kkgen.hash_u32(seed, 1, k): murmur3 fmix32 rounds keyed by the seed). ref_prbs = 0
+   * (default): a NULL ref argument means no error counting. */
+  int32_t ref_prbs;
+  uint32_t ref_seed;
+  int32_t reserved2;
 } kk_config;
 
 /* Counters (all uint64, summed over calls until kk_reset_stats; index i = log2(M) − 2 for M = 4..64).
@@ -136,7 +145,8 @@ kk_status kk_eq_taps(const kk_ctx* ctx, int32_t* taps);
  *               int16, uint8 or float32 per cfg.input_dtype; must be 16-byte aligned.
  *   first_sample global index, multiple of 16384 (frame grid), ≥ 0.
  *   n_samples   multiple of 16384, 16384 ≤ n_samples ≤ max_samples_per_call.
- *   d_ref       nullable device uint8[n_samples/4]: transmitted labels; if given, error counters update.
+ *   d_ref       nullable device uint8[n_samples/4]: transmitted labels; if given, error counters update. NULL
+ *               with kk_config.ref_prbs = 1: the transmitter's known labels are generated on the device instead.
  *               Any alignment; 16-byte aligned enables K3's TMA staging (byte loads otherwise, ~15 % slower K3).
  *   d_decisions nullable device uint8[n_samples/4]: decided labels out.
  * Symbol/bit/frame/clamp counters always update. Errors: KK_ERR_NULL, KK_ERR_ALIGN, KK_ERR_SHORT,
@@ -155,7 +165,8 @@ kk_status kk_process_frames_ex(kk_ctx* ctx, const void* d_adc, int64_t first_sam
 /* End-to-end variant with HOST buffers (pinned recommended): copies [h_adc − left, h_adc + n + right)
  * host→device, runs kk_process_frames, copies decisions device→host, in chunks of ≤ min(max_samples_per_call, 2^26)
  * with two internal streams so the copies of chunk i+1 overlap the kernels of chunk i. Blocks until done.
- * h_ref / h_decisions nullable host uint8[n_samples/4]. Same constraints/errors as kk_process_frames,
+ * h_ref / h_decisions nullable host uint8[n_samples/4] (h_ref NULL with ref_prbs = 1: generated labels, so only
+ * the samples cross PCIe). Same constraints/errors as kk_process_frames,
  * except n_samples may exceed max_samples_per_call (it must be a multiple of 16384). */
 kk_status kk_process_frames_host(kk_ctx* ctx, const void* h_adc, int64_t first_sample, int64_t n_samples,
                                  const uint8_t* h_ref, uint8_t* h_decisions);

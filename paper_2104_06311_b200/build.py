@@ -20,7 +20,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include")]
 # diagnostics only (e.g. KK_NVCC_DEFINES=-DKK_PHASE_TIMING with --force); never set for a measured build
 FLAGS += os.environ.get("KK_NVCC_DEFINES", "").split()
-SOURCES = ["k1_kk.cu", "k1u_kk.cu", "k2_mf.cu", "k3_eq.cu", "k3_ddlms.cu", "kk_host.cpp"]
+SOURCES = ["k1_kk.cu", "k1u_kk.cu", "k2_mf.cu", "k3_eq.cu", "k3_ddlms.cu", "kref.cu", "kk_host.cpp"]
 
 
 def _newer(target: str, deps) -> bool:

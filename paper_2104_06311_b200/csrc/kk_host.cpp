@@ -48,6 +48,8 @@ struct kk_ctx {
   int64_t halo = 0;              // kk_halo: kHalo, or kHaloUp with upsample = 2
   double hb_odd[8] = {0};        // odd half-band taps f[1], f[3], …, f[15] (upsample = 2)
   uint8_t* d_sched = nullptr;
+  uint32_t ref_key = 0;          // ref_prbs: key of the transmitter's label hash (kk::ref_prbs_key(ref_seed))
+  uint8_t* d_refgen = nullptr;   // ref_prbs: generated reference labels of a device-buffer call
   // scratch
   int64_t nmax = 0;
   float2* d_E = nullptr;
@@ -270,6 +272,7 @@ kk_status validate(const kk_config& c, std::string& why) {
   if (!(c.fs_hz > 0) || !(c.baud_hz > 0) || std::fabs(c.fs_hz / c.baud_hz - 4.0) > 1e-9) return bad("fs/baud must be 4");
   if (c.debug_guard != 0 && c.debug_guard != 1) return bad("debug_guard must be 0 or 1");
   if (c.upsample != 1 && c.upsample != 2) return bad("upsample must be 1 or 2");
+  if (c.ref_prbs != 0 && c.ref_prbs != 1) return bad("ref_prbs must be 0 or 1");
   if (c.lo_den <= 0 || c.lo_den > 4096 || c.lo_num < 0 || c.lo_num >= c.lo_den) return bad("lo_num/lo_den out of range");
   if (c.sideband != 1 && c.sideband != -1) return bad("sideband must be +1 or -1");
   if (!(c.rolloff > 0 && c.rolloff <= 1)) return bad("rolloff must be in (0,1]");
@@ -391,7 +394,9 @@ void kk_config_default(kk_config* c) {
   c->ddlms_mu_warm = 2e-3;
   c->ddlms_mu = 2.5e-4;
   c->upsample = 1;
-  c->reserved1 = 0;
+  c->ref_prbs = 0;
+  c->ref_seed = 0;
+  c->reserved2 = 0;
 }
 
 size_t kk_config_sizeof(void) { return sizeof(kk_config); }
@@ -534,6 +539,10 @@ kk_status kk_init(const kk_config* cfg, kk_ctx** out) {
   if (cfg->keep_intermediate) chk(dalloc(c, "z", &c->d_z, (size_t)(n / 4) * sizeof(float2)));
   if (ddlms) chk(dalloc(c, "segpow", &c->d_segpow, (size_t)((n / 2 + 2 * c->Ky) / 512 + 2 * (c->mfKeep / 512) + 16) * sizeof(float)));
   chk(dalloc(c, "counters", &c->d_counters, 32 * sizeof(unsigned long long)));
+  if (cfg->ref_prbs) {
+    chk(dalloc(c, "refgen", &c->d_refgen, (size_t)(n / 4)));
+    c->ref_key = kk::ref_prbs_key(cfg->ref_seed);
+  }
   chk(cudaMemset(c->d_counters, 0, 32 * sizeof(unsigned long long)));
   if (e == cudaSuccess) {
     const size_t k3 = kk::k3_smem_bytes(c->K);
@@ -582,6 +591,10 @@ kk_status kk_process_frames_ex(kk_ctx* c, const void* d_adc, int64_t first, int6
   const kk_config& cf = c->cfg;
   const size_t esz = cf.input_dtype == KK_IN_FLOAT32 ? 4 : cf.input_dtype == KK_IN_UINT8 ? 1 : 2;
   const int F = kk::kFrameSamp;
+  if (!d_ref && cf.ref_prbs) {                   // the transmitter's known labels, generated on the device
+    kk::launch_ref_prbs(c->d_refgen, first / 4, n / 4, c->ref_key, c->d_sched, cf.n_segments, cf.segment_frames, s);
+    d_ref = c->d_refgen;
+  }
 
   // K1 over blocks [ (first − F)/512, (first + n + F)/512 )
   const int64_t jb0 = (first - F) / kk::kHilbertHop;

@@ -86,6 +86,11 @@ void launch_k3(const float2* y, int64_t frame0, int64_t n_frames, int K, const f
                int64_t clamp_frame_off, const uint8_t* ref, uint8_t* dec, float2* z, unsigned long long* counters,
                const K3Params& p, int num_sms, cudaStream_t s);
 
+// Reference labels of the synthetic transmitter for global symbols [sym0, sym0 + n_sym) (kk_config.ref_prbs).
+uint32_t ref_prbs_key(uint32_t seed);
+void launch_ref_prbs(uint8_t* out, int64_t sym0, int64_t n_sym, uint32_t key, const uint8_t* schedule,
+                     int n_segments, int64_t segment_frames, cudaStream_t s);
+
 // K3 (paper arrangement): 4-tap T/2-spaced widely-linear DDLMS, one thread per restart block.
 void launch_k3_ddlms(const float2* y, int64_t y_base, int64_t sym_first, int64_t n_blocks, int B, int W,
                      const int* clampcnt, int64_t clamp_frame_off, const uint8_t* ref, uint8_t* dec, float2* z,

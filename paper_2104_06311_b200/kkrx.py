@@ -9,7 +9,7 @@ from __future__ import annotations
 
 import ctypes
 import os
-from ctypes import POINTER, c_char_p, c_double, c_float, c_int, c_int32, c_int64, c_size_t, c_uint8, c_uint64, c_void_p
+from ctypes import POINTER, c_char_p, c_double, c_float, c_int, c_int32, c_int64, c_size_t, c_uint8, c_uint32, c_uint64, c_void_p
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libkkrx.so")
@@ -38,7 +38,7 @@ class kk_config(ctypes.Structure):
         ("keep_intermediate", c_int32),
         ("eq_mode", c_int32), ("ddlms_block", c_int32), ("ddlms_warmup", c_int32), ("debug_guard", c_int32),
         ("ddlms_mu_warm", c_double), ("ddlms_mu", c_double),
-        ("upsample", c_int32), ("reserved1", c_int32),
+        ("upsample", c_int32), ("ref_prbs", c_int32), ("ref_seed", c_uint32), ("reserved2", c_int32),
     ]
 
 
