@@ -469,13 +469,18 @@ def main():
             "flops_per_launch": u["flops"], "bytes_per_launch": u["bytes"],
             "frac_alu": u["flops"] / (avg_ms * 1e-3) / 1e12 / peak_fp32,
             "frac_hbm": u["bytes"] / (avg_ms * 1e-3) / 1e9 / hbm_peak,
+            # SURVEY §8(d)'s reading: fraction of the kernel's attainable roofline min(BW·AI, P_FP32)
+            "attainable_tflops": min(hbm_peak * 1e-3 * u["flops"] / u["bytes"], peak_fp32),
+            "frac_attainable": (u["flops"] / (avg_ms * 1e-3) / 1e12)
+            / min(hbm_peak * 1e-3 * u["flops"] / u["bytes"], peak_fp32),
         }
     dom = max(kernels, key=lambda k: kernels[k]["share"])
     kd = kernels[dom]
     roofline = {"kernel": dom, "bound": "alu", "achieved": kd["tflops"], "peak": peak_fp32, "unit": "TFLOP/s",
                 "frac": kd["tflops"] / peak_fp32, "traffic": traffic.get(dom),
                 "peak_source": "148 SM x 128 FP32 lanes x 2 x clocks.max.sm (derived, DESIGN.md §6)",
-                "hbm_gbs": kd["gbs"], "hbm_frac_of_measured": kd["frac_hbm"]}
+                "hbm_gbs": kd["gbs"], "hbm_frac_of_measured": kd["frac_hbm"],
+                "attainable": kd["attainable_tflops"], "frac_attainable": kd["frac_attainable"]}
 
     # ---------------- end to end through the host-buffer C-ABI call (pinned memory, copies inside)
     e2e = None
