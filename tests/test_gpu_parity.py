@@ -138,6 +138,20 @@ def test_chunk_and_shard_invariance():
     assert np.array_equal(np.concatenate(decs), whole["dec"])
 
 
+def test_decision_paths_agree():
+    """K3's decision phase has a specialised loop for the common case (square/rectangular format, labels staged
+    by TMA, no z output) next to the general one (32-cross frames, z output, dead frames): both must give the
+    same decisions and counters — run once without and once with the z output on a mixed 4…64-QAM stream."""
+    case = make_case(formats=(4, 8, 16, 32, 64), segment_frames=1, dl=32000.0, cspr=10.0, esn0=15.0, n=10 * F,
+                     seed=17)
+    fast = run_gpu(case, keep=False)
+    general = run_gpu(case, keep=True)
+    assert np.array_equal(fast["dec"], general["dec"])
+    for k in ("sym", "sym_err", "bits", "bit_err", "clamped", "frames", "bad_frames"):
+        assert fast["stats"][k] == general["stats"][k], k
+    assert sum(fast["stats"]["sym_err"]) > 0
+
+
 # ----------------------------------------------------------------------------- edge cases
 def test_single_frame_and_stream_start():
     case = make_case(M=4, n=F, first=0, esn0=10.0, seed=5)        # first frame of the stream, n = one frame
