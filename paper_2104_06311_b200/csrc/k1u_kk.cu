@@ -22,7 +22,7 @@
 // E₂ at the positions the decimation needs goes to group scratch as even/odd polyphase arrays (both
 // blocks); each warp then decimates one block, 4 adjacent outputs per lane-step from one 20-sample odd
 // window (16-B loads, conflict-free through the chunk swizzle swz2) with 16-B coalesced stores. I, a₂ and the
-// polyphase arrays are stored chunk-swizzled (swz4 / swz2) so that the 32- and 64-B lane-stride vector accesses
+// polyphase arrays are stored chunk-swizzled (swz4, swz4x, swz2 in kk_device.cuh) so that the 32- and 64-B lane-stride vector accesses
 // of the conversion, the interpolation and the decimation are conflict-free (ncu: 36 % excess wavefronts before).
 #include "kk_device.cuh"
 #include "kk_params.h"
@@ -126,7 +126,7 @@ k1u_kk_kernel(const Tin* __restrict__ adc0, float2* __restrict__ E, float2* __re
     }
 #pragma unroll
     for (int t = 0; t < 4; ++t)
-      *reinterpret_cast<float4*>(a2 + swz4(16 * g + 4 * t)) = make_float4(out[4 * t], out[4 * t + 1], out[4 * t + 2], out[4 * t + 3]);
+      *reinterpret_cast<float4*>(a2 + swz4x(16 * g + 4 * t)) = make_float4(out[4 * t], out[4 * t + 1], out[4 * t + 2], out[4 * t + 3]);
   }
   __syncthreads();
 
@@ -138,7 +138,7 @@ k1u_kk_kernel(const Tin* __restrict__ adc0, float2* __restrict__ E, float2* __re
   const int k1p = 16 * wg + (lane & 15), h = lane >> 4;   // role after the transpose: (k1', parity of t)
   float2 v[32];
 #pragma unroll
-  for (int r = 0; r < 32; ++r) v[r] = make_float2(a2[swz4(w0i + t + 64 * r)], a2[swz4(w1i + t + 64 * r)]);
+  for (int r = 0; r < 32; ++r) v[r] = make_float2(a2[swz4x(w0i + t + 64 * r)], a2[swz4x(w1i + t + 64 * r)]);
   dft_reg<32, -1>(v);                               // Y[t][k1] = Σ_r x[t + 64r]·W₃₂^{r·k1}
   twiddle32<-1, 64>(v, tw + t);               // × W₂₀₄₈^{t·k1}
 #pragma unroll
@@ -200,10 +200,10 @@ k1u_kk_kernel(const Tin* __restrict__ adc0, float2* __restrict__ E, float2* __re
     if (need) {
       float sn, cs;
       __sincosf(v[r].x * sc, &sn, &cs);
-      float m = __expf(a2[swz4(w0i + pos)] + p.half_ln_iref);
+      float m = __expf(a2[swz4x(w0i + pos)] + p.half_ln_iref);
       poly0[swz2(idx)] = make_float2(m * cs, m * sn);
       __sincosf(v[r].y * sc, &sn, &cs);
-      m = __expf(a2[swz4(w1i + pos)] + p.half_ln_iref);
+      m = __expf(a2[swz4x(w1i + pos)] + p.half_ln_iref);
       poly1[swz2(idx)] = make_float2(m * cs, m * sn);
     }
   }

@@ -198,12 +198,14 @@ __device__ __forceinline__ void twiddle32(float2 (&v)[32], const float2* __restr
   }
 }
 
-// 16-B chunk XOR swizzles within 128-B rows (the row index selects the permutation), so that the vector
-// accesses with a 32- or 64-B lane stride of K1/K1U hit 8 distinct chunk positions per 8 lanes (conflict-free),
-// while scalar accesses to 32 consecutive floats (one row) stay conflict-free:
-//   swz4: float index (32 floats per row, chunks of 4);  swz2: float2 index (16 float2 per row, chunks of 2)
-__device__ __forceinline__ int swz4(int m) { return m ^ (((m >> 5) & 7) << 2); }
-__device__ __forceinline__ int swz2(int m) { return m ^ (((m >> 4) & 7) << 1); }
+// 16-B chunk XOR swizzles within 128-B rows (K1U's shared arrays). A quarter-warp's eight 16-B accesses are
+// conflict-free iff they hit eight distinct chunk positions of their rows; scalar accesses to 32 consecutive floats
+// (one row) stay conflict-free under any chunk permutation of the row.
+//   swz4x: float index, chunk bits ^= row bits (3) — for 64-B lane strides (4 chunks per lane);
+//   swz4 / swz2: float / float2 index, chunk bit 0 ^= row bit 0 — for 32-B lane strides (2 chunks per lane).
+__device__ __forceinline__ int swz4x(int m) { return m ^ (((m >> 5) & 7) << 2); }
+__device__ __forceinline__ int swz4(int m) { return m ^ (((m >> 5) & 1) << 2); }
+__device__ __forceinline__ int swz2(int m) { return m ^ (((m >> 4) & 1) << 1); }
 
 // ------------------------------------------------------------------ reductions
 __device__ __forceinline__ float warp_sum(float v) {
