@@ -19,8 +19,19 @@
 #include <algorithm>
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX v3: host-side ranges for nsys / ncu --nvtx timelines
 
 #include "../../include/kkrx.h"
+
+namespace {
+// NVTX range around a library call or one of its kernel launches (SURVEY §5 tracing); no-op cost without a tool
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+}  // namespace
 #include "kk_params.h"
 
 namespace kk {
@@ -580,6 +591,7 @@ kk_status kk_process_frames(kk_ctx* c, const void* d_adc, int64_t first, int64_t
 
 kk_status kk_process_frames_ex(kk_ctx* c, const void* d_adc, int64_t first, int64_t n, const uint8_t* d_ref,
                                uint8_t* d_dec, uint32_t* d_ferr, kk_stream_t stream) {
+  NvtxRange call_("kk_process_frames");
   if (!c || !d_adc) return fail(c, KK_ERR_NULL, "kk_process_frames: NULL ctx or input");
   if (n < kk::kFrameSamp) return fail(c, KK_ERR_SHORT, "kk_process_frames: n_samples < one frame");
   if (first < 0 || first % kk::kFrameSamp || n % kk::kFrameSamp)
@@ -592,6 +604,7 @@ kk_status kk_process_frames_ex(kk_ctx* c, const void* d_adc, int64_t first, int6
   const size_t esz = cf.input_dtype == KK_IN_FLOAT32 ? 4 : cf.input_dtype == KK_IN_UINT8 ? 1 : 2;
   const int F = kk::kFrameSamp;
   if (!d_ref && cf.ref_prbs) {                   // the transmitter's known labels, generated on the device
+    NvtxRange r_("kk::ref_prbs");
     kk::launch_ref_prbs(c->d_refgen, first / 4, n / 4, c->ref_key, c->d_sched, cf.n_segments, cf.segment_frames, s);
     d_ref = c->d_refgen;
   }
@@ -623,11 +636,14 @@ kk_status kk_process_frames_ex(kk_ctx* c, const void* d_adc, int64_t first, int6
     for (auto& e : tev) e = take_event(c);
     cudaEventRecord(tev[0], s);
   }
-  if (cf.upsample == 2)
+  if (cf.upsample == 2) {
+    NvtxRange r_("kk::K1U KK front end + Hilbert (8 sps)");
     kk::launch_k1u(static_cast<const char*>(d_adc) - (int64_t)kk::kHaloUp * (int64_t)esz, cf.input_dtype, nblk,
                    c->d_E, c->d_part, c->d_clamp, c->d_tw2048u, pu, s);
-  else
+  } else {
+    NvtxRange r_("kk::K1 KK front end + Hilbert");
     kk::launch_k1(adc0, cf.input_dtype, nblk / 2, c->d_E, c->d_part, c->d_clamp, c->d_tw1024, p1, s);
+  }
 
   // K2 over the MF tiles covering y[first/2 − K, (first + n)/2 + K)
   const int64_t y_first = first / 2 - c->Ky;
@@ -651,8 +667,11 @@ kk_status kk_process_frames_ex(kk_ctx* c, const void* d_adc, int64_t first, int6
       p2.rho[r] = make_float2((float)std::cos(a), (float)std::sin(a));
     }
   }
-  kk::launch_k2(c->mfN, c->d_E, first - F, c->d_part, c->d_clamp, jb0, t_lo, t_hi - t_lo + 1, c->d_y, y_first,
-                y_count, c->d_H, c->d_Hc, c->d_lo, c->d_tw256, c->d_twN, c->d_twI, p2, c->num_sms, s);
+  {
+    NvtxRange r2_("kk::K2 carrier removal + mixer + MF + decimation");
+    kk::launch_k2(c->mfN, c->d_E, first - F, c->d_part, c->d_clamp, jb0, t_lo, t_hi - t_lo + 1, c->d_y, y_first,
+                  y_count, c->d_H, c->d_Hc, c->d_lo, c->d_tw256, c->d_twN, c->d_twI, p2, c->num_sms, s);
+  }
 
   if (c->timing) cudaEventRecord(tev[2], s);
   // K3 one CTA per frame
@@ -677,10 +696,12 @@ kk_status kk_process_frames_ex(kk_ctx* c, const void* d_adc, int64_t first, int6
     pd.widely_linear = cf.eq_widely_linear;
     pd.frame_err = d_ref ? d_ferr : nullptr;
     if (pd.frame_err) cudaMemsetAsync(pd.frame_err, 0, (size_t)(n / F) * 2 * sizeof(uint32_t), s);
+    NvtxRange r3_("kk::K3' DDLMS");
     kk::launch_k3_ddlms(c->d_y, c->Ky, first / 4, n / 4 / cf.ddlms_block, cf.ddlms_block, cf.ddlms_warmup,
                         c->d_clamp, (int64_t)F / kk::kHilbertHop, d_ref, d_dec,
                         cf.keep_intermediate ? c->d_z : nullptr, c->d_counters, pd, s);
   } else {
+    NvtxRange r3_("kk::K3 block-LS EQ + CPR + decisions");
     kk::launch_k3(c->d_y, first / F, nfr, c->K, c->d_wcd, c->d_clamp, (int64_t)F / kk::kHilbertHop /*skip frame −1*/,
                   d_ref, d_dec, cf.keep_intermediate ? c->d_z : nullptr, c->d_counters, p3, c->num_sms, s);
   }
@@ -700,6 +721,7 @@ kk_status kk_process_frames_ex(kk_ctx* c, const void* d_adc, int64_t first, int6
 
 kk_status kk_process_frames_host(kk_ctx* c, const void* h_adc, int64_t first, int64_t n, const uint8_t* h_ref,
                                  uint8_t* h_dec) {
+  NvtxRange call_("kk_process_frames_host");
   if (!c || !h_adc) return fail(c, KK_ERR_NULL, "kk_process_frames_host: NULL ctx or input");
   if (n < kk::kFrameSamp) return fail(c, KK_ERR_SHORT, "kk_process_frames_host: n_samples < one frame");
   if (first < 0 || first % kk::kFrameSamp || n % kk::kFrameSamp)
