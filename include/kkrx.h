@@ -68,7 +68,7 @@ typedef struct kk_config {
   int32_t frame_symbols;         /* 4096 [fixed] (R23)                                                   */
   int32_t eq_taps;               /* 0 = tap-count rule of SURVEY §8(a); else odd L in [3, 15]           */
   int32_t eq_widely_linear;      /* 1 = widely linear ("widely-linear"), 0 = linear only    */
-  int32_t cpr_window;            /* 256 symbols; one of 16,32,64,128,256,512 (R12)                       */
+  int32_t cpr_window;            /* 256 symbols; one of 256, 512, 1024, 2048, 4096 (R12; whole 256-blocks)   */
   double  eq_ridge;              /* 1e-3: λ = ridge·tr(R)/(2L) (R10)                                     */
   double  dispersion_ps_per_nm;  /* accumulated D·L, e.g. 200000 for 10,000 km at 20 ps/nm/km          */
   double  lambda_m;              /* 1550.51e-9                                             */
