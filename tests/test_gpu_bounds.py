@@ -112,3 +112,23 @@ def test_guarded_host_path_and_repeated_calls():
     assert st["frames"] == case["n"] // F and st["bad_frames"] == 0
     assert int(np.sum(dec.numpy() != case["ref"].numpy())) == sum(st["sym_err"])   # every decision written
     rx.close()
+
+
+@pytest.mark.parametrize("eq_mode", ["block_ls", "ddlms"])
+def test_guarded_generated_reference(eq_mode):
+    """kk_config.ref_prbs: the generated label buffer is canary-guarded too, and counting against it equals
+    counting against the caller's label buffer (no ref argument: the generator's labels are used)."""
+    n = 3 * F
+    case = make_case(formats=(4, 8, 16, 32, 64), segment_frames=1, dl=32000.0, esn0=16.0, n=n, first=5 * F,
+                     seed=902, eq_mode=eq_mode)
+    rx0 = receiver_for(case, keep=False, max_samples=n)
+    rx1 = receiver_for(case, keep=False, max_samples=n, debug_guard=True, ref_prbs_seed=case["lc"].seed)
+    codes = case["codes"].cuda()
+    d0 = torch.zeros(n // 4, dtype=torch.uint8, device="cuda")
+    d1 = torch.zeros(n // 4, dtype=torch.uint8, device="cuda")
+    rx0.process(codes, case["first"], n, ref=case["ref"].cuda(), decisions=d0)
+    rx1.process(codes, case["first"], n, decisions=d1)
+    assert rx1.check_guards() >= 7                 # + the generated-label buffer
+    assert torch.equal(d0, d1) and rx0.stats() == rx1.stats()
+    rx0.close()
+    rx1.close()
