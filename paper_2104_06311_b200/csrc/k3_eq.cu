@@ -651,7 +651,15 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
           cr += __shfl_xor_sync(0xffffffffu, cr, o);
           ci += __shfl_xor_sync(0xffffffffu, ci, o);
         }
-        if (j == 0) { red[2 * blk] = cr; red[2 * blk + 1] = ci; }
+        if (j == 0) {
+          if (p.cpr_window == 256) {                   // window = block: its rotation right here (the window sum
+            const float m2 = cr * cr + ci * ci;          // below would add the single block to 0: same value)
+            const float rs = (m2 > 0.f && isfinite(m2)) ? rsqrtf(m2) : 0.f;
+            rot[blk] = (rs > 0.f) ? make_float2(cr * rs, -ci * rs) : make_float2(1.f, 0.f);
+          } else {
+            red[2 * blk] = cr; red[2 * blk + 1] = ci;
+          }
+        }
       }
       __syncthreads();
       // the frame buffer (ys, reused for the CPR products) is dead now: start the next frame's sample copy
@@ -660,16 +668,18 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
         const int nf = fl + (int)gridDim.x;
         if (nf < n_frames) { issue_y(nf); early = true; }
       }
-      if (tid < K3_SPT) {                              // window = (W/256) consecutive blocks, fixed order
-        const int per = p.cpr_window / K3_THREADS;
-        const int w0 = (tid / per) * per;
-        float cr = 0.f, ci = 0.f;
-        for (int q = 0; q < per; ++q) { cr += red[2 * (w0 + q)]; ci += red[2 * (w0 + q) + 1]; }
-        const float m2 = cr * cr + ci * ci;            // rotation conj(c)/|c|; none if c = 0
-        const float rs = (m2 > 0.f && isfinite(m2)) ? rsqrtf(m2) : 0.f;
-        rot[tid] = (rs > 0.f) ? make_float2(cr * rs, -ci * rs) : make_float2(1.f, 0.f);
+      if (p.cpr_window != 256) {                       // kernel-uniform
+        if (tid < K3_SPT) {                            // window = (W/256) consecutive blocks, fixed order
+          const int per = p.cpr_window / K3_THREADS;
+          const int w0 = (tid / per) * per;
+          float cr = 0.f, ci = 0.f;
+          for (int q = 0; q < per; ++q) { cr += red[2 * (w0 + q)]; ci += red[2 * (w0 + q) + 1]; }
+          const float m2 = cr * cr + ci * ci;          // rotation conj(c)/|c|; none if c = 0
+          const float rs = (m2 > 0.f && isfinite(m2)) ? rsqrtf(m2) : 0.f;
+          rot[tid] = (rs > 0.f) ? make_float2(cr * rs, -ci * rs) : make_float2(1.f, 0.f);
+        }
+        __syncthreads();
       }
-      __syncthreads();
       KK_PT(6);
     }
 
