@@ -236,7 +236,9 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
     // computed here for the CTA's first frame, later ones during the previous frame and published at its end
     if (it == 0 && tid == 32) misc[2] = frame_order(frame0 + fl);
     mbar_wait(bar, it & 1);
-    __syncthreads();
+    // the previous frame's closing barrier already ordered misc[] (the QAM order) and every read of the buffers;
+    // the TMA data is visible through the mbarrier — only the CTA's first frame needs a barrier here
+    if (it == 0) __syncthreads();
     KK_PT(0);
     const int M = misc[2];
     const int bi = (M == 4) ? 0 : (M == 8) ? 1 : (M == 16) ? 2 : (M == 32) ? 3 : 4;
