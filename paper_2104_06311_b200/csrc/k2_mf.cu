@@ -187,7 +187,7 @@ k2_mf_kernel(const float2* __restrict__ E, int64_t E_first, const float2* __rest
 #pragma unroll
         for (int r = 0; r < R3; ++r) v3[it][r] = src[r * (256 + 16)];
       }
-      __syncthreads();
+      // no barrier: the folded outputs Y2[j + 256 r] (r < R3/2) overwrite only this thread's own inputs
 #pragma unroll
       for (int it = 0; it < PER3; ++it) {
         const int j = tid + T * it;
