@@ -128,10 +128,15 @@ struct K3Layout {
   static constexpr int WS = N + 3;                 // odd row stride (doubles) of the real system [A | q1 q2]
   static constexpr int RED_B = K3_WARPS * NRED * 4;
   static constexpr int MAT_B = N * WS * 8;
+  // two label buffers (the next frame's labels land while this frame's are read) when two CTAs per SM still
+  // fit in the SM's 228 KB with them (1 KB reserved per CTA): K ≤ 6
+  static constexpr int TOTAL1 = YS * 8 + kFrameSym + kFrameSym * 8 + (RED_B > MAT_B ? RED_B : MAT_B) +
+                                (NRED > 128 ? NRED : 128) * 8 + 2 * L * 8 + 16 * 8 + 32 * 4 + 16 + 64 * 4;
+  static constexpr int NREFB = (2 * (TOTAL1 + kFrameSym + 1024) <= 228 * 1024) ? 2 : 1;
   // shared memory (bytes)
   static constexpr int Y = 0;                      // frame samples; reused for the CPR products after pass 2
-  static constexpr int REF = Y + YS * 8;
-  static constexpr int US = REF + kFrameSym;       // y¹ → u → z per symbol (float2 × 4096)
+  static constexpr int REF = Y + YS * 8;           // NREFB × 4096 labels
+  static constexpr int US = REF + NREFB * kFrameSym;   // y¹ → u → z per symbol (float2 × 4096)
   static constexpr int RED = US + kFrameSym * 8;   // warp partial sums; the solve's matrix aliases it
   static constexpr int MAT = RED;
   static constexpr int DRES = RED + (RED_B > MAT_B ? RED_B : MAT_B);
@@ -141,6 +146,7 @@ struct K3Layout {
   static constexpr int BAR = CC + 32 * 4;          // mbarrier
   static constexpr int MISC = BAR + 16;
   static constexpr int TOTAL = MISC + 64 * 4;
+  static_assert(TOTAL == TOTAL1 + (NREFB - 1) * kFrameSym, "layout size");
   static_assert(N <= 32, "one matrix row per lane");
   static_assert((YS * 8) % 16 == 0, "TMA size");
 };
@@ -181,22 +187,28 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
   const bool wl = p.widely_linear != 0;
   float* red_w = red + warp * NRED;
   const bool ref_tma = ref && ((reinterpret_cast<uintptr_t>(ref) & 15) == 0);
+  // double-buffered labels: frame `it` of this CTA reads buffer it & 1; the next frame's labels are requested
+  // as soon as this frame's copies have landed (its own buffer was last read before the previous frame's
+  // closing barrier), so the frame start no longer waits for a label copy issued at the end of the frame
+  const bool dbl = (Lay::NREFB == 2) && ref_tma;
+  auto ref_buf = [&](int b) { return ref_s + (dbl ? (b & 1) * kFrameSym : 0); };
   constexpr uint32_t YBYTES = Lay::YS * 8;
 
   // thread 0: TMA the frame samples (and, separately, its labels) into shared memory. One arrival with the
-  // total byte count; the two copies may be issued at different times (the phase completes when both land).
+  // total byte count; the copies may be issued at different times (the phase completes when all land). The
+  // arrival comes with the first copy of the frame: the samples' (single label buffer) or the labels' (dbl).
   auto issue_y = [&](int fl) {
     fence_proxy_async_smem();                     // the frame buffer was written by generic stores (CPR products)
-    const uint32_t bytes = YBYTES + 128u + (ref_tma ? (uint32_t)kFrameSym : 0u);
-    mbar_arrive_expect_tx(bar, bytes);
+    if (!dbl) mbar_arrive_expect_tx(bar, YBYTES + 128u + (ref_tma ? (uint32_t)kFrameSym : 0u));
     tma_bulk_g2s(ys, y + (int64_t)fl * (2 * kFrameSym), YBYTES, bar);
     tma_bulk_g2s(smem + Lay::CC, clampcnt + clamp_frame_off + (int64_t)fl * 32, 128u, bar);
   };
-  auto issue_ref = [&](int fl) {
-    if (ref_tma) fence_proxy_async_smem();
-    if (ref_tma) tma_bulk_g2s(ref_s, ref + (int64_t)fl * kFrameSym, kFrameSym, bar);
+  auto issue_ref = [&](int fl, int b) {
+    if (!ref_tma) return;
+    fence_proxy_async_smem();
+    if (dbl) mbar_arrive_expect_tx(bar, YBYTES + 128u + (uint32_t)kFrameSym);
+    tma_bulk_g2s(ref_buf(b), ref + (int64_t)fl * kFrameSym, kFrameSym, bar);
   };
-  auto issue = [&](int fl) { issue_y(fl); issue_ref(fl); };
   auto prefetch = [&](int fl) {
     prefetch_l2(y + (int64_t)fl * (2 * kFrameSym), YBYTES);
     if (ref_tma) prefetch_l2(ref + (int64_t)fl * kFrameSym, kFrameSym);
@@ -207,7 +219,8 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
   if (tid == 0) mbar_init(bar, 1);
   __syncthreads();
   if (tid == 0 && (int)blockIdx.x < n_frames) {
-    issue(blockIdx.x);
+    if (dbl) { issue_ref(blockIdx.x, 0); issue_y(blockIdx.x); }
+    else { issue_y(blockIdx.x); issue_ref(blockIdx.x, 0); }
     if ((int)blockIdx.x + (int)gridDim.x < n_frames) prefetch(blockIdx.x + gridDim.x);
   }
   float2 wc[L];
@@ -236,6 +249,10 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
     // computed here for the CTA's first frame, later ones during the previous frame and published at its end
     if (it == 0 && tid == 32) misc[2] = frame_order(frame0 + fl);
     mbar_wait(bar, it & 1);
+    // dbl: arm the next frame's phase now and request its labels into the other buffer (the phase cannot
+    // complete before its samples are requested after the CPR sums, when every thread is past this wait)
+    if (dbl && tid == 0 && fl + (int)gridDim.x < n_frames) issue_ref(fl + (int)gridDim.x, it + 1);
+    const uint8_t* ref_cur = ref_buf(it);
     // the previous frame's closing barrier already ordered misc[] (the QAM order) and every read of the buffers;
     // the TMA data is visible through the mbarrier — only the CTA's first frame needs a barrier here
     if (it == 0) __syncthreads();
@@ -665,7 +682,8 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
       }
       __syncthreads();
       // the frame buffer (ys, reused for the CPR products) is dead now: start the next frame's sample copy
-      // so that it overlaps the decisions (its labels follow at the end of the frame, after ref_s is read)
+      // so that it overlaps the decisions (its labels: already requested (dbl), else at the end of the frame,
+      // after the single label buffer is read)
       if (tid == 0) {
         const int nf = fl + (int)gridDim.x;
         if (nf < n_frames) { issue_y(nf); early = true; }
@@ -694,7 +712,7 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
       for (int s = 0; s < K3_SPT; ++s) {
         const int kl = tid + K3_THREADS * s;
         const int lab = sl.label_sq(cmul(us[kl], rot[s]));
-        const int r = (int)ref_s[kl];
+        const int r = (int)ref_cur[kl];
         serr += (lab != r);
         berr += __popc(lab ^ r);
         dec[sym0 + kl] = (uint8_t)lab;
@@ -706,7 +724,7 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
         const float2 zz = dead ? make_float2(0.f, 0.f) : cmul(us[kl], rot[s]);
         const int lab = sl.label(zz);
         if (ref) {
-          const int r = ref_tma ? (int)ref_s[kl] : (int)__ldg(&ref[sym0 + kl]);
+          const int r = ref_tma ? (int)ref_cur[kl] : (int)__ldg(&ref[sym0 + kl]);
           serr += (lab != r);
           berr += __popc(lab ^ r);
         }
@@ -728,7 +746,9 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
     if (tid == 0) {
       const int nf = fl + (int)gridDim.x;
       if (nf < n_frames) {
-        if (early) issue_ref(nf); else issue(nf);             // from L2 (prefetched one frame ago)
+        // from L2 (prefetched one frame ago); dbl: the labels were requested at the frame start
+        if (!early) issue_y(nf);
+        if (!dbl) issue_ref(nf, 0);
         if (nf + (int)gridDim.x < n_frames) prefetch(nf + gridDim.x);
       }
       if (ref) {
