@@ -148,6 +148,8 @@ struct K3Layout {
   static constexpr int TOTAL = MISC + 64 * 4;
   static_assert(TOTAL == TOTAL1 + (NREFB - 1) * kFrameSym, "layout size");
   static_assert(N <= 32, "one matrix row per lane");
+  static_assert((2 * ND - 1) * (K + 1) <= K3_THREADS, "one thread per chain point");
+  static_assert(2 * (K + 1) * 8 <= 2 * L * 8, "trace terms fit in th");
   static_assert((YS * 8) % 16 == 0, "TMA size");
 };
 
@@ -354,42 +356,37 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
       __syncthreads();
       KK_PT(3);
 
-      // ---- solve: warp 0 assembles the real system from S, T, p; Gauss–Jordan by warp 0 (N ≤ kGJWarpN) or the CTA
-      int fail = 0;
-      if (warp == 0) {
+      // ---- solve: the CTA assembles the real system from S, T (one thread per chain point), warp 0 adds the
+      //      ridge and the right-hand sides; Gauss–Jordan by warp 0 (N ≤ kGJWarpN) or the CTA.
+      //      Chain (ρ, d) holds S(i, i+d), T(i, i+d) at i = −K+ρ+2m (m < npts), linked by the exact sliding
+      //      recurrence S(i+2, d) = S(i, d) + inc_m with edge samples y[2(k0−1) − i] ↔ y_s[K − 2 − i] and
+      //      y[2(k1−1) − i] ↔ y_s[8190 + K − i]. Thread (chain, m) forms the sum of the chain's first m increments
+      //      itself — the additions of a serial walk, in its order — so no point waits for another. The d = 0
+      //      points leave their diagonal's contribution to tr(G) (WL: rr + ii = Re S; linear: 2·Re S) in tl[].
+      double* tl = reinterpret_cast<double*>(th);   // 2(K+1) trace terms (th is written only after the solve)
+      {
         double* A = mat;   // row-major N × WS: [G + λI | q1 q2]
         constexpr int W = Lay::WS;
-        // lane c < 2·ND walks one (ρ, d) chain S(i, i+d), T(i, i+d), i = −K+ρ, −K+ρ+2, … ≤ K − d, using the
-        // exact sliding recurrence; edge samples y[2(k0−1) − i] ↔ y_s[K − 2 − i], y[2(k1−1) − i] ↔ y_s[8190 + K − i].
-        // The recurrence increments are formed first (all edge loads issued before any store to A, which the
-        // compiler cannot reorder across), then the chain is a running sum. The d = 0 chains also return the
-        // diagonal's contribution to tr(G) (WL: rr + ii = Re S; linear: 2·Re S) for the ridge.
-        double* trp = reinterpret_cast<double*>(th);  // 2 partial traces (th is written only after the solve)
-        if (lane < 2 * ND - 1) {
-          const int rho = lane / ND, d = lane % ND;
-          const int npts = (2 * K - d - rho) / 2 + 1;  // chain points (i = −K + ρ + 2m, m < npts)
-          // edge samples of step m (i → i + 2) are loaded one step ahead, before the step's stores to A
-          float2 a1 = make_float2(0.f, 0.f), a2 = a1, b1 = a1, b2 = a1;
-          auto load_edges = [&](int m) {
-            const int i = -K + rho + 2 * m;
-            a1 = ys[K - 2 - i]; a2 = ys[K - 2 - i - d]; b1 = ys[8190 + K - i]; b2 = ys[8190 + K - i - d];
-          };
-          if (npts > 1) load_edges(0);
-          const double A1 = dres[Lay::NP + 8 * d + 4 * rho], A3 = dres[Lay::NP + 8 * d + 4 * rho + 1];
-          const double A4 = dres[Lay::NP + 8 * d + 4 * rho + 2], A2 = dres[Lay::NP + 8 * d + 4 * rho + 3];
-          double sr = A1 + A2, si = A3 - A4, tr_ = A1 - A2, ti = A3 + A4;   // S = Σ conj(a)·b, T = Σ a·b
-          double tsum = 0.0;
+        const int c = tid / (K + 1), m = tid % (K + 1);
+        if (c < 2 * ND - 1) {
+          const int rho = c / ND, d = c % ND;
+          const int npts = (2 * K - d - rho) / 2 + 1;  // chain points
+          if (m < npts) {
+            const double A1 = dres[Lay::NP + 8 * d + 4 * rho], A3 = dres[Lay::NP + 8 * d + 4 * rho + 1];
+            const double A4 = dres[Lay::NP + 8 * d + 4 * rho + 2], A2 = dres[Lay::NP + 8 * d + 4 * rho + 3];
+            double sr = A1 + A2, si = A3 - A4, tr_ = A1 - A2, ti = A3 + A4;   // S = Σ conj(a)·b, T = Σ a·b
 #pragma unroll
-          for (int m = 0; m <= K; ++m) {
-            if (m >= npts) break;
-            // fp32 edge increments: O(|y|²) terms added to fp64 sums of 4096 such terms
-            float i0 = 0.f, i1 = 0.f, i2 = 0.f, i3 = 0.f;
-            if (m + 1 < npts) {
-              i0 = fmaf(a1.x, a2.x, a1.y * a2.y) - fmaf(b1.x, b2.x, b1.y * b2.y);
-              i1 = fmaf(a1.x, a2.y, -a1.y * a2.x) - fmaf(b1.x, b2.y, -b1.y * b2.x);
-              i2 = fmaf(a1.x, a2.x, -a1.y * a2.y) - fmaf(b1.x, b2.x, -b1.y * b2.y);
-              i3 = fmaf(a1.x, a2.y, a1.y * a2.x) - fmaf(b1.x, b2.y, b1.y * b2.x);
-              if (m + 2 < npts) load_edges(m + 1);
+            for (int mm = 0; mm < K; ++mm) {
+              if (mm < m) {
+                // fp32 edge increments: O(|y|²) terms added to fp64 sums of 4096 such terms
+                const int i = -K + rho + 2 * mm;
+                const float2 a1 = ys[K - 2 - i], a2 = ys[K - 2 - i - d], b1 = ys[8190 + K - i], b2 = ys[8190 + K - i - d];
+                const float i0 = fmaf(a1.x, a2.x, a1.y * a2.y) - fmaf(b1.x, b2.x, b1.y * b2.y);
+                const float i1 = fmaf(a1.x, a2.y, -a1.y * a2.x) - fmaf(b1.x, b2.y, -b1.y * b2.x);
+                const float i2 = fmaf(a1.x, a2.x, -a1.y * a2.y) - fmaf(b1.x, b2.x, -b1.y * b2.y);
+                const float i3 = fmaf(a1.x, a2.y, a1.y * a2.x) - fmaf(b1.x, b2.y, b1.y * b2.x);
+                sr += (double)i0; si += (double)i1; tr_ += (double)i2; ti += (double)i3;
+              }
             }
             const int i = -K + rho + 2 * m;
             const int r = i + K, q = i + d + K;     // S(r, q) = Σ conj(a_r)·a_q, T(r, q) = Σ a_r·a_q
@@ -401,25 +398,35 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
               A[(L + r) * W + (L + q)] = ii; A[(L + q) * W + (L + r)] = ii;
               A[r * W + (L + q)] = ri;       A[(L + q) * W + r] = ri;
               A[(L + r) * W + q] = ir;       A[q * W + (L + r)] = ir;
-              tsum += rr + ii;
+              if (d == 0) tl[rho * (K + 1) + m] = rr + ii;
             } else {
               // real form of the Hermitian R11: [[Re R, −Im R], [Im R, Re R]], R[r][q] = S, R[q][r] = conj(S)
               A[r * W + q] = sr;             A[q * W + r] = sr;
               A[(L + r) * W + (L + q)] = sr; A[(L + q) * W + (L + r)] = sr;
               A[(L + r) * W + q] = si;       A[(L + q) * W + r] = -si;
               A[r * W + (L + q)] = -si;      A[q * W + (L + r)] = si;
-              tsum += sr + sr;
+              if (d == 0) tl[rho * (K + 1) + m] = sr + sr;
             }
-            sr += (double)i0; si += (double)i1; tr_ += (double)i2; ti += (double)i3;
           }
-          if (d == 0) trp[rho] = tsum;
         }
-        __syncwarp();
-        KK_PT(8);
+      }
+      __syncthreads();
+      KK_PT(8);
+      int fail = 0;
+      if (warp == 0) {
+        double* A = mat;
+        constexpr int W = Lay::WS;
         // ridge (R10): λ_c = ridge·tr(R)/n_c. WL: real form uses λ_c/2 and tr(R) = 2·tr(G). Linear: tr(M) = 2·tr(R11)
-        const double trG = trp[0] + trp[1];
+        // tr(G): the d = 0 terms in chain order (ρ = 0: K + 1 points, ρ = 1: K points)
+        double t0 = 0.0, t1 = 0.0;
+#pragma unroll
+        for (int m = 0; m <= K; ++m) t0 += tl[m];
+#pragma unroll
+        for (int m = 0; m < K; ++m) t1 += tl[K + 1 + m];
+        const double trG = t0 + t1;
         KK_PT(9);
-        const double lam = wl ? (double)p.ridge * trG / (double)N : (double)p.ridge * 0.5 * trG / (double)L;
+        // (the factor ridge/n_c does not wait for the trace)
+        const double lam = trG * (wl ? (double)p.ridge / (double)N : (double)p.ridge * 0.5 / (double)L);
         if (lane < L) {
           const int e = lane;
           const double B1 = dres[4 * e], B3 = dres[4 * e + 1], B4 = dres[4 * e + 2], B2 = dres[4 * e + 3];
