@@ -136,7 +136,7 @@ struct K3Layout {
   // shared memory (bytes)
   static constexpr int Y = 0;                      // frame samples; reused for the CPR products after pass 2
   static constexpr int REF = Y + YS * 8;           // NREFB × 4096 labels
-  static constexpr int US = REF + NREFB * kFrameSym;   // y¹ → u → z per symbol (float2 × 4096)
+  static constexpr int US = REF + NREFB * kFrameSym;   // y⁰ (pass 1), then y¹ (pass 2) per symbol (float2 × 4096)
   static constexpr int RED = US + kFrameSym * 8;   // warp partial sums; the solve's matrix aliases it
   static constexpr int MAT = RED;
   static constexpr int DRES = RED + (RED_B > MAT_B ? RED_B : MAT_B);
@@ -658,8 +658,7 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
 #pragma unroll 4
       for (int s = 0; s < K3_SPT; ++s) {
         const int kl = tid + K3_THREADS * s;
-        const float2 uu = cscale(us[kl], sc);
-        us[kl] = uu;
+        const float2 uu = cscale(us[kl], sc);    // (u itself is not stored: the decisions apply sc with the rotation)
         cb[kl] = cmulc(uu, sl.point(uu));
       }
       __syncthreads();
@@ -681,7 +680,8 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
           if (p.cpr_window == 256) {                   // window = block: its rotation right here (the window sum
             const float m2 = cr * cr + ci * ci;          // below would add the single block to 0: same value)
             const float rs = (m2 > 0.f && isfinite(m2)) ? rsqrtf(m2) : 0.f;
-            rot[blk] = (rs > 0.f) ? make_float2(cr * rs, -ci * rs) : make_float2(1.f, 0.f);
+            const float rsc = rs * sc;                   // z = y¹·(sc·conj(c)/|c|)
+            rot[blk] = (rs > 0.f) ? make_float2(cr * rsc, -ci * rsc) : make_float2(sc, 0.f);
           } else {
             red[2 * blk] = cr; red[2 * blk + 1] = ci;
           }
@@ -703,7 +703,8 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
           for (int q = 0; q < per; ++q) { cr += red[2 * (w0 + q)]; ci += red[2 * (w0 + q) + 1]; }
           const float m2 = cr * cr + ci * ci;          // rotation conj(c)/|c|; none if c = 0
           const float rs = (m2 > 0.f && isfinite(m2)) ? rsqrtf(m2) : 0.f;
-          rot[tid] = (rs > 0.f) ? make_float2(cr * rs, -ci * rs) : make_float2(1.f, 0.f);
+          const float rsc = rs * sc;
+          rot[tid] = (rs > 0.f) ? make_float2(cr * rsc, -ci * rsc) : make_float2(sc, 0.f);
         }
         __syncthreads();
       }
