@@ -118,6 +118,18 @@ k2_mf_kernel(const float2* __restrict__ E, int64_t E_first, const float2* __rest
   }
   const int dq = (int)(((p.lo_den - ((int64_t)gridDim.x * HOP) % p.lo_den) % p.lo_den) * p.lo_num % p.lo_den);
 
+  // warps 0, 1: this lane's K1 block sum of the tile's first / second frame (A_f, R5), loaded one tile ahead so
+  // that the carrier estimate at a tile's start does not wait for a global load
+  auto load_part = [&](int64_t ti_) -> float2 {
+    const int64_t s0_ = (tile0 + (n_tiles - 1 - ti_)) * HOP - LEAD;
+    const int64_t fa_ = floordiv(s0_, kFrameSamp);
+    float2 a = make_float2(0.f, 0.f);
+    if (warp == 0 || s0_ + NF > (fa_ + 1) * kFrameSamp) a = part[(fa_ + warp) * 32 - jb0 + lane];
+    return a;
+  };
+  float2 pa = make_float2(0.f, 0.f);
+  if (warp < 2 && (int64_t)blockIdx.x < n_tiles) pa = load_part(blockIdx.x);
+
   // tiles are visited from the END of the range: K1 wrote E front to back, so its most recent (L2-resident)
   // output is consumed first; K3 then walks y front to back, again reading K2's most recent writes first.
   for (int64_t ti = blockIdx.x; ti < n_tiles; ti += gridDim.x) {
@@ -139,9 +151,8 @@ k2_mf_kernel(const float2* __restrict__ E, int64_t E_first, const float2* __rest
     qb += dq; qb -= (qb >= p.lo_den) ? p.lo_den : 0;
     // carrier estimates A_fa, A_fa+1 from K1's per-512-block sums (fixed order → deterministic)
     if (warp < 2) {
-      const int64_t f = fa + warp;
-      float2 a = make_float2(0.f, 0.f);
-      if (warp == 0 || s0 + NF > fsplit) a = part[f * 32 - jb0 + lane];
+      float2 a = pa;
+      if (ti + gridDim.x < n_tiles) pa = load_part(ti + gridDim.x);
       a.x = warp_sum(a.x); a.y = warp_sum(a.y);
       if (lane == 0) A_s[warp] = make_float2(a.x * (1.0f / kFrameSamp), a.y * (1.0f / kFrameSamp));
     }
