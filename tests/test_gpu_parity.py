@@ -152,6 +152,32 @@ def test_decision_paths_agree():
     assert sum(fast["stats"]["sym_err"]) > 0
 
 
+@pytest.mark.parametrize("dl", [32000.0, 200000.0])    # K = 4 (double-buffered labels) and K = 7 (single buffer)
+def test_unaligned_reference_labels(dl):
+    """K3 stages the reference labels by TMA only from a 16-B-aligned buffer (kkrx.h: any alignment is
+    accepted); a label buffer at an odd address takes the per-symbol load path. Decisions and every counter
+    must equal the aligned run's, for both label-buffer layouts of K3 (two buffers for K ≤ 6, one for K = 7)."""
+    from gpu_case import receiver_for
+    case = make_case(formats=(4, 16, 64), segment_frames=1, dl=dl, cspr=10.0, esn0=15.0, n=6 * F, seed=23)
+    n, first = case["n"], case["first"]
+    codes = case["codes"].cuda()
+    outs = []
+    for off in (0, 1):
+        buf = torch.zeros(n // 4 + 16, dtype=torch.uint8, device="cuda")
+        ref = buf[off:off + n // 4]
+        ref.copy_(case["ref"].cuda())
+        assert (ref.data_ptr() % 16 == 0) == (off == 0)
+        dec = torch.zeros(n // 4, dtype=torch.uint8, device="cuda")
+        rx = receiver_for(case, keep=False)
+        rx.process(codes, first, n, ref=ref, decisions=dec, offset=0)
+        outs.append((dec.cpu().numpy(), rx.stats()))
+        rx.close()
+    assert np.array_equal(outs[0][0], outs[1][0])
+    for k in ("sym", "sym_err", "bits", "bit_err", "clamped", "frames", "bad_frames"):
+        assert outs[0][1][k] == outs[1][1][k], k
+    assert sum(outs[0][1]["sym_err"]) > 0
+
+
 # ----------------------------------------------------------------------------- edge cases
 def test_single_frame_and_stream_start():
     case = make_case(M=4, n=F, first=0, esn0=10.0, seed=5)        # first frame of the stream, n = one frame
