@@ -59,36 +59,10 @@ k1_kk_kernel(const Tin* __restrict__ adc0, float2* __restrict__ E, float2* __res
   const float sc_in = p.adc_scale * p.inv_iref, off_in = -p.adc_offset * p.adc_scale * p.inv_iref;
   for (int gi = tid; gi < K1_SAMPLES / 8; gi += K1_THREADS) {
     float x[8];
-    // integer codes → float without I2F: the code c (biased to u = c + 32768 ≥ 0 for int16) becomes the low
-    // mantissa bits of 2²³ by one byte permute (bits 0x4B00_0000 | u = 2²³ + u exactly), and one packed
-    // subtraction of 2²³ (+ 32768) recovers (float)c exactly (all values are integers < 2²⁴); then the same fmaf
     if constexpr (sizeof(Tin) == 2) {
-      const uint4 raw = reinterpret_cast<const uint4*>(stage)[gi];
-      const unsigned w[4] = {raw.x ^ 0x80008000u, raw.y ^ 0x80008000u, raw.z ^ 0x80008000u, raw.w ^ 0x80008000u};
-      constexpr float kBias = 8388608.0f + 32768.0f;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        float2 f = make_float2(__uint_as_float(__byte_perm(w[q], 0x4B000000u, 0x7410)),
-                               __uint_as_float(__byte_perm(w[q], 0x4B000000u, 0x7432)));
-        f = csub(f, make_float2(kBias, kBias));
-        float2 o = make_float2(off_in, off_in);
-        ffma2s(o, sc_in, f);                                   // per lane fmaf(c, sc_in, off_in)
-        x[2 * q] = o.x; x[2 * q + 1] = o.y;
-      }
+      codes8_to_float(reinterpret_cast<const uint4*>(stage)[gi], sc_in, off_in, x);   // no I2F (kk_device.cuh)
     } else if constexpr (sizeof(Tin) == 1) {
-      const uint2 raw = reinterpret_cast<const uint2*>(stage)[gi];
-      constexpr float kBias = 8388608.0f;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const unsigned wq = (q < 2) ? raw.x : raw.y;
-        const unsigned sel0 = 0x7440u | (unsigned)(2 * (q & 1)), sel1 = 0x7440u | (unsigned)(2 * (q & 1) + 1);
-        float2 f = make_float2(__uint_as_float(__byte_perm(wq, 0x4B000000u, sel0)),
-                               __uint_as_float(__byte_perm(wq, 0x4B000000u, sel1)));
-        f = csub(f, make_float2(kBias, kBias));
-        float2 o = make_float2(off_in, off_in);
-        ffma2s(o, sc_in, f);
-        x[2 * q] = o.x; x[2 * q + 1] = o.y;
-      }
+      codes8_to_float(reinterpret_cast<const uint2*>(stage)[gi], sc_in, off_in, x);
     } else {
       const float4 r0 = reinterpret_cast<const float4*>(stage)[2 * gi];
       const float4 r1 = reinterpret_cast<const float4*>(stage)[2 * gi + 1];

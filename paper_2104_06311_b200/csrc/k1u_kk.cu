@@ -78,14 +78,9 @@ k1u_kk_kernel(const Tin* __restrict__ adc0, float2* __restrict__ E, float2* __re
   for (int gi = tid; gi < K1U_IN / 8; gi += K1U_THREADS) {
     float x[8];
     if constexpr (sizeof(Tin) == 2) {
-      const int4 raw = reinterpret_cast<const int4*>(stage)[gi];
-      const short* h = reinterpret_cast<const short*>(&raw);
-#pragma unroll
-      for (int j = 0; j < 8; ++j) x[j] = fmaf((float)h[j], sc_in, off_in);
+      codes8_to_float(reinterpret_cast<const uint4*>(stage)[gi], sc_in, off_in, x);   // no I2F (kk_device.cuh)
     } else if constexpr (sizeof(Tin) == 1) {
-      const uint2 raw = reinterpret_cast<const uint2*>(stage)[gi];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) x[j] = fmaf((float)(((j < 4 ? raw.x : raw.y) >> (8 * (j & 3))) & 0xffu), sc_in, off_in);
+      codes8_to_float(reinterpret_cast<const uint2*>(stage)[gi], sc_in, off_in, x);
     } else {
       const float4 r0 = reinterpret_cast<const float4*>(stage)[2 * gi];
       const float4 r1 = reinterpret_cast<const float4*>(stage)[2 * gi + 1];

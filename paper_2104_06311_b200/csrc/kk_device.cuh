@@ -207,6 +207,39 @@ __device__ __forceinline__ int swz4x(int m) { return m ^ (((m >> 5) & 7) << 2); 
 __device__ __forceinline__ int swz4(int m) { return m ^ (((m >> 5) & 1) << 2); }
 __device__ __forceinline__ int swz2(int m) { return m ^ (((m >> 4) & 1) << 1); }
 
+// ------------------------------------------------------------------ ADC codes → float (K1, K1U)
+// x_j = fmaf((float)c_j, sc, off) for 8 consecutive codes, without I2F: code c (biased to u = c + 32768 ≥ 0 for
+// int16) becomes the low mantissa bits of 2²³ by one byte permute (bits 0x4B00_0000 | u = 2²³ + u exactly), one
+// packed subtraction of 2²³ (+ 32768) recovers (float)c exactly (all values are integers < 2²⁴), then a packed
+// FMA per pair (each lane the scalar fmaf) — bit-identical to the I2F form.
+__device__ __forceinline__ void codes8_to_float(uint4 raw, float sc, float off, float (&x)[8]) {   // int16
+  const unsigned w[4] = {raw.x ^ 0x80008000u, raw.y ^ 0x80008000u, raw.z ^ 0x80008000u, raw.w ^ 0x80008000u};
+  constexpr float kBias = 8388608.0f + 32768.0f;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    float2 f = make_float2(__uint_as_float(__byte_perm(w[q], 0x4B000000u, 0x7410)),
+                           __uint_as_float(__byte_perm(w[q], 0x4B000000u, 0x7432)));
+    f = csub(f, make_float2(kBias, kBias));
+    float2 o = make_float2(off, off);
+    ffma2s(o, sc, f);
+    x[2 * q] = o.x; x[2 * q + 1] = o.y;
+  }
+}
+__device__ __forceinline__ void codes8_to_float(uint2 raw, float sc, float off, float (&x)[8]) {   // uint8
+  constexpr float kBias = 8388608.0f;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const unsigned wq = (q < 2) ? raw.x : raw.y;
+    const unsigned b0 = 2u * (unsigned)(q & 1);
+    float2 f = make_float2(__uint_as_float(__byte_perm(wq, 0x4B000000u, 0x7440u | b0)),
+                           __uint_as_float(__byte_perm(wq, 0x4B000000u, 0x7440u | (b0 + 1u))));
+    f = csub(f, make_float2(kBias, kBias));
+    float2 o = make_float2(off, off);
+    ffma2s(o, sc, f);
+    x[2 * q] = o.x; x[2 * q + 1] = o.y;
+  }
+}
+
 // ------------------------------------------------------------------ reductions
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
