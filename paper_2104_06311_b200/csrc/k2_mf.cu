@@ -86,8 +86,15 @@ __device__ __forceinline__ int64_t floordiv(int64_t a, int64_t b) {
 
 // CH = false: real H (RRC matched filter, north star). CH = true: complex H_cd = RRC × CD inverse (the paper's
 // static filter, eq_mode DDLMS). NF = 4096 or 8192 (the OLS grid).
+// Resident CTAs per SM of the persistent grid (register-limited: 65536 / (T · regs)).
+#ifndef K2_CTAS_4096
+#define K2_CTAS_4096 4
+#endif
+template <int NF>
+constexpr int k2_ctas_per_sm() { return NF == 4096 ? K2_CTAS_4096 : 16384 / NF; }
+
 template <int NF, bool CH>
-__global__ void __launch_bounds__(NF / 32, 16384 / NF)
+__global__ void __launch_bounds__(NF / 32, k2_ctas_per_sm<NF>())
 k2_mf_kernel(const float2* __restrict__ E, int64_t E_first, const float2* __restrict__ part, int64_t jb0,
              int64_t tile0, int64_t n_tiles, float2* __restrict__ y, int64_t y_first, int64_t y_count,
              const float* __restrict__ Hs, const float2* __restrict__ Hc, const float2* __restrict__ lo_tab,
@@ -280,7 +287,7 @@ static void launch_k2_t(const float2* E, int64_t E_first, const float2* part, in
                         const float2* Hc, const float2* lo_tab, const float2* tw256, const float2* twN,
                         const float2* twI, const K2Params& p, int num_sms, cudaStream_t s) {
   constexpr int T = NF / 32;
-  int64_t grid = (int64_t)num_sms * (16384 / NF);
+  int64_t grid = (int64_t)num_sms * k2_ctas_per_sm<NF>();
   if (grid > n_tiles) grid = n_tiles;
   const size_t dyn = (size_t)(NF + NF / 16) * sizeof(float2) +
                      (CH ? (size_t)(NF / 2 - 512) / 512 * (NF / 1024) * sizeof(float) : 0);
