@@ -124,6 +124,7 @@ k1_kk_kernel(const Tin* __restrict__ adc0, float2* __restrict__ E, float2* __res
 
   // ---- a4: E = √I_ref·e^{a}·e^{iσφ} on the central 512 samples; per-block ΣE
   const float sc = p.sideband * (1.0f / 1024.0f);
+  const float l2m = p.half_ln_iref * 1.4426950408889634f;           // log2 √I_ref
   const int64_t blk0 = cta * (2 * K1_WARPS) + 2 * warp;    // block index relative to jb0
   float2* E0 = E + blk0 * kHilbertHop - kHilbertLead;
   float2* E1 = E0 + kHilbertHop;
@@ -134,7 +135,9 @@ k1_kk_kernel(const Tin* __restrict__ adc0, float2* __restrict__ E, float2* __res
     float sn0, cs0, sn1, cs1;
     __sincosf(v[r].x * sc, &sn0, &cs0);
     __sincosf(v[r].y * sc, &sn1, &cs1);
-    const float m0 = __expf(ab0[pos] + p.half_ln_iref), m1 = __expf(ab1[pos] + p.half_ln_iref);
+    // e^{a + ½ln I_ref} = 2^{a·log2 e + log2 √I_ref}: one FFMA + MUFU.EX2 (__expf adds first, then scales)
+    const float m0 = ex2_approx(fmaf(ab0[pos], 1.4426950408889634f, l2m)),
+                m1 = ex2_approx(fmaf(ab1[pos], 1.4426950408889634f, l2m));
     const float2 e0 = cscale(make_float2(cs0, sn0), m0), e1 = cscale(make_float2(cs1, sn1), m1);
     E0[pos] = e0;
     E1[pos] = e1;

@@ -184,6 +184,7 @@ k1u_kk_kernel(const Tin* __restrict__ adc0, float2* __restrict__ E, float2* __re
   // Ev[n] = E₂[2n + 512] (n ∈ [0, 512)), Od[m + 8] = E₂[2m + 513] (m ∈ [−8, 520)); then
   // E[n] = ½·Ev[n] + Σ_{i=1..8} c_i·(Od[n + 8 − i] + Od[n + 7 + i]).
   const float sc = p.sideband * (1.0f / 2048.0f);
+  const float l2m = p.half_ln_iref * 1.4426950408889634f;   // log2 √I_ref (e^{a + ½ln I_ref} = 2^{a·log2 e + l2m})
   float2* poly0 = S;
   float2* poly1 = S + K1U_POLY;
 #pragma unroll
@@ -195,10 +196,10 @@ k1u_kk_kernel(const Tin* __restrict__ adc0, float2* __restrict__ E, float2* __re
     if (need) {
       float sn, cs;
       __sincosf(v[r].x * sc, &sn, &cs);
-      float m = __expf(a2[swz4x(w0i + pos)] + p.half_ln_iref);
+      float m = ex2_approx(fmaf(a2[swz4x(w0i + pos)], 1.4426950408889634f, l2m));
       poly0[swz2(idx)] = make_float2(m * cs, m * sn);
       __sincosf(v[r].y * sc, &sn, &cs);
-      m = __expf(a2[swz4x(w1i + pos)] + p.half_ln_iref);
+      m = ex2_approx(fmaf(a2[swz4x(w1i + pos)], 1.4426950408889634f, l2m));
       poly1[swz2(idx)] = make_float2(m * cs, m * sn);
     }
   }

@@ -54,6 +54,12 @@ __device__ __forceinline__ float2 cmulc(float2 a, float2 b) {
   return r;
 }
 __device__ __forceinline__ float2 cconj(float2 a) { return make_float2(a.x, -a.y); }
+// 2^x by one MUFU.EX2 (flush-to-zero; the same instruction __expf issues after its ×log2 e)
+__device__ __forceinline__ float ex2_approx(float x) {
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
 // a·s as one packed FP32x2 multiply with a scalar-broadcast operand (FMUL2; bit-identical to two FMULs)
 __device__ __forceinline__ float2 cscale(float2 a, float s) {
   float2 r;
