@@ -264,14 +264,16 @@ def static_filter_taps(cfg: OracleConfig) -> np.ndarray:
     return full[j % N]
 
 
-def o8_ddlms_block(y: np.ndarray, m0: int, n0: int, nwarm: int, nkeep: int, M: int, cfg: OracleConfig):
+def o8_ddlms_block(y: np.ndarray, m0: int, n0: int, nwarm: int, nkeep: int, M: int, cfg: OracleConfig,
+                   decide=nearest):
     """4-tap T/2-spaced widely-linear DDLMS, restarted per block.
     Symbols n = n0 .. n0 + nwarm + nkeep − 1 (global); x_n = [u[2n+1], u[2n], u[2n−1], u[2n−2]] with
     u = g·y, g = (mean_n |y[2n]|²)^(−½) (AGC over the block and its warm-up);
     out_n = wᵀx_n + vᵀconj(x_n), d_n = D(out_n), e_n = d_n − out_n, w += μ·e·conj(x), v += μ·e·x;
     w starts as the centre spike on u[2n], v = 0 (and stays 0 when eq_widely_linear is False);
     μ = ddlms_mu_warm over the warm-up, ddlms_mu after.
-    Returns the outputs of the nkeep kept symbols (before each one's update)."""
+    Returns the outputs of the nkeep kept symbols (before each one's update). `decide` is the hard
+    decision D (default: brute-force nearest point; tests substitute a recording/flipping wrapper)."""
     nn = np.arange(n0, n0 + nwarm + nkeep)
     centres = y[2 * nn - m0]
     P = np.mean(np.abs(centres) ** 2)
@@ -282,7 +284,7 @@ def o8_ddlms_block(y: np.ndarray, m0: int, n0: int, nwarm: int, nkeep: int, M: i
     for i, n in enumerate(nn):
         x = g * y[2 * n - m0 + np.array([1, 0, -1, -2])]
         o = np.dot(w, x) + np.dot(v, np.conj(x))
-        d, _ = nearest(np.array([o]), M)
+        d, _ = decide(np.array([o]), M)
         e = d[0] - o
         mu = cfg.ddlms_mu_warm if i < nwarm else cfg.ddlms_mu
         if i >= nwarm:
@@ -297,9 +299,11 @@ def o8_ddlms_block(y: np.ndarray, m0: int, n0: int, nwarm: int, nkeep: int, M: i
 # O8–O10: per-frame equalizer, CPR, decisions
 # ------------------------------------------------------------------------------------------
 def o8_equalize_frame(yf: np.ndarray, K: int, w_cd: np.ndarray, M: int, cfg: OracleConfig,
-                      widely_linear: Optional[bool] = None):
+                      widely_linear: Optional[bool] = None, decide=nearest):
     """One frame. yf = y[2k0 − K, 2k0 + 2F − 2 + K] (length 2F − 1 + 2K). Returns (u, info) with
-    u the unbiased pass-2 output of the frame's F symbols (SURVEY §8(a) a7 steps 1–7)."""
+    u the unbiased pass-2 output of the frame's F symbols (SURVEY §8(a) a7 steps 1–7). `decide` is the
+    hard decision D used for the training (pass-1) and unbias decisions (default: brute-force nearest
+    point; tests substitute a recording/flipping wrapper)."""
     wl = cfg.eq_widely_linear if widely_linear is None else widely_linear
     L = 2 * K + 1
     F = (len(yf) - 2 * K + 1) // 2
@@ -321,7 +325,7 @@ def o8_equalize_frame(yf: np.ndarray, K: int, w_cd: np.ndarray, M: int, cfg: Ora
     th0 = g * th0
     # (4) pass 1 and decisions
     y0 = Phi @ th0
-    d, _ = nearest(y0, M)
+    d, _ = decide(y0, M)
     # (5) DD least squares with ridge toward θ₀: θ₁ = (R + λI)^(−1)(p + λθ₀), λ = ridge·tr(R)/(2L)
     R = Phi.conj().T @ Phi
     p = Phi.conj().T @ d
@@ -336,19 +340,27 @@ def o8_equalize_frame(yf: np.ndarray, K: int, w_cd: np.ndarray, M: int, cfg: Ora
         th1, bad = th0, True
     # (6) pass 2
     y1 = Phi @ th1
-    # (7) gain unbias: γ = Σ y¹·conj(D(y¹)) / Σ|D(y¹)|² ; y¹ ← y¹/|γ|   (R27)
-    d1, _ = nearest(y1, M)
-    gam = np.sum(y1 * np.conj(d1)) / np.sum(np.abs(d1) ** 2)
-    if abs(gam) > 0 and np.isfinite(abs(gam)):
-        u = y1 / abs(gam)
-    else:
-        u, bad = y1, True
+    # (7) gain unbias (R27)
+    u, gam, ok = o8_unbias(y1, M, decide)
+    bad = bad or not ok
     return u, dict(theta0=th0, theta1=th1, g=g, gamma=gam, bad=bad, R=R, p=p, lam=lam)
 
 
-def o9_cpr(u: np.ndarray, M: int, W: int):
+def o8_unbias(y1: np.ndarray, M: int, decide=nearest):
+    """Gain unbias (R27): γ = Σ y¹·conj(D(y¹)) / Σ|D(y¹)|², u = y¹/|γ|.
+    The LS (MMSE) solution shrinks the constellation by the factor |γ| < 1 under noise; dividing by |γ|
+    restores unit decision-directed gain (the phase of γ is left to the CPR). Returns (u, γ, ok); ok is
+    False (and u = y¹) when |γ| is zero or not finite (counted as a bad frame by the caller)."""
+    d1, _ = decide(y1, M)
+    gam = np.sum(y1 * np.conj(d1)) / np.sum(np.abs(d1) ** 2)
+    if abs(gam) > 0 and np.isfinite(abs(gam)):
+        return y1 / abs(gam), gam, True
+    return y1, gam, False
+
+
+def o9_cpr(u: np.ndarray, M: int, W: int, decide=nearest):
     """ϑ_b = arg Σ_{k∈b} u_k·conj(D(u_k)) per W-symbol window aligned to the frame; z = u·e^{−iϑ_b} (R12)."""
-    d, _ = nearest(u, M)
+    d, _ = decide(u, M)
     s = (u * np.conj(d)).reshape(-1, W).sum(axis=1)
     th = np.where(s != 0, np.angle(s), 0.0)
     return u * np.repeat(np.exp(-1j * th), W), th
@@ -445,7 +457,7 @@ def receive(codes: np.ndarray, first: int, n: int, cfg: OracleConfig, ref: Optio
             counts["bit_err"][bi] += frame_err[fi, 1]
         if keep:
             infos.append(info)
-    out = dict(z=z, dec=dec, counts=counts, A=A, K=K, L=L, frame_err=frame_err)
+    out = dict(z=z, dec=dec, counts=counts, A=A, K=K, L=L, frame_err=frame_err, first=first, n=n)
     if keep:
         out.update(E=E, E0=e0, y=y, m0=m0, a=a, phi=phi, b=b, frames=infos, w_cd=w_cd, h=h)
     return out

@@ -27,7 +27,7 @@ def _check_all(case, gpu, orc, dec_min=0.9999, z_tol=1e-4):
     assert gpu["m0"] == orc["m0"]
     ye = rel(gpu["y"], orc["y"])
     assert ye <= 1e-4, f"MF rel err {ye:.3e}"
-    ze, _, _ = eq_check(gpu["z"], orc["z"], tol=z_tol)
+    ze, _, _ = eq_check(gpu["z"], orc, case["ocfg"], tol=z_tol)
     agree = np.mean(gpu["dec"] == orc["dec"])
     assert agree >= dec_min, f"decision agreement {agree}"
     return fe, ye, ze, agree

@@ -43,4 +43,4 @@ def test_ssfm_workload_parity():
     out = R.receive(codes, first, n, ocfg, ref=w["labels"][first // 4:(first + n) // 4].cpu().numpy())
     d = dec[first // 4:(first + n) // 4].cpu().numpy()
     assert np.mean(d == out["dec"]) >= 0.9999
-    eq_check(z[first // 4:(first + n) // 4], out["z"])
+    eq_check(z[first // 4:(first + n) // 4], out, ocfg)

@@ -21,7 +21,7 @@ def _check(gpu, orc, dec_min=0.9999):
     assert fe <= 1e-4, f"field rel err {fe:.3e}"
     ye = rel(gpu["y"], orc["y"])
     assert ye <= 1e-4, f"MF rel err {ye:.3e}"
-    ze, _, _ = eq_check(gpu["z"], orc["z"])
+    ze, _, _ = eq_check(gpu["z"], orc, case["ocfg"])
     agree = np.mean(gpu["dec"] == orc["dec"])
     assert agree >= dec_min, f"decision agreement {agree}"
     return fe, ye, ze

@@ -348,10 +348,69 @@ def test_p10_noiseless_zero_errors(M, dl, cspr):
     assert _evm_db(out["z"], M) < -35
 
 
+# ------------------------------------------------------------------ R8: per-frame carrier estimate (O5)
+def test_r8_carrier_removal_exact_per_frame():
+    """R8 (BASELINE north_star "carrier removal"): A_f is the complex mean of E over the
+    16384-sample frame f of the global grid. Closed form: E = A_f + s with a distinct known A_f per frame and
+    s[n] = 0.3·e^{2πi·3n/F} + 0.2·e^{−2πi·5n/F} (zero mean over every frame, NOT over 512-sample blocks or any
+    other sub-frame grid) ⇒ o5 returns exactly A_f and e = s. A per-block mean, a whole-range mean, a
+    frame grid not anchored at global 0, or no removal all fail."""
+    cfg = _cfg()
+    F = cfg.frame_samples
+    e0, nf = 3 * F, 4
+    n = np.arange(e0, e0 + nf * F)
+    s = 0.3 * np.exp(2j * np.pi * 3 * n / F) + 0.2 * np.exp(-2j * np.pi * 5 * n / F)
+    A_true = np.array([1.0 + 0.25j, 0.7 - 0.4j, -0.2 + 1.1j, 2.0 + 0.0j])
+    E = np.repeat(A_true, F) + s
+    e, A = R.o5_carrier_removal(E, e0, cfg)
+    assert np.max(np.abs(A - A_true)) < 1e-12
+    assert np.max(np.abs(e - s)) < 1e-12
+    # the signal part is not zero-mean over 512-blocks: a sub-frame estimate would leave ≥ 0.1 of it
+    blk = s.reshape(-1, 512).mean(axis=1)
+    assert np.max(np.abs(blk)) > 0.05
+
+
+def test_r8_carrier_removal_frame_grid_is_global():
+    """The frame grid is anchored at global sample 0 (R8, R23): a range that starts mid-frame is refused,
+    and the estimate of a frame does not depend on where the range begins."""
+    cfg = _cfg()
+    F = cfg.frame_samples
+    rng = np.random.default_rng(5)
+    E = rng.standard_normal(3 * F) + 1j * rng.standard_normal(3 * F) + 0.8
+    _, A3 = R.o5_carrier_removal(E, 7 * F, cfg)
+    _, A1 = R.o5_carrier_removal(E[F:2 * F], 8 * F, cfg)
+    assert A1[0] == A3[1]
+    with pytest.raises(AssertionError):
+        R.o5_carrier_removal(E[512:512 + 2 * F], 7 * F + 512, cfg)
+
+
+# ------------------------------------------------------------------ R27: gain unbias (O8 step 7)
+@pytest.mark.parametrize("M", [4, 8, 16, 32, 64])
+def test_r27_unbias_exact_on_scaled_points(M):
+    """R27: u = y¹/|γ| with γ = Σ y¹·conj(D(y¹)) / Σ|D(y¹)|². Closed form: y¹ = c·d for exact constellation
+    points d and a known complex c whose rotation keeps D(c·d) = d ⇒ γ = c and |u_k| = |d_k| exactly,
+    u = d·c/|c| (the phase is left to the CPR)."""
+    rng = np.random.default_rng(M)
+    pts, _ = C.constellation(M)
+    d = pts[rng.integers(0, M, 4096)]
+    for c in (0.9 * np.exp(0.02j), 1.1 * np.exp(-0.015j), 0.95 + 0.0j):   # |c| inside (6/7, 6/5): D(c·d) = d
+        u, gam, ok = R.o8_unbias(c * d, M)
+        assert ok
+        assert abs(gam - c) < 1e-12
+        assert np.max(np.abs(np.abs(u) - np.abs(d))) < 1e-12
+        assert np.max(np.abs(u - d * c / abs(c))) < 1e-12
+
+
+def test_r27_unbias_degenerate_gain_flags_bad():
+    """|γ| = 0 (all-zero pass-2 output) is not divided by; the frame is flagged bad (§8(b) errors)."""
+    u, gam, ok = R.o8_unbias(np.zeros(256, complex), 16)
+    assert not ok and np.all(u == 0)
+
+
 # ------------------------------------------------------------------ P11: AWGN calibration against theory
 @pytest.mark.parametrize("M,es,noise,shift,tol", [
-    (4, 9.0, "analytic", 0.0, 0.12), (16, 15.0, "analytic", 0.0, 0.12), (64, 21.0, "analytic", 0.0, 0.12),
-    (16, 18.0, "white", -10 * math.log10(2), 0.2)])
+    (4, 9.0, "analytic", 0.0, 0.12), (16, 15.0, "analytic", 0.0, 0.05), (64, 21.0, "analytic", 0.0, 0.05),
+    (8, 12.0, "analytic", 0.0, 0.05), (16, 18.0, "white", -10 * math.log10(2), 0.2)])
 def test_p11_awgn_q_vs_theory(M, es, noise, shift, tol):
     n = 1 << 21                                                         # 2^19 symbols
     out, _, _, _ = _chain(M, cspr=16.0, esn0=es, noise=noise, n=n, seed=17)

@@ -1,0 +1,115 @@
+#!/usr/bin/env python
+"""Mutation check of the oracle's pins (test infrastructure; CPU only).
+
+Each mutation below is a plausible mistake in `oracle/` — a dropped term, a wrong sign or index, a
+sub-frame grid, a missing step. For each, a scratch copy of `oracle/`, `kkgen/` and `tests/` is mutated and
+`tests/test_oracle_pins.py` is run; the mutation is "killed" if at least one pin fails. A surviving
+mutation means a reading the pins do not fix ("parity unpinned").
+
+    python tools/oracle_mutations.py [name ...]      # all by default; prints one line per mutation + JSON
+"""
+from __future__ import annotations
+
+import json
+import os
+import shutil
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+# (name, file, original text, mutated text, what it breaks)
+MUTATIONS = [
+    ("r8_per_block_mean", "oracle/receiver.py",
+     "    A = E.reshape(-1, F).mean(axis=1)\n    return E - np.repeat(A, F), A",
+     "    A = E.reshape(-1, F).mean(axis=1)\n    Ab = E.reshape(-1, 512).mean(axis=1)\n    return E - np.repeat(Ab, 512), A",
+     "R8: carrier estimate per 512-sample block instead of per frame"),
+    ("r8_no_removal", "oracle/receiver.py",
+     "    return E - np.repeat(A, F), A",
+     "    return E.copy(), A",
+     "R8: no carrier removal"),
+    ("r27_no_unbias", "oracle/receiver.py",
+     "    u, gam, ok = o8_unbias(y1, M, decide)\n",
+     "    u, gam, ok = y1, 1.0, True\n",
+     "R27: gain unbias deleted"),
+    ("r2_hilbert_sign", "oracle/receiver.py",
+     "mult = np.where((q > 0) & (q < N // 2), -1j, np.where(q > N // 2, 1j, 0.0))\n    phi = np.empty",
+     "mult = np.where((q > 0) & (q < N // 2), 1j, np.where(q > N // 2, -1j, 0.0))\n    phi = np.empty",
+     "R2: Hilbert multiplier sign"),
+    ("r1_keep_first_half", "oracle/receiver.py",
+     "blk[lead:lead + hop]", "blk[0:hop]",
+     "R1: OLS keeps the first hop samples instead of the centre"),
+    ("o2_no_half", "oracle/receiver.py",
+     "return 0.5 * np.log(Ic), np.sqrt(Ic), clamped", "return np.log(Ic), np.sqrt(Ic), clamped",
+     "O2: ln I instead of ½ ln I"),
+    ("r9_lo_sign", "oracle/receiver.py",
+     "return e * np.exp(-2j * np.pi * cfg.sideband * q / cfg.lo_den)",
+     "return e * np.exp(2j * np.pi * cfg.sideband * q / cfg.lo_den)",
+     "R9: LO shifts the wrong way"),
+    ("r6_odd_decimation", "oracle/receiver.py",
+     "n = 2 * np.arange(m0, m1, dtype=np.int64)", "n = 2 * np.arange(m0, m1, dtype=np.int64) + 1",
+     "R6: decimation keeps the odd phase"),
+    ("r10_ridge_to_zero", "oracle/receiver.py",
+     "np.linalg.solve(Lc, p + lam * th0)", "np.linalg.solve(Lc, p)",
+     "R10: ridge pulls toward 0 instead of θ₀"),
+    ("r10_no_conj_branch", "oracle/receiver.py",
+     "Phi = np.concatenate([U, np.conj(U)], axis=1) if wl else U",
+     "Phi = np.concatenate([U, U], axis=1) if wl else U",
+     "R10: widely-linear branch uses u instead of conj(u)"),
+    ("r12_cpr_sign", "oracle/receiver.py",
+     "return u * np.repeat(np.exp(-1j * th), W), th", "return u * np.repeat(np.exp(1j * th), W), th",
+     "R12: CPR rotates the wrong way"),
+    ("r25_no_agc", "oracle/receiver.py",
+     "    th0 = g * th0\n", "    th0 = th0\n",
+     "R25: AGC dropped"),
+    ("o11_q_no_sqrt2", "oracle/theory.py",
+     "return 20.0 * math.log10(math.sqrt(2.0) * special.erfcinv(2.0 * ber))",
+     "return 20.0 * math.log10(special.erfcinv(2.0 * ber))",
+     "O11: Q without the √2"),
+    ("r13_gray_16", "oracle/constellation.py",
+     "labs.append((_gray(iI) << half_bits) | _gray(iQ))", "labs.append((iI << half_bits) | _gray(iQ))",
+     "R13: natural instead of Gray labels on I"),
+    ("seq_ddlms_no_carry", "oracle/receiver.py",
+     "        w, v = w_next, v_next\n", "        w, v = np.array([0, 1, 0, 0], complex), np.zeros(4, complex)\n",
+     "NEXT-1: sequential DDLMS state not carried across frames"),
+]
+
+
+def run(names):
+    results = []
+    for name, rel, old, new, what in MUTATIONS:
+        if names and name not in names:
+            continue
+        tmp = tempfile.mkdtemp(prefix=f"mut_{name}_")
+        try:
+            for d in ("oracle", "kkgen", "tests"):
+                shutil.copytree(os.path.join(ROOT, d), os.path.join(tmp, d),
+                                ignore=shutil.ignore_patterns("__pycache__"))
+            shutil.copy(os.path.join(ROOT, "pytest.ini"), tmp)
+            p = os.path.join(tmp, rel)
+            src = open(p).read()
+            if src.count(old) != 1:
+                results.append(dict(name=name, what=what, status="not-applicable"))
+                print(f"{name:24s} NOT APPLICABLE (pattern count {src.count(old)})", flush=True)
+                continue
+            open(p, "w").write(src.replace(old, new))
+            t = time.time()
+            r = subprocess.run([sys.executable, "-m", "pytest", "tests/test_oracle_pins.py", "-x", "-q",
+                                "-p", "no:cacheprovider"], cwd=tmp, capture_output=True, text=True)
+            failed = [ln.split("::", 1)[1].split(" ")[0] for ln in r.stdout.splitlines()
+                      if ln.startswith("FAILED")]
+            status = "killed" if r.returncode != 0 else "SURVIVED"
+            results.append(dict(name=name, what=what, status=status, first_failing_pin=failed[:1],
+                                seconds=round(time.time() - t, 1)))
+            print(f"{name:24s} {status:8s} {failed[:1]} ({time.time() - t:.0f} s)", flush=True)
+        finally:
+            shutil.rmtree(tmp, ignore_errors=True)
+    print(json.dumps(results))
+    return results
+
+
+if __name__ == "__main__":
+    res = run(sys.argv[1:])
+    sys.exit(0 if all(r["status"] != "SURVIVED" for r in res) else 1)
