@@ -157,6 +157,11 @@ class LinkConfig:
     seed: int = 101
     wander_rad: float = 0.0               # optional data-vs-tone phase wander amplitude (CPR fixtures)
     wander_hz: float = 50e3
+    # optional physical laser phase noise (CPR fixture P12(v)): the tone and the data share one laser, so after
+    # dispersion the data sees φ(t − τ) − φ(t) for a Wiener φ of linewidth Δν ("100 kHz" ECL) and
+    # the data-vs-tone delay τ (0.83 ns at 10,000 km)
+    linewidth_hz: float = 0.0
+    pn_delay_s: float = 0.83e-9
     sideband: int = +1
     adc_bits: int = 15                    # 15 → int16 codes 0..32767 (R20); ≤ 8 → uint8 codes (SPEC S:199's 8-bit ADC)
 
@@ -252,7 +257,31 @@ def _data_field(cfg: LinkConfig, s0: int, s1: int, device, guard_sym: int = 1024
     ph = cfg.sideband * 2 * math.pi * q / LO_DEN
     if cfg.wander_rad:
         ph = ph + cfg.wander_rad * torch.sin(2 * math.pi * cfg.wander_hz * n.to(torch.float64) / FS)
+    if cfg.linewidth_hz:
+        ph = ph + differential_phase_noise(cfg, n)
     return x * torch.exp(1j * ph)
+
+
+def differential_phase_noise(cfg: LinkConfig, n: torch.Tensor) -> torch.Tensor:
+    """φ(n − τf_s) − φ(n) for a Wiener laser phase φ with per-sample increments δ_j ~ N(0, 2πΔν/f_s) drawn
+    from the counter hash (stream 13): = −(δ_n + … + δ_{n−D+1}) − √r·δ_{n−D}, D = ⌊τf_s⌋, r = τf_s − D.
+    Only the increments inside the delay window enter, so the value is local and chunk-invariant; its
+    variance is 2πΔν·τ (the Wiener variance over τ)."""
+    d = cfg.pn_delay_s * FS
+    D = int(math.floor(d))
+    r = d - D
+    sd = math.sqrt(2 * math.pi * cfg.linewidth_hz / FS)
+
+    def inc(j):
+        u1, u2 = uniform01(cfg.seed, 13, j), uniform01(cfg.seed, 14, j)
+        return sd * torch.sqrt(-2.0 * torch.log(u1)) * torch.cos(2.0 * math.pi * u2)
+
+    out = torch.zeros(n.shape, dtype=torch.float64, device=n.device)
+    for m in range(D):
+        out -= inc(n - m)
+    if r > 0:
+        out -= math.sqrt(r) * inc(n - D)
+    return out
 
 
 GEN_GRID = 1 << 18        # samples per generation chunk on the CPU, anchored at global sample 0

@@ -62,6 +62,7 @@ class OracleConfig:
     adc_offset: float = 0.0
     ref_intensity: float = 1.0
     clamp_rel: float = 1e-12          # R7
+    p0_min_rel: float = 1e-20         # silent-frame rule: AGC power ≤ p0_min_rel·I_ref ⇒ bad frame, z = 0
     formats: Sequence[int] = (4,)     # per-segment QAM order (R26)
     segment_frames: int = 1 << 30
     # paper arrangement: eq_mode "ddlms" folds the CD inverse
@@ -318,10 +319,12 @@ def o8_equalize_frame(yf: np.ndarray, K: int, w_cd: np.ndarray, M: int, cfg: Ora
     # (3) AGC: g = (mean |φ̃ᵀθ₀|²)^(−½) ; θ₀ ← g·θ₀   (R25)
     y0 = Phi @ th0
     P0 = np.mean(np.abs(y0) ** 2)
+    if not (P0 > cfg.p0_min_rel * cfg.ref_intensity and np.isfinite(P0)):
+        # no signal power to train on (e.g. the tone without modulation): a bad frame, z = 0, decisions D(0)
+        return np.zeros(F, complex), dict(theta0=th0, theta1=th0, g=1.0, gamma=0.0, bad=True, silent=True,
+                                          R=None, p=None, lam=0.0)
     bad = False
-    g = 1.0 / math.sqrt(P0) if (P0 > 0 and np.isfinite(P0)) else float("nan")
-    if not np.isfinite(g):
-        g, bad = 1.0, True
+    g = 1.0 / math.sqrt(P0)
     th0 = g * th0
     # (4) pass 1 and decisions
     y0 = Phi @ th0
@@ -441,10 +444,14 @@ def receive(codes: np.ndarray, first: int, n: int, cfg: OracleConfig, ref: Optio
         else:
             yf = y[2 * k0: 2 * k0 + 2 * Fs - 1 + 2 * K]
             u, info = o8_equalize_frame(yf, K, w_cd, M, cfg)
-            zf, th = o9_cpr(u, M, cfg.cpr_window)
-            info["cpr"] = th
             counts["bad_frames"] += int(info["bad"])
-            _, lab = nearest(zf, M)
+            if info.get("silent"):
+                zf = np.zeros(Fs, complex)
+                _, lab = nearest(np.full(Fs, -1e-9 - 1e-9j), M)   # D(0) with ties to the lower level (R15)
+            else:
+                zf, th = o9_cpr(u, M, cfg.cpr_window)
+                info["cpr"] = th
+                _, lab = nearest(zf, M)
         z[k0:k0 + Fs] = zf
         dec[k0:k0 + Fs] = lab
         bi = int(round(math.log2(M))) - 2

@@ -273,6 +273,7 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
     const bool dead = (ccount >= kFrameSamp);
 
     int bad = 0;
+    bool zero = dead;                    // z = 0, decisions D(0): dead frame, or no signal power (silent)
     if (!dead) {
       // ---- sweep A: lag sums for bases ρ = 0 (i = −K, w[0]) and ρ = 1 (i = −K+1, w[1]) + pass-1 power
       //      S_ρ(d) = Σ conj(w[ρ])·w[ρ + d],  T_ρ(d) = Σ w[ρ]·w[ρ + d];  y⁰ = Σ_e w_cd[e]·w[e]
@@ -328,9 +329,12 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
 #pragma unroll
       for (int w8 = 0; w8 < K3_WARPS; ++w8) P0 += (double)red[w8 * NRED + Lay::IPOW];
       P0 /= (double)kFrameSym;
-      const bool p0ok = (P0 > 0.0) && isfinite(P0);
-      const float g = p0ok ? (float)(1.0 / sqrt(P0)) : 1.0f;   // AGC (R25)
-      bad |= !p0ok;
+      // AGC (R25). A frame without signal power (P0 ≤ p0_min = 1e-20·I_ref, or not finite: e.g. the tone
+      // without modulation) cannot be trained: it is a bad frame with z = 0 and decisions D(0)
+      const bool p0ok = (P0 > (double)p.p0_min) && isfinite(P0);
+      if (!p0ok) { bad = 1; zero = true; }
+      if (p0ok) {
+      const float g = (float)(1.0 / sqrt(P0));
 
       // ---- sweep B: decisions on g·y⁰ and p1[e] = Σ conj(a_j)·d, p2[e] = Σ a_j·d  (a_j = w[e])
       {
@@ -709,11 +713,12 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
         __syncthreads();
       }
       KK_PT(6);
+      }  // p0ok
     }
 
-    // ---- decisions, counts, outputs: z = u·e^{−iϑ_b} (dead frame: z = 0)
+    // ---- decisions, counts, outputs: z = u·e^{−iϑ_b} (dead or silent frame: z = 0)
     int serr = 0, berr = 0;
-    if (!dead && !sl.cross && ref_tma && dec && !zout) {
+    if (!zero && !sl.cross && ref_tma && dec && !zout) {
       // the common case as its own loop (square/rectangular slicer, labels from shared memory, no z output):
       // no per-symbol tests of runtime-uniform flags
 #pragma unroll 4
@@ -729,7 +734,7 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
 #pragma unroll 4
       for (int s = 0; s < K3_SPT; ++s) {
         const int kl = tid + K3_THREADS * s;
-        const float2 zz = dead ? make_float2(0.f, 0.f) : cmul(us[kl], rot[s]);
+        const float2 zz = zero ? make_float2(0.f, 0.f) : cmul(us[kl], rot[s]);
         const int lab = sl.label(zz);
         if (ref) {
           const int r = ref_tma ? (int)ref_cur[kl] : (int)__ldg(&ref[sym0 + kl]);

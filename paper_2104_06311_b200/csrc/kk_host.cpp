@@ -682,6 +682,7 @@ kk_status kk_process_frames_ex(kk_ctx* c, const void* d_adc, int64_t first, int6
   p3.ridge = (float)cf.eq_ridge;
   p3.widely_linear = cf.eq_widely_linear;
   p3.cpr_window = cf.cpr_window;
+  p3.p0_min = (float)(1e-20 * cf.ref_intensity);
   p3.frame_err = d_ref ? d_ferr : nullptr;
   const int64_t nfr = n / F;
   if (c->ddlms) {

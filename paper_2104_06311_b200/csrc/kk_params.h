@@ -54,6 +54,7 @@ struct K3Params {
   float ridge;
   int widely_linear;
   int cpr_window;                    // symbols
+  float p0_min;                      // AGC power at or below which a frame is silent (bad; z = 0): 1e-20·I_ref
   unsigned* frame_err;               // nullable: [2f] symbol errors, [2f+1] bit errors per local frame
 };
 

@@ -15,10 +15,11 @@ HALO = 16640
 
 
 def make_case(M=4, dl=0.0, cspr=12.0, esn0=None, n=1 << 16, first=2 * F, seed=7, noise="white", formats=None,
-              segment_frames=1 << 30, wander_rad=0.0, sideband=1, **ocfg_kw):
+              segment_frames=1 << 30, wander_rad=0.0, wander_hz=50e3, linewidth_hz=0.0, sideband=1, **ocfg_kw):
     formats = tuple(formats) if formats else (M,)
     lc = kkgen.LinkConfig(formats=formats, segment_frames=segment_frames, dl_ps_nm=dl, cspr_db=cspr,
-                          esn0_db=esn0, seed=seed, noise=noise, wander_rad=wander_rad, sideband=sideband)
+                          esn0_db=esn0, seed=seed, noise=noise, wander_rad=wander_rad, wander_hz=wander_hz,
+                          linewidth_hz=linewidth_hz, sideband=sideband)
     ocfg = R.OracleConfig(dispersion_ps_per_nm=dl, adc_scale=lc.adc_scale, ref_intensity=lc.i_ref,
                           formats=formats, segment_frames=segment_frames, sideband=sideband, **ocfg_kw)
     H = R.halo(ocfg)                      # 16640, or 16656 with upsample = 2 (= kk_halo)
@@ -204,3 +205,21 @@ def eq_check(z_gpu, orc, cfg, tol=1e-4, delta=2e-5, frame_symbols=4096):
     ce = rel(zg[clean], zo[clean]) if clean.any() else 0.0
     assert ce <= tol, f"EQ rel err on clean frames {ce:.3e}"
     return ce, proven, float(fe.max())
+
+
+def make_silent_case(M=16, dl=32000.0, n=12 * F, first=2 * F, seed=17, quiet=(2, 9)):
+    """Float-intensity input (I/I_ref, so I_ref = 1) whose core frames quiet[0] … quiet[1]−1 carry the tone
+    without modulation (I = I_ref exactly): the tone's KK field is exactly constant there, so the frames at
+    least two frames inside the quiet stretch have e = E − A_f = 0 and an MF output of exactly zero — no signal
+    power to train on (the silent-frame rule: bad frame, z = 0, decisions D(0))."""
+    case = make_case(M=M, dl=dl, cspr=12.0, n=n, first=first, seed=seed)
+    lc, H = case["lc"], case["halo"]
+    I = case["codes"].to(torch.float64) * (lc.adc_scale / lc.i_ref)
+    a, b = H + quiet[0] * F, H + quiet[1] * F
+    I[a:b] = 1.0
+    case["codes"] = I.to(torch.float32)
+    case["ocfg"] = R.OracleConfig(dispersion_ps_per_nm=dl, adc_scale=1.0, ref_intensity=1.0, formats=case["formats"])
+    case["float_input"] = True
+    case["silent_frames"] = list(range(quiet[0] + 2, quiet[1] - 2))
+    case["edge_frames"] = [quiet[0] + 1, quiet[1] - 2]   # y partly exactly zero: decided on the oracle's rounding
+    return case
