@@ -71,3 +71,20 @@ def test_codes_bit_identical_for_any_subrange():
         sub = kkgen.generate(lc, a, b)
         assert torch.equal(sub["codes"], full["codes"][a - lo:b - lo])
         assert torch.equal(sub["labels"], full["labels"][(a - lo) // 4:(b - lo) // 4])
+
+
+def test_differential_phase_noise_statistics():
+    """P12(v) fixture: φ(t − τ) − φ(t) of a Wiener phase with linewidth Δν has variance 2πΔν·τ (PAPER.md:50
+    100 kHz ECL; τ = 0.83 ns), is a function of the global index only (chunk-invariant) and decorrelates
+    beyond the delay window."""
+    cfg = kkgen.LinkConfig(linewidth_hz=100e3, pn_delay_s=0.83e-9, seed=4)
+    n = torch.arange(-(1 << 19), 1 << 19, dtype=torch.int64)
+    d = kkgen.differential_phase_noise(cfg, n).numpy()
+    var = 2 * math.pi * 100e3 * 0.83e-9
+    assert abs(np.var(d) / var - 1) < 0.02 and abs(np.mean(d)) < 0.01 * math.sqrt(var)
+    assert np.array_equal(kkgen.differential_phase_noise(cfg, n[1000:2000]).numpy(), d[1000:2000])
+    # adjacent samples share two whole increments and the fractional one (weights 1 and √0.32 against 1):
+    # correlation (2 + √0.32)/3.32; lag 4 shares none
+    c1 = np.corrcoef(d[:-1], d[1:])[0, 1]
+    c4 = np.corrcoef(d[:-4], d[4:])[0, 1]
+    assert abs(c1 - (2 + math.sqrt(0.32)) / 3.32) < 0.01 and abs(c4) < 0.01

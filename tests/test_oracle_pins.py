@@ -277,7 +277,7 @@ def test_p8_cd_fit(dl, L, maxdb):
 # ------------------------------------------------------------------ chain helpers
 def _chain(M, dl=0.0, cspr=12.0, esn0=None, n=1 << 16, seed=7, noise="white", first=2 * 16384, **ocfg):
     lc = kkgen.LinkConfig(formats=(M,), dl_ps_nm=dl, cspr_db=cspr, esn0_db=esn0, seed=seed, noise=noise,
-                          **{k: ocfg.pop(k) for k in ("wander_rad", "wander_hz") if k in ocfg})
+                          **{k: ocfg.pop(k) for k in ("wander_rad", "wander_hz", "linewidth_hz") if k in ocfg})
     cfg = _cfg(dispersion_ps_per_nm=dl, adc_scale=lc.adc_scale, ref_intensity=lc.i_ref, formats=(M,), **ocfg)
     H = R.halo(cfg)
     g = kkgen.generate(lc, first - H, first + n + H)
@@ -440,6 +440,61 @@ def test_p12_cpr_tracks_phase_wander():
                               cpr_window=4096)
     on, off = _evm_db(out_on["z"], 16), _evm_db(out_off["z"], 16)
     assert on < -45 and off > on + 6, (on, off)
+
+
+def test_p12_cpr_does_not_degrade_under_laser_phase_noise():
+    """P12(v): the physical differential phase noise of a 100 kHz ECL at τ = 0.83 ns (variance σ² = 2πΔντ =
+    5.2e-4 rad²) is white at the symbol rate — no window can track it; CPR on (W = 256) and off (W = frame)
+    give the same EVM within 0.2 dB, and the EVM is set by σ² (the matched filter averages ≈ 3 correlated
+    samples: between σ² − 3 dB and σ² + 0.5 dB)."""
+    kw = dict(dl=200000.0, cspr=16.0, n=4 * 16384, seed=9, linewidth_hz=100e3)
+    on = _evm_db(_chain(16, **kw)[0]["z"], 16)
+    off = _evm_db(_chain(16, cpr_window=4096, **kw)[0]["z"], 16)
+    s2 = 10 * math.log10(2 * math.pi * 100e3 * 0.83e-9)
+    assert abs(on - off) < 0.2, (on, off)
+    assert s2 - 3 < on < s2 + 0.5, (on, s2)
+
+
+# ------------------------------------------------------------------ R25: AGC makes the chain gain-invariant
+def test_r25_agc_gain_invariance():
+    """R25: a photodiode/ADC gain c scales I by c, E by √c (φ is unchanged: ½ln c is a constant, which the
+    Hilbert transform maps to 0), and y by √c; the AGC divides it out, so z and every decision are invariant
+    (to rounding) — without the AGC the pass-1 decisions of a scaled 16-QAM frame are wrong."""
+    out, cfg, g, ref = _chain(16, dl=32000.0, cspr=12.0, esn0=20.0, n=2 * 16384)
+    for c in (2.0, 0.5):
+        cfg2 = _cfg(dispersion_ps_per_nm=32000.0, adc_scale=cfg.adc_scale * c, ref_intensity=cfg.ref_intensity,
+                    formats=(16,))
+        o2 = R.receive(g["codes"].numpy(), 2 * 16384, 2 * 16384, cfg2, ref=ref)
+        assert np.array_equal(o2["dec"], out["dec"])
+        assert np.max(np.abs(o2["z"] - out["z"])) < 1e-9
+
+
+# ------------------------------------------------------------------ silent frames (§8(b) bad-frame fallback)
+def test_silent_frames_are_bad_with_zero_output():
+    """Frames carrying the tone without modulation (I = I_ref exactly) have e = E − A_f = 0 and no power to
+    train on: the silent-frame rule counts them in bad_frames, outputs z = 0 and decides D(0) — ties to the
+    lower level on each axis (R15) — while a frame ≥ 3 frames away from the quiet stretch is untouched (its
+    neighbour's carrier estimate A_f, which its MF reach sees, is not)."""
+    import sys
+    sys.path.insert(0, os.path.dirname(__file__))
+    from gpu_case import make_case, make_silent_case
+    case = make_silent_case()
+    out = R.receive(case["codes"].numpy().astype(np.float64), case["first"], case["n"], case["ocfg"],
+                    ref=case["ref"].numpy())
+    assert out["counts"]["bad_frames"] == 3 and out["counts"]["dead_frames"] == 0
+    zf = out["z"].reshape(-1, 4096)
+    df = out["dec"].reshape(-1, 4096)
+    pts, labs = C.constellation(16)
+    lower = labs[np.argmin(np.abs(pts - (-1 - 1j) / math.sqrt(10)))]   # 0 sits on the ±1 boundaries: −1 on both
+    for fi in case["silent_frames"]:
+        assert out["frames"][fi]["bad"] and np.all(zf[fi] == 0) and np.all(df[fi] == lower)
+    base = make_case(M=16, dl=32000.0, cspr=12.0, n=12 * 16384, seed=17)
+    lc = base["lc"]
+    cfgf = R.OracleConfig(dispersion_ps_per_nm=32000.0, adc_scale=1.0, ref_intensity=1.0, formats=(16,))
+    I = base["codes"].numpy().astype(np.float64) * (lc.adc_scale / lc.i_ref)
+    o0 = R.receive(I.astype(np.float32).astype(np.float64), base["first"], base["n"], cfgf, ref=base["ref"].numpy())
+    assert np.max(np.abs(zf[11] - o0["z"].reshape(-1, 4096)[11])) < 1e-9
+    assert np.max(np.abs(zf[0] - o0["z"].reshape(-1, 4096)[0])) > 1e-6
 
 
 # ------------------------------------------------------------------ P13: shard / halo invariance
