@@ -3,6 +3,7 @@ same int16 codes. (Test infrastructure: imports the oracle, which the product ne
 from __future__ import annotations
 
 import math
+import os
 
 import numpy as np
 import torch
@@ -204,7 +205,14 @@ def eq_check(z_gpu, orc, cfg, tol=1e-4, delta=2e-5, frame_symbols=4096):
             proven.append((fi, proof))
     ce = rel(zg[clean], zo[clean]) if clean.any() else 0.0
     assert ce <= tol, f"EQ rel err on clean frames {ce:.3e}"
+    PROOFS.append(dict(test=os.environ.get("PYTEST_CURRENT_TEST", "").split(" ")[0], frames=len(fe),
+                       clean_err=float(ce), worst_raw=float(fe.max()),
+                       proven=[dict(frame=p[0], block=(p[1] if len(p) == 3 else None),
+                                    flips=[dict(call=int(c), index=int(k)) for c, k, _ in p[-1]]) for p in proven]))
     return ce, proven, float(fe.max())
+
+
+PROOFS = []   # one record per eq_check call (tests/conftest.py writes them to $KK_EQ_PROOF_LOG)
 
 
 def make_silent_case(M=16, dl=32000.0, n=12 * F, first=2 * F, seed=17, quiet=(2, 9)):

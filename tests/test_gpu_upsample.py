@@ -16,7 +16,7 @@ if not torch.cuda.is_available():  # pragma: no cover - CPU box
 from oracle import theory  # noqa: E402
 
 
-def _check(gpu, orc, dec_min=0.9999):
+def _check(case, gpu, orc, dec_min=0.9999):
     fe = field_rel_err(gpu, orc)
     assert fe <= 1e-4, f"field rel err {fe:.3e}"
     ye = rel(gpu["y"], orc["y"])
@@ -37,7 +37,7 @@ def test_up_halo_is_16656():
 def test_up_noiseless_parity_and_exact_counts():
     case = make_case(M=16, cspr=8.0, n=1 << 16, seed=111, upsample=2)
     gpu, orc = run_gpu(case), run_oracle(case)
-    _check(gpu, orc, dec_min=1.0)
+    _check(case, gpu, orc, dec_min=1.0)
     s, c = gpu["stats"], orc["counts"]
     assert s["bit_err"] == list(c["bit_err"]) == [0] * 5 and s["sym"] == list(c["sym"])
     assert s["clamped"] == c["clamped"] and s["bad_frames"] == 0
@@ -52,7 +52,7 @@ def test_up_noiseless_parity_and_exact_counts():
 def test_up_awgn_parity(M, dl, cspr, esn0, noise):
     case = make_case(M=M, dl=dl, cspr=cspr, esn0=esn0, noise=noise, n=1 << 17, seed=112, upsample=2)
     gpu, orc = run_gpu(case), run_oracle(case)
-    _check(gpu, orc)
+    _check(case, gpu, orc)
     bits = sum(gpu["stats"]["bits"])
     be_g, be_o = sum(gpu["stats"]["bit_err"]), int(orc["counts"]["bit_err"].sum())
     if be_o > 20:
@@ -63,7 +63,7 @@ def test_up_mixed_formats_ddlms_lower_sideband():
     case = make_case(formats=(4, 8, 16, 32, 64), segment_frames=1, dl=32000.0, cspr=10.0, esn0=24.0,
                      n=5 * F, seed=113, sideband=-1, upsample=2, eq_mode="ddlms")
     gpu, orc = run_gpu(case), run_oracle(case)
-    _check(gpu, orc)
+    _check(case, gpu, orc)
 
 
 def test_up_chunk_invariance():
