@@ -35,7 +35,7 @@ from typing import Optional, Sequence
 import numpy as np
 from scipy import signal
 
-from .constellation import nearest, popcount
+from .constellation import constellation, nearest, popcount
 
 C_LIGHT = 299792458.0
 
@@ -67,11 +67,14 @@ class OracleConfig:
     segment_frames: int = 1 << 30
     # paper arrangement: eq_mode "ddlms" folds the CD inverse
     # into the static filter and equalizes with the 4-tap T/2-spaced widely-linear DDLMS
-    eq_mode: str = "block_ls"         # "block_ls" (north star, default) | "ddlms" (paper)
+    eq_mode: str = "block_ls"         # "block_ls" (north star, default) | "ddlms" (paper, restart grid) |
+                                      # "ddlms_seq" (paper, one recursion in stream order: the definition)
     ddlms_mu_warm: float = 2e-3       # step size over the warm-up symbols
     ddlms_mu: float = 2.5e-4          # step size over the kept symbols (SPEC S:377 schedule end)
     ddlms_block: int = 256            # symbols kept per DDLMS restart (global grid)
     ddlms_warmup: int = 512           # symbols run before each block from the centre-spike state
+    ddlms_seq_mu0: float = 1e-3       # sequential form: μ over the first ddlms_seq_switch symbols
+    ddlms_seq_switch: int = 10000     # … then ddlms_mu (2.5e-4)
     # KK upsampling (O3u): 1 = the paper's 4-sps chain; 2 = interpolate I to 8 sps before sqrt/log
     upsample: int = 1
     halfband_t: int = 8               # odd half-band taps per side (f[±1], f[±3], …, f[±(2T−1)])
@@ -265,7 +268,7 @@ def static_filter_taps(cfg: OracleConfig) -> np.ndarray:
     return full[j % N]
 
 
-def o8_ddlms_block(y: np.ndarray, m0: int, n0: int, nwarm: int, nkeep: int, M: int, cfg: OracleConfig,
+def o8_ddlms_block(y: np.ndarray, m0: int, n0: int, nwarm: int, nkeep: int, M, cfg: OracleConfig,
                    decide=nearest):
     """4-tap T/2-spaced widely-linear DDLMS, restarted per block.
     Symbols n = n0 .. n0 + nwarm + nkeep − 1 (global); x_n = [u[2n+1], u[2n], u[2n−1], u[2n−2]] with
@@ -273,7 +276,9 @@ def o8_ddlms_block(y: np.ndarray, m0: int, n0: int, nwarm: int, nkeep: int, M: i
     out_n = wᵀx_n + vᵀconj(x_n), d_n = D(out_n), e_n = d_n − out_n, w += μ·e·conj(x), v += μ·e·x;
     w starts as the centre spike on u[2n], v = 0 (and stays 0 when eq_widely_linear is False);
     μ = ddlms_mu_warm over the warm-up, ddlms_mu after.
-    Returns the outputs of the nkeep kept symbols (before each one's update). `decide` is the hard
+    M is the QAM order of every symbol (an int, or one per symbol: each symbol is decided in its own frame's
+    format, "d[n] = nearest constellation point"). Returns the outputs of the nkeep kept symbols
+    (before each one's update). `decide` is the hard
     decision D (default: brute-force nearest point; tests substitute a recording/flipping wrapper)."""
     nn = np.arange(n0, n0 + nwarm + nkeep)
     centres = y[2 * nn - m0]
@@ -282,10 +287,11 @@ def o8_ddlms_block(y: np.ndarray, m0: int, n0: int, nwarm: int, nkeep: int, M: i
     w = np.array([0, 1, 0, 0], complex)
     v = np.zeros(4, complex)
     out = np.zeros(nkeep, complex)
+    Ms = np.broadcast_to(np.asarray(M), (len(nn),))
     for i, n in enumerate(nn):
         x = g * y[2 * n - m0 + np.array([1, 0, -1, -2])]
         o = np.dot(w, x) + np.dot(v, np.conj(x))
-        d, _ = decide(np.array([o]), M)
+        d, _ = decide(np.array([o]), int(Ms[i]))
         e = d[0] - o
         mu = cfg.ddlms_mu_warm if i < nwarm else cfg.ddlms_mu
         if i >= nwarm:
@@ -294,6 +300,53 @@ def o8_ddlms_block(y: np.ndarray, m0: int, n0: int, nwarm: int, nkeep: int, M: i
         if cfg.eq_widely_linear:
             v = v + mu * e * x
     return out
+
+
+def o8_ddlms_sequential(y: np.ndarray, m0: int, n0: int, Ms: np.ndarray, cfg: OracleConfig, state=None):
+    """The paper's 4-tap T/2-spaced widely-linear DDLMS as ONE recursion in stream order ("four-tap
+    adaptive time-domain DDLMS widely-linear equalizer", "sequential time-domain algorithms such as DDLMS";
+    SPEC S:351 "Sequential over n; state' carries taps for the next frame in stream order"; S:377 w = centre
+    spike, v = 0, μ = 1e-3 then 2.5e-4 after 10^4 symbols). Symbols n = n0 … n0 + len(Ms) − 1 (global), QAM
+    order Ms[i] per symbol:
+        x_n = g·[y[2n+1], y[2n], y[2n−1], y[2n−2]],  out_n = wᵀx_n + vᵀconj(x_n),  d_n = D(out_n),
+        e_n = d_n − out_n,  w += μ_n·e_n·conj(x_n),  v += μ_n·e_n·x_n   (v ≡ 0 when eq_widely_linear is False)
+    with μ_n = ddlms_seq_mu0 for the stream's first ddlms_seq_switch symbols, ddlms_mu after. `state` = None
+    starts the stream: w = [0, 1, 0, 0] (the spike on the symbol centre y[2n], the restart form's convention),
+    v = 0, and the gain g = (mean |y[2n]|² over the stream's first frame)^(−½), kept for the stream (the
+    paper states no AGC; a fixed input normalisation is the reading). Returns (outputs before each update,
+    state') with state' = dict(w, v, g, count) for the next call."""
+    nsym = len(Ms)
+    if state is None:
+        c = y[2 * np.arange(n0, n0 + min(nsym, cfg.frame_symbols)) - m0]
+        P = float(np.mean(np.abs(c) ** 2))
+        state = dict(w=np.array([0, 1, 0, 0], complex), v=np.zeros(4, complex),
+                     g=1.0 / math.sqrt(P) if P > 0 else 1.0, count=0)
+    w, v, g, cnt = state["w"].copy(), state["v"].copy(), state["g"], state["count"]
+    tabs = {}
+    out = np.zeros(nsym, complex)
+    taps = np.array([1, 0, -1, -2])
+    for i in range(nsym):
+        M = int(Ms[i])
+        if M not in tabs:
+            tabs[M] = constellation(M)[0]
+        pts = tabs[M]
+        x = g * y[2 * (n0 + i) - m0 + taps]
+        o = np.dot(w, x) + np.dot(v, np.conj(x))
+        d = pts[np.argmin(np.abs(pts - o))]                 # D: brute-force nearest point
+        e = d - o
+        mu = cfg.ddlms_seq_mu0 if cnt < cfg.ddlms_seq_switch else cfg.ddlms_mu
+        out[i] = o
+        w = w + mu * e * np.conj(x)
+        if cfg.eq_widely_linear:
+            v = v + mu * e * x
+        cnt += 1
+    return out, dict(w=w, v=v, g=g, count=cnt)
+
+
+def _symbol_formats(n0: int, count: int, cfg: OracleConfig) -> np.ndarray:
+    """QAM order of global symbols n0 … n0 + count − 1 (format per frame, R26)."""
+    fr = np.arange(n0, n0 + count) // cfg.frame_symbols
+    return np.array([cfg.fmt_of_frame(int(f)) for f in fr])
 
 
 # ------------------------------------------------------------------------------------------
@@ -407,12 +460,16 @@ def receive(codes: np.ndarray, first: int, n: int, cfg: OracleConfig, ref: Optio
     b = o6_mixer(e, e0, cfg)
     # O7 over the 2-sps range the frames need
     ddlms = cfg.eq_mode == "ddlms"
+    seq = cfg.eq_mode == "ddlms_seq"
+    assert cfg.eq_mode in ("block_ls", "ddlms", "ddlms_seq")
     L = tap_count(cfg)
     K = (L - 1) // 2
     if ddlms:
         K = 2 * cfg.ddlms_warmup + 2                   # warm-up reaches 2W + 2 samples before the core
+    if seq:
+        K = 2                                          # taps y[2n+1] … y[2n−2]
     m0, m1 = first // 2 - K, (first + n) // 2 + K
-    h = static_filter_taps(cfg) if ddlms else rrc_taps(cfg)
+    h = static_filter_taps(cfg) if (ddlms or seq) else rrc_taps(cfg)
     y = o7_matched_filter(b, e0, m0, m1, h)
     # O8–O10 per frame
     w_cd = cd_init_taps(cfg)
@@ -425,6 +482,7 @@ def receive(codes: np.ndarray, first: int, n: int, cfg: OracleConfig, ref: Optio
                   dead_frames=0, bad_frames=0)
     frame_err = np.zeros((nfr, 2), np.int64)           # per-frame (symbol, bit) errors (PAPER.md:112 bins)
     infos = []
+    seq_state = None                                   # ddlms_seq: equalizer state carried in stream order
     for fi in range(nfr):
         f = first // F + fi
         M = cfg.fmt_of_frame(f)
@@ -435,10 +493,17 @@ def receive(codes: np.ndarray, first: int, n: int, cfg: OracleConfig, ref: Optio
             zf = np.zeros(Fs, complex)
             _, lab = nearest(np.full(Fs, -1e-9 - 1e-9j), M)   # D(0) with ties to the lower level (R15)
             info = dict(dead=True, bad=False)
+        elif seq:
+            kg0 = first // cfg.sps + k0
+            zf, seq_next = o8_ddlms_sequential(y, m0, kg0, np.full(Fs, M), cfg, seq_state)
+            seq_state = seq_next
+            info = dict(dead=False, bad=False)
+            _, lab = nearest(zf, M)
         elif ddlms:
             B, W = cfg.ddlms_block, cfg.ddlms_warmup
             kg0 = first // cfg.sps + k0                 # global symbol index of the frame start
-            zf = np.concatenate([o8_ddlms_block(y, m0, kg0 + bb - W, W, B, M, cfg) for bb in range(0, Fs, B)])
+            zf = np.concatenate([o8_ddlms_block(y, m0, kg0 + bb - W, W, B, _symbol_formats(kg0 + bb - W, W + B, cfg),
+                                                cfg) for bb in range(0, Fs, B)])
             info = dict(dead=False, bad=False)
             _, lab = nearest(zf, M)
         else:
@@ -464,7 +529,8 @@ def receive(codes: np.ndarray, first: int, n: int, cfg: OracleConfig, ref: Optio
             counts["bit_err"][bi] += frame_err[fi, 1]
         if keep:
             infos.append(info)
-    out = dict(z=z, dec=dec, counts=counts, A=A, K=K, L=L, frame_err=frame_err, first=first, n=n)
+    out = dict(z=z, dec=dec, counts=counts, A=A, K=K, L=L, frame_err=frame_err, first=first, n=n,
+               seq_state=seq_state)
     if keep:
         out.update(E=E, E0=e0, y=y, m0=m0, a=a, phi=phi, b=b, frames=infos, w_cd=w_cd, h=h)
     return out

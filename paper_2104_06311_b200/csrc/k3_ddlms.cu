@@ -7,7 +7,8 @@
 //   x_n = g·[y[2n+1], y[2n], y[2n−1], y[2n−2]],  g = (mean |y[2n]|²)^(−½) over the block and its warm-up
 //   (the power comes from K2's per-64-symbol segment sums)
 //   o_n = wᵀx_n + vᵀconj(x_n),  d_n = D(o_n),  e_n = d_n − o_n,  w += μ e conj(x),  v += μ e x
-//   w₀ = centre spike on y[2n], v₀ = 0; μ = mu_warm over the warm-up, mu over the kept symbols.
+//   w₀ = centre spike on y[2n], v₀ = 0; μ = mu_warm over the warm-up, mu over the kept symbols; every symbol
+//   is decided in its own frame's QAM order (warm-up symbols in the previous frame in that frame's order).
 // The paper carries the equalizer state across 2^22-sample buffers in stream order (events serialise the
 // streams). Here the recursion restarts on a global grid of B-symbol blocks, each preceded by W
 // warm-up symbols: blocks are independent, so they run in parallel and any sharding gives the
@@ -37,10 +38,19 @@ k3_ddlms_kernel(const float2* __restrict__ y, int64_t y_base, int64_t sym_first,
   const int64_t n_keep0 = (int64_t)blk * B;                  // local index of the first kept symbol
   const int fl = (int)(n_keep0 / kFrameSym);                 // local frame
   const int64_t f = sym_first / kFrameSym + fl;
-  const int M = (int)p.schedule[(int)(((f / p.segment_frames) % p.n_segments + p.n_segments) % p.n_segments)];
+  // QAM order of global frame g: schedule[floor(g / segment_frames) mod n_segments] (floor: g may be < 0)
+  auto fmt = [&](int64_t g) {
+    int64_t sg = g / p.segment_frames;
+    if (g < 0 && sg * p.segment_frames != g) --sg;
+    return (int)p.schedule[(int)(((sg % p.n_segments) + p.n_segments) % p.n_segments)];
+  };
+  const int M = fmt(f);
   const int bi = (M == 4) ? 0 : (M == 8) ? 1 : (M == 16) ? 2 : (M == 32) ? 3 : 4;
   Slicer sl;
   sl.init(M);
+  // warm-up symbols before the frame start belong to frame f − 1 and are decided in its format (W < 4096)
+  Slicer slp;
+  slp.init(fmt(f - 1));
   int ccount = 0;
   for (int q = 0; q < 32; ++q) ccount += __ldg(&clampcnt[clamp_frame_off + (int64_t)fl * 32 + q]);
   const bool dead = (ccount >= kFrameSamp);
@@ -90,8 +100,10 @@ k3_ddlms_kernel(const float2* __restrict__ y, int64_t y_base, int64_t sym_first,
     uint2 ra = make_uint2(0u, 0u), rb = make_uint2(0u, 0u);
     if (ref8 && 0 >= W) ra = rword(0);
     if (ref8 && PF >= W && PF < total) rb = rword(PF);
+    const int wprev = (int)((int64_t)fl * kFrameSym - n0);    // warm-up symbols in frame f − 1 (≤ 0: none)
     for (int i0 = 0; i0 < total; i0 += PF) {
       const bool kept = i0 >= W;
+      const Slicer sc = (i0 < wprev) ? slp : sl;                 // chunk-uniform (wprev is a multiple of 64)
       const uint2 rcur = ra;
       ra = rb;
       if (ref8 && i0 + 2 * PF >= W && i0 + 2 * PF < total) rb = rword(i0 + 2 * PF);
@@ -116,7 +128,7 @@ k3_ddlms_kernel(const float2* __restrict__ y, int64_t y_base, int64_t sym_first,
         }
         const float2 o = cadd(o0, o1);
         int lab = 0;
-        const float2 d = kept ? sl.decide(o, lab) : sl.point(o);   // kept: point and label from one slicing
+        const float2 d = kept ? sl.decide(o, lab) : sc.point(o);   // kept: point and label from one slicing
         const float2 e = csub(d, o);
         const float mu = kept ? p.mu : p.mu_warm;
         if (kept) {

@@ -138,11 +138,11 @@ def _frame_rerun(orc, cfg, fi, flips):
 
 def _ddlms_block_rerun(orc, cfg, fi, bb, flips):
     B, W = cfg.ddlms_block, cfg.ddlms_warmup
-    M = cfg.fmt_of_frame(orc["first"] // cfg.frame_samples + fi)
     kg0 = orc["first"] // cfg.sps + fi * cfg.frame_symbols + bb
+    Ms = R._symbol_formats(kg0 - W, W + B, cfg)               # one QAM order per call (= per symbol)
     dec = _Decide(flips)
-    z = R.o8_ddlms_block(orc["y"], orc["m0"], kg0 - W, W, B, M, cfg, decide=dec)
-    return z, dec, M
+    z = R.o8_ddlms_block(orc["y"], orc["m0"], kg0 - W, W, B, Ms, cfg, decide=dec)
+    return z, dec, Ms
 
 
 def _prove_flip(target, rerun, tol, delta, max_flips=4):
@@ -156,7 +156,8 @@ def _prove_flip(target, rerun, tol, delta, max_flips=4):
     flips = []
     for _ in range(max_flips):
         best = None
-        cands = [(c, k, p) for c, zc in enumerate(dec.calls) for (k, p, _t) in _near_boundary(zc, M, delta)
+        cands = [(c, k, p) for c, zc in enumerate(dec.calls)
+                 for (k, p, _t) in _near_boundary(zc, int(M[c]) if np.ndim(M) else M, delta)
                  if (c, k) not in {(f[0], f[1]) for f in flips}]
         for cand in cands:
             zt, _, _ = rerun(tuple(flips) + (cand,))

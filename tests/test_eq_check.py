@@ -54,8 +54,8 @@ def test_eq_check_ddlms_block_flip():
     orc = run_oracle(case)
     cfg = case["ocfg"]
     fi, bb = 1, 512
-    _, dec, M = _ddlms_block_rerun(orc, cfg, fi, bb, ())
-    c, k, p, t = _closest_candidate(dec.calls, M)
+    _, dec, Ms = _ddlms_block_rerun(orc, cfg, fi, bb, ())
+    c, k, p, t = _closest_candidate(dec.calls, 16)
     zb, _, _ = _ddlms_block_rerun(orc, cfg, fi, bb, ((c, k, p),))
     zg = orc["z"].copy()
     s0 = fi * 4096 + bb

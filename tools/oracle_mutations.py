@@ -72,7 +72,7 @@ MUTATIONS = [
      "labs.append((_gray(iI) << half_bits) | _gray(iQ))", "labs.append((iI << half_bits) | _gray(iQ))",
      "R13: natural instead of Gray labels on I"),
     ("seq_ddlms_no_carry", "oracle/receiver.py",
-     "        w, v = w_next, v_next\n", "        w, v = np.array([0, 1, 0, 0], complex), np.zeros(4, complex)\n",
+     "            seq_state = seq_next\n", "            seq_state = None\n",
      "NEXT-1: sequential DDLMS state not carried across frames"),
 ]
 
