@@ -4,14 +4,15 @@
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl kkrx|reference]
   python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 --master-port P bench.py --gpus N
 
-Workload (BASELINE.json configs[4], "C5"): a continuous mixed 4→8→16→32→64-QAM stream (format cycling per
-256-frame segment), 1 GBaud at 4 GS/s, 1600 km of accumulated dispersion (32,000 ps/nm), CSPR 12 dB,
-nominal Es/N0 26 dB white noise, int16 ADC codes — generated on the device from the seeded generator
-(kkgen). Each rank owns 2^32 samples (8 GiB of int16) of the global stream, a contiguous frame range with
-its 16,640-sample halos: per-GPU work is fixed as N grows ("weak" scaling). One step = the whole hot path
-(K1 KK → K2 MF → K3 EQ/CPR/decisions, in 2^28-sample calls through the C ABI) over the rank's 2^32
-samples, plus the NCCL allreduce of the 24 error counters — the only cross-GPU traffic. Inputs (8 GiB) are
-far larger than the 126 MB L2, so no L2 flush is needed between steps.
+Workload (BASELINE.json configs[4], "C5"): "continuous 2^32-sample mixed 4/8/16/32/64-QAM stream sharded over
+1/2/4/8 GPUs with halo overlap" — format cycling per 256-frame segment, 1 GBaud at 4 GS/s, 1600 km of accumulated
+dispersion (32,000 ps/nm), CSPR 12 dB, nominal Es/N0 26 dB white noise, int16 ADC codes, generated on the device
+from the seeded generator (kkgen). By default (--scaling strong) the ONE 2^32-sample stream (8 GiB of int16) is
+split into N contiguous frame ranges (shard.plan_strong), each rank holding its range plus 16,640-sample halos:
+total work is fixed as N grows. (--scaling weak: every rank owns --samples-per-gpu samples of the stream.) One
+step = the whole hot path (K1 KK → K2 MF → K3 EQ/CPR/decisions, in ≤ 2^28-sample calls through the C ABI) over
+the rank's samples, plus the NCCL allreduce of the 24 error counters — the only cross-GPU traffic. Inputs (≥ 1 GiB
+per rank at N = 8) are far larger than the 126 MB L2, so no L2 flush is needed between steps.
 
 value = total core samples of all ranks × K / (max over ranks of the CUDA-event time of K steps), in GS/s.
 """
@@ -43,7 +44,11 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="kkrx", choices=["kkrx", "reference"])
     ap.add_argument("--workload", default="C5")
-    ap.add_argument("--samples-per-gpu", type=int, default=1 << 32)
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="strong: one --samples stream split over the ranks (BASELINE configs[4]); "
+                         "weak: --samples-per-gpu per rank")
+    ap.add_argument("--samples", type=int, default=1 << 32, help="stream length for --scaling strong")
+    ap.add_argument("--samples-per-gpu", type=int, default=1 << 32, help="per-rank samples for --scaling weak")
     ap.add_argument("--chunk", type=int, default=1 << 28,
                     help="samples per kk_process_frames call (2^28: launch gaps and tail waves amortised)")
     ap.add_argument("--e2e-samples", type=int, default=1 << 30)
@@ -234,7 +239,7 @@ def run_reference(a, rank, world):
     cores = max(1, min(len(os.sched_getaffinity(0)), 32))
     frames_per_run = 4
     n_runs = cores
-    S = a.samples_per_gpu
+    S = a.samples if a.scaling == "strong" else a.samples_per_gpu
     HALO = halo_of(a)
     # sample: n_runs runs of 4 frames spread over the rank-0 shard (generated on the CPU)
     runs = []
@@ -256,7 +261,7 @@ def run_reference(a, rank, world):
     value = samples * len(times) / T / 1e9
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "GS/s", "n_gpus": world, "steps": a.steps,
-        "warmup": a.warmup, "ms_per_step": 1e3 * T / len(times), "higher_is_better": True, "scaling": "weak",
+        "warmup": a.warmup, "ms_per_step": 1e3 * T / len(times), "higher_is_better": True, "scaling": a.scaling,
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"{a.workload}: mixed 4/8/16/32/64-QAM, 1600 km, CSPR 12 dB, Es/N0 26 dB; "
                                f"oracle sample of {n_runs} runs x {frames_per_run} frames per step"},
@@ -316,7 +321,8 @@ def e2e_single_ingest(a, rx, lc, HALO, chunk, rank, world, dev, SH, kkrx, kkgen,
     them point-to-point (NCCL over NVLink); each rank runs kk_process_frames on what it receives. Timed per
     step: distribution + processing + the D2H read of the counters; max over ranks."""
     from paper_2104_06311_b200 import ingest
-    En = min(a.e2e_samples, 1 << 28, a.samples_per_gpu)
+    En = min(a.e2e_samples, 1 << 28, a.samples // world if a.scaling == "strong" else a.samples_per_gpu)
+    En -= En % F
     shards = SH.plan_weak(En, world, halo=HALO)
     lo, hi = shards[0].read_first, shards[-1].read_first + shards[-1].read_count
     host = None
@@ -381,12 +387,28 @@ def main():
             dist.init_process_group("gloo")
     wl = kkgen.WORKLOADS[a.workload]
     lc = wl["cfg"]
-    S = a.samples_per_gpu
-    chunk = min(a.chunk, S)
-    assert S % chunk == 0 and chunk % F == 0
     HALO = halo_of(a)
-    my = SH.plan_weak(S, world, halo=HALO)[rank]        # weak scaling: rank r owns [r·S, (r+1)·S)
+    if a.scaling == "strong":                           # one stream, N contiguous frame ranges (configs[4])
+        plan = SH.plan_strong(a.samples, world, halo=HALO)
+    else:                                               # rank r owns [r·S, (r+1)·S)
+        plan = SH.plan_weak(a.samples_per_gpu, world, halo=HALO)
+    my = plan[rank]
+    S = my.n
     first = my.first
+    chunk = min(a.chunk, S)
+    assert chunk % F == 0 and S % F == 0
+    calls = [(c0, min(chunk, S - c0)) for c0 in range(0, S, chunk)]
+    dist_info = None
+    if world > 1:                                       # evidence of the process group the counters cross
+        me = {"rank": rank, "local_rank": local, "device": torch.cuda.get_device_name(dev),
+              "pci_bus_id": torch.cuda.get_device_properties(dev).pci_bus_id if hasattr(
+                  torch.cuda.get_device_properties(dev), "pci_bus_id") else None,
+              "host": os.uname().nodename, "shard_first": first, "shard_samples": S}
+        allinfo = [None] * world
+        dist.all_gather_object(allinfo, me)
+        dist_info = {"backend": dist.get_backend(), "world_size": dist.get_world_size(),
+                     "nccl_version": ".".join(map(str, torch.cuda.nccl.version())) if a.dist_backend == "nccl" else None,
+                     "ranks": allinfo}
 
     t0 = time.perf_counter()
     g = kkgen.generate(lc, my.read_first, my.read_first + my.read_count, device=dev, chunk=1 << 24)
@@ -405,12 +427,12 @@ def main():
     dec = torch.empty(S // 4, dtype=torch.uint8, device=dev)
     counters = torch.zeros(kkrx.KK_STATS_WORDS, dtype=torch.int64, device=dev)
     stream = torch.cuda.current_stream(dev)
-    calls_per_step = S // chunk
+    calls_per_step = len(calls)
 
     def step():
-        for c0 in range(0, S, chunk):
-            rx.process(codes, first + c0, chunk, ref=ref[c0 // 4:(c0 + chunk) // 4],
-                       decisions=dec[c0 // 4:(c0 + chunk) // 4], offset=c0, stream=stream)
+        for c0, cn in calls:
+            rx.process(codes, first + c0, cn, ref=ref[c0 // 4:(c0 + cn) // 4],
+                       decisions=dec[c0 // 4:(c0 + cn) // 4], offset=c0, stream=stream)
         rx.stats_device(counters, stream)
         SH.allreduce_counters(counters)                 # the only cross-GPU data movement (24 × 8 B, NCCL)
 
@@ -436,7 +458,7 @@ def main():
     kkrx.kk_enable_timing(rx.ctx, False)
     kt_ms, kt_n = kkrx.kk_kernel_times(rx.ctx, reset=True)
     ms_max = SH.max_over_ranks(ms, device=dev)
-    total_samples = S * world * a.steps
+    total_samples = sum(x.n for x in plan) * a.steps
     value = total_samples / (ms_max * 1e-3) / 1e9
     st = stats_from_words(counters.cpu().tolist())
 
@@ -570,11 +592,13 @@ def main():
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "GS/s", "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
-            "ms_per_step": ms_max / a.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "ms_per_step": ms_max / a.steps, "higher_is_better": True, "scaling": a.scaling, "vs_baseline": None,
             "dtype": "f32", "data": "synthetic (kkgen seeded generator, generated on device)",
             "config": {"workload": f"{a.workload}: continuous mixed 4/8/16/32/64-QAM stream (256-frame segments), "
                                    f"1 GBaud @ 4 GS/s, 1600 km (32000 ps/nm), CSPR 12 dB, Es/N0 26 dB white, int16 ADC",
+                       "stream_samples": (a.samples if a.scaling == "strong" else a.samples_per_gpu * world),
                        "samples_per_gpu": S, "chunk_samples": chunk, "eq_taps": L, "eq_mode": a.eq_mode,
+                       "parallelism": f"{world} contiguous frame-range shards + halos, counters allreduced",
                        "kk_upsample": a.upsample, "mf_grid": f"FFT{a.mf_n}/hop {a.mf_n - 1024}",
                        **({"ddlms_block": a.ddlms_block, "ddlms_warmup": a.ddlms_warmup,
                            "ddlms_mu_warm": a.ddlms_mu_warm} if a.eq_mode == "ddlms" else {}),
@@ -588,7 +612,9 @@ def main():
             "kernels": kernels,
             "cpu_baseline": cpu,
             "quality": {"per_format": q, "frames": st["frames"], "dead_frames": st["dead_frames"],
-                        "bad_frames": st["bad_frames"], "clamped": st["clamped"]},
+                        "bad_frames": st["bad_frames"], "clamped": st["clamped"],
+                        "counts": {k: st[k] for k in ("sym", "sym_err", "bits", "bit_err")}},
+            "dist": dist_info,
             "gen_seconds": t_gen,
         }
         print(json.dumps(line), flush=True)
