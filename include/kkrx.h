@@ -167,7 +167,9 @@ kk_status kk_process_frames_ex(kk_ctx* ctx, const void* d_adc, int64_t first_sam
  * with two internal streams so the copies of chunk i+1 overlap the kernels of chunk i. Blocks until done.
  * h_ref / h_decisions nullable host uint8[n_samples/4] (h_ref NULL with ref_prbs = 1: generated labels, so only
  * the samples cross PCIe). Same constraints/errors as kk_process_frames,
- * except n_samples may exceed max_samples_per_call (it must be a multiple of 16384). */
+ * except n_samples may exceed max_samples_per_call (it must be a multiple of 16384). Ordering: the internal
+ * streams first wait for work already queued on the legacy default stream and on the stream of the context's
+ * last kk_process_frames / kk_reset_stats call, so no caller synchronisation is needed before it. */
 kk_status kk_process_frames_host(kk_ctx* ctx, const void* h_adc, int64_t first_sample, int64_t n_samples,
                                  const uint8_t* h_ref, uint8_t* h_decisions);
 

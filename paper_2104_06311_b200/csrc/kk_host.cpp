@@ -76,6 +76,7 @@ struct kk_ctx {
   uint8_t* d_dec[2] = {nullptr, nullptr};
   cudaStream_t hs[2] = {nullptr, nullptr};
   cudaEvent_t ev[2] = {nullptr, nullptr};
+  cudaEvent_t entry_ev[2] = {nullptr, nullptr};   // host path: order after the legacy stream and the last caller stream
   // last call
   bool have_call = false;
   int64_t last_first = 0, last_n = 0;
@@ -358,6 +359,7 @@ void free_all(kk_ctx* c) {
   for (int i = 0; i < 2; ++i) {
     if (c->hs[i]) cudaStreamDestroy(c->hs[i]);
     if (c->ev[i]) cudaEventDestroy(c->ev[i]);
+    if (c->entry_ev[i]) cudaEventDestroy(c->entry_ev[i]);
   }
 }
 
@@ -741,8 +743,19 @@ kk_status kk_process_frames_host(kk_ctx* c, const void* h_adc, int64_t first, in
     if (!c->d_dec[i]) chk(dalloc(c, "host_dec", &c->d_dec[i], (size_t)(hc / 4)));
     if (!c->hs[i]) chk(cudaStreamCreateWithFlags(&c->hs[i], cudaStreamNonBlocking));
     if (!c->ev[i]) chk(cudaEventCreateWithFlags(&c->ev[i], cudaEventDisableTiming));
+    if (!c->entry_ev[i]) chk(cudaEventCreateWithFlags(&c->entry_ev[i], cudaEventDisableTiming));
   }
   if (e != cudaSuccess) return fail(c, e == cudaErrorMemoryAllocation ? KK_ERR_NOMEM : KK_ERR_CUDA, cudaGetErrorString(e));
+  // The staging streams are non-blocking: order them after work still in flight on the legacy default stream
+  // (e.g. kk_reset_stats(ctx, NULL)) and on the stream of the context's last device call (kk_process_frames /
+  // kk_reset_stats on a caller stream), which share the scratch buffers and the counters with this call.
+  chk(cudaEventRecord(c->entry_ev[0], cudaStreamLegacy));
+  const bool own_last = c->last_stream == nullptr || c->last_stream == c->hs[0] || c->last_stream == c->hs[1];
+  if (!own_last) chk(cudaEventRecord(c->entry_ev[1], c->last_stream));
+  for (int i = 0; i < 2; ++i) {
+    chk(cudaStreamWaitEvent(c->hs[i], c->entry_ev[0], 0));
+    if (!own_last) chk(cudaStreamWaitEvent(c->hs[i], c->entry_ev[1], 0));
+  }
   const char* src = static_cast<const char*>(h_adc);
   int64_t done = 0;
   int k = 0;
@@ -792,6 +805,7 @@ kk_status kk_reset_stats(kk_ctx* c, kk_stream_t stream) {
   if (!c) return KK_ERR_NULL;
   DeviceGuard g(c->device);
   cudaError_t e = cudaMemsetAsync(c->d_counters, 0, 32 * sizeof(unsigned long long), static_cast<cudaStream_t>(stream));
+  if (stream) c->last_stream = static_cast<cudaStream_t>(stream);   // the host path orders itself after it
   return e == cudaSuccess ? KK_OK : fail(c, KK_ERR_CUDA, cudaGetErrorString(e));
 }
 

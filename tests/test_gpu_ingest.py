@@ -44,3 +44,38 @@ def test_single_ingest_matches_direct(upsample):
     assert rx0.stats() == rx1.stats()
     rx0.close()
     rx1.close()
+
+
+def test_host_path_orders_after_reset_and_caller_stream():
+    """kk_process_frames_host must not race work still queued on the legacy stream (kk_reset_stats
+    with stream NULL) or on the caller stream of the context's previous device call — no synchronisation in
+    between. Each stream is first kept busy (torch.cuda._sleep) so that an unordered host path would run ahead."""
+    from gpu_case import F, make_case, receiver_for
+    case = make_case(M=16, dl=112000.0, cspr=10.0, esn0=14.0, n=16 * F, seed=27)
+    codes_d, ref_d = case["codes"].cuda(), case["ref"].cuda()
+    codes_h, ref_h = case["codes"].pin_memory(), case["ref"].pin_memory()
+    rx = receiver_for(case, keep=False, max_samples=4 * F)
+    rx.process_host(codes_h, case["first"], case["n"], ref=ref_h)
+    want = rx.stats()
+    keys = ("sym", "sym_err", "bits", "bit_err", "frames")
+    s1 = torch.cuda.Stream()
+    for _ in range(3):
+        # (a) a device call and the reset queued on a caller stream behind a busy kernel
+        torch.cuda.synchronize()
+        with torch.cuda.stream(s1):
+            torch.cuda._sleep(50_000_000)
+            for c0 in range(0, case["n"], 4 * F):
+                rx.process(codes_d, case["first"] + c0, 4 * F, ref=ref_d[c0 // 4:(c0 + 4 * F) // 4], offset=c0,
+                           stream=s1)
+            rx.reset_stats(stream=s1)
+        rx.process_host(codes_h, case["first"], case["n"], ref=ref_h)
+        got = rx.stats()
+        assert all(got[k] == want[k] for k in keys), ("caller stream", got, want)
+        # (b) the reset on the legacy default stream behind a busy kernel
+        torch.cuda.synchronize()
+        torch.cuda._sleep(50_000_000)                   # current stream = the legacy default stream
+        rx.reset_stats()
+        rx.process_host(codes_h, case["first"], case["n"], ref=ref_h)
+        got = rx.stats()
+        assert all(got[k] == want[k] for k in keys), ("legacy stream", got, want)
+    rx.close()
