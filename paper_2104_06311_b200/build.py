@@ -32,6 +32,11 @@ def _newer(target: str, deps) -> bool:
 
 def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(BUILD, exist_ok=True)
+    # the compile flags (incl. KK_NVCC_DEFINES) are part of every object's identity: a change rebuilds all
+    stamp = os.path.join(BUILD, "flags.stamp")
+    want = " ".join([NVCC] + ARCH + FLAGS)
+    if not os.path.exists(stamp) or open(stamp).read() != want:
+        force = True
     headers = [os.path.join(CSRC, h) for h in os.listdir(CSRC) if h.endswith((".h", ".cuh"))]
     headers.append(os.path.join(ROOT, "include", "kkrx.h"))
     objs = []
@@ -62,6 +67,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr[-4000:]}")
+    with open(stamp, "w") as f:
+        f.write(want)
     return LIB
 
 
