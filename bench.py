@@ -71,8 +71,8 @@ def parse():
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="process group for N > 1 (gloo only for functional smoke runs of the multi-rank path on "
                          "fewer GPUs than ranks; never for timing)")
-    ap.add_argument("--ddlms-block", type=int, default=256)
-    ap.add_argument("--ddlms-warmup", type=int, default=512)
+    ap.add_argument("--ddlms-block", type=int, default=512)
+    ap.add_argument("--ddlms-warmup", type=int, default=1024)
     ap.add_argument("--ddlms-mu-warm", type=float, default=2e-3)
     return ap.parse_args()
 
@@ -96,7 +96,7 @@ def k2_tile_flops(n: int) -> float:
     return 5.0 * n * math.log2(n) + 5.0 * (n // 2) * math.log2(n // 2) + 6.0 * (n // 2) + 8.0 * n
 
 
-def kernel_units(chunk: int, L: int, eq_mode: str = "block_ls", ddlms_block: int = 256, ddlms_warmup: int = 512,
+def kernel_units(chunk: int, L: int, eq_mode: str = "block_ls", ddlms_block: int = 512, ddlms_warmup: int = 1024,
                  upsample: int = 1, mf_n: int = 4096):
     """Algorithmic flops and HBM bytes per launch of each kernel for one call of `chunk` samples."""
     K = (L - 1) // 2

@@ -88,10 +88,10 @@ typedef struct kk_config {
    * static filter = RRC × CD inverse (the "offline-optimized filter"), then the 4-tap T/2-spaced widely-linear
    * DDLMS, restarted every ddlms_block symbols after ddlms_warmup warm-up symbols (global grid). */
   int32_t eq_mode;
-  int32_t ddlms_block;           /* 256 … 4096, power of two (kept symbols per restart; default 256)     */
-  int32_t ddlms_warmup;          /* 0 … 3136, multiple of 64 (default 512): warm-up from the centre spike */
+  int32_t ddlms_block;           /* 256 … 4096, power of two (kept symbols per restart; default 512)     */
+  int32_t ddlms_warmup;          /* 0 … 3136, multiple of 64 (default 1024): warm-up from the centre spike */
   int32_t debug_guard;           /* 1: surround every device scratch buffer with 64 KiB canaries (kk_check_guards) */
-  double  ddlms_mu_warm;         /* 2e-3 step size during warm-up                                        */
+  double  ddlms_mu_warm;         /* 2e-3 step size over the first half of the warm-up (then ddlms_mu_mid) */
   double  ddlms_mu;              /* 2.5e-4 step size on kept symbols                                     */
   /* KK upsampling (SPEC S:277 upsample_factor; DESIGN.md §3 "KK upsampling"):
    * 1 = the paper's chain (KK at the ADC rate); 2 = interpolate I to 8 sps with a 31-tap half-band filter,
@@ -107,6 +107,7 @@ typedef struct kk_config {
   int32_t ref_prbs;
   uint32_t ref_seed;
   int32_t reserved2;
+  double  ddlms_mu_mid;          /* 5e-4 step size over the second half of the warm-up     */
 } kk_config;
 
 /* Counters (all uint64, summed over calls until kk_reset_stats; index i = log2(M) − 2 for M = 4..64).

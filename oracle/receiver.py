@@ -69,10 +69,11 @@ class OracleConfig:
     # into the static filter and equalizes with the 4-tap T/2-spaced widely-linear DDLMS
     eq_mode: str = "block_ls"         # "block_ls" (north star, default) | "ddlms" (paper, restart grid) |
                                       # "ddlms_seq" (paper, one recursion in stream order: the definition)
-    ddlms_mu_warm: float = 2e-3       # step size over the warm-up symbols
+    ddlms_mu_warm: float = 2e-3       # step size over the first half of the warm-up
+    ddlms_mu_mid: float = 5e-4        # … over the second half of the warm-up
     ddlms_mu: float = 2.5e-4          # step size over the kept symbols (SPEC S:377 schedule end)
-    ddlms_block: int = 256            # symbols kept per DDLMS restart (global grid)
-    ddlms_warmup: int = 512           # symbols run before each block from the centre-spike state
+    ddlms_block: int = 512            # symbols kept per DDLMS restart (global grid)
+    ddlms_warmup: int = 1024          # symbols run before each block from the centre-spike state
     ddlms_seq_mu0: float = 1e-3       # sequential form: μ over the first ddlms_seq_switch symbols
     ddlms_seq_switch: int = 10000     # … then ddlms_mu (2.5e-4)
     # KK upsampling (O3u): 1 = the paper's 4-sps chain; 2 = interpolate I to 8 sps before sqrt/log
@@ -275,7 +276,7 @@ def o8_ddlms_block(y: np.ndarray, m0: int, n0: int, nwarm: int, nkeep: int, M, c
     u = g·y, g = (mean_n |y[2n]|²)^(−½) (AGC over the block and its warm-up);
     out_n = wᵀx_n + vᵀconj(x_n), d_n = D(out_n), e_n = d_n − out_n, w += μ·e·conj(x), v += μ·e·x;
     w starts as the centre spike on u[2n], v = 0 (and stays 0 when eq_widely_linear is False);
-    μ = ddlms_mu_warm over the warm-up, ddlms_mu after.
+    μ = ddlms_mu_warm over the first half of the warm-up, ddlms_mu_mid over its second half, ddlms_mu after.
     M is the QAM order of every symbol (an int, or one per symbol: each symbol is decided in its own frame's
     format, "d[n] = nearest constellation point"). Returns the outputs of the nkeep kept symbols
     (before each one's update). `decide` is the hard
@@ -293,7 +294,7 @@ def o8_ddlms_block(y: np.ndarray, m0: int, n0: int, nwarm: int, nkeep: int, M, c
         o = np.dot(w, x) + np.dot(v, np.conj(x))
         d, _ = decide(np.array([o]), int(Ms[i]))
         e = d[0] - o
-        mu = cfg.ddlms_mu_warm if i < nwarm else cfg.ddlms_mu
+        mu = cfg.ddlms_mu_warm if i < nwarm // 2 else cfg.ddlms_mu_mid if i < nwarm else cfg.ddlms_mu
         if i >= nwarm:
             out[i - nwarm] = o
         w = w + mu * e * np.conj(x)

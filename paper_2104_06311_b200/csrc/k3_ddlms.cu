@@ -7,7 +7,8 @@
 //   x_n = g·[y[2n+1], y[2n], y[2n−1], y[2n−2]],  g = (mean |y[2n]|²)^(−½) over the block and its warm-up
 //   (the power comes from K2's per-64-symbol segment sums)
 //   o_n = wᵀx_n + vᵀconj(x_n),  d_n = D(o_n),  e_n = d_n − o_n,  w += μ e conj(x),  v += μ e x
-//   w₀ = centre spike on y[2n], v₀ = 0; μ = mu_warm over the warm-up, mu over the kept symbols; every symbol
+//   w₀ = centre spike on y[2n], v₀ = 0; μ = mu_warm over the first half of the warm-up, mu_mid over the second
+//   half (the taps settle toward the small-μ state before the kept symbols), mu over the kept symbols; every symbol
 //   is decided in its own frame's QAM order (warm-up symbols in the previous frame in that frame's order).
 // The paper carries the equalizer state across 2^22-sample buffers in stream order (events serialise the
 // streams). Here the recursion restarts on a global grid of B-symbol blocks, each preceded by W
@@ -130,7 +131,7 @@ k3_ddlms_kernel(const float2* __restrict__ y, int64_t y_base, int64_t sym_first,
         int lab = 0;
         const float2 d = kept ? sl.decide(o, lab) : sc.point(o);   // kept: point and label from one slicing
         const float2 e = csub(d, o);
-        const float mu = kept ? p.mu : p.mu_warm;
+        const float mu = kept ? p.mu : (i0 < (W >> 1) ? p.mu_warm : p.mu_mid);   // chunk-uniform
         if (kept) {
           const int64_t kl = n;                                // local kept symbol index
           if (ref) {

@@ -319,7 +319,7 @@ kk_status validate(const kk_config& c, std::string& why) {
     if (c.ddlms_warmup < 0 || c.ddlms_warmup % 64 ||
         2 * (2 * c.ddlms_warmup + 2) + 2 * keep - 2 + 512 > kk::kFrameSamp)
       return bad("ddlms_warmup must be a multiple of 64 in [0, 3136] (MF 4096) or [0, 2112] (MF 8192)");
-    if (!(c.ddlms_mu_warm >= 0) || !(c.ddlms_mu >= 0)) return bad("ddlms step sizes must be >= 0");
+    if (!(c.ddlms_mu_warm >= 0) || !(c.ddlms_mu >= 0) || !(c.ddlms_mu_mid >= 0)) return bad("ddlms step sizes must be >= 0");
   }
   return KK_OK;
 }
@@ -401,11 +401,12 @@ void kk_config_default(kk_config* c) {
   c->device = 0;
   c->keep_intermediate = 0;
   c->eq_mode = KK_EQ_BLOCK_LS;
-  c->ddlms_block = 256;
-  c->ddlms_warmup = 512;
+  c->ddlms_block = 512;
+  c->ddlms_warmup = 1024;
   c->debug_guard = 0;
   c->ddlms_mu_warm = 2e-3;
   c->ddlms_mu = 2.5e-4;
+  c->ddlms_mu_mid = 5e-4;
   c->upsample = 1;
   c->ref_prbs = 0;
   c->ref_seed = 0;
@@ -696,6 +697,7 @@ kk_status kk_process_frames_ex(kk_ctx* c, const void* d_adc, int64_t first, int6
     pd.segment_frames = cf.segment_frames;
     pd.mu_warm = (float)cf.ddlms_mu_warm;
     pd.mu = (float)cf.ddlms_mu;
+    pd.mu_mid = (float)cf.ddlms_mu_mid;
     pd.widely_linear = cf.eq_widely_linear;
     pd.frame_err = d_ref ? d_ferr : nullptr;
     if (pd.frame_err) cudaMemsetAsync(pd.frame_err, 0, (size_t)(n / F) * 2 * sizeof(uint32_t), s);

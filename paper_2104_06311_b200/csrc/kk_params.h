@@ -64,7 +64,7 @@ struct K3DParams {
   const uint8_t* schedule;
   int n_segments;
   int64_t segment_frames;
-  float mu_warm, mu;
+  float mu_warm, mu, mu_mid;         // μ: first half of the warm-up, kept symbols, second half of the warm-up
   int widely_linear;
   unsigned* frame_err;               // nullable, zeroed by the host before the launch
 };

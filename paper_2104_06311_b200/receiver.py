@@ -20,8 +20,9 @@ class Receiver:
                  eq_taps: int = 0, widely_linear: bool = True, cpr_window: int = 256, eq_ridge: float = 1e-3,
                  input_float: bool = False, input_uint8: bool = False, sideband: int = 1, lo_num: int = 129, lo_den: int = 1000,
                  clamp_rel: float = 1e-12, rolloff: float = 0.01, rrc_span_sym: int = 256,
-                 eq_mode: str = "block_ls", ddlms_block: int = 256, ddlms_warmup: int = 512,
-                 ddlms_mu_warm: float = 2e-3, ddlms_mu: float = 2.5e-4, debug_guard: bool = False,
+                 eq_mode: str = "block_ls", ddlms_block: int = 512, ddlms_warmup: int = 1024,
+                 ddlms_mu_warm: float = 2e-3, ddlms_mu: float = 2.5e-4, ddlms_mu_mid: float = 5e-4,
+                 debug_guard: bool = False,
                  upsample: int = 1, mf_fft_n: int = 4096, ref_prbs_seed: Optional[int] = None):
         cfg = kkrx.kk_config_default()
         cfg.adc_scale, cfg.adc_offset, cfg.ref_intensity = adc_scale, adc_offset, ref_intensity
@@ -39,7 +40,7 @@ class Receiver:
         cfg.clamp_rel, cfg.rolloff, cfg.rrc_span_sym = clamp_rel, rolloff, rrc_span_sym
         cfg.eq_mode = {"block_ls": kkrx.KK_EQ_BLOCK_LS, "ddlms": kkrx.KK_EQ_DDLMS}[eq_mode]
         cfg.ddlms_block, cfg.ddlms_warmup = ddlms_block, ddlms_warmup
-        cfg.ddlms_mu_warm, cfg.ddlms_mu = ddlms_mu_warm, ddlms_mu
+        cfg.ddlms_mu_warm, cfg.ddlms_mu, cfg.ddlms_mu_mid = ddlms_mu_warm, ddlms_mu, ddlms_mu_mid
         cfg.debug_guard = int(debug_guard)
         cfg.upsample = upsample
         cfg.mf_fft_n, cfg.mf_hop = mf_fft_n, mf_fft_n - 1024      # MF overlap-save grid (4096/3072 or 8192/7168)

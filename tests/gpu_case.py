@@ -43,7 +43,8 @@ def receiver_for(case, keep=True, max_samples=None, **kw):
                     max_samples_per_call=max_samples or max(case["n"], F), keep_intermediate=keep,
                     eq_taps=o.eq_taps, widely_linear=o.eq_widely_linear, cpr_window=o.cpr_window,
                     eq_mode=o.eq_mode, ddlms_block=o.ddlms_block, ddlms_warmup=o.ddlms_warmup,
-                    ddlms_mu_warm=o.ddlms_mu_warm, ddlms_mu=o.ddlms_mu, sideband=o.sideband, upsample=o.upsample,
+                    ddlms_mu_warm=o.ddlms_mu_warm, ddlms_mu=o.ddlms_mu, ddlms_mu_mid=o.ddlms_mu_mid,
+                    sideband=o.sideband, upsample=o.upsample,
                     **kw)
 
 

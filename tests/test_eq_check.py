@@ -60,7 +60,8 @@ def test_eq_check_ddlms_block_flip():
     zg = orc["z"].copy()
     s0 = fi * 4096 + bb
     zg[s0:s0 + cfg.ddlms_block] = zb
-    raw = np.linalg.norm(zb - orc["z"][s0:s0 + cfg.ddlms_block]) / np.linalg.norm(zb)
+    f0 = fi * 4096
+    raw = np.linalg.norm(zg[f0:f0 + 4096] - orc["z"][f0:f0 + 4096]) / np.linalg.norm(orc["z"][f0:f0 + 4096])
     if raw < 1e-7:
         pytest.skip("closest boundary decision does not move this block's outputs")
     tol = min(1e-4, raw / 2)

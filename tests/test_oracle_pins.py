@@ -563,7 +563,7 @@ def test_dd_static_filter_zero_km_is_rrc_and_inverts_cd():
 def test_dd_mu_zero_is_identity():
     rng = np.random.default_rng(4)
     y = rng.standard_normal(6000) + 1j * rng.standard_normal(6000)
-    cfg = _dd_cfg(ddlms_mu_warm=0.0, ddlms_mu=0.0)
+    cfg = _dd_cfg(ddlms_mu_warm=0.0, ddlms_mu_mid=0.0, ddlms_mu=0.0)
     out = R.o8_ddlms_block(y, 0, 10, 100, 500, 16, cfg)
     nn = np.arange(110, 610)
     g = 1 / np.sqrt(np.mean(np.abs(y[2 * np.arange(10, 610)]) ** 2))
