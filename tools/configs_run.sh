@@ -2,10 +2,10 @@
 set -e
 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')"
 mkdir -p gpurun_out/cfg
-python bench.py --workload C1 --samples-per-gpu 65536 --steps 20 --warmup 5 --no-e2e --cpu-frames 4 > gpurun_out/cfg/C1.json 2>&1
-python bench.py --workload C2 --samples-per-gpu 4194304 --steps 10 --warmup 3 --no-e2e --cpu-frames 32 > gpurun_out/cfg/C2.json 2>&1
-python bench.py --workload C3 --samples-per-gpu 16777216 --steps 10 --warmup 3 --no-e2e --cpu-frames 32 > gpurun_out/cfg/C3.json 2>&1
-python bench.py --workload C4 --samples-per-gpu 67108864 --steps 5 --warmup 3 --no-e2e --cpu-frames 32 > gpurun_out/cfg/C4.json 2>&1
+python bench.py --workload C1 --samples 65536 --steps 20 --warmup 5 --no-e2e --cpu-frames 4 > gpurun_out/cfg/C1.json 2>&1
+python bench.py --workload C2 --samples 4194304 --steps 10 --warmup 3 --no-e2e --cpu-frames 32 > gpurun_out/cfg/C2.json 2>&1
+python bench.py --workload C3 --samples 16777216 --steps 10 --warmup 3 --no-e2e --cpu-frames 32 > gpurun_out/cfg/C3.json 2>&1
+python bench.py --workload C4 --samples 67108864 --steps 5 --warmup 3 --no-e2e --cpu-frames 32 > gpurun_out/cfg/C4.json 2>&1
 python bench.py --workload C5 --steps 5 --warmup 3 --cpu-frames 64 > gpurun_out/cfg/C5.json 2>&1
 python bench.py --workload C5 --steps 3 --warmup 3 --upsample 2 --no-e2e --cpu-frames 32 > gpurun_out/cfg/C5_up2.json 2>&1
 python bench.py --workload C5 --steps 3 --warmup 3 --eq-mode ddlms --no-e2e --cpu-frames 32 > gpurun_out/cfg/C5_ddlms.json 2>&1

@@ -43,7 +43,7 @@ def main(report, launches, out_md, traffic_json=None):
     hdr, units, data = raw(report)
     col = {h: i for i, h in enumerate(hdr)}
     lines = [f"# ncu summary — `{report}`", "", "Captured with `ncu --set full --clock-control none --import-source on`"
-             " on one B200 (bench.py --samples-per-gpu 2^28, one 2^28-sample call per kernel). Values per launch.", ""]
+             " on one B200 (bench.py --samples 2^28, one 2^28-sample call per kernel). Values per launch.", ""]
     names = [r[col["Kernel Name"]].split("(")[0].replace("void ", "") for r in data]
     lines.append("| metric | " + " | ".join(names) + " |")
     lines.append("|---|" + "---|" * len(names))

@@ -11,7 +11,7 @@ NAMES = {"C1": "C1 4-QAM b2b, 2^16", "C2": "C2 16-QAM 5600 km, CSPR 6 dB @ OSNR 
          "C5_ddlms": "C5, paper arrangement (static RRC×CD⁻¹ + 4-tap WL DDLMS)"}
 HDR = """# Round-1 results per BASELINE.json configuration (1× B200, final code of the round)
 
-`bench.py --workload Cx --samples-per-gpu S` (device-resident inputs, calls of min(2^28, S) samples, CUDA-event
+`bench.py --workload Cx --samples S` (device-resident inputs, calls of min(2^28, S) samples, CUDA-event
 timing, clocks 1965 MHz with no throttle reasons in every run). Kernel times are per call (µs, live events
 inside the timed region); "dominant kernel" is the roofline object of the line (algorithmic TFLOP/s — the
 real-arithmetic counts of DESIGN.md §5 — and the fraction of the 74.4 TFLOP/s FP32 peak); the oracle column is
