@@ -10,10 +10,11 @@ import sys
 from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
-LIB = os.path.join(HERE, "libkkrx.so")
-BUILD = os.path.join(ROOT, "build")
+# A/B experiments only (tools/ab_dirs.sh): another source tree, object directory and library path
+CSRC = os.environ.get("KK_CSRC", os.path.join(HERE, "csrc"))
+LIB = os.environ.get("KK_LIB", os.path.join(HERE, "libkkrx.so"))
+BUILD = os.environ.get("KK_BUILD_DIR", os.path.join(ROOT, "build"))
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

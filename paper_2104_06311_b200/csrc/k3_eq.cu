@@ -117,6 +117,14 @@ template <int K>
 struct K3Layout {
   static constexpr int L = 2 * K + 1;
   static constexpr int ND = 2 * K + 1;             // lags 0..2K for base i = −K (ρ = 0); 0..2K−1 for ρ = 1
+  // K ≤ 4: every lane works on groups of GS = 4 consecutive symbols (a group's K + 4 window pairs serve its 4
+  // symbols' windows: 2 instead of K + 1 16-B loads per symbol) on a frame buffer written by tensor TMA with the
+  // 64-B swizzle (conflict-free group loads); lags [0, LA) are summed in sweep A (with pass 1), [LA, ND) in
+  // sweep B (with p). K ≥ 5: one symbol at a time (GS = 1), plain bulk copy, all lags in sweep A.
+  static constexpr bool SW = (K <= 4);
+  static constexpr int GS = SW ? 4 : 1;
+  static constexpr int LA = SW ? (K + 2 < ND ? K + 2 : ND) : ND;
+  static constexpr int LB = ND - LA;
   static constexpr int N = 2 * L;                  // real system size
   static constexpr int NP = 4 * L;                 // p floats: p1, p2 complex
   static constexpr int RG = (K <= 4) ? ND : 8;     // lags per R sweep (register budget)
@@ -124,24 +132,25 @@ struct K3Layout {
   static constexpr int NR = 8 * RG * NRG;          // S0,T0,S1,T1 per lag (padded to whole groups)
   static constexpr int NRED = ((NP + NR + 1 + 31) / 32) * 32;   // + frame power
   static constexpr int IPOW = NP + NR;             // index of the frame power in the reduction
-  static constexpr int YS = 2 * kFrameSym + 2 * K; // float2 loaded per frame (y_s[0 .. 8191 + 2K])
+  static constexpr int YS = 2 * kFrameSym + 2 * K; // float2 used per frame (y_s[0 .. 8191 + 2K])
+  static constexpr int YB = SW ? (1024 + 8) * 64 : YS * 8;   // frame buffer bytes (SW: 8 × 128 + 8 rows of 64 B)
   static constexpr int WS = N + 3;                 // odd row stride (doubles) of the real system [A | q1 q2]
   static constexpr int RED_B = K3_WARPS * NRED * 4;
   static constexpr int MAT_B = N * WS * 8;
   // two label buffers (the next frame's labels land while this frame's are read) when two CTAs per SM still
   // fit in the SM's 228 KB with them (1 KB reserved per CTA): K ≤ 6
-  static constexpr int TOTAL1 = YS * 8 + kFrameSym + kFrameSym * 8 + (RED_B > MAT_B ? RED_B : MAT_B) +
+  static constexpr int TOTAL1 = YB + kFrameSym + kFrameSym * 8 + (RED_B > MAT_B ? RED_B : MAT_B) +
                                 (NRED > 128 ? NRED : 128) * 8 + 2 * L * 8 + 16 * 8 + 32 * 4 + 16 + 64 * 4;
   static constexpr int NREFB = (2 * (TOTAL1 + kFrameSym + 1024) <= 228 * 1024) ? 2 : 1;
   // shared memory (bytes)
   static constexpr int Y = 0;                      // frame samples; reused for the CPR products after pass 2
-  static constexpr int REF = Y + YS * 8;           // NREFB × 4096 labels
+  static constexpr int REF = Y + YB;               // NREFB × 4096 labels
   static constexpr int US = REF + NREFB * kFrameSym;   // y⁰ (pass 1), then y¹ (pass 2) per symbol (float2 × 4096)
   static constexpr int RED = US + kFrameSym * 8;   // warp partial sums; the solve's matrix aliases it
   static constexpr int MAT = RED;
   static constexpr int DRES = RED + (RED_B > MAT_B ? RED_B : MAT_B);
   static constexpr int TH = DRES + (NRED > 128 ? NRED : 128) * 8;   // (dres doubles as the GJ pivot rows)
-  static constexpr int ROT = TH + 2 * L * 8;       // 16 CPR rotations
+  static constexpr int ROT = TH + 2 * L * 8;       // (spare: 16 float2)
   static constexpr int CC = ROT + 16 * 8;          // the frame's 32 per-block clamp counts (TMA, with the samples)
   static constexpr int BAR = CC + 32 * 4;          // mbarrier
   static constexpr int MISC = BAR + 16;
@@ -150,11 +159,19 @@ struct K3Layout {
   static_assert(N <= 32, "one matrix row per lane");
   static_assert((2 * ND - 1) * (K + 1) <= K3_THREADS, "one thread per chain point");
   static_assert(2 * (K + 1) * 8 <= 2 * L * 8, "trace terms fit in th");
-  static_assert((YS * 8) % 16 == 0, "TMA size");
+  static_assert((YS * 8) % 16 == 0 && YB >= YS * 8, "TMA size");
 };
 
 __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+// 2-D tensor TMA (tile mode) into shared memory, completion on the mbarrier (the tensor map carries the swizzle)
+__device__ __forceinline__ void tma_tensor_2d(void* dst_smem, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+      ::"r"(smem_u32(dst_smem)), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
 }
 
 #ifdef KK_PHASE_TIMING   // debug: per-phase SM clocks of CTA 0 (tools/k3_phases.py), printed at kernel exit
@@ -168,10 +185,12 @@ __global__ void __launch_bounds__(K3_THREADS, 2)
 k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const float2* __restrict__ w_cd,
              const int* __restrict__ clampcnt, int64_t clamp_frame_off, const uint8_t* __restrict__ ref,
              uint8_t* __restrict__ dec, float2* __restrict__ zout, unsigned long long* __restrict__ counters,
-             K3Params p) {
+             K3Params p, const __grid_constant__ CUtensorMap ymap, const __grid_constant__ CUtensorMap ymap_tail) {
   using Lay = K3Layout<K>;
   constexpr int L = Lay::L, ND = Lay::ND, N = Lay::N, NRED = Lay::NRED;
-  extern __shared__ __align__(128) unsigned char smem[];
+  constexpr bool SW = Lay::SW;
+  constexpr int GS = Lay::GS, NG = K3_SPT / GS, NW = K + GS, LA = Lay::LA, LB = Lay::LB;
+  extern __shared__ __align__(1024) unsigned char smem[];
   float2* ys = reinterpret_cast<float2*>(smem + Lay::Y);
   const float4* ys4 = reinterpret_cast<const float4*>(smem + Lay::Y);
   uint8_t* ref_s = smem + Lay::REF;
@@ -180,7 +199,6 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
   double* dres = reinterpret_cast<double*>(smem + Lay::DRES);
   double* mat = reinterpret_cast<double*>(smem + Lay::MAT);
   float2* th = reinterpret_cast<float2*>(smem + Lay::TH);
-  float2* rot = reinterpret_cast<float2*>(smem + Lay::ROT);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + Lay::BAR);
   const int* cc_s = reinterpret_cast<const int*>(smem + Lay::CC);
   int* misc = reinterpret_cast<int*>(smem + Lay::MISC);
@@ -194,7 +212,7 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
   // closing barrier), so the frame start no longer waits for a label copy issued at the end of the frame
   const bool dbl = (Lay::NREFB == 2) && ref_tma;
   auto ref_buf = [&](int b) { return ref_s + (dbl ? (b & 1) * kFrameSym : 0); };
-  constexpr uint32_t YBYTES = Lay::YS * 8;
+  constexpr uint32_t YBYTES = Lay::YB;
 
   // thread 0: TMA the frame samples (and, separately, its labels) into shared memory. One arrival with the
   // total byte count; the copies may be issued at different times (the phase completes when all land). The
@@ -202,7 +220,13 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
   auto issue_y = [&](int fl) {
     fence_proxy_async_smem();                     // the frame buffer was written by generic stores (CPR products)
     if (!dbl) mbar_arrive_expect_tx(bar, YBYTES + 128u + (ref_tma ? (uint32_t)kFrameSym : 0u));
-    tma_bulk_g2s(ys, y + (int64_t)fl * (2 * kFrameSym), YBYTES, bar);
+    if constexpr (SW) {                           // 8 boxes of 128 rows + one of 8 rows (64-B rows of 8 float2)
+#pragma unroll
+      for (int b = 0; b < 8; ++b) tma_tensor_2d(smem + Lay::Y + b * 8192, &ymap, 0, fl * 1024 + 128 * b, bar);
+      tma_tensor_2d(smem + Lay::Y + 65536, &ymap_tail, 0, fl * 1024 + 1024, bar);
+    } else {
+      tma_bulk_g2s(ys, y + (int64_t)fl * (2 * kFrameSym), YBYTES, bar);
+    }
     tma_bulk_g2s(smem + Lay::CC, clampcnt + clamp_frame_off + (int64_t)fl * 32, 128u, bar);
   };
   auto issue_ref = [&](int fl, int b) {
@@ -212,7 +236,7 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
     tma_bulk_g2s(ref_buf(b), ref + (int64_t)fl * kFrameSym, kFrameSym, bar);
   };
   auto prefetch = [&](int fl) {
-    prefetch_l2(y + (int64_t)fl * (2 * kFrameSym), YBYTES);
+    prefetch_l2(y + (int64_t)fl * (2 * kFrameSym), Lay::YS * 8);
     if (ref_tma) prefetch_l2(ref + (int64_t)fl * kFrameSym, kFrameSym);
   };
   auto frame_order = [&](int64_t f) -> int {     // QAM order of global frame f (R26)
@@ -231,6 +255,38 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
 
   // tap window of local symbol kl: w[e] = y_s[2kl + 2K − e] = y[2k − (e − K)], e = 0..2K;
   // loaded as K+1 16-B pairs (y_s[2kl + 2m], y_s[2kl + 2m + 1]) = (w[2K − 2m], w[2K − 2m − 1])
+  // symbol ownership: warp w owns the 512 consecutive symbols [512w, 512w + 512), lane l the 16 symbols
+  // 512w + 32s + l (s < 16) — each warp-wide access covers 32 consecutive symbols (conflict-free 16-B window
+  // loads), and a 256-symbol CPR window is one half of a warp (s < 8 or s ≥ 8)
+  auto KL = [&](int s) { return 512 * warp + 32 * s + lane; };
+  // groups (GS consecutive symbols per lane): the lane's group g starts at symbol G0(g); 32·GS symbols per warp step
+  auto G0 = [&](int g) { return 512 * warp + 32 * GS * g + GS * lane; };
+  // frame buffer: float4 i (samples 2i, 2i + 1) lives at swz(i) — TMA SWIZZLE_64B XORs the 16-B chunk bits 4–5 of
+  // the address with bits 7–8 (the buffer is 1024-B aligned); a group window is NW consecutive float4 from G0(g),
+  // at the same lane-relative offsets for every g (32·GS·g float4 is a multiple of 4 rows of 128 B)
+  auto swz = [](int i) { return SW ? (i ^ ((i >> 3) & 3)) : i; };
+  auto ysw = [&](int e) -> float2 { const int q = e >> 1; return ys[2 * swz(q) + (e & 1)]; };   // sample e
+  int woff[NW];
+#pragma unroll
+  for (int t = 0; t < NW; ++t) woff[t] = swz(GS * lane + t) - GS * lane;
+  auto load_group = [&](int g, float4 (&F)[NW]) {
+    const float4* b = ys4 + G0(g);
+#pragma unroll
+    for (int t = 0; t < NW; ++t) F[t] = b[woff[t]];
+  };
+  // window of the group's symbol j from the group's float4 (compile-time indices after unrolling)
+  auto win = [&](const float4 (&F)[NW], int j, float2 (&w)[L]) {
+#pragma unroll
+    for (int m = 0; m <= K; ++m) {
+      w[2 * K - 2 * m] = make_float2(F[j + m].x, F[j + m].y);
+      if (m < K) w[2 * K - 2 * m - 1] = make_float2(F[j + m].z, F[j + m].w);
+    }
+  };
+  // per-symbol values (y⁰, then y¹) in groups: float4 q = symbols (2q, 2q + 1) at uswz(q) (conflict-free 16-B
+  // accesses at the 32-B lane stride of 4-symbol groups)
+  float4* us4 = reinterpret_cast<float4*>(smem + Lay::US);
+  auto uswz = [](int q) { return SW ? (q ^ ((q >> 3) & 1)) : q; };
+  auto uget = [&](int kl) -> float2 { const int q = kl >> 1; return us[2 * uswz(q) + (kl & 1)]; };
   auto load_window = [&](int kl, float2 (&w)[L]) {
 #pragma unroll
     for (int m = 0; m <= K; ++m) {
@@ -274,9 +330,64 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
 
     int bad = 0;
     bool zero = dead;                    // z = 0, decisions D(0): dead frame, or no signal power (silent)
+    float2 rA = make_float2(0.f, 0.f), rB = make_float2(0.f, 0.f);   // CPR rotations (× unbias) of the warp's halves
     if (!dead) {
       // ---- sweep A: lag sums for bases ρ = 0 (i = −K, w[0]) and ρ = 1 (i = −K+1, w[1]) + pass-1 power
       //      S_ρ(d) = Σ conj(w[ρ])·w[ρ + d],  T_ρ(d) = Σ w[ρ]·w[ρ + d];  y⁰ = Σ_e w_cd[e]·w[e]
+      //      conj(a)·b and a·b share the four real products: accumulate Σ ar·br, Σ ai·bi, Σ ar·bi, Σ ai·br
+      //      (4 FMA for both); S = (A1 + A2, A3 − A4), T = (A1 − A2, A3 + A4) after the fp64 reduction;
+      //      packed: (A1, A3) += ar·(br, bi), (A4, A2) += ai·(br, bi) — 2 FFMA2
+      // red layout: [0, NP) {B1, B3, B4, B2} per tap; [NP + 8·d + {A1, A3, A4, A2} (ρ = 0), + 4 + {…} (ρ = 1)];
+      // [IPOW] power  (A1 = Σ ar·br, A2 = Σ ai·bi, A3 = Σ ar·bi, A4 = Σ ai·br; B likewise with d)
+      auto lag_acc = [&](float* acc, const float2 (&w)[L], int d0, int nd) {
+#pragma unroll
+        for (int gg = 0; gg < nd; ++gg) {
+          const int d = d0 + gg;
+          if (d < ND) {
+            ffma2s(acc[8 * gg], acc[8 * gg + 1], w[0].x, w[d]);
+            ffma2s(acc[8 * gg + 2], acc[8 * gg + 3], w[0].y, w[d]);
+            if (d < ND - 1) {
+              ffma2s(acc[8 * gg + 4], acc[8 * gg + 5], w[1].x, w[1 + d]);
+              ffma2s(acc[8 * gg + 6], acc[8 * gg + 7], w[1].y, w[1 + d]);
+            }
+          }
+        }
+      };
+      auto pass1 = [&](const float2 (&w)[L]) {   // w_cd·a = ar·(wr, wi) + ai·(−wi, wr)
+        float2 y0 = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int e = 0; e < L; ++e) {
+          ffma2s(y0, w[e].x, wc[e]);
+          ffma2s(y0, w[e].y, make_float2(-wc[e].y, wc[e].x));
+        }
+        return y0;
+      };
+      if constexpr (SW) {
+        float acc[8 * LA];
+#pragma unroll
+        for (int i = 0; i < 8 * LA; ++i) acc[i] = 0.f;
+        float pw = 0.f;
+#pragma unroll 1
+        for (int g = 0; g < NG; ++g) {
+          float4 F[NW];
+          load_group(g, F);
+          float2 y0[GS];
+#pragma unroll
+          for (int j = 0; j < GS; ++j) {
+            float2 w[L];
+            win(F, j, w);
+            lag_acc(acc, w, 0, LA);
+            y0[j] = pass1(w);
+            pw = fmaf(y0[j].x, y0[j].x, fmaf(y0[j].y, y0[j].y, pw));
+          }
+          const int q = G0(g) >> 1;                // y⁰ of the group (kept in us until sweep B)
+          us4[uswz(q)] = make_float4(y0[0].x, y0[0].y, y0[1].x, y0[1].y);
+          us4[uswz(q + 1)] = make_float4(y0[2].x, y0[2].y, y0[3].x, y0[3].y);
+        }
+        warp_partials<8 * LA>(acc, red_w, Lay::NP, lane);
+        pw = warp_sum(pw);
+        if (lane == 0) red_w[Lay::IPOW] = pw;
+      } else {
 #pragma unroll
       for (int grp = 0; grp < Lay::NRG; ++grp) {
         constexpr int G = Lay::RG;
@@ -288,40 +399,20 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
 #pragma unroll 2
         for (int s = 0; s < K3_SPT; ++s) {
           float2 w[L];
-          load_window(tid + K3_THREADS * s, w);
-#pragma unroll
-          for (int gg = 0; gg < G; ++gg) {
-            const int d = d0 + gg;
-            if (d < ND) {
-              // conj(a)·b and a·b share the four real products: accumulate Σ ar·br, Σ ai·bi, Σ ar·bi, Σ ai·br
-              // (4 FMA for both); S = (A1 + A2, A3 − A4), T = (A1 − A2, A3 + A4) after the fp64 reduction
-              // packed: (A1, A3) += ar·(br, bi), (A4, A2) += ai·(br, bi)  — 2 FFMA2
-              ffma2s(acc[8 * gg], acc[8 * gg + 1], w[0].x, w[d]);
-              ffma2s(acc[8 * gg + 2], acc[8 * gg + 3], w[0].y, w[d]);
-              if (d < ND - 1) {
-                ffma2s(acc[8 * gg + 4], acc[8 * gg + 5], w[1].x, w[1 + d]);
-                ffma2s(acc[8 * gg + 6], acc[8 * gg + 7], w[1].y, w[1 + d]);
-              }
-            }
-          }
+          load_window(KL(s), w);
+          lag_acc(acc, w, d0, G);
           if (grp == 0) {                      // pass 1 (kept in us until sweep B) and its power
-            float2 y0 = make_float2(0.f, 0.f);
-#pragma unroll
-            for (int e = 0; e < L; ++e) {        // w_cd·a = ar·(wr, wi) + ai·(−wi, wr)
-              ffma2s(y0, w[e].x, wc[e]);
-              ffma2s(y0, w[e].y, make_float2(-wc[e].y, wc[e].x));
-            }
-            us[tid + K3_THREADS * s] = y0;
+            const float2 y0 = pass1(w);
+            us[KL(s)] = y0;
             pw = fmaf(y0.x, y0.x, fmaf(y0.y, y0.y, pw));
           }
         }
-        // red layout: [0, NP) {B1, B3, B4, B2} per tap; [NP + 8·d + {A1, A3, A4, A2} (ρ = 0), + 4 + {…} (ρ = 1)];
-        // [IPOW] power  (A1 = Σ ar·br, A2 = Σ ai·bi, A3 = Σ ar·bi, A4 = Σ ai·br; B likewise with d)
         warp_partials<8 * G>(acc, red_w, Lay::NP + 8 * d0, lane);
         if (grp == 0) {
           pw = warp_sum(pw);
           if (lane == 0) red_w[Lay::IPOW] = pw;
         }
+      }
       }
       __syncthreads();
       KK_PT(1);
@@ -334,23 +425,52 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
       const bool p0ok = (P0 > (double)p.p0_min) && isfinite(P0);
       if (!p0ok) { bad = 1; zero = true; }
       if (p0ok) {
-      const float g = (float)(1.0 / sqrt(P0));
+      const float g_agc = (float)(1.0 / sqrt(P0));
+      const float g = g_agc;
 
-      // ---- sweep B: decisions on g·y⁰ and p1[e] = Σ conj(a_j)·d, p2[e] = Σ a_j·d  (a_j = w[e])
-      {
+      // ---- sweep B: decisions on g·y⁰ and p1[e] = Σ conj(a_j)·d, p2[e] = Σ a_j·d  (a_j = w[e]);
+      //      (SW: plus the lags [LA, ND) of the lag sums)
+      auto p_acc = [&](float* acc, const float2 (&w)[L], float2 d) {
+#pragma unroll
+        for (int e = 0; e < L; ++e) {       // (B1, B3) += ar·(dr, di), (B4, B2) += ai·(dr, di): p1, p2 later
+          ffma2s(acc[4 * e], acc[4 * e + 1], w[e].x, d);
+          ffma2s(acc[4 * e + 2], acc[4 * e + 3], w[e].y, d);
+        }
+      };
+      if constexpr (SW) {
+        float acc[Lay::NP];
+        float accl[8 * (LB > 0 ? LB : 1)];
+#pragma unroll
+        for (int i = 0; i < Lay::NP; ++i) acc[i] = 0.f;
+#pragma unroll
+        for (int i = 0; i < 8 * (LB > 0 ? LB : 1); ++i) accl[i] = 0.f;
+#pragma unroll 1
+        for (int g = 0; g < NG; ++g) {
+          float4 F[NW];
+          load_group(g, F);
+          const int q = G0(g) >> 1;
+          const float4 ya = us4[uswz(q)], yb = us4[uswz(q + 1)];
+          const float2 y0[4] = {make_float2(ya.x, ya.y), make_float2(ya.z, ya.w), make_float2(yb.x, yb.y),
+                                make_float2(yb.z, yb.w)};
+#pragma unroll
+          for (int j = 0; j < GS; ++j) {
+            float2 w[L];
+            win(F, j, w);
+            p_acc(acc, w, sl.point(cscale(y0[j], g_agc)));
+            if constexpr (LB > 0) lag_acc(accl, w, LA, LB);
+          }
+        }
+        warp_partials<Lay::NP>(acc, red_w, 0, lane);
+        if constexpr (LB > 0) warp_partials<8 * LB>(accl, red_w, Lay::NP + 8 * LA, lane);
+      } else {
         float acc[Lay::NP];
 #pragma unroll
         for (int i = 0; i < Lay::NP; ++i) acc[i] = 0.f;
 #pragma unroll 2
         for (int s = 0; s < K3_SPT; ++s) {
           float2 w[L];
-          load_window(tid + K3_THREADS * s, w);
-          const float2 d = sl.point(cscale(us[tid + K3_THREADS * s], g));
-#pragma unroll
-          for (int e = 0; e < L; ++e) {       // (B1, B3) += ar·(dr, di), (B4, B2) += ai·(dr, di): p1, p2 later
-            ffma2s(acc[4 * e], acc[4 * e + 1], w[e].x, d);
-            ffma2s(acc[4 * e + 2], acc[4 * e + 3], w[e].y, d);
-          }
+          load_window(KL(s), w);
+          p_acc(acc, w, sl.point(cscale(us[KL(s)], g_agc)));
         }
         warp_partials<Lay::NP>(acc, red_w, 0, lane);
       }
@@ -384,7 +504,7 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
               if (mm < m) {
                 // fp32 edge increments: O(|y|²) terms added to fp64 sums of 4096 such terms
                 const int i = -K + rho + 2 * mm;
-                const float2 a1 = ys[K - 2 - i], a2 = ys[K - 2 - i - d], b1 = ys[8190 + K - i], b2 = ys[8190 + K - i - d];
+                const float2 a1 = ysw(K - 2 - i), a2 = ysw(K - 2 - i - d), b1 = ysw(8190 + K - i), b2 = ysw(8190 + K - i - d);
                 const float i0 = fmaf(a1.x, a2.x, a1.y * a2.y) - fmaf(b1.x, b2.x, b1.y * b2.y);
                 const float i1 = fmaf(a1.x, a2.y, -a1.y * a2.x) - fmaf(b1.x, b2.y, -b1.y * b2.x);
                 const float i2 = fmaf(a1.x, a2.x, -a1.y * a2.y) - fmaf(b1.x, b2.x, -b1.y * b2.y);
@@ -628,27 +748,55 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
           cr[e] = make_float2(tw.x + tv.x, tw.y + tv.y);
           ci[e] = make_float2(tv.y - tw.y, tw.x - tv.x);
         }
-#pragma unroll 2
-        for (int s = 0; s < K3_SPT; ++s) {
-          const int kl = tid + K3_THREADS * s;
-          float2 w[L];
-          load_window(kl, w);
+        auto pass2 = [&](const float2 (&w)[L]) {
           float2 o = make_float2(0.f, 0.f);
 #pragma unroll
           for (int e = 0; e < L; ++e) {         // o += ar·(c1, c3) + ai·(c2, c4)
             ffma2s(o, w[e].x, cr[e]);
             ffma2s(o, w[e].y, ci[e]);
           }
-          us[kl] = o;
           const float2 dd = sl.point(o);        // γ = Σ y¹·conj(D(y¹)) / Σ|D(y¹)|²
           const float2 c = cmulc(o, dd);
           gr += c.x; gi += c.y; gd = fmaf(dd.x, dd.x, fmaf(dd.y, dd.y, gd));
+          return o;
+        };
+        if constexpr (SW) {
+#pragma unroll 1
+          for (int g = 0; g < NG; ++g) {
+            float4 F[NW];
+            load_group(g, F);
+            float2 o[GS];
+#pragma unroll
+            for (int j = 0; j < GS; ++j) {
+              float2 w[L];
+              win(F, j, w);
+              o[j] = pass2(w);
+            }
+            const int q = G0(g) >> 1;
+            us4[uswz(q)] = make_float4(o[0].x, o[0].y, o[1].x, o[1].y);
+            us4[uswz(q + 1)] = make_float4(o[2].x, o[2].y, o[3].x, o[3].y);
+          }
+        } else {
+#pragma unroll 2
+          for (int s = 0; s < K3_SPT; ++s) {
+            const int kl = KL(s);
+            float2 w[L];
+            load_window(kl, w);
+            us[kl] = pass2(w);
+          }
         }
       }
       gr = warp_sum(gr); gi = warp_sum(gi); gd = warp_sum(gd);
       if (lane == 0) { red_w[0] = gr; red_w[1] = gi; red_w[2] = gd; }
       __syncthreads();
       KK_PT(5);
+      // the frame buffer is dead now (every thread is past sweep C): start the next frame's sample copy so that it
+      // overlaps the CPR and the decisions (its labels: already requested (dbl), else at the end of the frame,
+      // after the single label buffer is read)
+      if (tid == 0) {
+        const int nf = fl + (int)gridDim.x;
+        if (nf < n_frames) { issue_y(nf); early = true; }
+      }
       float sc = 1.0f;
       {
         double Gr = 0, Gi = 0, Gd = 0;
@@ -657,84 +805,106 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
         const double ag = sqrt(Gr * Gr + Gi * Gi) / Gd;
         if (ag > 0.0 && isfinite(ag)) sc = (float)(1.0 / ag); else bad = 1;
       }
-      // ---- CPR (R12): products c_k = u_k·conj(D(u_k)), u = y¹/|γ|, into the (now dead) frame buffer
-      float2* cb = ys;
-#pragma unroll 4
-      for (int s = 0; s < K3_SPT; ++s) {
-        const int kl = tid + K3_THREADS * s;
-        const float2 uu = cscale(us[kl], sc);    // (u itself is not stored: the decisions apply sc with the rotation)
-        cb[kl] = cmulc(uu, sl.point(uu));
-      }
-      __syncthreads();
-      // fixed-order sum per 256-symbol block: 16 threads per block, thread j sums entries j, j+16, …
+      // ---- CPR (R12): c_b = Σ_{k∈b} u_k·conj(D(u_k)) with u = sc·y¹; rotation conj(c_b)/|c_b| (none if c_b = 0).
+      //      The warp owns 512 consecutive symbols (two 256-symbol halves, s < 8 and s ≥ 8): W = 256 / 512 windows
+      //      are summed inside the warp (fixed order: s ascending, then lane butterflies); larger windows add
+      //      the warps' sums in warp order through shared memory.
       {
-        const int blk = tid >> 4, j = tid & 15;
-        float cr = 0.f, ci = 0.f;
-#pragma unroll 4
-        for (int q = 0; q < 16; ++q) {
-          const float2 c = cb[256 * blk + j + 16 * q];
+        float cr0 = 0.f, ci0 = 0.f, cr1 = 0.f, ci1 = 0.f;
+        auto prod = [&](float2 y1v, float& cr, float& ci) {
+          const float2 uu = cscale(y1v, sc);
+          const float2 c = cmulc(uu, sl.point(uu));
           cr += c.x; ci += c.y;
+        };
+        if constexpr (SW) {
+          auto grp = [&](int g, float& cr, float& ci) {
+            const int q = G0(g) >> 1;
+            const float4 a = us4[uswz(q)], b = us4[uswz(q + 1)];
+            prod(make_float2(a.x, a.y), cr, ci); prod(make_float2(a.z, a.w), cr, ci);
+            prod(make_float2(b.x, b.y), cr, ci); prod(make_float2(b.z, b.w), cr, ci);
+          };
+#pragma unroll
+          for (int g = 0; g < NG / 2; ++g) grp(g, cr0, ci0);
+#pragma unroll
+          for (int g = NG / 2; g < NG; ++g) grp(g, cr1, ci1);
+        } else {
+#pragma unroll 4
+          for (int s = 0; s < K3_SPT / 2; ++s) prod(us[KL(s)], cr0, ci0);
+#pragma unroll 4
+          for (int s = K3_SPT / 2; s < K3_SPT; ++s) prod(us[KL(s)], cr1, ci1);
         }
 #pragma unroll
-        for (int o = 8; o > 0; o >>= 1) {
-          cr += __shfl_xor_sync(0xffffffffu, cr, o);
-          ci += __shfl_xor_sync(0xffffffffu, ci, o);
+        for (int o = 16; o > 0; o >>= 1) {
+          cr0 += __shfl_xor_sync(0xffffffffu, cr0, o);
+          ci0 += __shfl_xor_sync(0xffffffffu, ci0, o);
+          cr1 += __shfl_xor_sync(0xffffffffu, cr1, o);
+          ci1 += __shfl_xor_sync(0xffffffffu, ci1, o);
         }
-        if (j == 0) {
-          if (p.cpr_window == 256) {                   // window = block: its rotation right here (the window sum
-            const float m2 = cr * cr + ci * ci;          // below would add the single block to 0: same value)
-            const float rs = (m2 > 0.f && isfinite(m2)) ? rsqrtf(m2) : 0.f;
-            const float rsc = rs * sc;                   // z = y¹·(sc·conj(c)/|c|)
-            rot[blk] = (rs > 0.f) ? make_float2(cr * rsc, -ci * rsc) : make_float2(sc, 0.f);
-          } else {
-            red[2 * blk] = cr; red[2 * blk + 1] = ci;
-          }
+        if (p.cpr_window != 256) { cr0 += cr1; ci0 += ci1; }          // the warp's 512 symbols
+        if (p.cpr_window > 512) {                                      // kernel-uniform: windows of W/512 warps
+          float* cw = red + K3_WARPS * NRED - 2 * K3_WARPS;            // (past the γ partials of every warp)
+          if (lane == 0) { cw[2 * warp] = cr0; cw[2 * warp + 1] = ci0; }
+          __syncthreads();
+          const int per = p.cpr_window / 512, w0 = (warp / per) * per;
+          cr0 = 0.f; ci0 = 0.f;
+          for (int q = 0; q < per; ++q) { cr0 += cw[2 * (w0 + q)]; ci0 += cw[2 * (w0 + q) + 1]; }
         }
-      }
-      __syncthreads();
-      // the frame buffer (ys, reused for the CPR products) is dead now: start the next frame's sample copy
-      // so that it overlaps the decisions (its labels: already requested (dbl), else at the end of the frame,
-      // after the single label buffer is read)
-      if (tid == 0) {
-        const int nf = fl + (int)gridDim.x;
-        if (nf < n_frames) { issue_y(nf); early = true; }
-      }
-      if (p.cpr_window != 256) {                       // kernel-uniform
-        if (tid < K3_SPT) {                            // window = (W/256) consecutive blocks, fixed order
-          const int per = p.cpr_window / K3_THREADS;
-          const int w0 = (tid / per) * per;
-          float cr = 0.f, ci = 0.f;
-          for (int q = 0; q < per; ++q) { cr += red[2 * (w0 + q)]; ci += red[2 * (w0 + q) + 1]; }
-          const float m2 = cr * cr + ci * ci;          // rotation conj(c)/|c|; none if c = 0
+        if (p.cpr_window != 256) { cr1 = cr0; ci1 = ci0; }
+        auto rotation = [&](float cr, float ci) {                      // z = y¹·(sc·conj(c)/|c|)
+          const float m2 = cr * cr + ci * ci;
           const float rs = (m2 > 0.f && isfinite(m2)) ? rsqrtf(m2) : 0.f;
           const float rsc = rs * sc;
-          rot[tid] = (rs > 0.f) ? make_float2(cr * rsc, -ci * rsc) : make_float2(sc, 0.f);
-        }
-        __syncthreads();
+          return (rs > 0.f) ? make_float2(cr * rsc, -ci * rsc) : make_float2(sc, 0.f);
+        };
+        rA = rotation(cr0, ci0);
+        rB = rotation(cr1, ci1);
       }
       KK_PT(6);
       }  // p0ok
     }
 
-    // ---- decisions, counts, outputs: z = u·e^{−iϑ_b} (dead or silent frame: z = 0)
+    // ---- decisions, counts, outputs: z = u·e^{−iϑ_b} (dead or silent frame: z = 0); rotation rA for the warp's
+    //      first 256 symbols (s < 8), rB for the second
     int serr = 0, berr = 0;
-    if (!zero && !sl.cross && ref_tma && dec && !zout) {
-      // the common case as its own loop (square/rectangular slicer, labels from shared memory, no z output):
-      // no per-symbol tests of runtime-uniform flags
-#pragma unroll 4
-      for (int s = 0; s < K3_SPT; ++s) {
-        const int kl = tid + K3_THREADS * s;
-        const int lab = sl.label_sq(cmul(us[kl], rot[s]));
-        const int r = (int)ref_cur[kl];
-        serr += (lab != r);
-        berr += __popc(lab ^ r);
-        dec[sym0 + kl] = (uint8_t)lab;
+    if (SW && !zero && !sl.cross && ref_tma && dec && ((reinterpret_cast<uintptr_t>(dec) & 3) == 0) && !zout) {
+      // the common case (square/rectangular slicer, labels from shared memory, no z output): a lane's 4 consecutive
+      // symbols — one 16-B pair of us loads, one 32-bit label word, one 32-bit decision store per group
+#pragma unroll 2
+      for (int g = 0; g < NG; ++g) {
+        const int kl = G0(g);
+        const float2 r = (g < NG / 2) ? rA : rB;
+        const int q = kl >> 1;
+        const float4 a = us4[uswz(q)], b = us4[uswz(q + 1)];
+        const uint32_t rw = *reinterpret_cast<const uint32_t*>(ref_cur + kl);
+        const uint32_t l0 = (uint32_t)sl.label_sq(cmul(make_float2(a.x, a.y), r));
+        const uint32_t l1 = (uint32_t)sl.label_sq(cmul(make_float2(a.z, a.w), r));
+        const uint32_t l2 = (uint32_t)sl.label_sq(cmul(make_float2(b.x, b.y), r));
+        const uint32_t l3 = (uint32_t)sl.label_sq(cmul(make_float2(b.z, b.w), r));
+        const uint32_t lw = l0 | (l1 << 8) | (l2 << 16) | (l3 << 24);
+        // per-byte compares: symbol errors = nonzero bytes of lw ^ rw, bit errors = popc(lw ^ rw)
+        const uint32_t x = lw ^ rw;
+        serr += __popc(__vcmpne4(x, 0u)) >> 3;
+        berr += __popc(x);
+        *reinterpret_cast<uint32_t*>(dec + sym0 + kl) = lw;
       }
+    } else if (!SW && !zero && !sl.cross && ref_tma && dec && !zout) {
+      auto fast = [&](int s, float2 r) {
+        const int kl = KL(s);
+        const int lab = sl.label_sq(cmul(us[kl], r));
+        const int rr = (int)ref_cur[kl];
+        serr += (lab != rr);
+        berr += __popc(lab ^ rr);
+        dec[sym0 + kl] = (uint8_t)lab;
+      };
+#pragma unroll 4
+      for (int s = 0; s < K3_SPT / 2; ++s) fast(s, rA);
+#pragma unroll 4
+      for (int s = K3_SPT / 2; s < K3_SPT; ++s) fast(s, rB);
     } else {
 #pragma unroll 4
       for (int s = 0; s < K3_SPT; ++s) {
-        const int kl = tid + K3_THREADS * s;
-        const float2 zz = zero ? make_float2(0.f, 0.f) : cmul(us[kl], rot[s]);
+        const int kl = SW ? G0(s / GS) + (s % GS) : KL(s);
+        const float2 zz = zero ? make_float2(0.f, 0.f) : cmul(SW ? uget(kl) : us[kl], s < K3_SPT / 2 ? rA : rB);
         const int lab = sl.label(zz);
         if (ref) {
           const int r = ref_tma ? (int)ref_cur[kl] : (int)__ldg(&ref[sym0 + kl]);
@@ -789,13 +959,42 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
 template <int K>
 static void launch_k3_t(const float2* y, int64_t frame0, int64_t n_frames, const float2* w_cd, const int* clampcnt,
                         int64_t clamp_frame_off, const uint8_t* ref, uint8_t* dec, float2* z,
-                        unsigned long long* counters, const K3Params& p, int num_sms, cudaStream_t s) {
+                        unsigned long long* counters, const K3Params& p, const CUtensorMap* ymaps, int num_sms,
+                        cudaStream_t s) {
   constexpr int smem = K3Layout<K>::TOTAL;
   cudaFuncSetAttribute(k3_eq_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   int64_t grid = (int64_t)num_sms * 2;
   if (grid > n_frames) grid = n_frames;
   k3_eq_kernel<K><<<(unsigned)grid, K3_THREADS, smem, s>>>(y, frame0, (int)n_frames, w_cd, clampcnt,
-                                                           clamp_frame_off, ref, dec, z, counters, p);
+                                                           clamp_frame_off, ref, dec, z, counters, p, ymaps[0],
+                                                           ymaps[1]);
+}
+
+// Tensor maps of the 2-sps buffer y (n_float2 entries) for the swizzled K ≤ 4 frame loads: a 2-D view of
+// 64-B rows (8 float2 as 8-byte elements), boxes of 128 rows (map 0) and 8 rows (map 1), SWIZZLE_64B, OOB rows
+// zero-filled. Returns false if the driver entry point is unavailable or the encode fails.
+bool k3_encode_ymaps(const float2* y, int64_t n_float2, CUtensorMap* maps) {
+  static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+  if (!enc) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+      return false;
+    enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  const cuuint64_t dims[2] = {8, (cuuint64_t)((n_float2 + 7) / 8)};
+  const cuuint64_t strides[1] = {64};
+  const cuuint32_t estr[2] = {1, 1};
+  const cuuint32_t rows[2] = {128, 8};
+  for (int i = 0; i < 2; ++i) {
+    const cuuint32_t box[2] = {8, rows[i]};
+    if (enc(&maps[i], CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, const_cast<float2*>(y), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return false;
+  }
+  return true;
 }
 
 size_t k3_smem_bytes(int K) {
@@ -813,8 +1012,8 @@ size_t k3_smem_bytes(int K) {
 
 void launch_k3(const float2* y, int64_t frame0, int64_t n_frames, int K, const float2* w_cd, const int* clampcnt,
                int64_t clamp_frame_off, const uint8_t* ref, uint8_t* dec, float2* z, unsigned long long* counters,
-               const K3Params& p, int num_sms, cudaStream_t s) {
-#define KK_K3(KV) case KV: launch_k3_t<KV>(y, frame0, n_frames, w_cd, clampcnt, clamp_frame_off, ref, dec, z, counters, p, num_sms, s); break;
+               const K3Params& p, const CUtensorMap* ymaps, int num_sms, cudaStream_t s) {
+#define KK_K3(KV) case KV: launch_k3_t<KV>(y, frame0, n_frames, w_cd, clampcnt, clamp_frame_off, ref, dec, z, counters, p, ymaps, num_sms, s); break;
   switch (K) {
     KK_K3(1) KK_K3(2) KK_K3(3) KK_K3(4) KK_K3(5) KK_K3(6) KK_K3(7)
     default: break;

@@ -67,6 +67,7 @@ struct kk_ctx {
   float2* d_part = nullptr;
   int* d_clamp = nullptr;
   float2* d_y = nullptr;
+  CUtensorMap ymaps[2];   // K3's tensor-TMA views of d_y (K ≤ 4)
   float2* d_z = nullptr;
   float* d_segpow = nullptr;     // DDLMS mode: K2's per-64-symbol power sums (K3′ AGC)
   unsigned long long* d_counters = nullptr;
@@ -550,6 +551,7 @@ kk_status kk_init(const kk_config* cfg, kk_ctx** out) {
   chk(dalloc(c, "part", &c->d_part, (size_t)(nE / kk::kHilbertHop) * sizeof(float2)));
   chk(dalloc(c, "clamp", &c->d_clamp, (size_t)(nE / kk::kHilbertHop) * sizeof(int)));
   chk(dalloc(c, "y", &c->d_y, (size_t)(n / 2 + 2 * c->Ky + 2) * sizeof(float2)));
+  if (c->d_y && !kk::k3_encode_ymaps(c->d_y, n / 2 + 2 * c->Ky + 2, c->ymaps) && e == cudaSuccess) e = cudaErrorNotSupported;
   if (cfg->keep_intermediate) chk(dalloc(c, "z", &c->d_z, (size_t)(n / 4) * sizeof(float2)));
   if (ddlms) chk(dalloc(c, "segpow", &c->d_segpow, (size_t)((n / 2 + 2 * c->Ky) / 512 + 2 * (c->mfKeep / 512) + 16) * sizeof(float)));
   chk(dalloc(c, "counters", &c->d_counters, 32 * sizeof(unsigned long long)));
@@ -708,7 +710,7 @@ kk_status kk_process_frames_ex(kk_ctx* c, const void* d_adc, int64_t first, int6
   } else {
     NvtxRange r3_("kk::K3 block-LS EQ + CPR + decisions");
     kk::launch_k3(c->d_y, first / F, nfr, c->K, c->d_wcd, c->d_clamp, (int64_t)F / kk::kHilbertHop /*skip frame −1*/,
-                  d_ref, d_dec, cf.keep_intermediate ? c->d_z : nullptr, c->d_counters, p3, c->num_sms, s);
+                  d_ref, d_dec, cf.keep_intermediate ? c->d_z : nullptr, c->d_counters, p3, c->ymaps, c->num_sms, s);
   }
   if (c->timing) {
     cudaEventRecord(tev[3], s);

@@ -12,7 +12,7 @@ import os
 from ctypes import POINTER, c_char_p, c_double, c_float, c_int, c_int32, c_int64, c_size_t, c_uint8, c_uint32, c_uint64, c_void_p
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libkkrx.so")
+LIB_PATH = os.environ.get("KK_LIB", os.path.join(HERE, "libkkrx.so"))   # KK_LIB: A/B experiments only
 
 KK_OK, KK_ERR_CONFIG, KK_ERR_ALIGN, KK_ERR_SHORT, KK_ERR_NULL = 0, -1, -2, -3, -4
 KK_ERR_NOMEM, KK_ERR_CUDA, KK_ERR_DOMAIN, KK_ERR_STATE = -5, -6, -7, -8
