@@ -266,13 +266,18 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
   // at the same lane-relative offsets for every g (32·GS·g float4 is a multiple of 4 rows of 128 B)
   auto swz = [](int i) { return SW ? (i ^ ((i >> 3) & 3)) : i; };
   auto ysw = [&](int e) -> float2 { const int q = e >> 1; return ys[2 * swz(q) + (e & 1)]; };   // sample e
-  int woff[NW];
+  // shared-memory byte address of the lane's window float4 t in group 0 (formed at the start of each sweep, so
+  // that it is not live across the solve); group g adds 512·GS·g bytes
+  auto make_wadr = [&](uint32_t (&wadr)[NW]) {
 #pragma unroll
-  for (int t = 0; t < NW; ++t) woff[t] = swz(GS * lane + t) - GS * lane;
-  auto load_group = [&](int g, float4 (&F)[NW]) {
-    const float4* b = ys4 + G0(g);
+    for (int t = 0; t < NW; ++t) wadr[t] = smem_u32(ys4 + 512 * warp + swz(GS * lane + t));
+  };
+  auto load_group = [&](const uint32_t (&wadr)[NW], int g, float4 (&F)[NW]) {
+    const uint32_t go = (uint32_t)(512 * GS * g);
 #pragma unroll
-    for (int t = 0; t < NW; ++t) F[t] = b[woff[t]];
+    for (int t = 0; t < NW; ++t)
+      asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                   : "=f"(F[t].x), "=f"(F[t].y), "=f"(F[t].z), "=f"(F[t].w) : "r"(wadr[t] + go));
   };
   // window of the group's symbol j from the group's float4 (compile-time indices after unrolling)
   auto win = [&](const float4 (&F)[NW], int j, float2 (&w)[L]) {
@@ -353,13 +358,10 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
           }
         }
       };
-      auto pass1 = [&](const float2 (&w)[L]) {   // w_cd·a = ar·(wr, wi) + ai·(−wi, wr)
+      auto pass1 = [&](const float2 (&w)[L]) {   // w_cd·a = wr·a + wi·(i·a), the cmul form (taps stay scalars)
         float2 y0 = make_float2(0.f, 0.f);
 #pragma unroll
-        for (int e = 0; e < L; ++e) {
-          ffma2s(y0, w[e].x, wc[e]);
-          ffma2s(y0, w[e].y, make_float2(-wc[e].y, wc[e].x));
-        }
+        for (int e = 0; e < L; ++e) cmac2(y0, w[e], wc[e]);
         return y0;
       };
       if constexpr (SW) {
@@ -367,10 +369,12 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
 #pragma unroll
         for (int i = 0; i < 8 * LA; ++i) acc[i] = 0.f;
         float pw = 0.f;
+uint32_t wadr[NW];
+        make_wadr(wadr);
 #pragma unroll 1
         for (int g = 0; g < NG; ++g) {
           float4 F[NW];
-          load_group(g, F);
+          load_group(wadr, g, F);
           float2 y0[GS];
 #pragma unroll
           for (int j = 0; j < GS; ++j) {
@@ -444,10 +448,12 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
         for (int i = 0; i < Lay::NP; ++i) acc[i] = 0.f;
 #pragma unroll
         for (int i = 0; i < 8 * (LB > 0 ? LB : 1); ++i) accl[i] = 0.f;
+uint32_t wadr[NW];
+        make_wadr(wadr);
 #pragma unroll 1
         for (int g = 0; g < NG; ++g) {
           float4 F[NW];
-          load_group(g, F);
+          load_group(wadr, g, F);
           const int q = G0(g) >> 1;
           const float4 ya = us4[uswz(q)], yb = us4[uswz(q + 1)];
           const float2 y0[4] = {make_float2(ya.x, ya.y), make_float2(ya.z, ya.w), make_float2(yb.x, yb.y),
@@ -761,10 +767,12 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
           return o;
         };
         if constexpr (SW) {
+uint32_t wadr[NW];
+          make_wadr(wadr);
 #pragma unroll 1
           for (int g = 0; g < NG; ++g) {
             float4 F[NW];
-            load_group(g, F);
+            load_group(wadr, g, F);
             float2 o[GS];
 #pragma unroll
             for (int j = 0; j < GS; ++j) {

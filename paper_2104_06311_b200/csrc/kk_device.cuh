@@ -53,6 +53,14 @@ __device__ __forceinline__ float2 cmulc(float2 a, float2 b) {
       : "=f"(r.x), "=f"(r.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(-b.y));
   return r;
 }
+// acc += a·b in the cmul form (FFMA2 + FFMA2): acc += b.x·a + b.y·(i·a) — the swap and the half-negation fold into
+// FFMA2 operand modifiers, so a tap b held as two scalars (e.g. uniform registers) needs no register pair
+__device__ __forceinline__ void cmac2(float2& acc, float2 a, float2 b) {
+  asm("{\n\t.reg .b64 pa, ps, pc, pn, pr;\n\tmov.b64 pa, {%2, %3};\n\tmov.b64 ps, {%3, %2};\n\t"
+      "mov.b64 pc, {%4, %4};\n\tmov.b64 pn, {%5, %6};\n\tmov.b64 pr, {%0, %1};\n\t"
+      "fma.rn.f32x2 pr, pa, pc, pr;\n\tfma.rn.f32x2 pr, ps, pn, pr;\n\tmov.b64 {%0, %1}, pr;\n\t}"
+      : "+f"(acc.x), "+f"(acc.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(-b.y), "f"(b.y));
+}
 __device__ __forceinline__ float2 cconj(float2 a) { return make_float2(a.x, -a.y); }
 // 2^x by one MUFU.EX2 (flush-to-zero; the same instruction __expf issues after its ×log2 e)
 __device__ __forceinline__ float ex2_approx(float x) {
