@@ -607,7 +607,7 @@ def main():
             "clocks": clk.summary(),
             "e2e": e2e,
             "e2e_uint8": e2e_u8,
-            "gpu_launches": 3 * calls_per_step * a.steps,
+            "gpu_launches": (3 if a.eq_mode == "ddlms" else 5) * calls_per_step * a.steps,
             "roofline": roofline,
             "kernels": kernels,
             "cpu_baseline": cpu,

@@ -15,6 +15,18 @@
 //   (5) per window b: c_b = Σ u·conj(D(u)),  z = u·conj(c_b)/|c_b|           (CPR: e^{−i·arg c_b})
 //   (6) label = D(z); counts vs reference labels.
 //
+// Three launches per call ("the batched per-frame equalizer", BASELINE north_star):
+//   K3a k3a_kernel  — steps (1)–(3)'s sums: persistent CTAs (2 per SM), one frame at a time: sweep A (lag sums,
+//                     pass 1, power), AGC, sweep B (training decisions, p, remaining lags), fixed-order fp64
+//                     reduction → one record per frame (the sums, g, flags) in global memory;
+//   K3s k3s_kernel  — step (3)'s solve for every frame at once: one small CTA per frame assembles the real system
+//                     from the sums and the frame's edge samples and eliminates it (fp64 Gauss–Jordan) → θ₁;
+//                     thousands of independent solves in flight hide their serial latency (inside K3a/K3c they
+//                     idled the CTA: the solve phase cost 11 % of the former single kernel);
+//   K3c k3c_kernel  — steps (4)–(6): persistent CTAs, θ₁ arrives by TMA with the frame: sweep C (pass 2, unbias
+//                     sums), CPR, decisions, counters.
+// The frame is loaded twice (K3a and K3c): 64 KiB per frame from HBM each time, far below K3's compute time.
+//
 // Structure used (exact identities):
 //  * R from lag sums: with a_j = y[2k − j],  S(i,d) = Σ_k conj(a_i)·a_{i+d},  T(i,d) = Σ_k a_i·a_{i+d}.
 //    Only the bases i = −K, −K+1 are accumulated (4L complex MACs per symbol); every other S(i,d), T(i,d)
@@ -24,19 +36,14 @@
 //    (G + λ/2·I)m_r = q_r + λ/2·m_r0 (r = 1, 2; G = Σ x xᵀ, q_1 = Σ x·Re d, q_2 = Σ x·Im d) with
 //    m_1 = [w_r + v_r; v_i − w_i], m_2 = [w_i + v_i; w_r − v_r]. G and q are read off S, T and p.
 //    Linear-only mode solves the real 2L form [[Re R, −Im R],[Im R, Re R]] of the Hermitian system.
-//    Both are solved in fp64 by one warp (Gauss–Jordan on the 2L × (2L + 2) augmented matrix in
-//    shared memory, no pivoting on an SPD matrix; failure ⇒ fall back to θ₀ and count a bad frame).
+//    Both are solved in fp64 (Gauss–Jordan with 2×2 pivots, no pivoting on an SPD matrix; failure ⇒ fall back
+//    to θ₀ and count a bad frame).
 //
-// Mapping: persistent CTAs (256 threads, 2 per SM), one frame at a time; thread t owns symbols t + 256·s
-// (s < 16). Each frame's 2-sps samples (64 KiB) and reference labels (4 KiB) arrive by one TMA bulk copy
-// (cp.async.bulk + mbarrier) from L2, where the CTA prefetched them (cp.async.bulk.prefetch.L2) while it was
-// working on its previous frame. A symbol's tap window y_s[2kl .. 2kl + 2K] is K+1 16-byte shared loads
-// (each warp load a contiguous 512-B access, conflict-free) with compile-time offsets (K is a template
-// parameter); every sweep does all of a symbol's MACs from registers. Sweeps: (A) lag sums + frame power,
-// (B) decisions + p, (C) pass 2 → y¹ per symbol in shared memory, then unbias, CPR and the decisions in
-// short loops (the kernel's instruction footprint is kept small: it runs once per frame).
-// Reductions: in-warp transpose-reduce (31 shuffles per 32 values), then fp64 over the 8 warps in fixed
-// order (deterministic).
+// Mapping (K3a, K3c): 256 threads per frame; warp w owns symbols [512w, 512w + 512). K ≤ 4: each lane works on
+// groups of 4 consecutive symbols, the frame's 2-sps samples (64 KiB) arriving by 2-D tensor TMA with the 64-B
+// swizzle (a group's K + 4 16-byte window pairs serve its 4 symbols; conflict-free); K ≥ 5: one symbol at a time
+// from a plain bulk copy. Reductions: in-warp transpose-reduce (31 shuffles per 32 values), then fp64 over the
+// 8 warps in fixed order (deterministic).
 #include "kk_device.cuh"
 #include "kk_params.h"
 
@@ -174,18 +181,22 @@ __device__ __forceinline__ void tma_tensor_2d(void* dst_smem, const CUtensorMap*
       : "memory");
 }
 
-#ifdef KK_PHASE_TIMING   // debug: per-phase SM clocks of CTA 0 (tools/k3_phases.py), printed at kernel exit
-#define KK_PT(i) do { if (tid == 0 && blockIdx.x == 0) { const long long c_ = clock64(); pt_[i] += c_ - pt_last_; pt_last_ = c_; } } while (0)
-#else
 #define KK_PT(i) do { } while (0)
-#endif
 
-template <int K>
+// per-frame records between the launches: K3a → K3s: the fp64 sums (NRED), g, flags; K3s → K3c: θ₁ (w, v), flags
+template <int K> struct K3Rec {
+  static constexpr int REC = K3Layout<K>::NRED + 2;   // doubles: [0, NRED) sums, [NRED] g, [NRED + 1] flags
+  static constexpr int TREC = 2 * K3Layout<K>::L + 2; // float2: [0, L) w, [L, 2L) v, [2L].x = flags (int bits)
+};
+constexpr int kFlagDead = 1, kFlagSilent = 2, kFlagFail = 4;
+
+template <int K, int PH>
 __global__ void __launch_bounds__(K3_THREADS, 2)
-k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const float2* __restrict__ w_cd,
-             const int* __restrict__ clampcnt, int64_t clamp_frame_off, const uint8_t* __restrict__ ref,
-             uint8_t* __restrict__ dec, float2* __restrict__ zout, unsigned long long* __restrict__ counters,
-             K3Params p, const __grid_constant__ CUtensorMap ymap, const __grid_constant__ CUtensorMap ymap_tail) {
+k3_frame_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const float2* __restrict__ w_cd,
+                const int* __restrict__ clampcnt, int64_t clamp_frame_off, const uint8_t* __restrict__ ref,
+                uint8_t* __restrict__ dec, float2* __restrict__ zout, unsigned long long* __restrict__ counters,
+                K3Params p, double* __restrict__ rec, const float2* __restrict__ threc,
+                const __grid_constant__ CUtensorMap ymap, const __grid_constant__ CUtensorMap ymap_tail) {
   using Lay = K3Layout<K>;
   constexpr int L = Lay::L, ND = Lay::ND, N = Lay::N, NRED = Lay::NRED;
   constexpr bool SW = Lay::SW;
@@ -206,7 +217,8 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const bool wl = p.widely_linear != 0;
   float* red_w = red + warp * NRED;
-  const bool ref_tma = ref && ((reinterpret_cast<uintptr_t>(ref) & 15) == 0);
+  const bool ref_tma = (PH == 1) && ref && ((reinterpret_cast<uintptr_t>(ref) & 15) == 0);
+  constexpr uint32_t TBYTES = (PH == 1) ? (uint32_t)(K3Rec<K>::TREC * 8) : 0u;   // θ record (K3c)
   // double-buffered labels: frame `it` of this CTA reads buffer it & 1; the next frame's labels are requested
   // as soon as this frame's copies have landed (its own buffer was last read before the previous frame's
   // closing barrier), so the frame start no longer waits for a label copy issued at the end of the frame
@@ -219,7 +231,7 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
   // arrival comes with the first copy of the frame: the samples' (single label buffer) or the labels' (dbl).
   auto issue_y = [&](int fl) {
     fence_proxy_async_smem();                     // the frame buffer was written by generic stores (CPR products)
-    if (!dbl) mbar_arrive_expect_tx(bar, YBYTES + 128u + (ref_tma ? (uint32_t)kFrameSym : 0u));
+    if (!dbl) mbar_arrive_expect_tx(bar, YBYTES + 128u + TBYTES + (ref_tma ? (uint32_t)kFrameSym : 0u));
     if constexpr (SW) {                           // 8 boxes of 128 rows + one of 8 rows (64-B rows of 8 float2)
 #pragma unroll
       for (int b = 0; b < 8; ++b) tma_tensor_2d(smem + Lay::Y + b * 8192, &ymap, 0, fl * 1024 + 128 * b, bar);
@@ -228,11 +240,12 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
       tma_bulk_g2s(ys, y + (int64_t)fl * (2 * kFrameSym), YBYTES, bar);
     }
     tma_bulk_g2s(smem + Lay::CC, clampcnt + clamp_frame_off + (int64_t)fl * 32, 128u, bar);
+    if constexpr (PH == 1) tma_bulk_g2s(th, threc + (int64_t)fl * K3Rec<K>::TREC, TBYTES, bar);
   };
   auto issue_ref = [&](int fl, int b) {
     if (!ref_tma) return;
     fence_proxy_async_smem();
-    if (dbl) mbar_arrive_expect_tx(bar, YBYTES + 128u + (uint32_t)kFrameSym);
+    if (dbl) mbar_arrive_expect_tx(bar, YBYTES + 128u + TBYTES + (uint32_t)kFrameSym);
     tma_bulk_g2s(ref_buf(b), ref + (int64_t)fl * kFrameSym, kFrameSym, bar);
   };
   auto prefetch = [&](int fl) {
@@ -301,9 +314,6 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
     }
   };
 
-#ifdef KK_PHASE_TIMING
-  long long pt_[13] = {}, pt_last_ = clock64();
-#endif
   int it = 0;
   for (int fl = blockIdx.x; fl < n_frames; fl += gridDim.x, ++it) {
     bool early = false;                                // thread 0: next frame's samples already requested
@@ -319,7 +329,6 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
     // the previous frame's closing barrier already ordered misc[] (the QAM order) and every read of the buffers;
     // the TMA data is visible through the mbarrier — only the CTA's first frame needs a barrier here
     if (it == 0) __syncthreads();
-    KK_PT(0);
     const int M = misc[2];
     const int bi = (M == 4) ? 0 : (M == 8) ? 1 : (M == 16) ? 2 : (M == 32) ? 3 : 4;
     Slicer sl;
@@ -332,11 +341,11 @@ k3_eq_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, const f
     const int fn = fl + (int)gridDim.x;
     const int m_next = (tid == 32 && fn < n_frames) ? frame_order(frame0 + fn) : 0;
     const bool dead = (ccount >= kFrameSamp);
-
-    int bad = 0;
-    bool zero = dead;                    // z = 0, decisions D(0): dead frame, or no signal power (silent)
-    float2 rA = make_float2(0.f, 0.f), rB = make_float2(0.f, 0.f);   // CPR rotations (× unbias) of the warp's halves
-    if (!dead) {
+    if constexpr (PH == 0) {
+      // ======== K3a: sums of steps (1)–(3) → the frame's record
+      int flags = dead ? kFlagDead : 0;
+      double* rg = rec + (int64_t)fl * K3Rec<K>::REC;
+      if (!dead) {
       // ---- sweep A: lag sums for bases ρ = 0 (i = −K, w[0]) and ρ = 1 (i = −K+1, w[1]) + pass-1 power
       //      S_ρ(d) = Σ conj(w[ρ])·w[ρ + d],  T_ρ(d) = Σ w[ρ]·w[ρ + d];  y⁰ = Σ_e w_cd[e]·w[e]
       //      conj(a)·b and a·b share the four real products: accumulate Σ ar·br, Σ ai·bi, Σ ar·bi, Σ ai·br
@@ -419,7 +428,6 @@ uint32_t wadr[NW];
       }
       }
       __syncthreads();
-      KK_PT(1);
       double P0 = 0.0;
 #pragma unroll
       for (int w8 = 0; w8 < K3_WARPS; ++w8) P0 += (double)red[w8 * NRED + Lay::IPOW];
@@ -427,11 +435,9 @@ uint32_t wadr[NW];
       // AGC (R25). A frame without signal power (P0 ≤ p0_min = 1e-20·I_ref, or not finite: e.g. the tone
       // without modulation) cannot be trained: it is a bad frame with z = 0 and decisions D(0)
       const bool p0ok = (P0 > (double)p.p0_min) && isfinite(P0);
-      if (!p0ok) { bad = 1; zero = true; }
+      const float g_agc = p0ok ? (float)(1.0 / sqrt(P0)) : 1.0f;
+      if (!p0ok) flags |= kFlagSilent;
       if (p0ok) {
-      const float g_agc = (float)(1.0 / sqrt(P0));
-      const float g = g_agc;
-
       // ---- sweep B: decisions on g·y⁰ and p1[e] = Σ conj(a_j)·d, p2[e] = Σ a_j·d  (a_j = w[e]);
       //      (SW: plus the lags [LA, ND) of the lag sums)
       auto p_acc = [&](float* acc, const float2 (&w)[L], float2 d) {
@@ -480,269 +486,33 @@ uint32_t wadr[NW];
         }
         warp_partials<Lay::NP>(acc, red_w, 0, lane);
       }
-      __syncthreads();
-      KK_PT(2);
-      cross_warp_sum(red, dres, NRED, NRED, tid);   // fp64, fixed order
-      __syncthreads();
-      KK_PT(3);
-
-      // ---- solve: the CTA assembles the real system from S, T (one thread per chain point), warp 0 adds the
-      //      ridge and the right-hand sides; Gauss–Jordan by warp 0 (N ≤ kGJWarpN) or the CTA.
-      //      Chain (ρ, d) holds S(i, i+d), T(i, i+d) at i = −K+ρ+2m (m < npts), linked by the exact sliding
-      //      recurrence S(i+2, d) = S(i, d) + inc_m with edge samples y[2(k0−1) − i] ↔ y_s[K − 2 − i] and
-      //      y[2(k1−1) − i] ↔ y_s[8190 + K − i]. Thread (chain, m) forms the sum of the chain's first m increments
-      //      itself — the additions of a serial walk, in its order — so no point waits for another. The d = 0
-      //      points leave their diagonal's contribution to tr(G) (WL: rr + ii = Re S; linear: 2·Re S) in tl[].
-      double* tl = reinterpret_cast<double*>(th);   // 2(K+1) trace terms (th is written only after the solve)
-      {
-        double* A = mat;   // row-major N × WS: [G + λI | q1 q2]
-        constexpr int W = Lay::WS;
-        const int c = tid / (K + 1), m = tid % (K + 1);
-        if (c < 2 * ND - 1) {
-          const int rho = c / ND, d = c % ND;
-          const int npts = (2 * K - d - rho) / 2 + 1;  // chain points
-          if (m < npts) {
-            const double A1 = dres[Lay::NP + 8 * d + 4 * rho], A3 = dres[Lay::NP + 8 * d + 4 * rho + 1];
-            const double A4 = dres[Lay::NP + 8 * d + 4 * rho + 2], A2 = dres[Lay::NP + 8 * d + 4 * rho + 3];
-            double sr = A1 + A2, si = A3 - A4, tr_ = A1 - A2, ti = A3 + A4;   // S = Σ conj(a)·b, T = Σ a·b
+      }
+      __syncthreads();   // every read of the frame buffer is done: request the next frame now
+      if (tid == 0 && fn < n_frames) { issue_y(fn); early = true; }
+      if (p0ok) {        // fp64 sums over the 8 warp partials, fixed order → the record
+        for (int v = tid; v < NRED; v += K3_THREADS) {
+          double s = 0.0;
 #pragma unroll
-            for (int mm = 0; mm < K; ++mm) {
-              if (mm < m) {
-                // fp32 edge increments: O(|y|²) terms added to fp64 sums of 4096 such terms
-                const int i = -K + rho + 2 * mm;
-                const float2 a1 = ysw(K - 2 - i), a2 = ysw(K - 2 - i - d), b1 = ysw(8190 + K - i), b2 = ysw(8190 + K - i - d);
-                const float i0 = fmaf(a1.x, a2.x, a1.y * a2.y) - fmaf(b1.x, b2.x, b1.y * b2.y);
-                const float i1 = fmaf(a1.x, a2.y, -a1.y * a2.x) - fmaf(b1.x, b2.y, -b1.y * b2.x);
-                const float i2 = fmaf(a1.x, a2.x, -a1.y * a2.y) - fmaf(b1.x, b2.x, -b1.y * b2.y);
-                const float i3 = fmaf(a1.x, a2.y, a1.y * a2.x) - fmaf(b1.x, b2.y, b1.y * b2.x);
-                sr += (double)i0; si += (double)i1; tr_ += (double)i2; ti += (double)i3;
-              }
-            }
-            const int i = -K + rho + 2 * m;
-            const int r = i + K, q = i + d + K;     // S(r, q) = Σ conj(a_r)·a_q, T(r, q) = Σ a_r·a_q
-            if (wl) {
-              // G = [[Σ ar arᵀ, Σ ar aiᵀ], [Σ ai arᵀ, Σ ai aiᵀ]] from S and T (both orders of (r, q))
-              const double rr = 0.5 * (sr + tr_), ii = 0.5 * (sr - tr_);
-              const double ri = 0.5 * (si + ti), ir = 0.5 * (ti - si);   // Σ ar_r·ai_q, Σ ai_r·ar_q
-              A[r * W + q] = rr;             A[q * W + r] = rr;
-              A[(L + r) * W + (L + q)] = ii; A[(L + q) * W + (L + r)] = ii;
-              A[r * W + (L + q)] = ri;       A[(L + q) * W + r] = ri;
-              A[(L + r) * W + q] = ir;       A[q * W + (L + r)] = ir;
-              if (d == 0) tl[rho * (K + 1) + m] = rr + ii;
-            } else {
-              // real form of the Hermitian R11: [[Re R, −Im R], [Im R, Re R]], R[r][q] = S, R[q][r] = conj(S)
-              A[r * W + q] = sr;             A[q * W + r] = sr;
-              A[(L + r) * W + (L + q)] = sr; A[(L + q) * W + (L + r)] = sr;
-              A[(L + r) * W + q] = si;       A[(L + q) * W + r] = -si;
-              A[r * W + (L + q)] = -si;      A[q * W + (L + r)] = si;
-              if (d == 0) tl[rho * (K + 1) + m] = sr + sr;
-            }
-          }
+          for (int w8 = 0; w8 < K3_WARPS; ++w8) s += (double)red[w8 * NRED + v];
+          rg[v] = s;
         }
       }
-      __syncthreads();
-      KK_PT(8);
-      int fail = 0;
-      if (warp == 0) {
-        double* A = mat;
-        constexpr int W = Lay::WS;
-        // ridge (R10): λ_c = ridge·tr(R)/n_c. WL: real form uses λ_c/2 and tr(R) = 2·tr(G). Linear: tr(M) = 2·tr(R11)
-        // tr(G): the d = 0 terms in chain order (ρ = 0: K + 1 points, ρ = 1: K points)
-        double t0 = 0.0, t1 = 0.0;
-#pragma unroll
-        for (int m = 0; m <= K; ++m) t0 += tl[m];
-#pragma unroll
-        for (int m = 0; m < K; ++m) t1 += tl[K + 1 + m];
-        const double trG = t0 + t1;
-        KK_PT(9);
-        // (the factor ridge/n_c does not wait for the trace)
-        const double lam = trG * (wl ? (double)p.ridge / (double)N : (double)p.ridge * 0.5 / (double)L);
-        if (lane < L) {
-          const int e = lane;
-          const double B1 = dres[4 * e], B3 = dres[4 * e + 1], B4 = dres[4 * e + 2], B2 = dres[4 * e + 3];
-          const double p1r = B1 + B2, p1i = B3 - B4, p2r = B1 - B2, p2i = B3 + B4;   // p1 = Σ conj(a)·d, p2 = Σ a·d
-          const float2 w0 = __ldg(&w_cd[e]);
-          const double w0r = (double)g * (double)w0.x, w0i = (double)g * (double)w0.y;
-          if (wl) {
-            // q1 = [Σ ar·dr; Σ ai·dr], q2 = [Σ ar·di; Σ ai·di];  m1₀ = [w0r; −w0i], m2₀ = [w0i; w0r]
-            A[e * W + N] = 0.5 * (p1r + p2r) + lam * w0r;
-            A[(L + e) * W + N] = 0.5 * (p2i - p1i) - lam * w0i;
-            A[e * W + N + 1] = 0.5 * (p1i + p2i) + lam * w0i;
-            A[(L + e) * W + N + 1] = 0.5 * (p1r - p2r) + lam * w0r;
-          } else {
-            A[e * W + N] = p1r + lam * w0r;
-            A[(L + e) * W + N] = p1i + lam * w0i;
-            A[e * W + N + 1] = 0.0;
-            A[(L + e) * W + N + 1] = 0.0;
-          }
-        }
-        if (lane < N) A[lane * W + lane] += lam;
-        if constexpr (N <= kGJWarpN) {
-        __syncwarp();
-        KK_PT(10);
-        // ---- Gauss–Jordan on [G + λI | q1 q2] by warp 0 with 2×2 pivot blocks (SPD ⇒ every leading 2×2 block
-        //      is SPD, no pivoting; N = 4K + 2 is even). Lane c holds column c in registers (a[i] = A[i][c]); per
-        //      step the two pivot lanes publish their columns as (A[i][k], A[i][k+1]) pairs in a double-buffered
-        //      shared strip (dres is consumed) that every lane reads with broadcast 16-B loads — no CTA barriers
-        //      and no shuffles (warp 0 runs this alone: shuffles in that branch would compile to collectives).
-        //      Division-free form: the pivot rows become s·adj(P)·[row k; row k+1] and every other row
-        //      row_i ← s·det(P)·row_i − A[i][k]·u0 − A[i][k+1]·u1, with s a power of two (≈ 1/pa², exact scaling
-        //      that keeps the rows bounded). The matrix ends as diag(D) with D = s·det·(later factors) per pivot
-        //      block, so x_i = rhs_i / D_i — one reciprocal per row at the end instead of one per step on the
-        //      serial path (each step's chain is ~5 dependent fp64 operations instead of ~11 + a conversion round
-        //      trip through MUFU.RCP).
-        double a[N];
-#pragma unroll
-        for (int i = 0; i < N; ++i) a[i] = (lane < N + 2) ? A[i * W + lane] : 0.0;
-#pragma unroll
-        for (int k = 0; k < N; k += 2) {
-          double* col = dres + ((k >> 1) & 1) * (2 * N);
-          if (lane == k || lane == k + 1) {
-#pragma unroll
-            for (int i = 0; i < N; ++i) col[2 * i + (lane - k)] = a[i];
-          }
-          __syncwarp();
-          const double2 pk = reinterpret_cast<const double2*>(col)[k];       // (A[k][k], A[k][k+1])
-          const double2 pk1 = reinterpret_cast<const double2*>(col)[k + 1];  // (A[k+1][k], A[k+1][k+1])
-          const double pa = pk.x, pb = pk.y, pc = pk1.x, pd = pk1.y;
-          const double det = pa * pd - pb * pc;
-          fail |= !(pa > 0.0) || !(det > 0.0) || !isfinite(det);
-          // s = 2^(−2e), e = unbiased exponent of pa (clamped so that s stays a normal double)
-          const int e = min(max((int)((__double_as_longlong(pa) >> 52) & 0x7ff) - 1023, -500), 500);
-          const double sc = __longlong_as_double((long long)(1023 - 2 * e) << 52);
-          const double r0 = a[k] * sc, r1 = a[k + 1] * sc;
-          const double u0 = pd * r0 - pb * r1, u1 = pa * r1 - pc * r0;        // s·adj(P)·[r0; r1]
-          const double ds = det * sc;
-#pragma unroll
-          for (int i = 0; i < N; ++i) {
-            if (i == k || i == k + 1) continue;
-            const double2 c = reinterpret_cast<const double2*>(col)[i];      // (A[i][k], A[i][k+1])
-            a[i] = fma(-c.y, u1, fma(-c.x, u0, a[i] * ds));
-          }
-          a[k] = u0;
-          a[k + 1] = u1;
-        }
-        {
-          // lane c < N owns D_c = a[c]: 1/D_c (fp32 seed + two Newton steps, full double precision) → strip
-          double* rD = dres + 4 * N;
-          if (lane < N) {
-            double dg = 0.0;
-#pragma unroll
-            for (int i = 0; i < N; ++i) dg = (i == lane) ? a[i] : dg;
-            double rc = (double)__frcp_rn((float)dg);
-            rc = rc * fma(-dg, rc, 2.0);
-            rc = rc * fma(-dg, rc, 2.0);
-            fail |= !(dg > 0.0) || !isfinite(rc) || !((float)dg > 0.f);
-            rD[lane] = rc;
-          }
-          __syncwarp();
-          if (lane == N || lane == N + 1) {
-#pragma unroll
-            for (int i = 0; i < N; ++i) a[i] *= rD[i];
-          }
-        }
-        // solution columns N, N+1 back to shared memory (rows < N)
-        if (lane == N || lane == N + 1) {
-#pragma unroll
-          for (int i = 0; i < N; ++i) A[i * W + lane] = a[i];
-        }
-        __syncwarp();
-        KK_PT(11);
-        }
+      if (tid == 0) rg[NRED] = (double)g_agc;
       }
-      // ---- Gauss–Jordan on [G + λI | q1 q2] by the whole CTA with 2×2 pivot blocks (SPD ⇒ every leading
-      //      2×2 block is SPD, no pivoting; N = 4K + 2 is even). The matrix lives in registers: lane = column c,
-      //      warp w owns rows w, w+8, w+16, w+24. Per step the pivot columns arrive by warp shuffles and the two
-      //      pivot rows through a double-buffered shared row pair — one barrier per step, N/2 steps.
-      if constexpr (N > kGJWarpN) {
-        __syncthreads();
-        constexpr int W = Lay::WS;
-        double* A = mat;
-        double* prow = dres;                          // 2 buffers × 2 rows × 32 columns (dres is consumed)
-        double a[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int i = warp + 8 * q;
-          a[q] = (i < N && lane < N + 2) ? A[i * W + lane] : 0.0;
-        }
-        for (int k = 0, par = 0; k < N; k += 2, par ^= 1) {
-          // owners of rows k, k+1 publish them (row k is row w = k % 8 of q = k / 8)
-          double* pr = prow + par * 64;
-          const int qk = k >> 3;
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            if (q == qk && warp == (k & 7)) pr[lane] = a[q];
-            if (q == ((k + 1) >> 3) && warp == ((k + 1) & 7)) pr[32 + lane] = a[q];
-          }
-          // this warp's rows' pivot-column entries A[i][k], A[i][k+1]
-          double ck[4], ck1[4];
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            ck[q] = __shfl_sync(0xffffffffu, a[q], k);
-            ck1[q] = __shfl_sync(0xffffffffu, a[q], k + 1);
-          }
-          __syncthreads();
-          const double pa = pr[k], pb = pr[k + 1], pc = pr[32 + k], pd = pr[32 + k + 1];
-          const double det = pa * pd - pb * pc;
-          fail |= !(pa > 0.0) || !(det > 0.0) || !isfinite(det);
-          // 1/det: fp32 seed + two Newton steps (relative error ~1e-28 → full double precision; det is the
-          // determinant of an SPD 2×2 pivot block ≥ λ² ≫ FLT_MIN, so the seed is finite when det is)
-          double idet = (double)__frcp_rn((float)det);
-          idet = idet * fma(-det, idet, 2.0);
-          idet = idet * fma(-det, idet, 2.0);
-          const double r0 = pr[lane], r1 = pr[32 + lane];
-          const double R0 = (pd * r0 - pb * r1) * idet, R1 = (pa * r1 - pc * r0) * idet;   // P⁻¹·[r0; r1]
-          if (lane >= k + 2) {                        // columns ≤ k+1 are never read again
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const int i = warp + 8 * q;
-              a[q] = (i == k) ? R0 : (i == k + 1) ? R1 : fma(-ck1[q], R1, fma(-ck[q], R0, a[q]));
-            }
-          }
-        }
-        // solution columns N, N+1 back to shared memory (rows < N)
-        __syncthreads();
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int i = warp + 8 * q;
-          if (i < N && (lane == N || lane == N + 1)) A[i * W + lane] = a[q];
-        }
-        __syncthreads();
+      if (tid == 0) rg[NRED + 1] = (double)flags;
+      if (tid == 32) misc[2] = m_next;                 // publish the next frame's QAM order
+      __syncthreads();   // all reads of ys / red / misc for this frame are done
+      if (tid == 0 && fn < n_frames) {
+        if (!early) issue_y(fn);
+        if (fn + (int)gridDim.x < n_frames) prefetch(fn + gridDim.x);
       }
-      // θ₁ from m1 = column N, m2 = column N+1 (rows e and L+e); fallback θ₀ on failure
-      if (warp == 0) {
-        __syncwarp();
-        constexpr int W = Lay::WS;
-        const double* A = mat;
-          if (lane < N) fail |= !isfinite(A[lane * W + N]) || !isfinite(A[lane * W + N + 1]);
-          fail = __any_sync(0xffffffffu, fail) ? 1 : 0;
-          if (lane < L) {
-            float2 wv, vv;
-            if (fail) {
-              const float2 w0 = __ldg(&w_cd[lane]);
-              wv = make_float2(g * w0.x, g * w0.y);
-              vv = make_float2(0.f, 0.f);
-            } else {
-              const double m1 = A[lane * W + N], m2 = A[lane * W + N + 1];
-              const double m1b = A[(L + lane) * W + N], m2b = A[(L + lane) * W + N + 1];
-              if (wl) {
-                wv = make_float2((float)(0.5 * (m1 + m2b)), (float)(0.5 * (m2 - m1b)));
-                vv = make_float2((float)(0.5 * (m1 - m2b)), (float)(0.5 * (m2 + m1b)));
-              } else {
-                wv = make_float2((float)m1, (float)m1b);
-                vv = make_float2(0.f, 0.f);
-              }
-            }
-            th[lane] = wv;
-            th[L + lane] = vv;
-          }
-          if (lane == 0) misc[1] = fail;
-          KK_PT(12);
-        }
-      __syncthreads();
-      KK_PT(4);
-      bad |= misc[1];
-
+    } else {
+      // ======== K3c: steps (4)–(6) with θ₁ from K3s (arrived with the frame)
+      const int fflags = __float_as_int(th[2 * L].x);
+      int bad = (fflags & (kFlagSilent | kFlagFail)) ? 1 : 0;   // silent frame or solve failure (θ₀ used)
+      const bool zero = dead || (fflags & kFlagSilent);    // z = 0, decisions D(0): dead or silent frame
+      float2 rA = make_float2(0.f, 0.f), rB = make_float2(0.f, 0.f);   // CPR rotations (× unbias) of the halves
+      if (!zero) {
       // ---- sweep C: pass 2 y¹ = Σ_e w_e·a + v_e·conj(a) → us, and the gain-unbias sums (R27)
       float gr = 0.f, gi = 0.f, gd = 0.f;
       {
@@ -867,9 +637,8 @@ uint32_t wadr[NW];
         rA = rotation(cr0, ci0);
         rB = rotation(cr1, ci1);
       }
-      KK_PT(6);
-      }  // p0ok
-    }
+      }
+
 
     // ---- decisions, counts, outputs: z = u·e^{−iϑ_b} (dead or silent frame: z = 0); rotation rA for the warp's
     //      first 256 symbols (s < 8), rB for the second
@@ -956,26 +725,301 @@ uint32_t wadr[NW];
       if (dead) atomicAdd(&counters[22], 1ull);
       if (!dead && bad) atomicAdd(&counters[23], 1ull);
     }
+    }
   }
-#ifdef KK_PHASE_TIMING
-  if (tid == 0 && blockIdx.x == 0)
-    printf("K3PHASES K=%d frames=%d wait %lld sweepA %lld sweepB %lld xwarp %lld solve %lld sweepC %lld cpr %lld decide %lld | chains %lld trG %lld rhs %lld gj %lld theta %lld\n",
-           K, it, pt_[0], pt_[1], pt_[2], pt_[3], pt_[4], pt_[5], pt_[6], pt_[7], pt_[8], pt_[9], pt_[10], pt_[11], pt_[12]);
-#endif
 }
 
+// ======== K3s: one CTA per frame: the real normal equations from the frame's sums and edge samples, eliminated in
+// fp64 (warp 0: Gauss–Jordan with 2×2 pivots and lanes holding columns, N ≤ 18; the CTA for larger N) → θ₁
+template <int K> struct K3S { static constexpr int THREADS = (K3Layout<K>::N <= kGJWarpN) ? 64 : 256; };
+
+template <int K>
+__global__ void __launch_bounds__(K3S<K>::THREADS)
+k3s_kernel(const double* __restrict__ rec, const float2* __restrict__ y, const float2* __restrict__ w_cd,
+           float2* __restrict__ threc, K3Params p) {
+  using Lay = K3Layout<K>;
+  constexpr int L = Lay::L, ND = Lay::ND, N = Lay::N, NRED = Lay::NRED, THREADS = K3S<K>::THREADS;
+  constexpr int K3_WARPS_S = THREADS / 32;
+  (void)K3_WARPS_S;
+  __shared__ __align__(16) double dres[NRED > 128 ? NRED : 128];
+  __shared__ __align__(16) double mat[N * Lay::WS];
+  __shared__ __align__(16) double tl[2 * (K + 1)];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int fl = blockIdx.x;
+  const bool wl = p.widely_linear != 0;
+  const double* rg = rec + (int64_t)fl * K3Rec<K>::REC;
+  float2* tr = threc + (int64_t)fl * K3Rec<K>::TREC;
+  const int flags = (int)rg[NRED + 1];
+  if (flags & (kFlagDead | kFlagSilent)) {             // no solve: K3c outputs z = 0 for this frame
+    if (tid == 0) tr[2 * L] = make_float2(__int_as_float(flags), 0.f);
+    return;
+  }
+  for (int v = tid; v < NRED; v += THREADS) dres[v] = rg[v];
+  const float g = (float)rg[NRED];
+  const float2* yf = y + (int64_t)fl * (2 * kFrameSym);
+  auto ysw = [&](int e) -> float2 { return __ldg(&yf[e]); };   // the frame's 2-sps sample e (edges only)
+  __syncthreads();
+  {
+      {
+        double* A = mat;   // row-major N × WS: [G + λI | q1 q2]
+        constexpr int W = Lay::WS;
+        for (int pt = tid; pt < (2 * ND - 1) * (K + 1); pt += THREADS) {
+          const int c = pt / (K + 1), m = pt % (K + 1);
+          const int rho = c / ND, d = c % ND;
+          const int npts = (2 * K - d - rho) / 2 + 1;  // chain points
+          if (m < npts) {
+            const double A1 = dres[Lay::NP + 8 * d + 4 * rho], A3 = dres[Lay::NP + 8 * d + 4 * rho + 1];
+            const double A4 = dres[Lay::NP + 8 * d + 4 * rho + 2], A2 = dres[Lay::NP + 8 * d + 4 * rho + 3];
+            double sr = A1 + A2, si = A3 - A4, tr_ = A1 - A2, ti = A3 + A4;   // S = Σ conj(a)·b, T = Σ a·b
+#pragma unroll
+            for (int mm = 0; mm < K; ++mm) {
+              if (mm < m) {
+                // fp32 edge increments: O(|y|²) terms added to fp64 sums of 4096 such terms
+                const int i = -K + rho + 2 * mm;
+                const float2 a1 = ysw(K - 2 - i), a2 = ysw(K - 2 - i - d), b1 = ysw(8190 + K - i), b2 = ysw(8190 + K - i - d);
+                const float i0 = fmaf(a1.x, a2.x, a1.y * a2.y) - fmaf(b1.x, b2.x, b1.y * b2.y);
+                const float i1 = fmaf(a1.x, a2.y, -a1.y * a2.x) - fmaf(b1.x, b2.y, -b1.y * b2.x);
+                const float i2 = fmaf(a1.x, a2.x, -a1.y * a2.y) - fmaf(b1.x, b2.x, -b1.y * b2.y);
+                const float i3 = fmaf(a1.x, a2.y, a1.y * a2.x) - fmaf(b1.x, b2.y, b1.y * b2.x);
+                sr += (double)i0; si += (double)i1; tr_ += (double)i2; ti += (double)i3;
+              }
+            }
+            const int i = -K + rho + 2 * m;
+            const int r = i + K, q = i + d + K;     // S(r, q) = Σ conj(a_r)·a_q, T(r, q) = Σ a_r·a_q
+            if (wl) {
+              // G = [[Σ ar arᵀ, Σ ar aiᵀ], [Σ ai arᵀ, Σ ai aiᵀ]] from S and T (both orders of (r, q))
+              const double rr = 0.5 * (sr + tr_), ii = 0.5 * (sr - tr_);
+              const double ri = 0.5 * (si + ti), ir = 0.5 * (ti - si);   // Σ ar_r·ai_q, Σ ai_r·ar_q
+              A[r * W + q] = rr;             A[q * W + r] = rr;
+              A[(L + r) * W + (L + q)] = ii; A[(L + q) * W + (L + r)] = ii;
+              A[r * W + (L + q)] = ri;       A[(L + q) * W + r] = ri;
+              A[(L + r) * W + q] = ir;       A[q * W + (L + r)] = ir;
+              if (d == 0) tl[rho * (K + 1) + m] = rr + ii;
+            } else {
+              // real form of the Hermitian R11: [[Re R, −Im R], [Im R, Re R]], R[r][q] = S, R[q][r] = conj(S)
+              A[r * W + q] = sr;             A[q * W + r] = sr;
+              A[(L + r) * W + (L + q)] = sr; A[(L + q) * W + (L + r)] = sr;
+              A[(L + r) * W + q] = si;       A[(L + q) * W + r] = -si;
+              A[r * W + (L + q)] = -si;      A[q * W + (L + r)] = si;
+              if (d == 0) tl[rho * (K + 1) + m] = sr + sr;
+            }
+          }
+        }
+      }
+  }
+  __syncthreads();
+      int fail = 0;
+      if (warp == 0) {
+        double* A = mat;
+        constexpr int W = Lay::WS;
+        // ridge (R10): λ_c = ridge·tr(R)/n_c. WL: real form uses λ_c/2 and tr(R) = 2·tr(G). Linear: tr(M) = 2·tr(R11)
+        // tr(G): the d = 0 terms in chain order (ρ = 0: K + 1 points, ρ = 1: K points)
+        double t0 = 0.0, t1 = 0.0;
+#pragma unroll
+        for (int m = 0; m <= K; ++m) t0 += tl[m];
+#pragma unroll
+        for (int m = 0; m < K; ++m) t1 += tl[K + 1 + m];
+        const double trG = t0 + t1;
+        // (the factor ridge/n_c does not wait for the trace)
+        const double lam = trG * (wl ? (double)p.ridge / (double)N : (double)p.ridge * 0.5 / (double)L);
+        if (lane < L) {
+          const int e = lane;
+          const double B1 = dres[4 * e], B3 = dres[4 * e + 1], B4 = dres[4 * e + 2], B2 = dres[4 * e + 3];
+          const double p1r = B1 + B2, p1i = B3 - B4, p2r = B1 - B2, p2i = B3 + B4;   // p1 = Σ conj(a)·d, p2 = Σ a·d
+          const float2 w0 = __ldg(&w_cd[e]);
+          const double w0r = (double)g * (double)w0.x, w0i = (double)g * (double)w0.y;
+          if (wl) {
+            // q1 = [Σ ar·dr; Σ ai·dr], q2 = [Σ ar·di; Σ ai·di];  m1₀ = [w0r; −w0i], m2₀ = [w0i; w0r]
+            A[e * W + N] = 0.5 * (p1r + p2r) + lam * w0r;
+            A[(L + e) * W + N] = 0.5 * (p2i - p1i) - lam * w0i;
+            A[e * W + N + 1] = 0.5 * (p1i + p2i) + lam * w0i;
+            A[(L + e) * W + N + 1] = 0.5 * (p1r - p2r) + lam * w0r;
+          } else {
+            A[e * W + N] = p1r + lam * w0r;
+            A[(L + e) * W + N] = p1i + lam * w0i;
+            A[e * W + N + 1] = 0.0;
+            A[(L + e) * W + N + 1] = 0.0;
+          }
+        }
+        if (lane < N) A[lane * W + lane] += lam;
+        if constexpr (N <= kGJWarpN) {
+        __syncwarp();
+          // ---- Gauss–Jordan on [G + λI | q1 q2] by warp 0 with 2×2 pivot blocks (SPD ⇒ every leading 2×2 block
+        //      is SPD, no pivoting; N = 4K + 2 is even). Lane c holds column c in registers (a[i] = A[i][c]); per
+        //      step the two pivot lanes publish their columns as (A[i][k], A[i][k+1]) pairs in a double-buffered
+        //      shared strip (dres is consumed) that every lane reads with broadcast 16-B loads — no CTA barriers
+        //      and no shuffles (warp 0 runs this alone: shuffles in that branch would compile to collectives).
+        //      Division-free form: the pivot rows become s·adj(P)·[row k; row k+1] and every other row
+        //      row_i ← s·det(P)·row_i − A[i][k]·u0 − A[i][k+1]·u1, with s a power of two (≈ 1/pa², exact scaling
+        //      that keeps the rows bounded). The matrix ends as diag(D) with D = s·det·(later factors) per pivot
+        //      block, so x_i = rhs_i / D_i — one reciprocal per row at the end instead of one per step on the
+        //      serial path (each step's chain is ~5 dependent fp64 operations instead of ~11 + a conversion round
+        //      trip through MUFU.RCP).
+        double a[N];
+#pragma unroll
+        for (int i = 0; i < N; ++i) a[i] = (lane < N + 2) ? A[i * W + lane] : 0.0;
+#pragma unroll
+        for (int k = 0; k < N; k += 2) {
+          double* col = dres + ((k >> 1) & 1) * (2 * N);
+          if (lane == k || lane == k + 1) {
+#pragma unroll
+            for (int i = 0; i < N; ++i) col[2 * i + (lane - k)] = a[i];
+          }
+          __syncwarp();
+          const double2 pk = reinterpret_cast<const double2*>(col)[k];       // (A[k][k], A[k][k+1])
+          const double2 pk1 = reinterpret_cast<const double2*>(col)[k + 1];  // (A[k+1][k], A[k+1][k+1])
+          const double pa = pk.x, pb = pk.y, pc = pk1.x, pd = pk1.y;
+          const double det = pa * pd - pb * pc;
+          fail |= !(pa > 0.0) || !(det > 0.0) || !isfinite(det);
+          // s = 2^(−2e), e = unbiased exponent of pa (clamped so that s stays a normal double)
+          const int e = min(max((int)((__double_as_longlong(pa) >> 52) & 0x7ff) - 1023, -500), 500);
+          const double sc = __longlong_as_double((long long)(1023 - 2 * e) << 52);
+          const double r0 = a[k] * sc, r1 = a[k + 1] * sc;
+          const double u0 = pd * r0 - pb * r1, u1 = pa * r1 - pc * r0;        // s·adj(P)·[r0; r1]
+          const double ds = det * sc;
+#pragma unroll
+          for (int i = 0; i < N; ++i) {
+            if (i == k || i == k + 1) continue;
+            const double2 c = reinterpret_cast<const double2*>(col)[i];      // (A[i][k], A[i][k+1])
+            a[i] = fma(-c.y, u1, fma(-c.x, u0, a[i] * ds));
+          }
+          a[k] = u0;
+          a[k + 1] = u1;
+        }
+        {
+          // lane c < N owns D_c = a[c]: 1/D_c (fp32 seed + two Newton steps, full double precision) → strip
+          double* rD = dres + 4 * N;
+          if (lane < N) {
+            double dg = 0.0;
+#pragma unroll
+            for (int i = 0; i < N; ++i) dg = (i == lane) ? a[i] : dg;
+            double rc = (double)__frcp_rn((float)dg);
+            rc = rc * fma(-dg, rc, 2.0);
+            rc = rc * fma(-dg, rc, 2.0);
+            fail |= !(dg > 0.0) || !isfinite(rc) || !((float)dg > 0.f);
+            rD[lane] = rc;
+          }
+          __syncwarp();
+          if (lane == N || lane == N + 1) {
+#pragma unroll
+            for (int i = 0; i < N; ++i) a[i] *= rD[i];
+          }
+        }
+        // solution columns N, N+1 back to shared memory (rows < N)
+        if (lane == N || lane == N + 1) {
+#pragma unroll
+          for (int i = 0; i < N; ++i) A[i * W + lane] = a[i];
+        }
+        __syncwarp();
+        }
+      }
+      // ---- Gauss–Jordan on [G + λI | q1 q2] by the whole CTA with 2×2 pivot blocks (SPD ⇒ every leading
+      //      2×2 block is SPD, no pivoting; N = 4K + 2 is even). The matrix lives in registers: lane = column c,
+      //      warp w owns rows w, w+8, w+16, w+24. Per step the pivot columns arrive by warp shuffles and the two
+      //      pivot rows through a double-buffered shared row pair — one barrier per step, N/2 steps.
+      if constexpr (N > kGJWarpN) {
+        __syncthreads();
+        constexpr int W = Lay::WS;
+        double* A = mat;
+        double* prow = dres;                          // 2 buffers × 2 rows × 32 columns (dres is consumed)
+        double a[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int i = warp + 8 * q;
+          a[q] = (i < N && lane < N + 2) ? A[i * W + lane] : 0.0;
+        }
+        for (int k = 0, par = 0; k < N; k += 2, par ^= 1) {
+          // owners of rows k, k+1 publish them (row k is row w = k % 8 of q = k / 8)
+          double* pr = prow + par * 64;
+          const int qk = k >> 3;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            if (q == qk && warp == (k & 7)) pr[lane] = a[q];
+            if (q == ((k + 1) >> 3) && warp == ((k + 1) & 7)) pr[32 + lane] = a[q];
+          }
+          // this warp's rows' pivot-column entries A[i][k], A[i][k+1]
+          double ck[4], ck1[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            ck[q] = __shfl_sync(0xffffffffu, a[q], k);
+            ck1[q] = __shfl_sync(0xffffffffu, a[q], k + 1);
+          }
+          __syncthreads();
+          const double pa = pr[k], pb = pr[k + 1], pc = pr[32 + k], pd = pr[32 + k + 1];
+          const double det = pa * pd - pb * pc;
+          fail |= !(pa > 0.0) || !(det > 0.0) || !isfinite(det);
+          // 1/det: fp32 seed + two Newton steps (relative error ~1e-28 → full double precision; det is the
+          // determinant of an SPD 2×2 pivot block ≥ λ² ≫ FLT_MIN, so the seed is finite when det is)
+          double idet = (double)__frcp_rn((float)det);
+          idet = idet * fma(-det, idet, 2.0);
+          idet = idet * fma(-det, idet, 2.0);
+          const double r0 = pr[lane], r1 = pr[32 + lane];
+          const double R0 = (pd * r0 - pb * r1) * idet, R1 = (pa * r1 - pc * r0) * idet;   // P⁻¹·[r0; r1]
+          if (lane >= k + 2) {                        // columns ≤ k+1 are never read again
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const int i = warp + 8 * q;
+              a[q] = (i == k) ? R0 : (i == k + 1) ? R1 : fma(-ck1[q], R1, fma(-ck[q], R0, a[q]));
+            }
+          }
+        }
+        // solution columns N, N+1 back to shared memory (rows < N)
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int i = warp + 8 * q;
+          if (i < N && (lane == N || lane == N + 1)) A[i * W + lane] = a[q];
+        }
+        __syncthreads();
+      }
+      // θ₁ from m1 = column N, m2 = column N+1 (rows e and L+e); fallback θ₀ on failure
+      if (warp == 0) {
+        __syncwarp();
+        constexpr int W = Lay::WS;
+        const double* A = mat;
+          if (lane < N) fail |= !isfinite(A[lane * W + N]) || !isfinite(A[lane * W + N + 1]);
+          fail = __any_sync(0xffffffffu, fail) ? 1 : 0;
+          if (lane < L) {
+            float2 wv, vv;
+            if (fail) {
+              const float2 w0 = __ldg(&w_cd[lane]);
+              wv = make_float2(g * w0.x, g * w0.y);
+              vv = make_float2(0.f, 0.f);
+            } else {
+              const double m1 = A[lane * W + N], m2 = A[lane * W + N + 1];
+              const double m1b = A[(L + lane) * W + N], m2b = A[(L + lane) * W + N + 1];
+              if (wl) {
+                wv = make_float2((float)(0.5 * (m1 + m2b)), (float)(0.5 * (m2 - m1b)));
+                vv = make_float2((float)(0.5 * (m1 - m2b)), (float)(0.5 * (m2 + m1b)));
+              } else {
+                wv = make_float2((float)m1, (float)m1b);
+                vv = make_float2(0.f, 0.f);
+              }
+            }
+            tr[lane] = wv;
+            tr[L + lane] = vv;
+          }
+          if (lane == 0) tr[2 * L] = make_float2(__int_as_float(flags | (fail ? kFlagFail : 0)), 0.f);
+          
+        }
+}
 template <int K>
 static void launch_k3_t(const float2* y, int64_t frame0, int64_t n_frames, const float2* w_cd, const int* clampcnt,
                         int64_t clamp_frame_off, const uint8_t* ref, uint8_t* dec, float2* z,
-                        unsigned long long* counters, const K3Params& p, const CUtensorMap* ymaps, int num_sms,
-                        cudaStream_t s) {
+                        unsigned long long* counters, const K3Params& p, const CUtensorMap* ymaps, double* rec,
+                        float2* threc, int num_sms, cudaStream_t s) {
   constexpr int smem = K3Layout<K>::TOTAL;
-  cudaFuncSetAttribute(k3_eq_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(k3_frame_kernel<K, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(k3_frame_kernel<K, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   int64_t grid = (int64_t)num_sms * 2;
   if (grid > n_frames) grid = n_frames;
-  k3_eq_kernel<K><<<(unsigned)grid, K3_THREADS, smem, s>>>(y, frame0, (int)n_frames, w_cd, clampcnt,
-                                                           clamp_frame_off, ref, dec, z, counters, p, ymaps[0],
-                                                           ymaps[1]);
+  k3_frame_kernel<K, 0><<<(unsigned)grid, K3_THREADS, smem, s>>>(y, frame0, (int)n_frames, w_cd, clampcnt,
+                                                                 clamp_frame_off, nullptr, nullptr, nullptr, counters,
+                                                                 p, rec, threc, ymaps[0], ymaps[1]);
+  k3s_kernel<K><<<(unsigned)n_frames, K3S<K>::THREADS, 0, s>>>(rec, y, w_cd, threc, p);
+  k3_frame_kernel<K, 1><<<(unsigned)grid, K3_THREADS, smem, s>>>(y, frame0, (int)n_frames, w_cd, clampcnt,
+                                                                 clamp_frame_off, ref, dec, z, counters, p, rec,
+                                                                 threc, ymaps[0], ymaps[1]);
 }
 
 // Tensor maps of the 2-sps buffer y (n_float2 entries) for the swizzled K ≤ 4 frame loads: a 2-D view of
@@ -1018,10 +1062,21 @@ size_t k3_smem_bytes(int K) {
   }
 }
 
+// per-frame record sizes (bytes) of the K3a → K3s and K3s → K3c hand-offs
+size_t k3_rec_bytes(int K) {
+  switch (K) {
+#define KK_R(KV) case KV: return (size_t)K3Rec<KV>::REC * 8;
+    KK_R(1) KK_R(2) KK_R(3) KK_R(4) KK_R(5) KK_R(6) KK_R(7)
+#undef KK_R
+    default: return 0;
+  }
+}
+size_t k3_threc_bytes(int K) { return (size_t)(2 * (2 * K + 1) + 2) * 8; }
+
 void launch_k3(const float2* y, int64_t frame0, int64_t n_frames, int K, const float2* w_cd, const int* clampcnt,
                int64_t clamp_frame_off, const uint8_t* ref, uint8_t* dec, float2* z, unsigned long long* counters,
-               const K3Params& p, const CUtensorMap* ymaps, int num_sms, cudaStream_t s) {
-#define KK_K3(KV) case KV: launch_k3_t<KV>(y, frame0, n_frames, w_cd, clampcnt, clamp_frame_off, ref, dec, z, counters, p, ymaps, num_sms, s); break;
+               const K3Params& p, const CUtensorMap* ymaps, double* rec, float2* threc, int num_sms, cudaStream_t s) {
+#define KK_K3(KV) case KV: launch_k3_t<KV>(y, frame0, n_frames, w_cd, clampcnt, clamp_frame_off, ref, dec, z, counters, p, ymaps, rec, threc, num_sms, s); break;
   switch (K) {
     KK_K3(1) KK_K3(2) KK_K3(3) KK_K3(4) KK_K3(5) KK_K3(6) KK_K3(7)
     default: break;

@@ -68,6 +68,8 @@ struct kk_ctx {
   int* d_clamp = nullptr;
   float2* d_y = nullptr;
   CUtensorMap ymaps[2];   // K3's tensor-TMA views of d_y (K ≤ 4)
+  double* d_k3rec = nullptr;   // K3a → K3s per-frame records
+  float2* d_k3th = nullptr;    // K3s → K3c per-frame θ₁ records
   float2* d_z = nullptr;
   float* d_segpow = nullptr;     // DDLMS mode: K2's per-64-symbol power sums (K3′ AGC)
   unsigned long long* d_counters = nullptr;
@@ -349,7 +351,7 @@ void resolve_timing(kk_ctx* c, size_t count) {
 
 void free_all(kk_ctx* c) {
   void* ptrs[] = {c->d_H, c->d_Hc, c->d_lo, c->d_wcd, c->d_tw1024, c->d_tw256, c->d_twN, c->d_twI, c->d_tw2048u, c->d_sched,
-                  c->d_E, c->d_part, c->d_clamp, c->d_y, c->d_z, c->d_segpow, c->d_counters,
+                  c->d_E, c->d_part, c->d_clamp, c->d_y, c->d_z, c->d_segpow, c->d_counters, c->d_k3rec, c->d_k3th,
                   c->d_in[0], c->d_in[1], c->d_ref[0], c->d_ref[1], c->d_dec[0], c->d_dec[1]};
   for (void* p : ptrs) dfree(c, p);
   c->guards.clear();
@@ -553,6 +555,10 @@ kk_status kk_init(const kk_config* cfg, kk_ctx** out) {
   chk(dalloc(c, "y", &c->d_y, (size_t)(n / 2 + 2 * c->Ky + 2) * sizeof(float2)));
   if (c->d_y && !kk::k3_encode_ymaps(c->d_y, n / 2 + 2 * c->Ky + 2, c->ymaps) && e == cudaSuccess) e = cudaErrorNotSupported;
   if (cfg->keep_intermediate) chk(dalloc(c, "z", &c->d_z, (size_t)(n / 4) * sizeof(float2)));
+  if (!ddlms) {
+    chk(dalloc(c, "k3rec", &c->d_k3rec, (size_t)(n / kk::kFrameSamp) * kk::k3_rec_bytes(c->K)));
+    chk(dalloc(c, "k3th", &c->d_k3th, (size_t)(n / kk::kFrameSamp) * kk::k3_threc_bytes(c->K)));
+  }
   if (ddlms) chk(dalloc(c, "segpow", &c->d_segpow, (size_t)((n / 2 + 2 * c->Ky) / 512 + 2 * (c->mfKeep / 512) + 16) * sizeof(float)));
   chk(dalloc(c, "counters", &c->d_counters, 32 * sizeof(unsigned long long)));
   if (cfg->ref_prbs) {
@@ -710,7 +716,8 @@ kk_status kk_process_frames_ex(kk_ctx* c, const void* d_adc, int64_t first, int6
   } else {
     NvtxRange r3_("kk::K3 block-LS EQ + CPR + decisions");
     kk::launch_k3(c->d_y, first / F, nfr, c->K, c->d_wcd, c->d_clamp, (int64_t)F / kk::kHilbertHop /*skip frame −1*/,
-                  d_ref, d_dec, cf.keep_intermediate ? c->d_z : nullptr, c->d_counters, p3, c->ymaps, c->num_sms, s);
+                  d_ref, d_dec, cf.keep_intermediate ? c->d_z : nullptr, c->d_counters, p3, c->ymaps, c->d_k3rec,
+                  c->d_k3th, c->num_sms, s);
   }
   if (c->timing) {
     cudaEventRecord(tev[3], s);

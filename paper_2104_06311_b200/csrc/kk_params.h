@@ -84,11 +84,14 @@ void launch_k2(int nf, const float2* E, int64_t E_first, const float2* part, con
                int64_t tile0, int64_t n_tiles, float2* y, int64_t y_first, int64_t y_count, const float* Hs,
                const float2* Hc, const float2* lo_tab, const float2* tw256, const float2* twN,
                const float2* twI, const K2Params& p, int num_sms, cudaStream_t s);
-// K3: per-frame widely-linear DD-LS equalizer, CPR, decisions, counters. ymaps: the two tensor maps of y from
-// k3_encode_ymaps (used for K ≤ 4).
+// K3: per-frame widely-linear DD-LS equalizer, CPR, decisions, counters — three launches (K3a sums, K3s batched
+// solves, K3c pass 2 / CPR / decisions). ymaps: the two tensor maps of y from k3_encode_ymaps (used for K ≤ 4);
+// rec / threc: n_frames records of k3_rec_bytes(K) / k3_threc_bytes(K) bytes (scratch).
 void launch_k3(const float2* y, int64_t frame0, int64_t n_frames, int K, const float2* w_cd, const int* clampcnt,
                int64_t clamp_frame_off, const uint8_t* ref, uint8_t* dec, float2* z, unsigned long long* counters,
-               const K3Params& p, const CUtensorMap* ymaps, int num_sms, cudaStream_t s);
+               const K3Params& p, const CUtensorMap* ymaps, double* rec, float2* threc, int num_sms, cudaStream_t s);
+size_t k3_rec_bytes(int K);
+size_t k3_threc_bytes(int K);
 bool k3_encode_ymaps(const float2* y, int64_t n_float2, CUtensorMap* maps);
 
 // Reference labels of the synthetic transmitter for global symbols [sym0, sym0 + n_sym) (kk_config.ref_prbs).
