@@ -731,7 +731,7 @@ uint32_t wadr[NW];
 
 // ======== K3s: one CTA per frame: the real normal equations from the frame's sums and edge samples, eliminated in
 // fp64 (warp 0: Gauss–Jordan with 2×2 pivots and lanes holding columns, N ≤ 18; the CTA for larger N) → θ₁
-template <int K> struct K3S { static constexpr int THREADS = (K3Layout<K>::N <= kGJWarpN) ? 64 : 256; };
+template <int K> struct K3S { static constexpr int THREADS = (K3Layout<K>::N <= kGJWarpN) ? 32 : 256; };
 
 template <int K>
 __global__ void __launch_bounds__(K3S<K>::THREADS)
@@ -756,8 +756,13 @@ k3s_kernel(const double* __restrict__ rec, const float2* __restrict__ y, const f
   }
   for (int v = tid; v < NRED; v += THREADS) dres[v] = rg[v];
   const float g = (float)rg[NRED];
+  // the chains read only the frame's edge samples: y_s[0, 2K] and y_s[8190 − 2K, 8190 + 2K] — one load per
+  // thread into shared memory (a single global round trip instead of one per chain step)
+  constexpr int NE_LO = 2 * K + 1, NE_HI = 4 * K + 1, HI0 = 8190 - 2 * K;
+  __shared__ float2 edge[NE_LO + NE_HI];
   const float2* yf = y + (int64_t)fl * (2 * kFrameSym);
-  auto ysw = [&](int e) -> float2 { return __ldg(&yf[e]); };   // the frame's 2-sps sample e (edges only)
+  for (int v = tid; v < NE_LO + NE_HI; v += THREADS) edge[v] = __ldg(&yf[v < NE_LO ? v : HI0 + (v - NE_LO)]);
+  auto ysw = [&](int e) -> float2 { return edge[e < NE_LO ? e : NE_LO + (e - HI0)]; };   // edge sample e
   __syncthreads();
   {
       {
