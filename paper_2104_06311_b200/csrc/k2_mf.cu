@@ -109,7 +109,7 @@ k2_mf_kernel(const float2* __restrict__ E, int64_t E_first, const float2* __rest
   constexpr int PER3 = 256 / T;              // last-pass DFTs per thread (2 / 1)
   extern __shared__ __align__(16) float2 k2_smem[];
   float2* buf = k2_smem;                                   // NF + NF/16 (padded tile)
-  __shared__ float2 A_s[2];
+  __shared__ float2 A_s[2][2];                             // [tile parity][frame fa, fa + 1]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // LO of local sample i = j + NJ1·r of a tile starting at global sample s0 (R9, exponents add mod lo_den):
   //   LO[(lo_num·(s0 + i)) mod lo_den] = φ_t · λ_j · ρ^r,  φ_t = LO[qb_t], qb_t = (lo_num·s0) mod lo_den,
@@ -134,8 +134,20 @@ k2_mf_kernel(const float2* __restrict__ E, int64_t E_first, const float2* __rest
     if (warp == 0 || s0_ + NF > (fa_ + 1) * kFrameSamp) a = part[(fa_ + warp) * 32 - jb0 + lane];
     return a;
   };
+  // the carrier estimates of a tile are formed one tile ahead (warps 0, 1, into A_s[parity]), so that the tile
+  // start needs no barrier: the previous tile's closing barrier orders them
+  // (the lane's block sum `pa` of the tile after next is loaded one tile earlier still, so no global-load wait)
+  auto form_A = [&](float2 a, int par) {
+    if (warp < 2) {
+      a.x = warp_sum(a.x); a.y = warp_sum(a.y);
+      if (lane == 0) A_s[par][warp] = make_float2(a.x * (1.0f / kFrameSamp), a.y * (1.0f / kFrameSamp));
+    }
+  };
   float2 pa = make_float2(0.f, 0.f);
-  if (warp < 2 && (int64_t)blockIdx.x < n_tiles) pa = load_part(blockIdx.x);
+  if (warp < 2 && (int64_t)blockIdx.x < n_tiles) form_A(load_part(blockIdx.x), 0);
+  if (warp < 2 && (int64_t)blockIdx.x + gridDim.x < n_tiles) pa = load_part(blockIdx.x + gridDim.x);
+  __syncthreads();
+  int par = 0;
 
   // tiles are visited from the END of the range: K1 wrote E front to back, so its most recent (L2-resident)
   // output is consumed first; K3 then walks y front to back, again reading K2's most recent writes first.
@@ -156,21 +168,15 @@ k2_mf_kernel(const float2* __restrict__ E, int64_t E_first, const float2* __rest
     }
     const float2 phi = __ldg(&lo_tab[qb]);
     qb += dq; qb -= (qb >= p.lo_den) ? p.lo_den : 0;
-    // carrier estimates A_fa, A_fa+1 from K1's per-512-block sums (fixed order → deterministic)
-    if (warp < 2) {
-      float2 a = pa;
-      if (ti + gridDim.x < n_tiles) pa = load_part(ti + gridDim.x);
-      a.x = warp_sum(a.x); a.y = warp_sum(a.y);
-      if (lane == 0) A_s[warp] = make_float2(a.x * (1.0f / kFrameSamp), a.y * (1.0f / kFrameSamp));
-    }
-    __syncthreads();
     // next tile's input (NF·8 bytes of E) → L2 while this tile computes
     if (tid == 0 && ti + gridDim.x < n_tiles) {
       const int64_t s0n = (t - gridDim.x) * HOP - LEAD;
       asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(E + (s0n - E_first)), "r"(NF * 8) : "memory");
     }
     {
-      const float2 A0 = A_s[0], A1 = A_s[1];
+      // carrier estimates A_fa, A_fa+1 from K1's per-512-block sums (fixed order → deterministic), formed during
+      // the previous tile
+      const float2 A0 = A_s[par][0], A1 = A_s[par][1];
       const int isplit = (int)(fsplit - s0);                 // first local sample of frame fa+1
 #pragma unroll
       for (int it = 0; it < 2; ++it) {
@@ -276,6 +282,11 @@ k2_mf_kernel(const float2* __restrict__ E, int64_t E_first, const float2* __rest
           p.seg_pow[t * NSEG + tid - p.seg_first] = a;
         }
       }
+      if (ti + gridDim.x < n_tiles) {                         // the next tile's carrier estimates
+        form_A(pa, par ^ 1);
+        if (warp < 2 && ti + 2 * (int64_t)gridDim.x < n_tiles) pa = load_part(ti + 2 * gridDim.x);
+      }
+      par ^= 1;
       __syncthreads();                                        // buf is rewritten by the next tile
     }
   }
