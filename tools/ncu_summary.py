@@ -58,8 +58,8 @@ def main(report, launches, out_md, traffic_json=None):
             rd = float(r[col["dram__bytes_read.sum"]].replace(",", ""))
             wr = float(r[col["dram__bytes_write.sum"]].replace(",", ""))
             scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(units[col["dram__bytes_read.sum"]], 1)
-            key = "K1u_kk" if "k1u_" in n else "K1_kk" if "k1_" in n else "K2_mf" if "k2_" in n else "K3_eq" if "k3_" in n else n
-            traffic[key] = (rd + wr) * scale
+            key = "K1u_kk" if "k1u_" in n else "K1_kk" if "k1_" in n else "K2_mf" if "k2_" in n else "K3_eq" if ("k3_" in n or "k3s_" in n) else n
+            traffic[key] = traffic.get(key, 0.0) + (rd + wr) * scale   # K3 = K3a + K3s + K3c
         except (KeyError, ValueError):
             pass
     # launch list shares
@@ -75,7 +75,7 @@ def main(report, launches, out_md, traffic_json=None):
             v = float(r["Metric Value"].replace(",", ""))
             tot[n] += v
             cnt[n] += 1
-        ours = {k: v for k, v in tot.items() if k.split("<")[0].split("::")[-1].startswith(("k1_", "k2_", "k3_"))}
+        ours = {k: v for k, v in tot.items() if k.split("<")[0].split("::")[-1].startswith(("k1_", "k2_", "k3_", "k3s_"))}
         s = sum(ours.values())
         lines += ["", "## Launch list (ncu `gpu__time_duration.sum`, cold-cache, serialised)", "",
                   "| kernel | launches | total (us) | share of K1+K2+K3 |", "|---|---|---|---|"]
