@@ -292,7 +292,7 @@ def e2e_uint8(a, lc, HALO, chunk, first, En, world, dev, SH, kkrx, kkgen, torch,
     rx8 = Receiver(adc_scale=lc8.adc_scale, ref_intensity=lc8.i_ref, dispersion_ps_per_nm=lc8.dl_ps_nm,
                    formats=lc8.formats, segment_frames=lc8.segment_frames, max_samples_per_call=chunk, device=dev.index,
                    input_uint8=True, upsample=a.upsample, mf_fft_n=a.mf_n,
-                   ref_prbs_seed=None if h_ref is not None else lc8.seed)
+                   ref_prbs_seed=None if h_ref is not None else lc8.seed, ref_prbs_kind=lc8.label_source)
     rx8.process_host(h_codes, first, En, ref=h_ref, decisions=h_dec)          # warm-up
     if world > 1:
         dist.barrier()
@@ -523,7 +523,7 @@ def main():
                            formats=lc.formats, segment_frames=lc.segment_frames, max_samples_per_call=chunk,
                            device=local, eq_mode=a.eq_mode, ddlms_block=a.ddlms_block, ddlms_warmup=a.ddlms_warmup,
                            ddlms_mu_warm=a.ddlms_mu_warm, upsample=a.upsample, mf_fft_n=a.mf_n,
-                           ref_prbs_seed=lc.seed)                            # label sequence (kk_config.ref_prbs)
+                           ref_prbs_seed=lc.seed, ref_prbs_kind=lc.label_source)   # (kk_config.ref_prbs)
         h_dec = torch.empty(En // 4, dtype=torch.uint8, pin_memory=True)
         n_chunks = (En + min(chunk, 1 << 26) - 1) // min(chunk, 1 << 26)    # host path stages ≤ 2^26 per sub-call
         rxe.process_host(h_codes, first, En, ref=h_ref, decisions=h_dec)     # warm-up (allocates staging)
@@ -543,7 +543,7 @@ def main():
                "d2h_bytes_per_step": int(En // 4 + 8 * kkrx.KK_STATS_WORDS),
                "samples_per_gpu": En, "api": "kk_process_frames_host (pinned host buffers, 2 streams)",
                "ref": ("host label buffer" if h_ref is not None else
-                       "transmitter label sequence generated on the GPU (kk_config.ref_prbs)"),
+                       f"transmitter label sequence generated on the GPU (kk_config.ref_prbs: {lc.label_source})"),
                "ber": {f"{M}QAM": st_e["bit_err"][i] / st_e["bits"][i]
                        for i, M in enumerate((4, 8, 16, 32, 64)) if st_e["bits"][i]}}
         if rxe is not rx:

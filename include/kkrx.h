@@ -102,8 +102,11 @@ typedef struct kk_config {
    * ref argument the library generates the transmitter's known label sequence on the device instead of reading
    * it — no host→device label transfer on the host path: label(k) = H(ref_seed, k) & (M(k) − 1) for global symbol
    * k, M(k) the QAM order of k's frame (R26 schedule) and H the synthetic transmitter's counter-based 32-bit hash
-   * (kkgen.hash_u32(seed, 1, k): murmur3 fmix32 rounds keyed by the seed). ref_prbs = 0
-   * (default): a NULL ref argument means no error counting. */
+   * (kkgen.hash_u32(seed, 1, k): murmur3 fmix32 rounds keyed by the seed). With ref_prbs = 2 the
+   * known sequence is the standard ITU-T O.150 PRBS-31 (x^31 + x^28 + 1) bit stream that real transmitters send:
+   * b[n] = b[n−28] ⊕ b[n−31], b[0..30] = bits of W0 = (ref_seed·0x9E3779B1 mod 2^32) >> 1 (1 if zero), symbol k's
+   * label = (bits 6k … 6k+5 of the stream, LSB first) & (M(k) − 1) (kkgen LinkConfig.label_source = "prbs31").
+   * ref_prbs = 0 (default): a NULL ref argument means no error counting. */
   int32_t ref_prbs;
   uint32_t ref_seed;
   int32_t reserved2;

@@ -164,6 +164,7 @@ class LinkConfig:
     pn_delay_s: float = 0.83e-9
     sideband: int = +1
     adc_bits: int = 15                    # 15 → int16 codes 0..32767 (R20); ≤ 8 → uint8 codes (SPEC S:199's 8-bit ADC)
+    label_source: str = "hash"            # "hash" (counter hash per symbol) | "prbs31" (ITU-T O.150 PRBS-31 bit stream)
 
     @property
     def px(self) -> float:  # mean |x|^2 of the shaped data at 4 sps with unit-energy taps
@@ -217,7 +218,123 @@ def beta2_l(dl_ps_nm: float, lam: float = LAMBDA_M) -> float:
 # ----------------------------------------------------------------------------------
 def symbol_labels(cfg: LinkConfig, k: torch.Tensor) -> torch.Tensor:
     M = cfg.format_of_symbols(k)
+    if cfg.label_source == "prbs31":
+        n = k.numel()
+        k0 = int(k[0]) if n else 0
+        assert n == 0 or bool(torch.equal(k, torch.arange(k0, k0 + n, dtype=torch.int64, device=k.device))), \
+            "prbs31 labels: contiguous symbol ranges only"
+        return (prbs31_slots(cfg.seed, k0, n, k.device) & (M - 1)).to(torch.uint8)
+    assert cfg.label_source == "hash"
     return (hash_u32(cfg.seed, 1, k) & (M - 1)).to(torch.uint8)
+
+
+# ----------------------------------------------------------------------------------
+# PRBS-31 label stream (ITU-T O.150: x^31 + x^28 + 1) — the pattern a real transmitter sends and a real-time
+# receiver syncs to (PAPER.md:112 counts BER against the known transmitted sequence). Bit stream b[n]:
+# b[n] = b[n−28] ⊕ b[n−31] (n ≥ 31), b[0..30] = the bits of the initial word W0(seed) (LSB = b[0]).
+# Symbol k owns the 6-bit slot b[6k .. 6k+5]: slot(k) = Σ_t b[6k+t]·2^t, label(k) = slot(k) & (M(k) − 1).
+# Any symbol range is generated independently: the 31-bit window W_n = Σ_i b[n+i]·2^i evolves linearly over GF(2)
+# (W_{n+1} = (W_n >> 1) | ((b[n] ⊕ b[n+3]) << 30)), so W_n = A^n·W0 by binary powers of A (jump-ahead).
+# ----------------------------------------------------------------------------------
+PRBS_MASK31 = (1 << 31) - 1
+PRBS_PERIOD = (1 << 31) - 1           # the order of A (x^31 + x^28 + 1 is primitive; 2^31 − 1 is prime)
+
+
+def prbs31_w0(seed: int) -> int:
+    w = ((seed * 0x9E3779B1) & 0xFFFFFFFF) >> 1
+    return w if w else 1
+
+
+def _gf2_apply(cols, w):
+    """M·w over GF(2) for the 31×31 matrix with columns cols (ints), w an int or an int64 tensor."""
+    if isinstance(w, int):
+        r = 0
+        for i in range(31):
+            if (w >> i) & 1:
+                r ^= cols[i]
+        return r
+    r = torch.zeros_like(w)
+    for i in range(31):
+        r ^= ((w >> i) & 1) * cols[i]
+    return r
+
+
+def _prbs_step_cols():
+    cols = []                                        # A·e_i: shift right by one, new bit 30 = b0 ⊕ b3
+    for i in range(31):
+        w = 1 << i
+        cols.append((w >> 1) | ((((w >> 0) ^ (w >> 3)) & 1) << 30))
+    return cols
+
+
+_PRBS_POW = {}   # n → columns of A^n (powers of two, times the 96-bit block stride)
+
+
+def prbs31_matrix(n_pow2: int):
+    """Columns of A^(2^n_pow2)."""
+    if n_pow2 not in _PRBS_POW:
+        if n_pow2 == 0:
+            _PRBS_POW[0] = _prbs_step_cols()
+        else:
+            prev = prbs31_matrix(n_pow2 - 1)
+            _PRBS_POW[n_pow2] = [_gf2_apply(prev, c) for c in prev]      # (A^m)² column by column
+    return _PRBS_POW[n_pow2]
+
+
+def prbs31_jump(w: int, n: int) -> int:
+    """W_n from W_0 = w."""
+    j = 0
+    while n:
+        if n & 1:
+            w = _gf2_apply(prbs31_matrix(j), w)
+        n >>= 1
+        j += 1
+    return w
+
+
+def prbs31_slots(seed: int, k0: int, n: int, device="cpu") -> torch.Tensor:
+    """slot(k) for k = k0 … k0 + n − 1 (int64). Blocks of 16 symbols (96 bits) from their 31-bit windows: the first
+    block's window by jump-ahead, the others by doubling (W of block b + 2^j = A^(96·2^j)·W of block b)."""
+    device = torch.device(device)
+    if n == 0:
+        return torch.zeros(0, dtype=torch.int64, device=device)
+    b0, b1 = k0 // 16, (k0 + n + 15) // 16
+    nb = b1 - b0
+    # the window at bit 96·b0 (negative positions — the pre-roll before global symbol 0 — by the period 2^31 − 1)
+    W = torch.tensor([prbs31_jump(prbs31_w0(seed), (96 * b0) % PRBS_PERIOD)], dtype=torch.int64, device=device)
+    j = 0
+    while W.numel() < nb:
+        # A^(96·2^j) = (A^96)^(2^j): columns from repeated squaring of A^96
+        key = ("b96", j)
+        if key not in _PRBS_POW:
+            if j == 0:
+                c96 = [prbs31_jump(1 << i, 96) for i in range(31)]
+            else:
+                prev = _PRBS_POW[("b96", j - 1)]
+                c96 = [_gf2_apply(prev, c) for c in prev]
+            _PRBS_POW[key] = c96
+        W = torch.cat([W, _gf2_apply(_PRBS_POW[key], W)])
+        j += 1
+    W = W[:nb]
+    m28 = (1 << 28) - 1
+    n1 = ((W >> 3) ^ W) & m28                                           # b[31 .. 58]
+    W1 = (W >> 28) | (n1 << 3)
+    n2 = ((W1 >> 3) ^ W1) & m28                                         # b[59 .. 86]
+    W2 = (W1 >> 28) | (n2 << 3)
+    n3 = ((W2 >> 3) ^ W2) & m28                                         # b[87 .. 114]
+    lo = W | (n1 << 31) | ((n2 & 31) << 59)                             # b[0 .. 63]
+    hi = (n2 >> 5) | (n3 << 23)                                         # b[64 .. 114]
+    kk = torch.arange(k0, k0 + n, dtype=torch.int64, device=device)
+    bi = kk // 16 - b0
+    off = 6 * (kk % 16)                                                 # 0 … 90
+    lo_k, hi_k = lo[bi], hi[bi]
+    # 6 bits starting at off from the 128-bit (hi:lo); lo is a signed int64: mask after the shift
+    lo_mask = torch.where(off <= 58, torch.full_like(off, 63), (1 << (64 - off).clamp(min=0, max=6)) - 1)
+    from_lo = (lo_k >> off.clamp(max=63)) & lo_mask                     # (arithmetic shift: keep only real bits)
+    from_lo = torch.where(off < 64, from_lo, torch.zeros_like(from_lo))
+    sh_hi = (64 - off).clamp(min=0)                                     # hi bits land at position 64 − off
+    from_hi = torch.where(off >= 64, (hi_k >> (off - 64).clamp(min=0)), (hi_k << sh_hi.clamp(max=63)))
+    return (from_lo | from_hi) & 63
 
 
 def _symbols(cfg: LinkConfig, k: torch.Tensor) -> torch.Tensor:
@@ -349,5 +466,5 @@ WORKLOADS = {
     "C4": dict(cfg=LinkConfig(formats=(4,), dl_ps_nm=200000.0, cspr_db=12.0, esn0_db=12.0, seed=401),
                samples=1 << 26),
     "C5": dict(cfg=LinkConfig(formats=(4, 8, 16, 32, 64), segment_frames=256, dl_ps_nm=32000.0,
-                              cspr_db=12.0, esn0_db=26.0, seed=501), samples=1 << 32),
+                              cspr_db=12.0, esn0_db=26.0, seed=501, label_source="prbs31"), samples=1 << 32),
 }

@@ -287,7 +287,7 @@ kk_status validate(const kk_config& c, std::string& why) {
   if (!(c.fs_hz > 0) || !(c.baud_hz > 0) || std::fabs(c.fs_hz / c.baud_hz - 4.0) > 1e-9) return bad("fs/baud must be 4");
   if (c.debug_guard != 0 && c.debug_guard != 1) return bad("debug_guard must be 0 or 1");
   if (c.upsample != 1 && c.upsample != 2) return bad("upsample must be 1 or 2");
-  if (c.ref_prbs != 0 && c.ref_prbs != 1) return bad("ref_prbs must be 0 or 1");
+  if (c.ref_prbs < 0 || c.ref_prbs > 2) return bad("ref_prbs must be 0, 1 (transmitter hash) or 2 (PRBS-31)");
   if (c.lo_den <= 0 || c.lo_den > 4096 || c.lo_num < 0 || c.lo_num >= c.lo_den) return bad("lo_num/lo_den out of range");
   if (c.sideband != 1 && c.sideband != -1) return bad("sideband must be +1 or -1");
   if (!(c.rolloff > 0 && c.rolloff <= 1)) return bad("rolloff must be in (0,1]");
@@ -563,7 +563,8 @@ kk_status kk_init(const kk_config* cfg, kk_ctx** out) {
   chk(dalloc(c, "counters", &c->d_counters, 32 * sizeof(unsigned long long)));
   if (cfg->ref_prbs) {
     chk(dalloc(c, "refgen", &c->d_refgen, (size_t)(n / 4)));
-    c->ref_key = kk::ref_prbs_key(cfg->ref_seed);
+    c->ref_key = cfg->ref_prbs == 2 ? kk::ref_prbs31_w0(cfg->ref_seed) : kk::ref_prbs_key(cfg->ref_seed);
+    if (cfg->ref_prbs == 2) chk(kk::ref_prbs31_init());
   }
   chk(cudaMemset(c->d_counters, 0, 32 * sizeof(unsigned long long)));
   if (e == cudaSuccess) {
@@ -616,7 +617,10 @@ kk_status kk_process_frames_ex(kk_ctx* c, const void* d_adc, int64_t first, int6
   const int F = kk::kFrameSamp;
   if (!d_ref && cf.ref_prbs) {                   // the transmitter's known labels, generated on the device
     NvtxRange r_("kk::ref_prbs");
-    kk::launch_ref_prbs(c->d_refgen, first / 4, n / 4, c->ref_key, c->d_sched, cf.n_segments, cf.segment_frames, s);
+    if (cf.ref_prbs == 2)
+      kk::launch_ref_prbs31(c->d_refgen, first / 4, n / 4, c->ref_key, c->d_sched, cf.n_segments, cf.segment_frames, s);
+    else
+      kk::launch_ref_prbs(c->d_refgen, first / 4, n / 4, c->ref_key, c->d_sched, cf.n_segments, cf.segment_frames, s);
     d_ref = c->d_refgen;
   }
 

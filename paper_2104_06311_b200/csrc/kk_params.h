@@ -98,6 +98,11 @@ bool k3_encode_ymaps(const float2* y, int64_t n_float2, CUtensorMap* maps);
 uint32_t ref_prbs_key(uint32_t seed);
 void launch_ref_prbs(uint8_t* out, int64_t sym0, int64_t n_sym, uint32_t key, const uint8_t* schedule,
                      int n_segments, int64_t segment_frames, cudaStream_t s);
+// ITU-T O.150 PRBS-31 labels (kk_config.ref_prbs = 2): init once (constant-memory jump matrices), then launch.
+uint32_t ref_prbs31_w0(uint32_t seed);
+cudaError_t ref_prbs31_init();
+void launch_ref_prbs31(uint8_t* out, int64_t sym0, int64_t n_sym, uint32_t w0, const uint8_t* schedule,
+                       int n_segments, int64_t segment_frames, cudaStream_t s);
 
 // K3 (paper arrangement): 4-tap T/2-spaced widely-linear DDLMS, one thread per restart block.
 void launch_k3_ddlms(const float2* y, int64_t y_base, int64_t sym_first, int64_t n_blocks, int B, int W,

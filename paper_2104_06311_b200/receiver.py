@@ -23,7 +23,8 @@ class Receiver:
                  eq_mode: str = "block_ls", ddlms_block: int = 512, ddlms_warmup: int = 1024,
                  ddlms_mu_warm: float = 2e-3, ddlms_mu: float = 2.5e-4, ddlms_mu_mid: float = 5e-4,
                  debug_guard: bool = False,
-                 upsample: int = 1, mf_fft_n: int = 4096, ref_prbs_seed: Optional[int] = None):
+                 upsample: int = 1, mf_fft_n: int = 4096, ref_prbs_seed: Optional[int] = None,
+                 ref_prbs_kind: str = "hash"):
         cfg = kkrx.kk_config_default()
         cfg.adc_scale, cfg.adc_offset, cfg.ref_intensity = adc_scale, adc_offset, ref_intensity
         cfg.dispersion_ps_per_nm = dispersion_ps_per_nm
@@ -45,7 +46,8 @@ class Receiver:
         cfg.upsample = upsample
         cfg.mf_fft_n, cfg.mf_hop = mf_fft_n, mf_fft_n - 1024      # MF overlap-save grid (4096/3072 or 8192/7168)
         if ref_prbs_seed is not None:                                # the transmitter's known labels, generated on the GPU
-            cfg.ref_prbs, cfg.ref_seed = 1, ref_prbs_seed & 0xFFFFFFFF
+            cfg.ref_prbs = {"hash": 1, "prbs31": 2}[ref_prbs_kind]      # the synthetic hash | ITU-T PRBS-31
+            cfg.ref_seed = ref_prbs_seed & 0xFFFFFFFF
         fm = list(formats)
         self._sched = (ctypes.c_uint8 * len(fm))(*fm)
         cfg.format_schedule = ctypes.cast(self._sched, ctypes.POINTER(ctypes.c_uint8))

@@ -16,11 +16,12 @@ HALO = 16640
 
 
 def make_case(M=4, dl=0.0, cspr=12.0, esn0=None, n=1 << 16, first=2 * F, seed=7, noise="white", formats=None,
-              segment_frames=1 << 30, wander_rad=0.0, wander_hz=50e3, linewidth_hz=0.0, sideband=1, **ocfg_kw):
+              segment_frames=1 << 30, wander_rad=0.0, wander_hz=50e3, linewidth_hz=0.0, sideband=1,
+              label_source="hash", **ocfg_kw):
     formats = tuple(formats) if formats else (M,)
     lc = kkgen.LinkConfig(formats=formats, segment_frames=segment_frames, dl_ps_nm=dl, cspr_db=cspr,
                           esn0_db=esn0, seed=seed, noise=noise, wander_rad=wander_rad, wander_hz=wander_hz,
-                          linewidth_hz=linewidth_hz, sideband=sideband)
+                          linewidth_hz=linewidth_hz, sideband=sideband, label_source=label_source)
     ocfg = R.OracleConfig(dispersion_ps_per_nm=dl, adc_scale=lc.adc_scale, ref_intensity=lc.i_ref,
                           formats=formats, segment_frames=segment_frames, sideband=sideband, **ocfg_kw)
     H = R.halo(ocfg)                      # 16640, or 16656 with upsample = 2 (= kk_halo)

@@ -88,3 +88,40 @@ def test_differential_phase_noise_statistics():
     c1 = np.corrcoef(d[:-1], d[1:])[0, 1]
     c4 = np.corrcoef(d[:-4], d[4:])[0, 1]
     assert abs(c1 - (2 + math.sqrt(0.32)) / 3.32) < 0.01 and abs(c4) < 0.01
+
+
+def test_prbs31_labels_follow_the_recurrence():
+    """ITU-T O.150 PRBS-31 (x^31 + x^28 + 1): kkgen's block/jump-ahead generation equals the plain bit-by-bit
+    recurrence b[n] = b[n−28] ⊕ b[n−31] from the seed's initial word, for arbitrary symbol ranges (slot(k) = bits
+    6k … 6k+5, LSB first)."""
+    for seed in (7, 501):
+        w = kkgen.prbs31_w0(seed)
+        b = [(w >> i) & 1 for i in range(31)]
+        while len(b) < 6 * 5000 + 64:
+            b.append(b[-28] ^ b[-31])
+        ref = torch.tensor([sum(b[6 * k + t] << t for t in range(6)) for k in range(5000)])
+        for k0, n in ((0, 5000), (7, 333), (16 * 40 + 5, 1200), (4999, 1)):
+            assert torch.equal(kkgen.prbs31_slots(seed, k0, n), ref[k0:k0 + n])
+
+
+def test_prbs31_period_and_negative_positions():
+    """A has order 2^31 − 1 (a primitive polynomial; 2^31 − 1 is prime, so no proper divisor returns to W0);
+    negative symbol indices (the generator's pre-roll) continue the same periodic stream."""
+    w = kkgen.prbs31_w0(3)
+    assert kkgen.prbs31_jump(w, kkgen.PRBS_PERIOD) == w
+    assert kkgen.prbs31_jump(w, 1) != w and kkgen.prbs31_jump(w, kkgen.PRBS_PERIOD - 1) != w
+    a = kkgen.prbs31_slots(3, -100, 300)
+    assert torch.equal(a[100:], kkgen.prbs31_slots(3, 0, 200))
+    # slot(−1) = bits −6 … −1 = bits P−6 … P−1 of one period
+    tail = kkgen.prbs31_jump(w, kkgen.PRBS_PERIOD - 6)
+    assert int(a[99]) == (tail & 63)
+
+
+def test_prbs31_link_labels_are_balanced_and_generated():
+    cfg = kkgen.LinkConfig(formats=(16, 64), segment_frames=1, seed=11, label_source="prbs31")
+    k = torch.arange(0, 4 * 4096, dtype=torch.int64)
+    lab = kkgen.symbol_labels(cfg, k).numpy()
+    assert lab[:4096].max() <= 15 and lab[4096:8192].max() <= 63
+    assert abs(np.mean(np.unpackbits(lab[4096:8192, None], axis=1)[:, 2:]) - 0.5) < 0.02
+    g = kkgen.generate(cfg, -16640, 16384 + 16640)
+    assert torch.equal(g["labels"], kkgen.symbol_labels(cfg, torch.arange(-4160, 8256, dtype=torch.int64)))

@@ -27,20 +27,25 @@ def _run(case, rx, with_ref, host=False):
     return rx.stats(), dec.cpu()
 
 
-@pytest.mark.parametrize("first,eq_mode,host", [(5 * F, "block_ls", False), ((1 << 34) + 3 * F, "block_ls", False),
-                                                (5 * F, "block_ls", True), (7 * F, "ddlms", False)])
-def test_generated_reference_equals_label_buffer(first, eq_mode, host):
+@pytest.mark.parametrize("first,eq_mode,host,kind", [(5 * F, "block_ls", False, "hash"),
+                                                     ((1 << 34) + 3 * F, "block_ls", False, "hash"),
+                                                     (5 * F, "block_ls", True, "hash"), (7 * F, "ddlms", False, "hash"),
+                                                     (5 * F, "block_ls", False, "prbs31"),
+                                                     ((1 << 36) + 9 * F, "block_ls", True, "prbs31"),
+                                                     (7 * F, "ddlms", False, "prbs31")])
+def test_generated_reference_equals_label_buffer(first, eq_mode, host, kind):
     """Mixed 4/8/16/32/64-QAM (one format per frame) with errors; symbol indices past 2^32 exercise the hash's
-    high word."""
+    high word and, for the ITU-T PRBS-31 stream (kk_config.ref_prbs = 2), the jump-ahead past many periods."""
     case = make_case(formats=(4, 8, 16, 32, 64), segment_frames=1, dl=32000.0, cspr=10.0, esn0=14.0, n=10 * F,
-                     first=first, seed=977, eq_mode=eq_mode)
+                     first=first, seed=977, eq_mode=eq_mode, label_source=kind)
     s_buf, d_buf = _run(case, receiver_for(case, keep=False), True, host)
-    rx = receiver_for(case, keep=False, ref_prbs_seed=case["lc"].seed)
+    rx = receiver_for(case, keep=False, ref_prbs_seed=case["lc"].seed, ref_prbs_kind=kind)
     s_gen, d_gen = _run(case, rx, False, host)
     assert sum(s_buf["sym_err"]) > 0 and sum(s_buf["sym"]) == 10 * F // 4
     for k in ("sym", "sym_err", "bits", "bit_err"):
         assert list(s_gen[k]) == list(s_buf[k]), k
     assert torch.equal(d_gen, d_buf)
     # a label buffer still wins over the generator
-    s_both, _ = _run(case, receiver_for(case, keep=False, ref_prbs_seed=case["lc"].seed ^ 1), True, host)
+    s_both, _ = _run(case, receiver_for(case, keep=False, ref_prbs_seed=case["lc"].seed ^ 1, ref_prbs_kind=kind), True,
+                     host)
     assert list(s_both["sym_err"]) == list(s_buf["sym_err"])
