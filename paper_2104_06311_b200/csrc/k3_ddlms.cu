@@ -34,6 +34,9 @@ k3_ddlms_kernel(const float2* __restrict__ y, int64_t y_base, int64_t sym_first,
                 const int* __restrict__ clampcnt, int64_t clamp_frame_off, const uint8_t* __restrict__ ref,
                 uint8_t* __restrict__ dec, float2* __restrict__ zout, unsigned long long* __restrict__ counters,
                 K3DParams p) {
+  __shared__ uint8_t lut32[36];                              // 32-cross label table
+  cross32_lut_fill(lut32, threadIdx.x, K3D_THREADS);
+  __syncthreads();
   const int blk = blockIdx.x * K3D_THREADS + threadIdx.x;
   if (blk >= n_blocks) return;
   const int64_t n_keep0 = (int64_t)blk * B;                  // local index of the first kept symbol
@@ -49,9 +52,11 @@ k3_ddlms_kernel(const float2* __restrict__ y, int64_t y_base, int64_t sym_first,
   const int bi = (M == 4) ? 0 : (M == 8) ? 1 : (M == 16) ? 2 : (M == 32) ? 3 : 4;
   Slicer sl;
   sl.init(M);
+  sl.lut = lut32;
   // warm-up symbols before the frame start belong to frame f − 1 and are decided in its format (W < 4096)
   Slicer slp;
   slp.init(fmt(f - 1));
+  slp.lut = lut32;
   int ccount = 0;
   for (int q = 0; q < 32; ++q) ccount += __ldg(&clampcnt[clamp_frame_off + (int64_t)fl * 32 + q]);
   const bool dead = (ccount >= kFrameSamp);

@@ -256,6 +256,8 @@ k3_frame_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, cons
     return (int)p.schedule[(int)(((f / p.segment_frames) % p.n_segments + p.n_segments) % p.n_segments)];
   };
   if (tid == 0) mbar_init(bar, 1);
+  uint8_t* lut32 = reinterpret_cast<uint8_t*>(misc + 32);   // 32-cross label table (36 bytes)
+  cross32_lut_fill(lut32, tid, K3_THREADS);
   __syncthreads();
   if (tid == 0 && (int)blockIdx.x < n_frames) {
     if (dbl) { issue_ref(blockIdx.x, 0); issue_y(blockIdx.x); }
@@ -333,6 +335,7 @@ k3_frame_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, cons
     const int bi = (M == 4) ? 0 : (M == 8) ? 1 : (M == 16) ? 2 : (M == 32) ? 3 : 4;
     Slicer sl;
     sl.init(M);
+    sl.lut = lut32;
     // frame clamp count (K1's 32 per-block counts, landed with the samples) → dead-frame rule; every warp sums
     // them itself (fixed order), so no extra barrier
     int ccount = cc_s[lane];
@@ -643,27 +646,31 @@ uint32_t wadr[NW];
     // ---- decisions, counts, outputs: z = u·e^{−iϑ_b} (dead or silent frame: z = 0); rotation rA for the warp's
     //      first 256 symbols (s < 8), rB for the second
     int serr = 0, berr = 0;
-    if (SW && !zero && !sl.cross && ref_tma && dec && ((reinterpret_cast<uintptr_t>(dec) & 3) == 0) && !zout) {
-      // the common case (square/rectangular slicer, labels from shared memory, no z output): a lane's 4 consecutive
-      // symbols — one 16-B pair of us loads, one 32-bit label word, one 32-bit decision store per group
+    if (SW && !zero && ref_tma && dec && ((reinterpret_cast<uintptr_t>(dec) & 3) == 0) && !zout) {
+      // the common case (labels from shared memory, no z output): a lane's 4 consecutive symbols — one 16-B pair of
+      // us loads, one 32-bit label word, one 32-bit decision store per group (the 32-cross labels from the table)
+      auto groups = [&](auto lab_of) {
 #pragma unroll 2
-      for (int g = 0; g < NG; ++g) {
-        const int kl = G0(g);
-        const float2 r = (g < NG / 2) ? rA : rB;
-        const int q = kl >> 1;
-        const float4 a = us4[uswz(q)], b = us4[uswz(q + 1)];
-        const uint32_t rw = *reinterpret_cast<const uint32_t*>(ref_cur + kl);
-        const uint32_t l0 = (uint32_t)sl.label_sq(cmul(make_float2(a.x, a.y), r));
-        const uint32_t l1 = (uint32_t)sl.label_sq(cmul(make_float2(a.z, a.w), r));
-        const uint32_t l2 = (uint32_t)sl.label_sq(cmul(make_float2(b.x, b.y), r));
-        const uint32_t l3 = (uint32_t)sl.label_sq(cmul(make_float2(b.z, b.w), r));
-        const uint32_t lw = l0 | (l1 << 8) | (l2 << 16) | (l3 << 24);
-        // per-byte compares: symbol errors = nonzero bytes of lw ^ rw, bit errors = popc(lw ^ rw)
-        const uint32_t x = lw ^ rw;
-        serr += __popc(__vcmpne4(x, 0u)) >> 3;
-        berr += __popc(x);
-        *reinterpret_cast<uint32_t*>(dec + sym0 + kl) = lw;
-      }
+        for (int g = 0; g < NG; ++g) {
+          const int kl = G0(g);
+          const float2 r = (g < NG / 2) ? rA : rB;
+          const int q = kl >> 1;
+          const float4 a = us4[uswz(q)], b = us4[uswz(q + 1)];
+          const uint32_t rw = *reinterpret_cast<const uint32_t*>(ref_cur + kl);
+          const uint32_t l0 = (uint32_t)lab_of(cmul(make_float2(a.x, a.y), r));
+          const uint32_t l1 = (uint32_t)lab_of(cmul(make_float2(a.z, a.w), r));
+          const uint32_t l2 = (uint32_t)lab_of(cmul(make_float2(b.x, b.y), r));
+          const uint32_t l3 = (uint32_t)lab_of(cmul(make_float2(b.z, b.w), r));
+          const uint32_t lw = l0 | (l1 << 8) | (l2 << 16) | (l3 << 24);
+          // per-byte compares: symbol errors = nonzero bytes of lw ^ rw, bit errors = popc(lw ^ rw)
+          const uint32_t x = lw ^ rw;
+          serr += __popc(__vcmpne4(x, 0u)) >> 3;
+          berr += __popc(x);
+          *reinterpret_cast<uint32_t*>(dec + sym0 + kl) = lw;
+        }
+      };
+      if (sl.cross) groups([&](float2 z) { return sl.label(z); });
+      else groups([&](float2 z) { return sl.label_sq(z); });
     } else if (!SW && !zero && !sl.cross && ref_tma && dec && !zout) {
       auto fast = [&](int s, float2 r) {
         const int kl = KL(s);

@@ -292,11 +292,32 @@ __device__ __forceinline__ int cross32_label(int iI, int iQ) {
 // first; both are exact ceil semantics, they can differ only within one fp32 ulp of a boundary). A NaN input
 // clamps to the lowest level on both paths.
 constexpr float kSliceMagic = 12582912.0f;   // 1.5·2^23
+// 32-cross labels as a 36-entry table (cell iI + 6·iQ), for a shared-memory copy (one LDS per label)
+__device__ __forceinline__ void cross32_lut_fill(uint8_t* lut, int tid, int nthreads) {
+  for (int c = tid; c < 36; c += nthreads) lut[c] = (uint8_t)cross32_label(c % 6, c / 6);
+}
 struct Slicer {
   int mI, mQ, hb, cross;
   float s, inv_s;
   float sh, loI, hiI, loQ, hiQ;   // s/2; clamp bounds of t per axis
   int offI, offQ;                 // level index = bits(t) − off
+  const uint8_t* lut = nullptr;   // 32-cross label table in shared memory (nullptr: cross32_label)
+  __device__ __forceinline__ int xlabel(int iI, int iQ) const {
+    return lut ? (int)lut[iI + 6 * iQ] : cross32_label(iI, iQ);
+  }
+  // 32-cross: a corner cell (level 0 or 5 on both axes) goes to the nearer of its two inner neighbours (exact
+  // tie: the lower label) — done on t (one level = ±1.0 exactly), so the point keeps the FMA-pipe form below
+  __device__ __forceinline__ float2 cross_fix(float2 t, float2 z) const {
+    const int iI = __float_as_int(t.x) - offI, iQ = __float_as_int(t.y) - offQ;
+    if (__builtin_expect((0x21u >> iI) & (0x21u >> iQ) & 1u, 0)) {
+      const float ax = fabsf(z.x * s), ay = fabsf(z.y * s);
+      const int dQ = (iQ == 0) ? 1 : -1, dI = (iI == 0) ? 1 : -1;
+      bool moveQ = ax > ay;
+      if (__builtin_expect(ax == ay, 0)) moveQ = xlabel(iI, iQ + dQ) < xlabel(iI + dI, iQ);
+      if (moveQ) t.y += (float)dQ; else t.x += (float)dI;
+    }
+    return t;
+  }
   __device__ __forceinline__ void init(int M) {
     cross = (M == 32);
     if (M == 8) { mI = 4; mQ = 2; hb = 1; s = 2.44948974278317810f; }
@@ -350,12 +371,11 @@ struct Slicer {
   __device__ __forceinline__ float2 point_i(int iI, int iQ) const {
     return make_float2((float)(2 * iI - (mI - 1)) * inv_s, (float)(2 * iQ - (mQ - 1)) * inv_s);
   }
-  // decided point
+  // decided point (the 32-cross corner rule on t; point_t(t) = point_i of t's levels, bit for bit: both round the
+  // exact (2r − 1)/s once)
   __device__ __forceinline__ float2 point(float2 z) const {
-    if (!cross) return point_t(tq(z));
-    int iI, iQ;
-    levels(z, iI, iQ);
-    return point_i(iI, iQ);
+    const float2 t = tq(z);
+    return point_t(cross ? cross_fix(t, z) : t);
   }
   __device__ __forceinline__ int label_i(int iI, int iQ) const {
     return cross ? cross32_label(iI, iQ) : ((gray(iI) << hb) | gray(iQ));
@@ -366,9 +386,10 @@ struct Slicer {
     return (gray(__float_as_int(t.x) - offI) << hb) | gray(__float_as_int(t.y) - offQ);
   }
   __device__ __forceinline__ int label(float2 z) const {
-    int iI, iQ;
-    levels(z, iI, iQ);
-    return label_i(iI, iQ);
+    float2 t = tq(z);
+    if (cross) t = cross_fix(t, z);
+    const int iI = __float_as_int(t.x) - offI, iQ = __float_as_int(t.y) - offQ;
+    return cross ? xlabel(iI, iQ) : ((gray(iI) << hb) | gray(iQ));
   }
   // point and label of one decision from a single slicing (same values as point() / label())
   __device__ __forceinline__ float2 decide(float2 z, int& lab) const {
@@ -377,10 +398,9 @@ struct Slicer {
       lab = (gray(__float_as_int(t.x) - offI) << hb) | gray(__float_as_int(t.y) - offQ);
       return point_t(t);
     }
-    int iI, iQ;
-    levels(z, iI, iQ);
-    lab = cross32_label(iI, iQ);
-    return point_i(iI, iQ);
+    const float2 t = cross_fix(tq(z), z);
+    lab = xlabel(__float_as_int(t.x) - offI, __float_as_int(t.y) - offQ);
+    return point_t(t);
   }
 };
 
