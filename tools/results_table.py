@@ -1,5 +1,5 @@
-"""Render profiles/r01_results.md from the per-configuration bench lines in profiles/r01_configs/*.json
-(produced by tools/configs_run.sh on a B200)."""
+"""Render profiles/<tag>_results.md from the per-configuration bench lines in profiles/<tag>_configs/*.json
+(produced by tools/configs_run.sh on a B200).   usage: python tools/results_table.py [tag]"""
 import json
 import os
 import sys
@@ -9,14 +9,14 @@ NAMES = {"C1": "C1 4-QAM b2b, 2^16", "C2": "C2 16-QAM 5600 km, CSPR 6 dB @ OSNR 
          "C3": "C3 64-QAM 1600 km, Es/N0 26 dB, 2^24", "C4": "C4 4-QAM 10,000 km, Es/N0 12 dB, 2^26 (L = 15)",
          "C5": "C5 mixed 4→64-QAM 1600 km, 2^32/GPU", "C5_up2": "C5 with 2× KK upsampling (K1U)",
          "C5_ddlms": "C5, paper arrangement (static RRC×CD⁻¹ + 4-tap WL DDLMS)"}
-HDR = """# Round-1 results per BASELINE.json configuration (1× B200, final code of the round)
+HDR = """# Results per BASELINE.json configuration (1× B200, {tag})
 
 `bench.py --workload Cx --samples S` (device-resident inputs, calls of min(2^28, S) samples, CUDA-event
 timing, clocks 1965 MHz with no throttle reasons in every run). Kernel times are per call (µs, live events
 inside the timed region); "dominant kernel" is the roofline object of the line (algorithmic TFLOP/s — the
 real-arithmetic counts of DESIGN.md §5 — and the fraction of the 74.4 TFLOP/s FP32 peak); the oracle column is
 the fp64 oracle on a sample of the same stream on the box's host cores, and the last column the fraction of GPU
-decisions identical to the oracle's on that sample. Raw lines: `profiles/r01_configs/*.json`. Parity at these
+decisions identical to the oracle's on that sample. Raw lines: `profiles/{tag}_configs/*.json`. Parity at these
 full sizes is also asserted by `tests/test_gpu_fullsize.py`.
 
 | config | GS/s | RT factor | K1 µs | K2 µs | K3 µs | dominant kernel TFLOP/s (frac) | oracle MS/s (cores) | BER | decisions = oracle |
@@ -26,14 +26,16 @@ FOOT = """
 C1–C3 are smaller than one 2^28 call, so they are launch/occupancy-bound (C1: 4 frames); throughput is judged
 on C4/C5. C4 runs L = 15 taps (10,000 km), hence the slower K3. In the DDLMS row K3 is the sequential 4-tap
 equalizer (one thread per 256-symbol block) and K2 carries the complex static filter and the AGC segment sums;
-in the upsampling row K1 is K1U. End to end from pinned host memory (C5): the `e2e` / `e2e_uint8` keys of `profiles/r01_configs/C5.json`.
+in the upsampling row K1 is K1U; from round 2 "K3" is K3a + K3s + K3c. End to end from pinned host memory (C5): the `e2e` /
+`e2e_uint8` keys of `profiles/{tag}_configs/C5.json`.
 """
 
 
-def main(out=os.path.join(ROOT, "profiles", "r01_results.md")):
+def main(tag="r02"):
+    out = os.path.join(ROOT, "profiles", tag + "_results.md")
     rows = []
     for f, name in NAMES.items():
-        path = os.path.join(ROOT, "profiles", "r01_configs", f + ".json")
+        path = os.path.join(ROOT, "profiles", tag + "_configs", f + ".json")
         if not os.path.exists(path):
             continue
         d = json.loads(open(path).read().strip().splitlines()[-1])
@@ -46,7 +48,7 @@ def main(out=os.path.join(ROOT, "profiles", "r01_results.md")):
                     f"{k['K2_mf']['avg_ms'] * 1e3:.0f} | {k['K3_eq']['avg_ms'] * 1e3:.0f} | {r['kernel']} "
                     f"{r['achieved']:.1f} ({r['frac']:.3f}) | {c.get('value', 0) * 1e3:.1f} ({c.get('cores')}) | "
                     f"{ber or '0'} | {c.get('parity_decisions_identical', 0):.4f} |")
-    open(out, "w").write(HDR + "\n".join(rows) + "\n" + FOOT)
+    open(out, "w").write(HDR.format(tag=tag) + "\n".join(rows) + "\n" + FOOT.format(tag=tag))
     print("\n".join(rows))
 
 
