@@ -124,13 +124,14 @@ template <int K>
 struct K3Layout {
   static constexpr int L = 2 * K + 1;
   static constexpr int ND = 2 * K + 1;             // lags 0..2K for base i = −K (ρ = 0); 0..2K−1 for ρ = 1
-  // K ≤ 4: every lane works on groups of GS = 4 consecutive symbols (a group's K + 4 window pairs serve its 4
-  // symbols' windows: 2 instead of K + 1 16-B loads per symbol) on a frame buffer written by tensor TMA with the
-  // 64-B swizzle (conflict-free group loads); lags [0, LA) are summed in sweep A (with pass 1), [LA, ND) in
-  // sweep B (with p). K ≥ 5: one symbol at a time (GS = 1), plain bulk copy, all lags in sweep A.
-  static constexpr bool SW = (K <= 4);
-  static constexpr int GS = SW ? 4 : 1;
-  static constexpr int LA = SW ? (K + 2 < ND ? K + 2 : ND) : ND;
+  // Every lane works on groups of GS consecutive symbols (a group's K + GS window pairs serve its GS symbols'
+  // windows) on a frame buffer written by tensor TMA with the 64-B swizzle (conflict-free group loads). K ≤ 4:
+  // GS = 4, lags [0, LA) in sweep A (with pass 1), [LA, ND) in sweep B (with p). K ≥ 5 (L ≥ 11): GS = 2 (register
+  // budget), lags [0, 7) with pass 1 and [7, ND) in two passes of sweep A, sweep B carries p only.
+  static constexpr bool SW = true;
+  static constexpr int GS = (K <= 4) ? 4 : 2;
+  static constexpr int LA = (K <= 4) ? (K + 2 < ND ? K + 2 : ND) : ND;   // lags of sweep A
+  static constexpr int LA1 = (K <= 4) ? LA : 7;                         // … of its first pass (with pass 1)
   static constexpr int LB = ND - LA;
   static constexpr int N = 2 * L;                  // real system size
   static constexpr int NP = 4 * L;                 // p floats: p1, p2 complex
@@ -307,6 +308,20 @@ k3_frame_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, cons
   float4* us4 = reinterpret_cast<float4*>(smem + Lay::US);
   auto uswz = [](int q) { return SW ? (q ^ ((q >> 3) & 1)) : q; };
   auto uget = [&](int kl) -> float2 { const int q = kl >> 1; return us[2 * uswz(q) + (kl & 1)]; };
+  auto ustore = [&](int g, const float2 (&v)[GS]) {        // the group's GS per-symbol values, 16 B at a time
+    const int q = G0(g) >> 1;
+#pragma unroll
+    for (int h = 0; h < GS / 2; ++h) us4[uswz(q + h)] = make_float4(v[2 * h].x, v[2 * h].y, v[2 * h + 1].x, v[2 * h + 1].y);
+  };
+  auto uload = [&](int g, float2 (&v)[GS]) {
+    const int q = G0(g) >> 1;
+#pragma unroll
+    for (int h = 0; h < GS / 2; ++h) {
+      const float4 a = us4[uswz(q + h)];
+      v[2 * h] = make_float2(a.x, a.y);
+      v[2 * h + 1] = make_float2(a.z, a.w);
+    }
+  };
   auto load_window = [&](int kl, float2 (&w)[L]) {
 #pragma unroll
     for (int m = 0; m <= K; ++m) {
@@ -377,9 +392,10 @@ k3_frame_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, cons
         return y0;
       };
       if constexpr (SW) {
-        float acc[8 * LA];
+        constexpr int LA1 = Lay::LA1;
+        float acc[8 * LA1];
 #pragma unroll
-        for (int i = 0; i < 8 * LA; ++i) acc[i] = 0.f;
+        for (int i = 0; i < 8 * LA1; ++i) acc[i] = 0.f;
         float pw = 0.f;
 uint32_t wadr[NW];
         make_wadr(wadr);
@@ -392,17 +408,34 @@ uint32_t wadr[NW];
           for (int j = 0; j < GS; ++j) {
             float2 w[L];
             win(F, j, w);
-            lag_acc(acc, w, 0, LA);
+            lag_acc(acc, w, 0, LA1);
             y0[j] = pass1(w);
             pw = fmaf(y0[j].x, y0[j].x, fmaf(y0[j].y, y0[j].y, pw));
           }
-          const int q = G0(g) >> 1;                // y⁰ of the group (kept in us until sweep B)
-          us4[uswz(q)] = make_float4(y0[0].x, y0[0].y, y0[1].x, y0[1].y);
-          us4[uswz(q + 1)] = make_float4(y0[2].x, y0[2].y, y0[3].x, y0[3].y);
+          ustore(g, y0);                           // y⁰ of the group (kept in us until sweep B)
         }
-        warp_partials<8 * LA>(acc, red_w, Lay::NP, lane);
+        warp_partials<8 * LA1>(acc, red_w, Lay::NP, lane);
         pw = warp_sum(pw);
         if (lane == 0) red_w[Lay::IPOW] = pw;
+        if constexpr (LA > LA1) {                  // second pass: lags [LA1, LA)
+          float acc2[8 * (LA - LA1)];
+#pragma unroll
+          for (int i = 0; i < 8 * (LA - LA1); ++i) acc2[i] = 0.f;
+          uint32_t wadr2[NW];
+          make_wadr(wadr2);
+#pragma unroll 1
+          for (int g = 0; g < NG; ++g) {
+            float4 F[NW];
+            load_group(wadr2, g, F);
+#pragma unroll
+            for (int j = 0; j < GS; ++j) {
+              float2 w[L];
+              win(F, j, w);
+              lag_acc(acc2, w, LA1, LA - LA1);
+            }
+          }
+          warp_partials<8 * (LA - LA1)>(acc2, red_w, Lay::NP + 8 * LA1, lane);
+        }
       } else {
 #pragma unroll
       for (int grp = 0; grp < Lay::NRG; ++grp) {
@@ -463,10 +496,8 @@ uint32_t wadr[NW];
         for (int g = 0; g < NG; ++g) {
           float4 F[NW];
           load_group(wadr, g, F);
-          const int q = G0(g) >> 1;
-          const float4 ya = us4[uswz(q)], yb = us4[uswz(q + 1)];
-          const float2 y0[4] = {make_float2(ya.x, ya.y), make_float2(ya.z, ya.w), make_float2(yb.x, yb.y),
-                                make_float2(yb.z, yb.w)};
+          float2 y0[GS];
+          uload(g, y0);
 #pragma unroll
           for (int j = 0; j < GS; ++j) {
             float2 w[L];
@@ -553,9 +584,7 @@ uint32_t wadr[NW];
               win(F, j, w);
               o[j] = pass2(w);
             }
-            const int q = G0(g) >> 1;
-            us4[uswz(q)] = make_float4(o[0].x, o[0].y, o[1].x, o[1].y);
-            us4[uswz(q + 1)] = make_float4(o[2].x, o[2].y, o[3].x, o[3].y);
+            ustore(g, o);
           }
         } else {
 #pragma unroll 2
@@ -599,10 +628,10 @@ uint32_t wadr[NW];
         };
         if constexpr (SW) {
           auto grp = [&](int g, float& cr, float& ci) {
-            const int q = G0(g) >> 1;
-            const float4 a = us4[uswz(q)], b = us4[uswz(q + 1)];
-            prod(make_float2(a.x, a.y), cr, ci); prod(make_float2(a.z, a.w), cr, ci);
-            prod(make_float2(b.x, b.y), cr, ci); prod(make_float2(b.z, b.w), cr, ci);
+            float2 v[GS];
+            uload(g, v);
+#pragma unroll
+            for (int j = 0; j < GS; ++j) prod(v[j], cr, ci);
           };
 #pragma unroll
           for (int g = 0; g < NG / 2; ++g) grp(g, cr0, ci0);
@@ -654,19 +683,19 @@ uint32_t wadr[NW];
         for (int g = 0; g < NG; ++g) {
           const int kl = G0(g);
           const float2 r = (g < NG / 2) ? rA : rB;
-          const int q = kl >> 1;
-          const float4 a = us4[uswz(q)], b = us4[uswz(q + 1)];
-          const uint32_t rw = *reinterpret_cast<const uint32_t*>(ref_cur + kl);
-          const uint32_t l0 = (uint32_t)lab_of(cmul(make_float2(a.x, a.y), r));
-          const uint32_t l1 = (uint32_t)lab_of(cmul(make_float2(a.z, a.w), r));
-          const uint32_t l2 = (uint32_t)lab_of(cmul(make_float2(b.x, b.y), r));
-          const uint32_t l3 = (uint32_t)lab_of(cmul(make_float2(b.z, b.w), r));
-          const uint32_t lw = l0 | (l1 << 8) | (l2 << 16) | (l3 << 24);
+          float2 v[GS];
+          uload(g, v);
+          const uint32_t rw = (GS == 4) ? *reinterpret_cast<const uint32_t*>(ref_cur + kl)
+                                        : (uint32_t)*reinterpret_cast<const uint16_t*>(ref_cur + kl);
+          uint32_t lw = 0u;
+#pragma unroll
+          for (int j = 0; j < GS; ++j) lw |= (uint32_t)lab_of(cmul(v[j], r)) << (8 * j);
           // per-byte compares: symbol errors = nonzero bytes of lw ^ rw, bit errors = popc(lw ^ rw)
           const uint32_t x = lw ^ rw;
           serr += __popc(__vcmpne4(x, 0u)) >> 3;
           berr += __popc(x);
-          *reinterpret_cast<uint32_t*>(dec + sym0 + kl) = lw;
+          if constexpr (GS == 4) *reinterpret_cast<uint32_t*>(dec + sym0 + kl) = lw;
+          else *reinterpret_cast<uint16_t*>(dec + sym0 + kl) = (uint16_t)lw;
         }
       };
       if (sl.cross) groups([&](float2 z) { return sl.label(z); });
