@@ -128,7 +128,6 @@ struct K3Layout {
   // windows) on a frame buffer written by tensor TMA with the 64-B swizzle (conflict-free group loads). K ≤ 4:
   // GS = 4, lags [0, LA) in sweep A (with pass 1), [LA, ND) in sweep B (with p). K ≥ 5 (L ≥ 11): GS = 2 (register
   // budget), lags [0, 7) with pass 1 and [7, ND) in two passes of sweep A, sweep B carries p only.
-  static constexpr bool SW = true;
   static constexpr int GS = (K <= 4) ? 4 : 2;
   static constexpr int LA = (K <= 4) ? (K + 2 < ND ? K + 2 : ND) : ND;   // lags of sweep A
   static constexpr int LA1 = (K <= 4) ? LA : 7;                         // … of its first pass (with pass 1)
@@ -141,7 +140,7 @@ struct K3Layout {
   static constexpr int NRED = ((NP + NR + 1 + 31) / 32) * 32;   // + frame power
   static constexpr int IPOW = NP + NR;             // index of the frame power in the reduction
   static constexpr int YS = 2 * kFrameSym + 2 * K; // float2 used per frame (y_s[0 .. 8191 + 2K])
-  static constexpr int YB = SW ? (1024 + 8) * 64 : YS * 8;   // frame buffer bytes (SW: 8 × 128 + 8 rows of 64 B)
+  static constexpr int YB = (1024 + 8) * 64;        // frame buffer bytes: 8 × 128 + 8 rows of 64 B (tensor TMA)
   static constexpr int WS = N + 3;                 // odd row stride (doubles) of the real system [A | q1 q2]
   static constexpr int RED_B = K3_WARPS * NRED * 4;
   static constexpr int MAT_B = N * WS * 8;
@@ -200,7 +199,6 @@ k3_frame_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, cons
                 const __grid_constant__ CUtensorMap ymap, const __grid_constant__ CUtensorMap ymap_tail) {
   using Lay = K3Layout<K>;
   constexpr int L = Lay::L, ND = Lay::ND, N = Lay::N, NRED = Lay::NRED;
-  constexpr bool SW = Lay::SW;
   constexpr int GS = Lay::GS, NG = K3_SPT / GS, NW = K + GS, LA = Lay::LA, LB = Lay::LB;
   extern __shared__ __align__(1024) unsigned char smem[];
   float2* ys = reinterpret_cast<float2*>(smem + Lay::Y);
@@ -233,12 +231,10 @@ k3_frame_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, cons
   auto issue_y = [&](int fl) {
     fence_proxy_async_smem();                     // the frame buffer was written by generic stores (CPR products)
     if (!dbl) mbar_arrive_expect_tx(bar, YBYTES + 128u + TBYTES + (ref_tma ? (uint32_t)kFrameSym : 0u));
-    if constexpr (SW) {                           // 8 boxes of 128 rows + one of 8 rows (64-B rows of 8 float2)
+    {                           // 8 boxes of 128 rows + one of 8 rows (64-B rows of 8 float2)
 #pragma unroll
       for (int b = 0; b < 8; ++b) tma_tensor_2d(smem + Lay::Y + b * 8192, &ymap, 0, fl * 1024 + 128 * b, bar);
       tma_tensor_2d(smem + Lay::Y + 65536, &ymap_tail, 0, fl * 1024 + 1024, bar);
-    } else {
-      tma_bulk_g2s(ys, y + (int64_t)fl * (2 * kFrameSym), YBYTES, bar);
     }
     tma_bulk_g2s(smem + Lay::CC, clampcnt + clamp_frame_off + (int64_t)fl * 32, 128u, bar);
     if constexpr (PH == 1) tma_bulk_g2s(th, threc + (int64_t)fl * K3Rec<K>::TREC, TBYTES, bar);
@@ -269,18 +265,15 @@ k3_frame_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, cons
 #pragma unroll
   for (int e = 0; e < L; ++e) wc[e] = __ldg(&w_cd[e]);    // w_cd[a], a = j + K; tap j ↔ window index e
 
-  // tap window of local symbol kl: w[e] = y_s[2kl + 2K − e] = y[2k − (e − K)], e = 0..2K;
-  // loaded as K+1 16-B pairs (y_s[2kl + 2m], y_s[2kl + 2m + 1]) = (w[2K − 2m], w[2K − 2m − 1])
-  // symbol ownership: warp w owns the 512 consecutive symbols [512w, 512w + 512), lane l the 16 symbols
-  // 512w + 32s + l (s < 16) — each warp-wide access covers 32 consecutive symbols (conflict-free 16-B window
-  // loads), and a 256-symbol CPR window is one half of a warp (s < 8 or s ≥ 8)
-  auto KL = [&](int s) { return 512 * warp + 32 * s + lane; };
-  // groups (GS consecutive symbols per lane): the lane's group g starts at symbol G0(g); 32·GS symbols per warp step
+  // tap window of local symbol kl: w[e] = y_s[2kl + 2K − e] = y[2k − (e − K)], e = 0..2K, i.e. the K+1 16-B pairs
+  // (y_s[2kl + 2m], y_s[2kl + 2m + 1]) = (w[2K − 2m], w[2K − 2m − 1]). Symbol ownership: warp w owns the 512
+  // consecutive symbols [512w, 512w + 512) — a 256-symbol CPR window is one half of a warp — in groups of GS
+  // consecutive symbols per lane: the lane's group g starts at symbol G0(g); 32·GS symbols per warp step
   auto G0 = [&](int g) { return 512 * warp + 32 * GS * g + GS * lane; };
   // frame buffer: float4 i (samples 2i, 2i + 1) lives at swz(i) — TMA SWIZZLE_64B XORs the 16-B chunk bits 4–5 of
   // the address with bits 7–8 (the buffer is 1024-B aligned); a group window is NW consecutive float4 from G0(g),
   // at the same lane-relative offsets for every g (32·GS·g float4 is a multiple of 4 rows of 128 B)
-  auto swz = [](int i) { return SW ? (i ^ ((i >> 3) & 3)) : i; };
+  auto swz = [](int i) { return i ^ ((i >> 3) & 3); };
   auto ysw = [&](int e) -> float2 { const int q = e >> 1; return ys[2 * swz(q) + (e & 1)]; };   // sample e
   // shared-memory byte address of the lane's window float4 t in group 0 (formed at the start of each sweep, so
   // that it is not live across the solve); group g adds 512·GS·g bytes
@@ -306,7 +299,7 @@ k3_frame_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, cons
   // per-symbol values (y⁰, then y¹) in groups: float4 q = symbols (2q, 2q + 1) at uswz(q) (conflict-free 16-B
   // accesses at the 32-B lane stride of 4-symbol groups)
   float4* us4 = reinterpret_cast<float4*>(smem + Lay::US);
-  auto uswz = [](int q) { return SW ? (q ^ ((q >> 3) & 1)) : q; };
+  auto uswz = [](int q) { return q ^ ((q >> 3) & 1); };
   auto uget = [&](int kl) -> float2 { const int q = kl >> 1; return us[2 * uswz(q) + (kl & 1)]; };
   auto ustore = [&](int g, const float2 (&v)[GS]) {        // the group's GS per-symbol values, 16 B at a time
     const int q = G0(g) >> 1;
@@ -320,14 +313,6 @@ k3_frame_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, cons
       const float4 a = us4[uswz(q + h)];
       v[2 * h] = make_float2(a.x, a.y);
       v[2 * h + 1] = make_float2(a.z, a.w);
-    }
-  };
-  auto load_window = [&](int kl, float2 (&w)[L]) {
-#pragma unroll
-    for (int m = 0; m <= K; ++m) {
-      const float4 v = ys4[kl + m];
-      w[2 * K - 2 * m] = make_float2(v.x, v.y);
-      if (m < K) w[2 * K - 2 * m - 1] = make_float2(v.z, v.w);
     }
   };
 
@@ -391,7 +376,7 @@ k3_frame_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, cons
         for (int e = 0; e < L; ++e) cmac2(y0, w[e], wc[e]);
         return y0;
       };
-      if constexpr (SW) {
+      {
         constexpr int LA1 = Lay::LA1;
         float acc[8 * LA1];
 #pragma unroll
@@ -436,32 +421,6 @@ uint32_t wadr[NW];
           }
           warp_partials<8 * (LA - LA1)>(acc2, red_w, Lay::NP + 8 * LA1, lane);
         }
-      } else {
-#pragma unroll
-      for (int grp = 0; grp < Lay::NRG; ++grp) {
-        constexpr int G = Lay::RG;
-        const int d0 = grp * G;
-        float acc[8 * G];
-#pragma unroll
-        for (int i = 0; i < 8 * G; ++i) acc[i] = 0.f;
-        float pw = 0.f;
-#pragma unroll 2
-        for (int s = 0; s < K3_SPT; ++s) {
-          float2 w[L];
-          load_window(KL(s), w);
-          lag_acc(acc, w, d0, G);
-          if (grp == 0) {                      // pass 1 (kept in us until sweep B) and its power
-            const float2 y0 = pass1(w);
-            us[KL(s)] = y0;
-            pw = fmaf(y0.x, y0.x, fmaf(y0.y, y0.y, pw));
-          }
-        }
-        warp_partials<8 * G>(acc, red_w, Lay::NP + 8 * d0, lane);
-        if (grp == 0) {
-          pw = warp_sum(pw);
-          if (lane == 0) red_w[Lay::IPOW] = pw;
-        }
-      }
       }
       __syncthreads();
       double P0 = 0.0;
@@ -475,7 +434,7 @@ uint32_t wadr[NW];
       if (!p0ok) flags |= kFlagSilent;
       if (p0ok) {
       // ---- sweep B: decisions on g·y⁰ and p1[e] = Σ conj(a_j)·d, p2[e] = Σ a_j·d  (a_j = w[e]);
-      //      (SW: plus the lags [LA, ND) of the lag sums)
+      //      (plus the lags [LA, ND) of the lag sums when K ≤ 4)
       auto p_acc = [&](float* acc, const float2 (&w)[L], float2 d) {
 #pragma unroll
         for (int e = 0; e < L; ++e) {       // (B1, B3) += ar·(dr, di), (B4, B2) += ai·(dr, di): p1, p2 later
@@ -483,7 +442,7 @@ uint32_t wadr[NW];
           ffma2s(acc[4 * e + 2], acc[4 * e + 3], w[e].y, d);
         }
       };
-      if constexpr (SW) {
+      {
         float acc[Lay::NP];
         float accl[8 * (LB > 0 ? LB : 1)];
 #pragma unroll
@@ -508,17 +467,6 @@ uint32_t wadr[NW];
         }
         warp_partials<Lay::NP>(acc, red_w, 0, lane);
         if constexpr (LB > 0) warp_partials<8 * LB>(accl, red_w, Lay::NP + 8 * LA, lane);
-      } else {
-        float acc[Lay::NP];
-#pragma unroll
-        for (int i = 0; i < Lay::NP; ++i) acc[i] = 0.f;
-#pragma unroll 2
-        for (int s = 0; s < K3_SPT; ++s) {
-          float2 w[L];
-          load_window(KL(s), w);
-          p_acc(acc, w, sl.point(cscale(us[KL(s)], g_agc)));
-        }
-        warp_partials<Lay::NP>(acc, red_w, 0, lane);
       }
       }
       __syncthreads();   // every read of the frame buffer is done: request the next frame now
@@ -570,7 +518,7 @@ uint32_t wadr[NW];
           gr += c.x; gi += c.y; gd = fmaf(dd.x, dd.x, fmaf(dd.y, dd.y, gd));
           return o;
         };
-        if constexpr (SW) {
+        {
 uint32_t wadr[NW];
           make_wadr(wadr);
 #pragma unroll 1
@@ -585,14 +533,6 @@ uint32_t wadr[NW];
               o[j] = pass2(w);
             }
             ustore(g, o);
-          }
-        } else {
-#pragma unroll 2
-          for (int s = 0; s < K3_SPT; ++s) {
-            const int kl = KL(s);
-            float2 w[L];
-            load_window(kl, w);
-            us[kl] = pass2(w);
           }
         }
       }
@@ -626,7 +566,7 @@ uint32_t wadr[NW];
           const float2 c = cmulc(uu, sl.point(uu));
           cr += c.x; ci += c.y;
         };
-        if constexpr (SW) {
+        {
           auto grp = [&](int g, float& cr, float& ci) {
             float2 v[GS];
             uload(g, v);
@@ -637,11 +577,6 @@ uint32_t wadr[NW];
           for (int g = 0; g < NG / 2; ++g) grp(g, cr0, ci0);
 #pragma unroll
           for (int g = NG / 2; g < NG; ++g) grp(g, cr1, ci1);
-        } else {
-#pragma unroll 4
-          for (int s = 0; s < K3_SPT / 2; ++s) prod(us[KL(s)], cr0, ci0);
-#pragma unroll 4
-          for (int s = K3_SPT / 2; s < K3_SPT; ++s) prod(us[KL(s)], cr1, ci1);
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
@@ -675,7 +610,7 @@ uint32_t wadr[NW];
     // ---- decisions, counts, outputs: z = u·e^{−iϑ_b} (dead or silent frame: z = 0); rotation rA for the warp's
     //      first 256 symbols (s < 8), rB for the second
     int serr = 0, berr = 0;
-    if (SW && !zero && ref_tma && dec && ((reinterpret_cast<uintptr_t>(dec) & 3) == 0) && !zout) {
+    if (!zero && ref_tma && dec && ((reinterpret_cast<uintptr_t>(dec) & 3) == 0) && !zout) {
       // the common case (labels from shared memory, no z output): a lane's 4 consecutive symbols — one 16-B pair of
       // us loads, one 32-bit label word, one 32-bit decision store per group (the 32-cross labels from the table)
       auto groups = [&](auto lab_of) {
@@ -700,24 +635,11 @@ uint32_t wadr[NW];
       };
       if (sl.cross) groups([&](float2 z) { return sl.label(z); });
       else groups([&](float2 z) { return sl.label_sq(z); });
-    } else if (!SW && !zero && !sl.cross && ref_tma && dec && !zout) {
-      auto fast = [&](int s, float2 r) {
-        const int kl = KL(s);
-        const int lab = sl.label_sq(cmul(us[kl], r));
-        const int rr = (int)ref_cur[kl];
-        serr += (lab != rr);
-        berr += __popc(lab ^ rr);
-        dec[sym0 + kl] = (uint8_t)lab;
-      };
-#pragma unroll 4
-      for (int s = 0; s < K3_SPT / 2; ++s) fast(s, rA);
-#pragma unroll 4
-      for (int s = K3_SPT / 2; s < K3_SPT; ++s) fast(s, rB);
     } else {
 #pragma unroll 4
       for (int s = 0; s < K3_SPT; ++s) {
-        const int kl = SW ? G0(s / GS) + (s % GS) : KL(s);
-        const float2 zz = zero ? make_float2(0.f, 0.f) : cmul(SW ? uget(kl) : us[kl], s < K3_SPT / 2 ? rA : rB);
+        const int kl = G0(s / GS) + (s % GS);
+        const float2 zz = zero ? make_float2(0.f, 0.f) : cmul(uget(kl), s < K3_SPT / 2 ? rA : rB);
         const int lab = sl.label(zz);
         if (ref) {
           const int r = ref_tma ? (int)ref_cur[kl] : (int)__ldg(&ref[sym0 + kl]);
