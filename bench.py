@@ -58,6 +58,8 @@ def parse():
     ap.add_argument("--eq-mode", default="block_ls", choices=["block_ls", "ddlms"],
                     help="block_ls: north-star per-frame WL least squares + CPR (default); "
                          "ddlms: the paper's static CD filter + 4-tap WL DDLMS")
+    ap.add_argument("--static-cd", action="store_true",
+                    help="block LS after the paper's static RRC x CD-inverse filter in K2 (L = 5; SURVEY NEXT-2)")
     ap.add_argument("--upsample", type=int, default=1, choices=[1, 2],
                     help="2: KK at 8 sps (half-band interpolation/decimation, K1U; DESIGN.md §3)")
     ap.add_argument("--ingest", default="local", choices=["local", "single"],
@@ -97,7 +99,7 @@ def k2_tile_flops(n: int) -> float:
 
 
 def kernel_units(chunk: int, L: int, eq_mode: str = "block_ls", ddlms_block: int = 512, ddlms_warmup: int = 1024,
-                 upsample: int = 1, mf_n: int = 4096):
+                 upsample: int = 1, mf_n: int = 4096, static_cd: bool = False):
     """Algorithmic flops and HBM bytes per launch of each kernel for one call of `chunk` samples."""
     K = (L - 1) // 2
     k1_samples = chunk + 2 * F
@@ -113,7 +115,7 @@ def kernel_units(chunk: int, L: int, eq_mode: str = "block_ls", ddlms_block: int
         k2_flops = k2_tile_flops(mf_n) + (mf_n // 2) * 8.0   # complex H: 8 more flops per folded bin
     else:
         k3 = dict(flops=k3_flops_per_symbol(L) * 4096 * frames, bytes=73728.0 * frames)
-        k2_flops = k2_tile_flops(mf_n)
+        k2_flops = k2_tile_flops(mf_n) + ((mf_n // 2) * 8.0 if static_cd else 0.0)   # complex H: +8 per folded bin
     # K1U (upsample 2), per output sample: FFT2048 pair 220 + decimation 50 + interpolation 27 + E₂ 13 + logs 7
     k1_flops = 317.0 if upsample == 2 else 107.0
     return {
@@ -216,7 +218,8 @@ def oracle_sample(runs, ocfg_kw, pool):
 def ocfg_kwargs(lc, eq_mode="block_ls", a=None):
     kw = dict(dispersion_ps_per_nm=lc.dl_ps_nm, adc_scale=lc.adc_scale, ref_intensity=lc.i_ref,
               formats=tuple(lc.formats), segment_frames=lc.segment_frames, eq_mode=eq_mode,
-              upsample=(a.upsample if a is not None else 1))
+              upsample=(a.upsample if a is not None else 1),
+              static_cd=bool(a.static_cd) if a is not None else False)
     if a is not None and eq_mode == "ddlms":
         kw.update(ddlms_block=a.ddlms_block, ddlms_warmup=a.ddlms_warmup, ddlms_mu_warm=a.ddlms_mu_warm)
     return kw
@@ -291,7 +294,7 @@ def e2e_uint8(a, lc, HALO, chunk, first, En, world, dev, SH, kkrx, kkgen, torch,
     h_dec = torch.empty(En // 4, dtype=torch.uint8, pin_memory=True)
     rx8 = Receiver(adc_scale=lc8.adc_scale, ref_intensity=lc8.i_ref, dispersion_ps_per_nm=lc8.dl_ps_nm,
                    formats=lc8.formats, segment_frames=lc8.segment_frames, max_samples_per_call=chunk, device=dev.index,
-                   input_uint8=True, upsample=a.upsample, mf_fft_n=a.mf_n,
+                   input_uint8=True, upsample=a.upsample, mf_fft_n=a.mf_n, static_cd=a.static_cd,
                    ref_prbs_seed=None if h_ref is not None else lc8.seed, ref_prbs_kind=lc8.label_source)
     rx8.process_host(h_codes, first, En, ref=h_ref, decisions=h_dec)          # warm-up
     if world > 1:
@@ -420,7 +423,7 @@ def main():
 
     rx = Receiver(adc_scale=lc.adc_scale, ref_intensity=lc.i_ref, dispersion_ps_per_nm=lc.dl_ps_nm,
                   formats=lc.formats, segment_frames=lc.segment_frames, max_samples_per_call=chunk, device=local,
-                  eq_mode=a.eq_mode, ddlms_block=a.ddlms_block, ddlms_warmup=a.ddlms_warmup,
+                  eq_mode=a.eq_mode, static_cd=a.static_cd, ddlms_block=a.ddlms_block, ddlms_warmup=a.ddlms_warmup,
                   ddlms_mu_warm=a.ddlms_mu_warm, upsample=a.upsample, mf_fft_n=a.mf_n)
     assert rx.halo == HALO
     L = rx.taps
@@ -471,7 +474,7 @@ def main():
         peak_fp32 = N_SMS * FP32_LANES_PER_SM * 2 * float(mp.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12
     except Exception:
         pass
-    units = kernel_units(chunk, L, a.eq_mode, a.ddlms_block, a.ddlms_warmup, a.upsample, a.mf_n)
+    units = kernel_units(chunk, L, a.eq_mode, a.ddlms_block, a.ddlms_warmup, a.upsample, a.mf_n, a.static_cd)
     traffic = {}
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
@@ -521,7 +524,7 @@ def main():
         else:                                                                # the receiver knows the transmitter's
             rxe = Receiver(adc_scale=lc.adc_scale, ref_intensity=lc.i_ref, dispersion_ps_per_nm=lc.dl_ps_nm,
                            formats=lc.formats, segment_frames=lc.segment_frames, max_samples_per_call=chunk,
-                           device=local, eq_mode=a.eq_mode, ddlms_block=a.ddlms_block, ddlms_warmup=a.ddlms_warmup,
+                           device=local, eq_mode=a.eq_mode, static_cd=a.static_cd, ddlms_block=a.ddlms_block, ddlms_warmup=a.ddlms_warmup,
                            ddlms_mu_warm=a.ddlms_mu_warm, upsample=a.upsample, mf_fft_n=a.mf_n,
                            ref_prbs_seed=lc.seed, ref_prbs_kind=lc.label_source)   # (kk_config.ref_prbs)
         h_dec = torch.empty(En // 4, dtype=torch.uint8, pin_memory=True)
@@ -600,6 +603,7 @@ def main():
                        "samples_per_gpu": S, "chunk_samples": chunk, "eq_taps": L, "eq_mode": a.eq_mode,
                        "parallelism": f"{world} contiguous frame-range shards + halos, counters allreduced",
                        "kk_upsample": a.upsample, "mf_grid": f"FFT{a.mf_n}/hop {a.mf_n - 1024}",
+                       "static_cd": bool(a.static_cd),
                        **({"ddlms_block": a.ddlms_block, "ddlms_warmup": a.ddlms_warmup,
                            "ddlms_mu_warm": a.ddlms_mu_warm} if a.eq_mode == "ddlms" else {}),
                        "l2": "inputs 8 GiB/GPU per step >> 126 MB L2, no flush needed", "seed": lc.seed},

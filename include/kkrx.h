@@ -111,6 +111,11 @@ typedef struct kk_config {
   uint32_t ref_seed;
   int32_t reserved2;
   double  ddlms_mu_mid;          /* 5e-4 step size over the second half of the warm-up     */
+  /* KK_EQ_BLOCK_LS only: 1 = the paper's static arrangement for the dispersion ("offline-optimized
+   * filter"): K2's static filter is RRC × CD inverse (as in KK_EQ_DDLMS) and the block-adaptive widely-linear
+   * FIR only trims the residual: θ₀ = the centre spike, L = eq_taps or 5 by default. */
+  int32_t static_cd;
+  int32_t reserved3;
 } kk_config;
 
 /* Counters (all uint64, summed over calls until kk_reset_stats; index i = log2(M) − 2 for M = 4..64).

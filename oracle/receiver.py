@@ -28,6 +28,7 @@ brute-force nearest point (O8–O10).
 """
 from __future__ import annotations
 
+import dataclasses
 import math
 from dataclasses import dataclass, field
 from typing import Optional, Sequence
@@ -67,6 +68,7 @@ class OracleConfig:
     segment_frames: int = 1 << 30
     # paper arrangement: eq_mode "ddlms" folds the CD inverse
     # into the static filter and equalizes with the 4-tap T/2-spaced widely-linear DDLMS
+    static_cd: bool = False           # block_ls after the paper's static RRC × CD-inverse filter (NEXT-2): θ₀ = spike
     eq_mode: str = "block_ls"         # "block_ls" (north star, default) | "ddlms" (paper, restart grid) |
                                       # "ddlms_seq" (paper, one recursion in stream order: the definition)
     ddlms_mu_warm: float = 2e-3       # step size over the first half of the warm-up
@@ -122,9 +124,12 @@ def beta2L(cfg: OracleConfig) -> float:
 
 
 def tap_count(cfg: OracleConfig) -> int:
-    """L = 2·⌈τ_max/(T/2)⌉ + 7, τ_max = |β₂L|·2π·(f_c + (1+β)R_s/2) (SURVEY §8(a) tap-count rule)."""
+    """L = 2·⌈τ_max/(T/2)⌉ + 7, τ_max = |β₂L|·2π·(f_c + (1+β)R_s/2) (SURVEY §8(a) tap-count rule); with the static
+    CD inverse in the MF (static_cd) the FIR only trims the residual: L = 5 unless set."""
     if cfg.eq_taps:
         return cfg.eq_taps
+    if cfg.static_cd and cfg.eq_mode == "block_ls":
+        return 5
     f_c = cfg.fs_hz * cfg.lo_num / cfg.lo_den
     tau = abs(beta2L(cfg)) * 2 * math.pi * (f_c + (1 + cfg.rolloff) * cfg.baud_hz / 2)
     return 2 * int(math.ceil(tau / (0.5 / cfg.baud_hz) - 1e-12)) + 7
@@ -470,10 +475,11 @@ def receive(codes: np.ndarray, first: int, n: int, cfg: OracleConfig, ref: Optio
     if seq:
         K = 2                                          # taps y[2n+1] … y[2n−2]
     m0, m1 = first // 2 - K, (first + n) // 2 + K
-    h = static_filter_taps(cfg) if (ddlms or seq) else rrc_taps(cfg)
+    h = static_filter_taps(cfg) if (ddlms or seq or cfg.static_cd) else rrc_taps(cfg)
     y = o7_matched_filter(b, e0, m0, m1, h)
     # O8–O10 per frame
-    w_cd = cd_init_taps(cfg)
+    # θ₀: the CD-inverse fit referenced to the carrier; the centre spike when the static filter already inverts CD
+    w_cd = cd_init_taps(dataclasses.replace(cfg, dispersion_ps_per_nm=0.0) if cfg.static_cd else cfg)
     Fs = cfg.frame_symbols
     nfr = n // F
     z = np.zeros(n // cfg.sps, complex)

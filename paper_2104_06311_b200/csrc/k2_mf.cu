@@ -260,7 +260,7 @@ k2_mf_kernel(const float2* __restrict__ E, int64_t E_first, const float2* __rest
           if constexpr (CH) pw[it][r] = (j & 1) ? 0.f : fmaf(v3[it][r].x, v3[it][r].x, v3[it][r].y * v3[it][r].y);
         }
       }
-      if constexpr (CH) {
+      if (CH && p.seg_pow) {                                  // (kernel-uniform; null without K3′)
         // per-256-symbol (512-sample) segment power for K3′'s AGC: output p = j + 256 r lies in tile segment
         // (r − 1)/2 for every j, so each thread sums its values per segment, then warp sums and the warps'
         // partials in fixed order → deterministic. Segment g (global) = m / 512.

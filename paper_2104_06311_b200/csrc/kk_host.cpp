@@ -313,6 +313,7 @@ kk_status validate(const kk_config& c, std::string& why) {
   }
   if (!(c.lambda_m > 0)) return bad("lambda_m must be > 0");
   if (c.eq_mode != KK_EQ_BLOCK_LS && c.eq_mode != KK_EQ_DDLMS) return bad("eq_mode");
+  if (c.static_cd != 0 && c.static_cd != 1) return bad("static_cd must be 0 or 1");
   if (c.eq_mode == KK_EQ_DDLMS) {
     if (c.ddlms_block < 256 || c.ddlms_block > kk::kFrameSym || !is_pow2(c.ddlms_block)) return bad("ddlms_block must be a power of two in [256, 4096]");
     // K2's outermost tiles must read E inside core ± one frame: with Ky = 2·W + 2 (2-sps margin) and
@@ -410,6 +411,7 @@ void kk_config_default(kk_config* c) {
   c->ddlms_mu_warm = 2e-3;
   c->ddlms_mu = 2.5e-4;
   c->ddlms_mu_mid = 5e-4;
+  c->static_cd = 0;
   c->upsample = 1;
   c->ref_prbs = 0;
   c->ref_seed = 0;
@@ -428,7 +430,8 @@ kk_status kk_init(const kk_config* cfg, kk_ctx** out) {
     return KK_ERR_CONFIG;
   }
   const bool ddlms = cfg->eq_mode == KK_EQ_DDLMS;
-  const int L = ddlms ? 3 : tap_rule(*cfg);   // (DDLMS mode: the block-LS taps are unused)
+  const bool scd = !ddlms && cfg->static_cd;  // block LS after the static CD inverse (NEXT-2 arrangement)
+  const int L = ddlms ? 3 : scd ? (cfg->eq_taps ? cfg->eq_taps : 5) : tap_rule(*cfg);   // (DDLMS: LS taps unused)
   if (L < 3 || L > 2 * kk::kMaxK + 1 || (L % 2) == 0) {
     std::fprintf(stderr, "kk_init: tap-count rule gives L=%d outside [3,15]\n", L);
     return KK_ERR_CONFIG;
@@ -481,7 +484,7 @@ kk_status kk_init(const kk_config* cfg, kk_ctx** out) {
   // j = −512..512 (the same definition as oracle.receiver.static_filter_taps: the taps live on the 4096 grid
   // whatever the MF grid), ×1/NM folded in
   std::vector<float2> Hc;
-  if (ddlms) {
+  if (ddlms || scd) {
     const int N = 4096;
     std::vector<double> Hr(N);
     for (int k = 0; k < N; ++k) {
@@ -519,14 +522,18 @@ kk_status kk_init(const kk_config* cfg, kk_ctx** out) {
       Hc[k] = make_float2((float)acc.real(), (float)acc.imag());
     }
   }
-  c->w_cd = cd_init_taps(*cfg, L);
+  {   // θ₀: the CD-inverse fit referenced to the carrier — the centre spike when K2 already inverts CD
+    kk_config c0 = *cfg;
+    if (scd) c0.dispersion_ps_per_nm = 0.0;
+    c->w_cd = cd_init_taps(c0, L);
+  }
   std::vector<float2> wcd(L);
   for (int i = 0; i < L; ++i) wcd[i] = make_float2((float)c->w_cd[i].real(), (float)c->w_cd[i].imag());
 
   e = cudaSuccess;
   auto chk = [&](cudaError_t r) { if (e == cudaSuccess) e = r; };
   chk(upload(&c->d_H, H));
-  if (ddlms) chk(upload(&c->d_Hc, Hc));
+  if (ddlms || scd) chk(upload(&c->d_Hc, Hc));
   chk(upload(&c->d_lo, lo));
   chk(upload(&c->d_wcd, wcd));
   chk(upload(&c->d_tw1024, twiddles(1024, 32, 32)));

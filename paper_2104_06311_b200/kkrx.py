@@ -39,7 +39,7 @@ class kk_config(ctypes.Structure):
         ("eq_mode", c_int32), ("ddlms_block", c_int32), ("ddlms_warmup", c_int32), ("debug_guard", c_int32),
         ("ddlms_mu_warm", c_double), ("ddlms_mu", c_double),
         ("upsample", c_int32), ("ref_prbs", c_int32), ("ref_seed", c_uint32), ("reserved2", c_int32),
-        ("ddlms_mu_mid", c_double),
+        ("ddlms_mu_mid", c_double), ("static_cd", c_int32), ("reserved3", c_int32),
     ]
 
 

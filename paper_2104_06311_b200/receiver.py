@@ -24,7 +24,7 @@ class Receiver:
                  ddlms_mu_warm: float = 2e-3, ddlms_mu: float = 2.5e-4, ddlms_mu_mid: float = 5e-4,
                  debug_guard: bool = False,
                  upsample: int = 1, mf_fft_n: int = 4096, ref_prbs_seed: Optional[int] = None,
-                 ref_prbs_kind: str = "hash"):
+                 ref_prbs_kind: str = "hash", static_cd: bool = False):
         cfg = kkrx.kk_config_default()
         cfg.adc_scale, cfg.adc_offset, cfg.ref_intensity = adc_scale, adc_offset, ref_intensity
         cfg.dispersion_ps_per_nm = dispersion_ps_per_nm
@@ -43,6 +43,7 @@ class Receiver:
         cfg.ddlms_block, cfg.ddlms_warmup = ddlms_block, ddlms_warmup
         cfg.ddlms_mu_warm, cfg.ddlms_mu, cfg.ddlms_mu_mid = ddlms_mu_warm, ddlms_mu, ddlms_mu_mid
         cfg.debug_guard = int(debug_guard)
+        cfg.static_cd = int(static_cd)
         cfg.upsample = upsample
         cfg.mf_fft_n, cfg.mf_hop = mf_fft_n, mf_fft_n - 1024      # MF overlap-save grid (4096/3072 or 8192/7168)
         if ref_prbs_seed is not None:                                # the transmitter's known labels, generated on the GPU

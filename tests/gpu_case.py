@@ -45,7 +45,7 @@ def receiver_for(case, keep=True, max_samples=None, **kw):
                     eq_taps=o.eq_taps, widely_linear=o.eq_widely_linear, cpr_window=o.cpr_window,
                     eq_mode=o.eq_mode, ddlms_block=o.ddlms_block, ddlms_warmup=o.ddlms_warmup,
                     ddlms_mu_warm=o.ddlms_mu_warm, ddlms_mu=o.ddlms_mu, ddlms_mu_mid=o.ddlms_mu_mid,
-                    sideband=o.sideband, upsample=o.upsample,
+                    sideband=o.sideband, upsample=o.upsample, static_cd=o.static_cd,
                     **kw)
 
 

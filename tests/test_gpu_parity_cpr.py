@@ -136,3 +136,19 @@ def test_short_equalizer_noisy_parity(L):
     case = make_case(M=16, dl=0.0, cspr=12.0, esn0=16.0, n=8 * F, seed=190 + L, eq_taps=L)
     gpu, orc = run_gpu(case), run_oracle(case)
     _parity(case, gpu, orc)
+
+
+# ----------------------------------------------------------------------------- static CD + short block LS (NEXT-2)
+@pytest.mark.parametrize("kw", [dict(M=4, dl=200000.0, esn0=12.0), dict(M=16, dl=112000.0, esn0=None),
+                                dict(formats=(4, 8, 16, 32, 64), segment_frames=1, dl=32000.0, esn0=24.0),
+                                dict(M=64, dl=32000.0, esn0=26.0, eq_taps=7)])
+def test_static_cd_short_fir_parity(kw):
+    """K2 with the complex RRC × CD-inverse filter (as in the DDLMS arrangement) feeding the block-LS K3 with
+    L = 5 (θ₀ = centre spike), against the oracle's same arrangement."""
+    case = make_case(cspr=12.0, n=8 * F, seed=211, static_cd=True, **kw)
+    rx = receiver_for(case, keep=True)
+    assert rx.taps == (kw.get("eq_taps") or 5)
+    gpu, orc = run_gpu(case, rx=rx), run_oracle(case)
+    _parity(case, gpu, orc, dec_min=1.0 if kw.get("esn0") is None else 0.9999)
+    if kw.get("esn0") is None:
+        assert gpu["stats"]["bit_err"] == [0] * 5 == list(orc["counts"]["bit_err"])

@@ -702,6 +702,31 @@ def test_restart_form_matches_sequential_definition(shape):
     assert abs(qa - qb) <= 0.1, (qa, qb)
 
 
+# ------------------------------------------------------------------ NEXT-2: static CD inverse + short block LS
+@pytest.mark.parametrize("M,dl", [(16, 200000.0), (64, 32000.0), (32, 112000.0)])
+def test_static_cd_short_fir_noiseless(M, dl):
+    """SURVEY §8(f) NEXT-2 ("offline-optimized filter"): with the CD inverse folded into the static MF
+    (the same h_cd as the DDLMS arrangement) the block-adaptive FIR needs only L = 5 taps (θ₀ = centre spike):
+    zero errors and the EVM of the full rule-sized FIR (L = 9…15) to 0.1 dB."""
+    out5, cfg5, _, _ = _chain(M, dl=dl, cspr=12.0, n=2 * 16384, static_cd=True)
+    outr, _, _, _ = _chain(M, dl=dl, cspr=12.0, n=2 * 16384)
+    assert out5["L"] == 5 and outr["L"] >= 9
+    assert out5["counts"]["bit_err"].sum() == 0
+    assert abs(_evm_db(out5["z"], M) - _evm_db(outr["z"], M)) < 0.1
+    th0 = out5["w_cd"]
+    assert abs(th0[2]) > 0.999 and np.sum(np.abs(th0) ** 2) - abs(th0[2]) ** 2 < 1e-6   # spike
+
+
+def test_static_cd_short_fir_q_matches_rule():
+    """Q of the static-CD + L = 5 arrangement within 0.1 dB of the rule-sized block LS at 10,000 km (C4 shape)."""
+    kw = dict(dl=200000.0, cspr=12.0, esn0=12.0, n=1 << 18, seed=909)
+    a, _, _, _ = _chain(4, static_cd=True, **kw)
+    b, _, _, _ = _chain(4, **kw)
+    qa = T.q_from_ber(a["counts"]["bit_err"].sum() / a["counts"]["bits"].sum())
+    qb = T.q_from_ber(b["counts"]["bit_err"].sum() / b["counts"]["bits"].sum())
+    assert abs(qa - qb) < 0.1, (qa, qb)
+
+
 def test_p14_q_vs_cspr_has_interior_maximum_at_fixed_osnr():
     """at fixed OSNR the KK Q-factor is concave in CSPR with an interior optimum (low CSPR: the
     minimum-phase condition fails; high CSPR: the tone takes the power, "we optimized CSPR")."""
