@@ -93,7 +93,7 @@ __device__ __forceinline__ int64_t floordiv(int64_t a, int64_t b) {
 template <int NF>
 constexpr int k2_ctas_per_sm() { return NF == 4096 ? K2_CTAS_4096 : 16384 / NF; }
 
-template <int NF, bool CH>
+template <int NF, bool CH, bool SP = CH>
 __global__ void __launch_bounds__(NF / 32, k2_ctas_per_sm<NF>())
 k2_mf_kernel(const float2* __restrict__ E, int64_t E_first, const float2* __restrict__ part, int64_t jb0,
              int64_t tile0, int64_t n_tiles, float2* __restrict__ y, int64_t y_first, int64_t y_count,
@@ -222,7 +222,9 @@ k2_mf_kernel(const float2* __restrict__ E, int64_t E_first, const float2* __rest
         for (int r = 0; r < R3 / 2; ++r) {
           const float2 a = v3[it][r], b = v3[it][r + R3 / 2];
           if constexpr (CH) {
-            dst[r * (256 + 16)] = cadd(cmul(a, __ldg(&Hc[j + 256 * r])), cmul(b, __ldg(&Hc[j + 256 * (r + R3 / 2)])));
+            float2 yv = cmul(a, __ldg(&Hc[j + 256 * r]));        // + b·H[…] in the cmul form: 4 packed ops
+            cmac2(yv, b, __ldg(&Hc[j + 256 * (r + R3 / 2)]));
+            dst[r * (256 + 16)] = yv;
           } else {
             const float ha = __ldg(&Hs[j + 256 * r]), hb = __ldg(&Hs[j + 256 * (r + R3 / 2)]);
             float2 yv = cscale(b, hb);                         // packed: b·hb, then + a·ha (same roundings)
@@ -257,10 +259,10 @@ k2_mf_kernel(const float2* __restrict__ E, int64_t E_first, const float2* __rest
         for (int r = 1; r < RI3 - 1; ++r) {                  // p = j + 256 r ∈ [256, NI − 256) ⇔ 1 ≤ r ≤ RI3 − 2
           const int64_t m = m_base + j + 256 * r;
           if (inside || (m >= y_first && m < y_first + y_count)) y[m - y_first] = v3[it][r];
-          if constexpr (CH) pw[it][r] = (j & 1) ? 0.f : fmaf(v3[it][r].x, v3[it][r].x, v3[it][r].y * v3[it][r].y);
+          if constexpr (SP) pw[it][r] = (j & 1) ? 0.f : fmaf(v3[it][r].x, v3[it][r].x, v3[it][r].y * v3[it][r].y);
         }
       }
-      if (CH && p.seg_pow) {                                  // (kernel-uniform; null without K3′)
+      if constexpr (SP) {                                     // K3′'s AGC segment powers
         // per-256-symbol (512-sample) segment power for K3′'s AGC: output p = j + 256 r lies in tile segment
         // (r − 1)/2 for every j, so each thread sums its values per segment, then warp sums and the warps'
         // partials in fixed order → deterministic. Segment g (global) = m / 512.
@@ -292,7 +294,7 @@ k2_mf_kernel(const float2* __restrict__ E, int64_t E_first, const float2* __rest
   }
 }
 
-template <int NF, bool CH>
+template <int NF, bool CH, bool SP>
 static void launch_k2_t(const float2* E, int64_t E_first, const float2* part, int64_t jb0, int64_t tile0,
                         int64_t n_tiles, float2* y, int64_t y_first, int64_t y_count, const float* Hs,
                         const float2* Hc, const float2* lo_tab, const float2* tw256, const float2* twN,
@@ -301,9 +303,9 @@ static void launch_k2_t(const float2* E, int64_t E_first, const float2* part, in
   int64_t grid = (int64_t)num_sms * k2_ctas_per_sm<NF>();
   if (grid > n_tiles) grid = n_tiles;
   const size_t dyn = (size_t)(NF + NF / 16) * sizeof(float2) +
-                     (CH ? (size_t)(NF / 2 - 512) / 512 * (NF / 1024) * sizeof(float) : 0);
-  cudaFuncSetAttribute(k2_mf_kernel<NF, CH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
-  k2_mf_kernel<NF, CH><<<(unsigned)grid, T, dyn, s>>>(E, E_first, part, jb0, tile0, n_tiles, y, y_first, y_count,
+                     (SP ? (size_t)(NF / 2 - 512) / 512 * (NF / 1024) * sizeof(float) : 0);
+  cudaFuncSetAttribute(k2_mf_kernel<NF, CH, SP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+  k2_mf_kernel<NF, CH, SP><<<(unsigned)grid, T, dyn, s>>>(E, E_first, part, jb0, tile0, n_tiles, y, y_first, y_count,
                                                       Hs, Hc, lo_tab, tw256, twN, twI, p);
 }
 
@@ -311,13 +313,18 @@ void launch_k2(int nf, const float2* E, int64_t E_first, const float2* part, con
                int64_t tile0, int64_t n_tiles, float2* y, int64_t y_first, int64_t y_count, const float* Hs,
                const float2* Hc, const float2* lo_tab, const float2* tw256, const float2* twN,
                const float2* twI, const K2Params& p, int num_sms, cudaStream_t s) {
+  // real H (RRC) | complex H (RRC × CD inverse) with K3′'s segment powers (p.seg_pow) | complex H alone (static CD)
+#define KK_K2(NFV, CHV, SPV) launch_k2_t<NFV, CHV, SPV>(E, E_first, part, jb0, tile0, n_tiles, y, y_first, y_count, Hs, Hc, lo_tab, tw256, twN, twI, p, num_sms, s)
   if (nf == 8192) {
-    if (Hc) launch_k2_t<8192, true>(E, E_first, part, jb0, tile0, n_tiles, y, y_first, y_count, Hs, Hc, lo_tab, tw256, twN, twI, p, num_sms, s);
-    else launch_k2_t<8192, false>(E, E_first, part, jb0, tile0, n_tiles, y, y_first, y_count, Hs, Hc, lo_tab, tw256, twN, twI, p, num_sms, s);
+    if (Hc && p.seg_pow) KK_K2(8192, true, true);
+    else if (Hc) KK_K2(8192, true, false);
+    else KK_K2(8192, false, false);
   } else {
-    if (Hc) launch_k2_t<4096, true>(E, E_first, part, jb0, tile0, n_tiles, y, y_first, y_count, Hs, Hc, lo_tab, tw256, twN, twI, p, num_sms, s);
-    else launch_k2_t<4096, false>(E, E_first, part, jb0, tile0, n_tiles, y, y_first, y_count, Hs, Hc, lo_tab, tw256, twN, twI, p, num_sms, s);
+    if (Hc && p.seg_pow) KK_K2(4096, true, true);
+    else if (Hc) KK_K2(4096, true, false);
+    else KK_K2(4096, false, false);
   }
+#undef KK_K2
 }
 
 }  // namespace kk
