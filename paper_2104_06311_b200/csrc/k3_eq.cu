@@ -465,12 +465,14 @@ uint32_t wadr[NW];
             if constexpr (LB > 0) lag_acc(accl, w, LA, LB);
           }
         }
+        __syncthreads();   // every read of the frame buffer is done: request the next frame (overlaps the reductions)
+        if (tid == 0 && fn < n_frames) { issue_y(fn); early = true; }
         warp_partials<Lay::NP>(acc, red_w, 0, lane);
         if constexpr (LB > 0) warp_partials<8 * LB>(accl, red_w, Lay::NP + 8 * LA, lane);
       }
       }
-      __syncthreads();   // every read of the frame buffer is done: request the next frame now
-      if (tid == 0 && fn < n_frames) { issue_y(fn); early = true; }
+      __syncthreads();
+      if (!p0ok && tid == 0 && fn < n_frames) { issue_y(fn); early = true; }   // silent: sweep A was the last reader
       if (p0ok) {        // fp64 sums over the 8 warp partials, fixed order → the record
         for (int v = tid; v < NRED; v += K3_THREADS) {
           double s = 0.0;

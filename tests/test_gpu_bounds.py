@@ -71,6 +71,9 @@ CASES = [
      dict(mf_fft_n=8192), "int16"),
     ("ddlms_warm0_blk4096", dict(M=4, dl=20000.0, esn0=12.0, eq_mode="ddlms", ddlms_block=4096, ddlms_warmup=0),
      {}, "int16"),
+    ("static_cd_L5", dict(M=32, dl=200000.0, esn0=20.0, static_cd=True), {}, "int16"),
+    ("blockls_K5_prbs", dict(formats=(4, 8, 16, 32, 64), segment_frames=1, dl=112000.0, esn0=22.0,
+                             label_source="prbs31"), {}, "int16"),
 ]
 
 
