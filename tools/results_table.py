@@ -8,6 +8,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 NAMES = {"C1": "C1 4-QAM b2b, 2^16", "C2": "C2 16-QAM 5600 km, CSPR 6 dB @ OSNR 17 dB, 2^22",
          "C3": "C3 64-QAM 1600 km, Es/N0 26 dB, 2^24", "C4": "C4 4-QAM 10,000 km, Es/N0 12 dB, 2^26 (L = 15)",
          "C5": "C5 mixed 4→64-QAM 1600 km, 2^32/GPU", "C5_up2": "C5 with 2× KK upsampling (K1U)",
+         "C5_scd": "C5, static CD inverse in the MF + 5-tap block LS (`--static-cd`)",
+         "C4_scd": "C4, static CD inverse in the MF + 5-tap block LS (`--static-cd`)",
          "C5_ddlms": "C5, paper arrangement (static RRC×CD⁻¹ + 4-tap WL DDLMS)"}
 HDR = """# Results per BASELINE.json configuration (1× B200, {tag})
 
