@@ -75,7 +75,7 @@ typedef struct kk_config {
   int32_t input_dtype;           /* KK_IN_INT16 / KK_IN_UINT8 (ADC codes) | KK_IN_FLOAT32 (intensities) */
   float   adc_scale, adc_offset; /* I = adc_scale·(code − adc_offset)                                    */
   float   ref_intensity;         /* I_ref > 0; ε = clamp_rel·I_ref (R7)                                  */
-  float   clamp_rel;             /* 1e-12                                                                */
+  float   clamp_rel;             /* 1e-12; a normal float (>= FLT_MIN), else kk_init fails               */
   const uint8_t* format_schedule;/* host array of n_segments QAM orders in {4,8,16,32,64}; NULL → default_format */
   int32_t n_segments;            /* entries in format_schedule (copied at kk_init)                       */
   int32_t default_format;        /* M when format_schedule is NULL                                       */

@@ -53,7 +53,9 @@ k1_kk_kernel(const Tin* __restrict__ adc0, float2* __restrict__ E, float2* __res
   }
   mbar_wait(bar, 0);
 
-  // ---- a1/a2: int → float, I/I_ref, ε-clamp, a = ½ ln(.)  (one MUFU.LG2 per staged sample)
+  // ---- a1/a2: int → float, I/I_ref, ε-clamp, b = log2(.) = 2·a/ln 2 with a = ½ ln(.) (one MUFU.LG2 per staged
+  //      sample, no denormal fix-up: the operand is ≥ ε, a normal float; the Hilbert transform is linear, so the
+  //      constant ½·ln 2 is applied after it, folded into the phase scale and into the magnitude's FFMA)
   // 8 consecutive samples per thread per step: one 16-B (int16) or two 16-B (float) shared loads, two
   // 16-B stores; the group never straddles a 512-block, so its clamp count goes to one block counter.
   const float sc_in = p.adc_scale * p.inv_iref, off_in = -p.adc_offset * p.adc_scale * p.inv_iref;
@@ -76,7 +78,7 @@ k1_kk_kernel(const Tin* __restrict__ adc0, float2* __restrict__ E, float2* __res
     for (int j = 0; j < 8; ++j) {
       const bool cl = !(x[j] >= p.clamp_rel);
       ncl += cl;
-      av[j] = 0.34657359027997264f * __log2f(cl ? p.clamp_rel : x[j]);   // ½·ln 2·log2 x
+      av[j] = lg2_approx(cl ? p.clamp_rel : x[j]);   // b = log2 x (a = ½·ln 2·b; the ½·ln 2 goes into sc and l2m's FFMA)
     }
     reinterpret_cast<float4*>(a_s)[2 * gi] = make_float4(av[0], av[1], av[2], av[3]);
     reinterpret_cast<float4*>(a_s)[2 * gi + 1] = make_float4(av[4], av[5], av[6], av[7]);
@@ -123,7 +125,7 @@ k1_kk_kernel(const Tin* __restrict__ adc0, float2* __restrict__ E, float2* __res
   dft_reg<32, +1>(v);                       // lane j holds 1024·(φ₀ + iφ₁)[j + 32 r]
 
   // ---- a4: E = √I_ref·e^{a}·e^{iσφ} on the central 512 samples; per-block ΣE
-  const float sc = p.sideband * (1.0f / 1024.0f);
+  const float sc = p.sideband * (0.34657359027997264f / 1024.0f);   // σ·(½·ln 2)/1024: φ = ½·ln 2·H{b}
   const float l2m = p.half_ln_iref * 1.4426950408889634f;           // log2 √I_ref
   const int64_t blk0 = cta * (2 * K1_WARPS) + 2 * warp;    // block index relative to jb0
   float2* E0 = E + blk0 * kHilbertHop - kHilbertLead;
@@ -135,9 +137,8 @@ k1_kk_kernel(const Tin* __restrict__ adc0, float2* __restrict__ E, float2* __res
     float sn0, cs0, sn1, cs1;
     __sincosf(v[r].x * sc, &sn0, &cs0);
     __sincosf(v[r].y * sc, &sn1, &cs1);
-    // e^{a + ½ln I_ref} = 2^{a·log2 e + log2 √I_ref}: one FFMA + MUFU.EX2 (__expf adds first, then scales)
-    const float m0 = ex2_approx(fmaf(ab0[pos], 1.4426950408889634f, l2m)),
-                m1 = ex2_approx(fmaf(ab1[pos], 1.4426950408889634f, l2m));
+    // e^{a + ½ln I_ref} = 2^{b/2 + log2 √I_ref}: one FFMA (immediate form) + MUFU.EX2
+    const float m0 = ex2_approx(fmaf(ab0[pos], 0.5f, l2m)), m1 = ex2_approx(fmaf(ab1[pos], 0.5f, l2m));
     const float2 e0 = cscale(make_float2(cs0, sn0), m0), e1 = cscale(make_float2(cs1, sn1), m1);
     E0[pos] = e0;
     E1[pos] = e1;

@@ -430,7 +430,7 @@ uint32_t wadr[NW];
       // AGC (R25). A frame without signal power (P0 ≤ p0_min = 1e-20·I_ref, or not finite: e.g. the tone
       // without modulation) cannot be trained: it is a bad frame with z = 0 and decisions D(0)
       const bool p0ok = (P0 > (double)p.p0_min) && isfinite(P0);
-      const float g_agc = p0ok ? (float)(1.0 / sqrt(P0)) : 1.0f;
+      const float g_agc = p0ok ? (float)rsqrt(P0) : 1.0f;
       if (!p0ok) flags |= kFlagSilent;
       if (p0ok) {
       // ---- sweep B: decisions on g·y⁰ and p1[e] = Σ conj(a_j)·d, p2[e] = Σ a_j·d  (a_j = w[e]);
@@ -554,8 +554,8 @@ uint32_t wadr[NW];
         double Gr = 0, Gi = 0, Gd = 0;
 #pragma unroll
         for (int w8 = 0; w8 < K3_WARPS; ++w8) { Gr += red[w8 * NRED]; Gi += red[w8 * NRED + 1]; Gd += red[w8 * NRED + 2]; }
-        const double ag = sqrt(Gr * Gr + Gi * Gi) / Gd;
-        if (ag > 0.0 && isfinite(ag)) sc = (float)(1.0 / ag); else bad = 1;
+        const double isc = Gd * rsqrt(Gr * Gr + Gi * Gi);          // 1/|γ| = Σ|D|² / |Σ y¹·conj(D)|
+        if (isc > 0.0 && isfinite(isc)) sc = (float)isc; else bad = 1;
       }
       // ---- CPR (R12): c_b = Σ_{k∈b} u_k·conj(D(u_k)) with u = sc·y¹; rotation conj(c_b)/|c_b| (none if c_b = 0).
       //      The warp owns 512 consecutive symbols (two 256-symbol halves, s < 8 and s ≥ 8): W = 256 / 512 windows

@@ -68,6 +68,11 @@ __device__ __forceinline__ float ex2_approx(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
   return r;
 }
+__device__ __forceinline__ float lg2_approx(float x) {   // MUFU.LG2 without the denormal fix-up (x normal or ≥ 1)
+  float r;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
 // a·s as one packed FP32x2 multiply with a scalar-broadcast operand (FMUL2; bit-identical to two FMULs)
 __device__ __forceinline__ float2 cscale(float2 a, float s) {
   float2 r;

@@ -9,6 +9,7 @@
 //   * FFT twiddle tables W_N^{r·k} in the [r][k] layouts the kernels read;
 // then allocates scratch for max_samples_per_call. kk_process_frames enqueues K1 → K2 → K3 on the caller's
 // stream with no host synchronisation.
+#include <cfloat>
 #include <cmath>
 #include <complex>
 #include <cstdio>
@@ -302,7 +303,8 @@ kk_status validate(const kk_config& c, std::string& why) {
     return bad("cpr_window must be one of 256,512,1024,2048,4096");
   if (!(c.eq_ridge >= 0)) return bad("eq_ridge must be >= 0");
   if (c.input_dtype != KK_IN_INT16 && c.input_dtype != KK_IN_FLOAT32 && c.input_dtype != KK_IN_UINT8) return bad("input_dtype");
-  if (!(c.ref_intensity > 0) || !(c.clamp_rel > 0)) return bad("ref_intensity and clamp_rel must be > 0");
+  if (!(c.ref_intensity > 0) || !(c.clamp_rel >= FLT_MIN))
+    return bad("ref_intensity must be > 0 and clamp_rel a normal float >= FLT_MIN");
   if (c.max_samples_per_call < kk::kFrameSamp || c.max_samples_per_call % kk::kFrameSamp) return bad("max_samples_per_call must be a positive multiple of 16384");
   auto okM = [](int M) { return M == 4 || M == 8 || M == 16 || M == 32 || M == 64; };
   if (c.format_schedule) {

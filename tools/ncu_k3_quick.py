@@ -1,5 +1,5 @@
 """Quick summary of a one-kernel ncu --set full report: throughputs, stall ratios, smem wavefronts, dynamic
-opcode mix. usage: python tools/ncu_k3_quick.py REPORT.ncu-rep [frames_per_launch]"""
+opcode mix. usage: python tools/ncu_k3_quick.py REPORT.ncu-rep [frames_per_launch] [kernel regex [launch skip]]"""
 import csv
 import io
 import re
@@ -9,10 +9,13 @@ from collections import defaultdict
 
 rep = sys.argv[1]
 frames = float(sys.argv[2]) if len(sys.argv) > 2 else 16384.0
+kern = ["-k", "regex:" + sys.argv[3]] if len(sys.argv) > 3 else []
+if len(sys.argv) > 4:
+    kern += ["--launch-skip", sys.argv[4], "--launch-count", "1"]
 
 
 def ncu(*a):
-    return subprocess.run(["ncu", "-i", rep] + list(a), capture_output=True, text=True).stdout
+    return subprocess.run(["ncu", "-i", rep] + kern + list(a), capture_output=True, text=True).stdout
 
 
 rows = list(csv.reader(io.StringIO(ncu("--page", "raw", "--csv"))))
@@ -32,9 +35,11 @@ srows = list(csv.reader(io.StringIO(ncu("--page", "source", "--csv", "--print-so
 hdr = srows[1]
 ie = hdr.index("Instructions Executed")
 agg = defaultdict(int)
+seen = set()
 for r in srows[2:]:
-    if len(r) <= ie or not r[ie].isdigit():
+    if len(r) <= ie or not r[ie].isdigit() or r[0] in seen:   # the page lists every address twice: count once
         continue
+    seen.add(r[0])
     m = re.match(r"(@!?U?P\w+\s+)?([A-Z0-9_]+)", r[1].strip())
     if m:
         agg[m.group(2)] += int(r[ie])
