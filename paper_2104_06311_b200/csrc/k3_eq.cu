@@ -186,7 +186,7 @@ __device__ __forceinline__ void tma_tensor_2d(void* dst_smem, const CUtensorMap*
 // per-frame records between the launches: K3a → K3s: the fp64 sums (NRED), g, flags; K3s → K3c: θ₁ (w, v), flags
 template <int K> struct K3Rec {
   static constexpr int REC = K3Layout<K>::NRED + 2;   // doubles: [0, NRED) sums, [NRED] g, [NRED + 1] flags
-  static constexpr int TREC = 2 * K3Layout<K>::L + 2; // float2: [0, L) w, [L, 2L) v, [2L].x = flags (int bits)
+  static constexpr int TREC = 2 * K3Layout<K>::L + 2; // float2: [0, L) cr = (wr + vr, wi + vi), [L, 2L) ci = (vi − wi, wr − vr) (θ₁ in pass 2's real form), [2L].x = flags (int bits)
 };
 constexpr int kFlagDead = 1, kFlagSilent = 2, kFlagFail = 4;
 
@@ -498,16 +498,13 @@ uint32_t wadr[NW];
       float2 rA = make_float2(0.f, 0.f), rB = make_float2(0.f, 0.f);   // CPR rotations (× unbias) of the halves
       if (!zero) {
       // ---- sweep C: pass 2 y¹ = Σ_e w_e·a + v_e·conj(a) → us, and the gain-unbias sums (R27)
-      float gr = 0.f, gi = 0.f, gd = 0.f;
+      float2 gacc = make_float2(0.f, 0.f), gdd = make_float2(0.f, 0.f);   // Σ y¹·conj(D), Σ (D.x², D.y²)
       {
-        // w·a + v·conj(a) = (ar·(wr + vr) + ai·(vi − wi), ar·(wi + vi) + ai·(wr − vr)): 4 FMA per tap
-        float2 cr[L], ci[L];                   // cr = (wr + vr, wi + vi), ci = (vi − wi, wr − vr)
+        // w·a + v·conj(a) = (ar·(wr + vr) + ai·(vi − wi), ar·(wi + vi) + ai·(wr − vr)): 4 FMA per tap; K3s
+        // delivers the taps in this form: th[e] = cr = (wr + vr, wi + vi), th[L + e] = ci = (vi − wi, wr − vr)
+        float2 cr[L], ci[L];
 #pragma unroll
-        for (int e = 0; e < L; ++e) {
-          const float2 tw = th[e], tv = th[L + e];
-          cr[e] = make_float2(tw.x + tv.x, tw.y + tv.y);
-          ci[e] = make_float2(tv.y - tw.y, tw.x - tv.x);
-        }
+        for (int e = 0; e < L; ++e) { cr[e] = th[e]; ci[e] = th[L + e]; }
         auto pass2 = [&](const float2 (&w)[L]) {
           float2 o = make_float2(0.f, 0.f);
 #pragma unroll
@@ -516,8 +513,8 @@ uint32_t wadr[NW];
             ffma2s(o, w[e].y, ci[e]);
           }
           const float2 dd = sl.point(o);        // γ = Σ y¹·conj(D(y¹)) / Σ|D(y¹)|²
-          const float2 c = cmulc(o, dd);
-          gr += c.x; gi += c.y; gd = fmaf(dd.x, dd.x, fmaf(dd.y, dd.y, gd));
+          cmacc2(gacc, o, dd);
+          ffma2(gdd, dd, dd);
           return o;
         };
         {
@@ -538,8 +535,10 @@ uint32_t wadr[NW];
           }
         }
       }
-      gr = warp_sum(gr); gi = warp_sum(gi); gd = warp_sum(gd);
-      if (lane == 0) { red_w[0] = gr; red_w[1] = gi; red_w[2] = gd; }
+      {
+        const float gr = warp_sum(gacc.x), gi = warp_sum(gacc.y), gd = warp_sum(gdd.x + gdd.y);
+        if (lane == 0) { red_w[0] = gr; red_w[1] = gi; red_w[2] = gd; }
+      }
       __syncthreads();
       KK_PT(5);
       // the frame buffer is dead now (every thread is past sweep C): start the next frame's sample copy so that it
@@ -551,9 +550,13 @@ uint32_t wadr[NW];
       }
       float sc = 1.0f;
       {
-        double Gr = 0, Gi = 0, Gd = 0;
+        // fp64 sums over the 8 warps' (gr, gi, gd), lane-parallel: lane 3·w8 + c holds warp w8's component c;
+        // a fixed tree over w8 (offsets 12, 6, 3 — the same in every warp) leaves component c in lane c
+        double gv = (lane < 3 * K3_WARPS) ? (double)red[(lane / 3) * NRED + lane % 3] : 0.0;
 #pragma unroll
-        for (int w8 = 0; w8 < K3_WARPS; ++w8) { Gr += red[w8 * NRED]; Gi += red[w8 * NRED + 1]; Gd += red[w8 * NRED + 2]; }
+        for (int o = 12; o >= 3; o >>= 1) gv += __shfl_down_sync(0xffffffffu, gv, o);
+        const double Gr = __shfl_sync(0xffffffffu, gv, 0), Gi = __shfl_sync(0xffffffffu, gv, 1),
+                     Gd = __shfl_sync(0xffffffffu, gv, 2);
         const double isc = Gd * rsqrt(Gr * Gr + Gi * Gi);          // 1/|γ| = Σ|D|² / |Σ y¹·conj(D)|
         if (isc > 0.0 && isfinite(isc)) sc = (float)isc; else bad = 1;
       }
@@ -562,24 +565,23 @@ uint32_t wadr[NW];
       //      are summed inside the warp (fixed order: s ascending, then lane butterflies); larger windows add
       //      the warps' sums in warp order through shared memory.
       {
-        float cr0 = 0.f, ci0 = 0.f, cr1 = 0.f, ci1 = 0.f;
-        auto prod = [&](float2 y1v, float& cr, float& ci) {
-          const float2 uu = cscale(y1v, sc);
-          const float2 c = cmulc(uu, sl.point(uu));
-          cr += c.x; ci += c.y;
-        };
+        float2 c0 = make_float2(0.f, 0.f), c1 = make_float2(0.f, 0.f);
         {
-          auto grp = [&](int g, float& cr, float& ci) {
+          auto grp = [&](int g, float2& c) {
             float2 v[GS];
             uload(g, v);
 #pragma unroll
-            for (int j = 0; j < GS; ++j) prod(v[j], cr, ci);
+            for (int j = 0; j < GS; ++j) {
+              const float2 uu = cscale(v[j], sc);
+              cmacc2(c, uu, sl.point(uu));
+            }
           };
 #pragma unroll
-          for (int g = 0; g < NG / 2; ++g) grp(g, cr0, ci0);
+          for (int g = 0; g < NG / 2; ++g) grp(g, c0);
 #pragma unroll
-          for (int g = NG / 2; g < NG; ++g) grp(g, cr1, ci1);
+          for (int g = NG / 2; g < NG; ++g) grp(g, c1);
         }
+        float cr0 = c0.x, ci0 = c0.y, cr1 = c1.x, ci1 = c1.y;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
           cr0 += __shfl_xor_sync(0xffffffffu, cr0, o);
@@ -944,25 +946,28 @@ k3s_kernel(const double* __restrict__ rec, const float2* __restrict__ y, const f
         const double* A = mat;
           if (lane < N) fail |= !isfinite(A[lane * W + N]) || !isfinite(A[lane * W + N + 1]);
           fail = __any_sync(0xffffffffu, fail) ? 1 : 0;
+          // tap e in K3c's real form: w·a + v·conj(a) = ar·cr + ai·ci with cr = (wr + vr, wi + vi),
+          // ci = (vi − wi, wr − vr); from the solution columns (w = ((m1 + m2b)/2, (m2 − m1b)/2),
+          // v = ((m1 − m2b)/2, (m2 + m1b)/2)) that is cr = (m1, m2), ci = (m1b, m2b) — one rounding each
           if (lane < L) {
-            float2 wv, vv;
-            if (fail) {
+            float2 cr, ci;
+            if (fail) {                          // θ₀: w = g·w_cd, v = 0
               const float2 w0 = __ldg(&w_cd[lane]);
-              wv = make_float2(g * w0.x, g * w0.y);
-              vv = make_float2(0.f, 0.f);
+              cr = make_float2(g * w0.x, g * w0.y);
+              ci = make_float2(-cr.y, cr.x);
             } else {
               const double m1 = A[lane * W + N], m2 = A[lane * W + N + 1];
               const double m1b = A[(L + lane) * W + N], m2b = A[(L + lane) * W + N + 1];
               if (wl) {
-                wv = make_float2((float)(0.5 * (m1 + m2b)), (float)(0.5 * (m2 - m1b)));
-                vv = make_float2((float)(0.5 * (m1 - m2b)), (float)(0.5 * (m2 + m1b)));
-              } else {
-                wv = make_float2((float)m1, (float)m1b);
-                vv = make_float2(0.f, 0.f);
+                cr = make_float2((float)m1, (float)m2);
+                ci = make_float2((float)m1b, (float)m2b);
+              } else {                           // strictly linear: w = (m1, m1b), v = 0
+                cr = make_float2((float)m1, (float)m1b);
+                ci = make_float2(-cr.y, cr.x);
               }
             }
-            tr[lane] = wv;
-            tr[L + lane] = vv;
+            tr[lane] = cr;
+            tr[L + lane] = ci;
           }
           if (lane == 0) tr[2 * L] = make_float2(__int_as_float(flags | (fail ? kFlagFail : 0)), 0.f);
           

@@ -53,6 +53,19 @@ __device__ __forceinline__ float2 cmulc(float2 a, float2 b) {
       : "=f"(r.x), "=f"(r.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(-b.y));
   return r;
 }
+// (acc.x, acc.y) += (a.x·b.x, a.y·b.y) as one packed FP32x2 FMA (each lane the scalar fmaf)
+__device__ __forceinline__ void ffma2(float2& acc, float2 a, float2 b) {
+  asm("{\n\t.reg .b64 pa, pb, pc;\n\tmov.b64 pa, {%2, %3};\n\tmov.b64 pb, {%4, %5};\n\tmov.b64 pc, {%0, %1};\n\t"
+      "fma.rn.f32x2 pc, pa, pb, pc;\n\tmov.b64 {%0, %1}, pc;\n\t}"
+      : "+f"(acc.x), "+f"(acc.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+}
+// acc += a·conj(b) in the cmul form (FFMA2 + FFMA2): acc += b.x·a − b.y·(i·a)
+__device__ __forceinline__ void cmacc2(float2& acc, float2 a, float2 b) {
+  asm("{\n\t.reg .b64 pa, ps, pc, pn, pr;\n\tmov.b64 pa, {%2, %3};\n\tmov.b64 ps, {%3, %2};\n\t"
+      "mov.b64 pc, {%4, %4};\n\tmov.b64 pn, {%5, %6};\n\tmov.b64 pr, {%0, %1};\n\t"
+      "fma.rn.f32x2 pr, pa, pc, pr;\n\tfma.rn.f32x2 pr, ps, pn, pr;\n\tmov.b64 {%0, %1}, pr;\n\t}"
+      : "+f"(acc.x), "+f"(acc.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(-b.y));
+}
 // acc += a·b in the cmul form (FFMA2 + FFMA2): acc += b.x·a + b.y·(i·a) — the swap and the half-negation fold into
 // FFMA2 operand modifiers, so a tap b held as two scalars (e.g. uniform registers) needs no register pair
 __device__ __forceinline__ void cmac2(float2& acc, float2 a, float2 b) {
