@@ -79,10 +79,9 @@ __device__ __forceinline__ void stockham_pass(float2* buf, const float2* __restr
   __syncthreads();
 }
 
-__device__ __forceinline__ int64_t floordiv(int64_t a, int64_t b) {
-  int64_t q = a / b;
-  return (a % b != 0 && ((a < 0) != (b < 0))) ? q - 1 : q;
-}
+// ⌊a / kFrameSamp⌋ for any sign: an arithmetic shift (kFrameSamp = 2^14)
+static_assert(kFrameSamp == 16384, "frame index by shift");
+__device__ __forceinline__ int64_t frame_of(int64_t a) { return a >> 14; }
 
 // CH = false: real H (RRC matched filter, north star). CH = true: complex H_cd = RRC × CD inverse (the paper's
 // static filter, eq_mode DDLMS). NF = 4096 or 8192 (the OLS grid).
@@ -129,7 +128,7 @@ k2_mf_kernel(const float2* __restrict__ E, int64_t E_first, const float2* __rest
   // that the carrier estimate at a tile's start does not wait for a global load
   auto load_part = [&](int64_t ti_) -> float2 {
     const int64_t s0_ = (tile0 + (n_tiles - 1 - ti_)) * HOP - LEAD;
-    const int64_t fa_ = floordiv(s0_, kFrameSamp);
+    const int64_t fa_ = frame_of(s0_);
     float2 a = make_float2(0.f, 0.f);
     if (warp == 0 || s0_ + NF > (fa_ + 1) * kFrameSamp) a = part[(fa_ + warp) * 32 - jb0 + lane];
     return a;
@@ -154,7 +153,7 @@ k2_mf_kernel(const float2* __restrict__ E, int64_t E_first, const float2* __rest
   for (int64_t ti = blockIdx.x; ti < n_tiles; ti += gridDim.x) {
     const int64_t t = tile0 + (n_tiles - 1 - ti);
     const int64_t s0 = t * HOP - LEAD;                       // global sample of x[0]
-    const int64_t fa = floordiv(s0, kFrameSamp);
+    const int64_t fa = frame_of(s0);
     const int64_t fsplit = (fa + 1) * kFrameSamp;            // first sample of frame fa+1 (NF < 16384: ≤ 2 frames)
     // ---- FFT pass 1 (radix 16, Ns = 1) fused with the load: x_i = (E_i − A_f(i))·LO_i, i = j + NJ1·r.
     //      The E loads are issued first so their latency overlaps the carrier estimate below.
