@@ -50,6 +50,13 @@ k1_kk_kernel(const Tin* __restrict__ adc0, float2* __restrict__ E, float2* __res
   if (tid == 0) {
     mbar_arrive_expect_tx(bar, bytes);
     tma_bulk_g2s(stage, src, bytes, bar);
+    // the input of the CTA that will follow this one on the GPU (blockIdx + 2 resident CTAs × SMs) → L2, so
+    // that its copy does not wait on DRAM (a CTA otherwise spends ~14 % of its stall samples in this wait)
+    uint32_t nsm;
+    asm("mov.u32 %0, %%nsmid;" : "=r"(nsm));
+    if (cta + 2 * (int64_t)nsm < (int64_t)gridDim.x)
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src + 2 * (int64_t)nsm * (K1_WARPS * 1024)),
+                   "r"(bytes) : "memory");
   }
   mbar_wait(bar, 0);
 
