@@ -46,10 +46,11 @@ __device__ __forceinline__ void apply_twiddles(float2 (&v)[R], const float2* __r
   for (int r = 1; r < R; ++r) v[r] = DIR < 0 ? cmul(v[r], w[r]) : cmulc(v[r], w[r]);
 }
 
-// One radix-R Stockham pass over an N-point array in shared memory (in place, barrier-separated).
+// One radix-R Stockham pass over an N-point array in shared memory, src → dst (the same buffer: in place, a
+// barrier between the reads and the writes; different buffers: no such barrier), closing barrier.
 // tw: table of W_{Ns·R}^{r·k} laid out [r][k] (k < Ns), conjugated when DIR = +1.
 template <int N, int R, int Ns, int DIR, int T>
-__device__ __forceinline__ void stockham_pass(float2* buf, const float2* __restrict__ tw, int tid) {
+__device__ __forceinline__ void stockham_pass(const float2* srcb, float2* buf, const float2* __restrict__ tw, int tid) {
   constexpr int NJ = N / R;
   constexpr int PER = NJ / T;
   static_assert(PER >= 1 && NJ % T == 0, "pass shape");
@@ -58,11 +59,11 @@ __device__ __forceinline__ void stockham_pass(float2* buf, const float2* __restr
 #pragma unroll
   for (int it = 0; it < PER; ++it) {
     const int j = tid + it * T;
-    const float2* src = buf + pad16(j);             // pad16(j + r·NJ) = pad16(j) + r·(NJ + NJ/16)
+    const float2* src = srcb + pad16(j);            // pad16(j + r·NJ) = pad16(j) + r·(NJ + NJ/16)
 #pragma unroll
     for (int r = 0; r < R; ++r) v[it][r] = src[r * (NJ + NJ / 16)];
   }
-  __syncthreads();
+  if (srcb == buf) __syncthreads();
 #pragma unroll
   for (int it = 0; it < PER; ++it) {
     const int j = tid + it * T;
@@ -198,7 +199,7 @@ k2_mf_kernel(const float2* __restrict__ E, int64_t E_first, const float2* __rest
       }
       __syncthreads();
     }
-    stockham_pass<NF, 16, 16, -1, T>(buf, tw256, tid);
+    stockham_pass<NF, 16, 16, -1, T>(buf, buf, tw256, tid);
     // ---- last forward pass (radix R3, Ns = 256) fused with × H and the fold: thread j owns Y[j + 256 r],
     //      r < R3, so Y2[j + 256 r] = Y[j + 256 r]·H[j + 256 r] + Y[j + 256 (r + R3/2)]·H[…], r < R3/2
     {
@@ -234,9 +235,11 @@ k2_mf_kernel(const float2* __restrict__ E, int64_t E_first, const float2* __rest
       }
       __syncthreads();
     }
-    // ---- IFFT_{NI} (radix 16, 16, RI3); the last pass stores the kept outputs straight to y
-    stockham_pass<NI, 16, 1, +1, T>(buf, nullptr, tid);
-    stockham_pass<NI, 16, 16, +1, T>(buf, tw256, tid);
+    // ---- IFFT_{NI} (radix 16, 16, RI3); the last pass stores the kept outputs straight to y. The NI-point
+    //      array needs half the tile buffer, so its first two passes ping-pong between the halves (A → B → A):
+    //      no barrier between a pass's reads and its writes (the fold's reads of B ended before its barrier)
+    stockham_pass<NI, 16, 1, +1, T>(buf, buf + (NI + NI / 16), nullptr, tid);
+    stockham_pass<NI, 16, 16, +1, T>(buf + (NI + NI / 16), buf, tw256, tid);
     {
       const int64_t m_base = t * KEEP - KEEP0;                // y index of IFFT output p: m_base + p
       float2 v3[PER3][RI3];
