@@ -261,9 +261,8 @@ k3_frame_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, cons
     else { issue_y(blockIdx.x); issue_ref(blockIdx.x, 0); }
     if ((int)blockIdx.x + (int)gridDim.x < n_frames) prefetch(blockIdx.x + gridDim.x);
   }
-  float2 wc[L];
-#pragma unroll
-  for (int e = 0; e < L; ++e) wc[e] = __ldg(&w_cd[e]);    // w_cd[a], a = j + K; tap j ↔ window index e
+  // θ₀'s taps w_cd[a], a = j + K (tap j ↔ window index e), read from the kernel parameters where they are used
+  static_assert(L <= 15, "K3Params::w_cd holds 15 taps");
 
   // tap window of local symbol kl: w[e] = y_s[2kl + 2K − e] = y[2k − (e − K)], e = 0..2K, i.e. the K+1 16-B pairs
   // (y_s[2kl + 2m], y_s[2kl + 2m + 1]) = (w[2K − 2m], w[2K − 2m − 1]). Symbol ownership: warp w owns the 512
@@ -373,7 +372,7 @@ k3_frame_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, cons
       auto pass1 = [&](const float2 (&w)[L]) {   // w_cd·a = wr·a + wi·(i·a), the cmul form (taps stay scalars)
         float2 y0 = make_float2(0.f, 0.f);
 #pragma unroll
-        for (int e = 0; e < L; ++e) cmac2(y0, w[e], wc[e]);
+        for (int e = 0; e < L; ++e) cmac2(y0, w[e], p.w_cd[e]);
         return y0;
       };
       {

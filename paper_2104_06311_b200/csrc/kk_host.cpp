@@ -708,6 +708,9 @@ kk_status kk_process_frames_ex(kk_ctx* c, const void* d_adc, int64_t first, int6
   p3.cpr_window = cf.cpr_window;
   p3.p0_min = (float)(1e-20 * cf.ref_intensity);
   p3.frame_err = d_ref ? d_ferr : nullptr;
+  for (int i = 0; i < 15; ++i)
+    p3.w_cd[i] = (i < (int)c->w_cd.size()) ? make_float2((float)c->w_cd[i].real(), (float)c->w_cd[i].imag())
+                                           : make_float2(0.f, 0.f);
   const int64_t nfr = n / F;
   if (c->ddlms) {
     kk::K3DParams pd;

@@ -58,6 +58,7 @@ struct K3Params {
   int cpr_window;                    // symbols
   float p0_min;                      // AGC power at or below which a frame is silent (bad; z = 0): 1e-20·I_ref
   unsigned* frame_err;               // nullable: [2f] symbol errors, [2f+1] bit errors per local frame
+  float2 w_cd[15];                   // θ₀'s CD taps by value (kernel-parameter space: uniform operands, no registers)
 };
 
 struct K3DParams {
