@@ -575,9 +575,9 @@ uint32_t wadr[NW];
               cmacc2(c, uu, sl.point(uu));
             }
           };
-#pragma unroll
+#pragma unroll 1
           for (int g = 0; g < NG / 2; ++g) grp(g, c0);
-#pragma unroll
+#pragma unroll 1
           for (int g = NG / 2; g < NG; ++g) grp(g, c1);
         }
         float cr0 = c0.x, ci0 = c0.y, cr1 = c1.x, ci1 = c1.y;
