@@ -75,16 +75,19 @@ __host__ __device__ constexpr int pow2_ceil(int n) { return n <= 1 ? 1 : 2 * pow
 // Whole groups of 32 values: in-warp transpose-reduce. A remainder of R < 32 values (padded to P = 2^⌈log2 R⌉):
 // plain butterflies over the lane bits ≥ P (every lane keeps all P values), then the transpose-reduce over the
 // low log2 P bits — about half the instructions of a zero-padded 32-value transpose for R = 4 or 8.
-template <int N>
-__device__ __forceinline__ void warp_partials(const float (&acc)[N], float* red_w, int base, int lane) {
+// Two segments (N1 < N): values [0, N1) go to red_w[base + i], values [N1, N) to red_w[base2 + i − N1] — one
+// reduction for two arrays (a single remainder instead of two).
+template <int N, int N1 = N>
+__device__ __forceinline__ void warp_partials(const float (&acc)[N], float* red_w, int base, int lane, int base2 = 0) {
   constexpr int NF = N / 32, R = N % 32, P = pow2_ceil(R);
+  auto out = [&](int i) { return (N1 >= N || i < N1) ? base + i : base2 + (i - N1); };
 #pragma unroll
   for (int b = 0; b < NF; ++b) {
     float t[32];
 #pragma unroll
     for (int i = 0; i < 32; ++i) t[i] = acc[b * 32 + i];
     const float r = warp_transpose_reduce(t, lane);
-    red_w[base + b * 32 + lane] = r;
+    red_w[out(b * 32 + lane)] = r;
   }
   if constexpr (R > 0) {
     float t[P];
@@ -105,7 +108,7 @@ __device__ __forceinline__ void warp_partials(const float (&acc)[N], float* red_
         t[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
       }
     }
-    if (lane < R) red_w[base + NF * 32 + lane] = t[0];   // lane l (< P) holds element l
+    if (lane < R) red_w[out(NF * 32 + lane)] = t[0];   // lane l (< P) holds element l
   }
 }
 
@@ -442,12 +445,11 @@ uint32_t wadr[NW];
         }
       };
       {
-        float acc[Lay::NP];
-        float accl[8 * (LB > 0 ? LB : 1)];
+        constexpr int NB = Lay::NP + 8 * LB;        // p sums, then the lags [LA, ND): one reduction
+        float acc[NB];
+        float* accl = acc + Lay::NP;
 #pragma unroll
-        for (int i = 0; i < Lay::NP; ++i) acc[i] = 0.f;
-#pragma unroll
-        for (int i = 0; i < 8 * (LB > 0 ? LB : 1); ++i) accl[i] = 0.f;
+        for (int i = 0; i < NB; ++i) acc[i] = 0.f;
 uint32_t wadr[NW];
         make_wadr(wadr);
 #pragma unroll 1
@@ -466,8 +468,7 @@ uint32_t wadr[NW];
         }
         __syncthreads();   // every read of the frame buffer is done: request the next frame (overlaps the reductions)
         if (tid == 0 && fn < n_frames) { issue_y(fn); early = true; }
-        warp_partials<Lay::NP>(acc, red_w, 0, lane);
-        if constexpr (LB > 0) warp_partials<8 * LB>(accl, red_w, Lay::NP + 8 * LA, lane);
+        warp_partials<NB, Lay::NP>(acc, red_w, 0, lane, Lay::NP + 8 * LA);
       }
       }
       __syncthreads();
