@@ -23,7 +23,7 @@ from oracle import theory  # noqa: E402
 from paper_2104_06311_b200 import Receiver  # noqa: E402
 
 F, H = 16384, 16640
-CHUNK = 1 << 28          # bench.py --chunk default
+CHUNK = 1 << 29          # bench.py --chunk default
 
 
 def _run_stream(lc, S, first=0, chunk=CHUNK):
@@ -99,9 +99,9 @@ def test_c4_full_size_sampled():
 
 
 def test_c5_bench_shard_sampled():
-    """The bench workload exactly: 2^32 samples of the mixed-format stream on one GPU in 2^28-sample calls;
+    """The bench workload exactly: 2^32 samples of the mixed-format stream on one GPU in 2^29-sample calls;
     sampled frames include every format, format switches, both ends of the shard and runs straddling call
-    boundaries (16384 frames per call)."""
+    boundaries (32768 frames per call: the pick 2·16384 − 1 straddles the first)."""
     lc = kkgen.WORKLOADS["C5"]["cfg"]
     S = 1 << 32
     nf = S // F
