@@ -13,7 +13,7 @@ NAMES = {"C1": "C1 4-QAM b2b, 2^16", "C2": "C2 16-QAM 5600 km, CSPR 6 dB @ OSNR 
          "C5_ddlms": "C5, paper arrangement (static RRC×CD⁻¹ + 4-tap WL DDLMS)"}
 HDR = """# Results per BASELINE.json configuration (1× B200, {tag})
 
-`bench.py --workload Cx --samples S` (device-resident inputs, calls of min(2^28, S) samples, CUDA-event
+`bench.py --workload Cx --samples S` (device-resident inputs, calls of min(2^29, S) samples, CUDA-event
 timing, clocks 1965 MHz with no throttle reasons in every run). Kernel times are per call (µs, live events
 inside the timed region); "dominant kernel" is the roofline object of the line (algorithmic TFLOP/s — the
 real-arithmetic counts of DESIGN.md §5 — and the fraction of the 74.4 TFLOP/s FP32 peak); the oracle column is
@@ -25,7 +25,7 @@ full sizes is also asserted by `tests/test_gpu_fullsize.py`.
 |---|---|---|---|---|---|---|---|---|---|
 """
 FOOT = """
-C1–C3 are smaller than one 2^28 call, so they are launch/occupancy-bound (C1: 4 frames); throughput is judged
+C1–C3 are smaller than one 2^29 call, so they are launch/occupancy-bound (C1: 4 frames); throughput is judged
 on C4/C5. C4 runs L = 15 taps (10,000 km), hence the slower K3. In the DDLMS row K3 is the sequential 4-tap
 equalizer (one thread per 256-symbol block) and K2 carries the complex static filter and the AGC segment sums;
 in the upsampling row K1 is K1U; from round 2 "K3" is K3a + K3s + K3c. End to end from pinned host memory (C5): the `e2e` /
