@@ -112,17 +112,6 @@ __device__ __forceinline__ void warp_partials(const float (&acc)[N], float* red_
   }
 }
 
-// fp64 sum over the 8 warp partials (per-warp stride `stride` floats) of values [0, n) into dres
-// (call after a __syncthreads).
-__device__ __forceinline__ void cross_warp_sum(const float* red, double* dres, int n, int stride, int tid) {
-  for (int v = tid; v < n; v += K3_THREADS) {
-    double s = 0.0;
-#pragma unroll
-    for (int w = 0; w < K3_WARPS; ++w) s += (double)red[w * stride + v];
-    dres[v] = s;
-  }
-}
-
 template <int K>
 struct K3Layout {
   static constexpr int L = 2 * K + 1;
@@ -184,7 +173,6 @@ __device__ __forceinline__ void tma_tensor_2d(void* dst_smem, const CUtensorMap*
       : "memory");
 }
 
-#define KK_PT(i) do { } while (0)
 
 // per-frame records between the launches: K3a → K3s: the fp64 sums (NRED), g, flags; K3s → K3c: θ₁ (w, v), flags
 template <int K> struct K3Rec {
@@ -209,8 +197,6 @@ k3_frame_kernel(const float2* __restrict__ y, int64_t frame0, int n_frames, cons
   uint8_t* ref_s = smem + Lay::REF;
   float2* us = reinterpret_cast<float2*>(smem + Lay::US);
   float* red = reinterpret_cast<float*>(smem + Lay::RED);
-  double* dres = reinterpret_cast<double*>(smem + Lay::DRES);
-  double* mat = reinterpret_cast<double*>(smem + Lay::MAT);
   float2* th = reinterpret_cast<float2*>(smem + Lay::TH);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + Lay::BAR);
   const int* cc_s = reinterpret_cast<const int*>(smem + Lay::CC);
@@ -540,7 +526,6 @@ uint32_t wadr[NW];
         if (lane == 0) { red_w[0] = gr; red_w[1] = gi; red_w[2] = gd; }
       }
       __syncthreads();
-      KK_PT(5);
       // the frame buffer is dead now (every thread is past sweep C): start the next frame's sample copy so that it
       // overlaps the CPR and the decisions (its labels: already requested (dbl), else at the end of the frame,
       // after the single label buffer is read)
@@ -664,7 +649,6 @@ uint32_t wadr[NW];
     }
     if (tid == 32) misc[2] = m_next;                   // publish the next frame's QAM order
     __syncthreads();   // all reads of ys / ref_s / misc for this frame are done
-    KK_PT(7);
     if (tid == 0) {
       const int nf = fl + (int)gridDim.x;
       if (nf < n_frames) {
