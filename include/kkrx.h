@@ -22,7 +22,9 @@
  *    frees caller memory. Buffers must stay valid until the stream passes the call.
  *  - Every call returns a kk_status; nothing throws across the ABI. Asynchronous kernel faults are
  *    reported at the next synchronising call (kk_stats) as KK_ERR_CUDA.
- *  - One context per (device, stream); calls on one context are not re-entrant.
+ *  - Calls on one context are not re-entrant (one host thread at a time). They may be queued on different
+ *    streams without synchronisation: a call on another stream than the context's previous device call first
+ *    waits (CUDA event) for the work queued there, since the calls share the context's scratch and counters.
  */
 #ifndef KKRX_H
 #define KKRX_H

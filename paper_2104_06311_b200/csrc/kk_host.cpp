@@ -86,6 +86,8 @@ struct kk_ctx {
   int64_t last_first = 0, last_n = 0;
   bool last_z = false;
   cudaStream_t last_stream = nullptr;
+  bool have_stream = false;                         // last_stream holds a call's stream (nullptr = legacy stream)
+  cudaEvent_t order_ev = nullptr;                   // cross-stream ordering of consecutive calls (order_after_last)
   std::string err;
   // debug_guard: canary-padded allocations {name, base, user bytes}
   struct GuardRec { const char* name; unsigned char* base; size_t bytes; };
@@ -367,6 +369,7 @@ void free_all(kk_ctx* c) {
     if (c->ev[i]) cudaEventDestroy(c->ev[i]);
     if (c->entry_ev[i]) cudaEventDestroy(c->entry_ev[i]);
   }
+  if (c->order_ev) cudaEventDestroy(c->order_ev);
 }
 
 }  // namespace
@@ -605,6 +608,18 @@ kk_status kk_eq_taps(const kk_ctx* c, int32_t* taps) {
   return KK_OK;
 }
 
+// Calls share the context's scratch buffers and counters. A call queued on a different stream than the context's
+// previous device call first waits (event) for the work queued there, so callers need not synchronise when they
+// switch streams. The host path's staging streams are exempt: it orders its own sub-calls and synchronises both
+// streams before it returns.
+static void order_after_last(kk_ctx* c, cudaStream_t s) {
+  if (!c->have_stream || s == c->last_stream) return;
+  if (c->last_stream != nullptr && (c->last_stream == c->hs[0] || c->last_stream == c->hs[1])) return;
+  if (!c->order_ev && cudaEventCreateWithFlags(&c->order_ev, cudaEventDisableTiming) != cudaSuccess) return;
+  if (cudaEventRecord(c->order_ev, c->last_stream) == cudaSuccess) cudaStreamWaitEvent(s, c->order_ev, 0);
+}
+static void set_last(kk_ctx* c, cudaStream_t s) { c->last_stream = s; c->have_stream = true; }
+
 kk_status kk_process_frames(kk_ctx* c, const void* d_adc, int64_t first, int64_t n, const uint8_t* d_ref,
                             uint8_t* d_dec, kk_stream_t stream) {
   return kk_process_frames_ex(c, d_adc, first, n, d_ref, d_dec, nullptr, stream);
@@ -621,6 +636,7 @@ kk_status kk_process_frames_ex(kk_ctx* c, const void* d_adc, int64_t first, int6
   if (reinterpret_cast<uintptr_t>(d_adc) % 16) return fail(c, KK_ERR_ALIGN, "kk_process_frames: input not 16-B aligned");
   DeviceGuard g(c->device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  order_after_last(c, s);
   const kk_config& cf = c->cfg;
   const size_t esz = cf.input_dtype == KK_IN_FLOAT32 ? 4 : cf.input_dtype == KK_IN_UINT8 ? 1 : 2;
   const int F = kk::kFrameSamp;
@@ -744,7 +760,7 @@ kk_status kk_process_frames_ex(kk_ctx* c, const void* d_adc, int64_t first, int6
   c->last_first = first;
   c->last_n = n;
   c->last_z = cf.keep_intermediate != 0;
-  c->last_stream = s;
+  set_last(c, s);
   if (e != cudaSuccess) return fail(c, KK_ERR_CUDA, std::string("kk_process_frames: launch: ") + cudaGetErrorString(e));
   return KK_OK;
 }
@@ -803,7 +819,7 @@ kk_status kk_process_frames_host(kk_ctx* c, const void* h_adc, int64_t first, in
   }
   chk(cudaStreamSynchronize(c->hs[0]));
   chk(cudaStreamSynchronize(c->hs[1]));
-  c->last_stream = c->hs[(k - 1) & 1];
+  set_last(c, c->hs[(k - 1) & 1]);
   if (e != cudaSuccess) return fail(c, KK_ERR_CUDA, std::string("kk_process_frames_host: ") + cudaGetErrorString(e));
   return KK_OK;
 }
@@ -823,16 +839,19 @@ kk_status kk_stats(kk_ctx* c, kk_stats_t* out) {
 kk_status kk_stats_device(kk_ctx* c, uint64_t* d_out, kk_stream_t stream) {
   if (!c || !d_out) return KK_ERR_NULL;
   DeviceGuard g(c->device);
+  order_after_last(c, static_cast<cudaStream_t>(stream));
   cudaError_t e = cudaMemcpyAsync(d_out, c->d_counters, KK_STATS_WORDS * 8, cudaMemcpyDeviceToDevice,
                                   static_cast<cudaStream_t>(stream));
+  set_last(c, static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? KK_OK : fail(c, KK_ERR_CUDA, cudaGetErrorString(e));
 }
 
 kk_status kk_reset_stats(kk_ctx* c, kk_stream_t stream) {
   if (!c) return KK_ERR_NULL;
   DeviceGuard g(c->device);
+  order_after_last(c, static_cast<cudaStream_t>(stream));
   cudaError_t e = cudaMemsetAsync(c->d_counters, 0, 32 * sizeof(unsigned long long), static_cast<cudaStream_t>(stream));
-  if (stream) c->last_stream = static_cast<cudaStream_t>(stream);   // the host path orders itself after it
+  set_last(c, static_cast<cudaStream_t>(stream));               // later calls (and the host path) order after it
   return e == cudaSuccess ? KK_OK : fail(c, KK_ERR_CUDA, cudaGetErrorString(e));
 }
 
@@ -858,7 +877,9 @@ kk_status kk_get_intermediate(kk_ctx* c, int stage, void* d_dst, size_t bytes, k
   if (bytes < (size_t)count * 8) return fail(c, KK_ERR_CONFIG, "kk_get_intermediate: destination too small");
   const void* src = stage == KK_STAGE_FIELD ? (const void*)c->d_E : stage == KK_STAGE_MF ? (const void*)c->d_y : (const void*)c->d_z;
   DeviceGuard g(c->device);
+  order_after_last(c, static_cast<cudaStream_t>(stream));
   cudaError_t e = cudaMemcpyAsync(d_dst, src, (size_t)count * 8, cudaMemcpyDeviceToDevice, static_cast<cudaStream_t>(stream));
+  set_last(c, static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? KK_OK : fail(c, KK_ERR_CUDA, cudaGetErrorString(e));
 }
 

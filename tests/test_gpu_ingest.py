@@ -79,3 +79,41 @@ def test_host_path_orders_after_reset_and_caller_stream():
         got = rx.stats()
         assert all(got[k] == want[k] for k in keys), ("legacy stream", got, want)
     rx.close()
+
+
+def test_device_calls_order_across_caller_streams():
+    """Consecutive kk_process_frames / kk_reset_stats / kk_stats_device calls of one context on DIFFERENT caller
+    streams, with no synchronisation between them: each waits for the work the previous call queued (they share
+    the scratch buffers and the counters). The first stream is kept busy (torch.cuda._sleep) so that an unordered
+    call would overtake it: a reset would land before the counts, a second call would overwrite the first's
+    scratch mid-flight."""
+    from gpu_case import F, make_case, receiver_for
+    case = make_case(M=16, dl=112000.0, cspr=10.0, esn0=14.0, n=8 * F, seed=31)
+    codes, ref = case["codes"].cuda(), case["ref"].cuda()
+    rx = receiver_for(case, keep=False, max_samples=4 * F)
+    n, h = case["n"], 4 * F
+    want_dec = torch.empty(n // 4, dtype=torch.uint8, device="cuda")
+    for c0 in range(0, n, h):                               # reference: one stream, synchronised
+        rx.process(codes, case["first"] + c0, h, ref=ref[c0 // 4:(c0 + h) // 4], decisions=want_dec[c0 // 4:(c0 + h) // 4],
+                   offset=c0)
+    want = rx.stats()
+    keys = ("sym", "sym_err", "bits", "bit_err", "frames")
+    sa, sb = torch.cuda.Stream(), torch.cuda.Stream()
+    for _ in range(3):
+        torch.cuda.synchronize()
+        dec = torch.zeros_like(want_dec)
+        cnt = torch.zeros(32, dtype=torch.int64, device="cuda")
+        with torch.cuda.stream(sa):
+            torch.cuda._sleep(50_000_000)
+            rx.reset_stats(stream=sa)
+            rx.process(codes, case["first"], h, ref=ref[:h // 4], decisions=dec[:h // 4], offset=0, stream=sa)
+        # the second half on another stream, then the counters copied on a third (the current) stream
+        rx.process(codes, case["first"] + h, h, ref=ref[h // 4:], decisions=dec[h // 4:], offset=h, stream=sb)
+        rx.stats_device(cnt)
+        torch.cuda.synchronize()
+        got = rx.stats()
+        assert all(got[k] == want[k] for k in keys), (got, want)
+        assert torch.equal(dec, want_dec)
+        # the device copy of the counters (words 0–23, kk_stats_t layout) ran after both calls
+        assert [int(v) for v in cnt[0:5]] == list(got["sym"]) and int(cnt[21]) == got["frames"]
+    rx.close()
