@@ -29,7 +29,9 @@ constexpr int K3D_THREADS = 64;
 // o = (Σ xr·c1 + xi·c2, Σ xr·c3 + xi·c4) and w += μe·conj(x), v += μe·x become c += 2μe ⊗ (xr, xi)
 // (4 FMA per tap for each instead of 8). WL = false: linear taps only (v ≡ 0), complex form.
 template <bool WL>
-__global__ void __launch_bounds__(K3D_THREADS)
+// 8 resident CTAs per SM (≤ 128 registers: 16 warps/SM instead of 14 at 140 registers; the recursion is
+// latency-bound, K3′ −7 %; 10 CTAs would spill)
+__global__ void __launch_bounds__(K3D_THREADS, 8)
 k3_ddlms_kernel(const float2* __restrict__ y, int64_t y_base, int64_t sym_first, int n_blocks, int B, int W,
                 const int* __restrict__ clampcnt, int64_t clamp_frame_off, const uint8_t* __restrict__ ref,
                 uint8_t* __restrict__ dec, float2* __restrict__ zout, unsigned long long* __restrict__ counters,
