@@ -680,7 +680,8 @@ uint32_t wadr[NW];
 template <int K> struct K3S { static constexpr int THREADS = (K3Layout<K>::N <= kGJWarpN) ? 32 : 256; };
 
 template <int K>
-__global__ void __launch_bounds__(K3S<K>::THREADS)
+// one-warp CTAs: 32 resident per SM (64 registers; the solve is latency-bound, −0.35 % of K3 despite 16 B of spill)
+__global__ void __launch_bounds__(K3S<K>::THREADS, (K3S<K>::THREADS == 32 ? 32 : 1))
 k3s_kernel(const double* __restrict__ rec, const float2* __restrict__ y, const float2* __restrict__ w_cd,
            float2* __restrict__ threc, K3Params p) {
   using Lay = K3Layout<K>;
