@@ -119,3 +119,30 @@ def test_c5_second_rank_shard_matches_whole_stream():
     _, _, dec1, _ = _run_stream(lc, S, first=S)
     _, _, dec_all, _ = _run_stream(lc, 2 * S, first=0)
     assert torch.equal(dec1, dec_all[S // 4:])
+
+
+def test_c5_whole_stream_in_one_call_matches_bench_chunking():
+    """Maximum call size: the whole 2^32-sample C5 stream in ONE kk_process_frames call (2^18 frames, 2^31 2-sps
+    MF outputs — every 64-bit index path, the K3 tensor maps over 2^28 rows) decides and counts exactly like the
+    bench's 2^29-sample calls (every grid is anchored at global sample 0)."""
+    lc = kkgen.WORKLOADS["C5"]["cfg"]
+    S = 1 << 32
+    dev = torch.device("cuda", 0)
+    g = kkgen.generate(lc, -H, S + H, device=dev, chunk=1 << 24)
+    codes, ref = g["codes"], g["labels"][H // 4:(H + S) // 4]
+    del g
+    outs = []
+    for chunk in (S, CHUNK):
+        rx = Receiver(adc_scale=lc.adc_scale, ref_intensity=lc.i_ref, dispersion_ps_per_nm=lc.dl_ps_nm,
+                      formats=lc.formats, segment_frames=lc.segment_frames, max_samples_per_call=chunk)
+        dec = torch.empty(S // 4, dtype=torch.uint8, device=dev)
+        for c0 in range(0, S, chunk):
+            rx.process(codes, c0, chunk, ref=ref[c0 // 4:(c0 + chunk) // 4], decisions=dec[c0 // 4:(c0 + chunk) // 4],
+                       offset=c0)
+        outs.append((dec, rx.stats()))
+        rx.close()
+        torch.cuda.empty_cache()
+    (d1, s1), (d2, s2) = outs
+    assert s1 == s2, (s1, s2)
+    assert s1["frames"] == S // F and sum(s1["sym"]) == S // 4
+    assert torch.equal(d1, d2)
