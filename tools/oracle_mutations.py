@@ -71,6 +71,22 @@ MUTATIONS = [
     ("r13_gray_16", "oracle/constellation.py",
      "labs.append((_gray(iI) << half_bits) | _gray(iQ))", "labs.append((iI << half_bits) | _gray(iQ))",
      "R13: natural instead of Gray labels on I"),
+    # (Not listed: the Hilbert multiplier's Nyquist bin set to ±i instead of 0 is an equivalent mutant — for real
+    # input X[N/2] is real, i·X[N/2] contributes a purely imaginary (−1)^n term that `.real` discards.)
+    ("r4_rolloff_x10", "oracle/receiver.py",
+     "    b = cfg.rolloff\n    h = np.zeros(2 * half + 1)", "    b = 10 * cfg.rolloff\n    h = np.zeros(2 * half + 1)",
+     "R4: RRC roll-off 10 % instead of 1 %"),
+    ("r4_rrc_denominator", "oracle/receiver.py",
+     "h[idx] = num / (math.pi * t * (1 - (4 * b * t) ** 2))", "h[idx] = num / (math.pi * t)",
+     "R4: RRC impulse response without its (1 − (4βt)²) denominator"),
+    ("r12_cpr_half_window", "oracle/receiver.py",
+     "    s = (u * np.conj(d)).reshape(-1, W).sum(axis=1)\n    th = np.where(s != 0, np.angle(s), 0.0)\n    return u * np.repeat(np.exp(-1j * th), W), th",
+     "    s = (u * np.conj(d)).reshape(-1, W // 2).sum(axis=1)\n    th = np.where(s != 0, np.angle(s), 0.0)\n    return u * np.repeat(np.exp(-1j * th), W // 2), th",
+     "R12: CPR windows of W/2 symbols"),
+    ("r9_lo_frequency", "oracle/receiver.py",
+     "q = np.mod(cfg.lo_num * np.mod(n, cfg.lo_den), cfg.lo_den)",
+     "q = np.mod((cfg.lo_num - 1) * np.mod(n, cfg.lo_den), cfg.lo_den)",
+     "R9: LO at 0.512 instead of 0.516 GHz"),
     ("seq_ddlms_no_carry", "oracle/receiver.py",
      "            seq_state = seq_next\n", "            seq_state = None\n",
      "NEXT-1: sequential DDLMS state not carried across frames"),
