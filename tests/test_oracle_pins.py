@@ -469,6 +469,24 @@ def test_r25_agc_gain_invariance():
         assert np.max(np.abs(o2["z"] - out["z"])) < 1e-9
 
 
+def test_r7_clamp_floor_relative_to_iref():
+    """R7: the log's floor ε = clamp_rel·I_ref is relative to the reference intensity, so the front end is
+    scale-covariant: scaling the photocurrent AND I_ref by c leaves every clamp decision unchanged and shifts
+    a = ½ ln max(I, ε) by exactly ½ ln c (an absolute floor would clamp different samples at different scales)."""
+    rng = np.random.default_rng(7)
+    I = np.exp(rng.uniform(np.log(1e-6), np.log(1e2), 4096))      # spans the floor ε = 1e-3·I_ref
+    base = _cfg(ref_intensity=1.0)
+    base.clamp_rel = 1e-3
+    a1, _, cl1 = R.o2_front_end(I, base)
+    assert 0 < cl1.sum() < len(I)
+    for c in (1e-4, 1e6):
+        cfg = _cfg(ref_intensity=c)
+        cfg.clamp_rel = 1e-3
+        a2, _, cl2 = R.o2_front_end(I * c, cfg)
+        assert np.array_equal(cl1, cl2)
+        assert np.max(np.abs(a2 - a1 - 0.5 * math.log(c))) < 1e-12
+
+
 # ------------------------------------------------------------------ silent frames (§8(b) bad-frame fallback)
 def test_silent_frames_are_bad_with_zero_output():
     """Frames carrying the tone without modulation (I = I_ref exactly) have e = E − A_f = 0 and no power to

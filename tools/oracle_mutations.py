@@ -87,6 +87,22 @@ MUTATIONS = [
      "q = np.mod(cfg.lo_num * np.mod(n, cfg.lo_den), cfg.lo_den)",
      "q = np.mod((cfg.lo_num - 1) * np.mod(n, cfg.lo_den), cfg.lo_den)",
      "R9: LO at 0.512 instead of 0.516 GHz"),
+    ("r7_eps_not_scaled", "oracle/receiver.py",
+     "def o2_front_end(I: np.ndarray, cfg: OracleConfig):\n    eps = cfg.clamp_rel * cfg.ref_intensity",
+     "def o2_front_end(I: np.ndarray, cfg: OracleConfig):\n    eps = cfg.clamp_rel",
+     "R7: clamp floor ε without the I_ref scale"),
+    ("r25_agc_no_sqrt", "oracle/receiver.py",
+     "    g = 1.0 / math.sqrt(P0)\n", "    g = 1.0 / P0\n",
+     "R25: AGC gain 1/P0 instead of 1/√P0"),
+    ("r10_ridge_unnormalised", "oracle/receiver.py",
+     "lam = cfg.eq_ridge * np.real(np.trace(R)) / n_par", "lam = cfg.eq_ridge * np.real(np.trace(R))",
+     "R10: ridge λ = ridge·tr(R) without the 1/(2L)"),
+    ("r27_unbias_by_output_power", "oracle/receiver.py",
+     "gam = np.sum(y1 * np.conj(d1)) / np.sum(np.abs(d1) ** 2)", "gam = np.sum(y1 * np.conj(d1)) / np.sum(np.abs(y1) ** 2)",
+     "R27: γ normalised by the output power instead of the decisions'"),
+    ("r10_training_on_unscaled", "oracle/receiver.py",
+     "    # (4) pass 1 and decisions\n    y0 = Phi @ th0\n", "    # (4) pass 1 and decisions\n    y0 = Phi @ (th0 / g)\n",
+     "R10/R25: training decisions on the pass-1 output before the AGC"),
     ("seq_ddlms_no_carry", "oracle/receiver.py",
      "            seq_state = seq_next\n", "            seq_state = None\n",
      "NEXT-1: sequential DDLMS state not carried across frames"),
