@@ -291,6 +291,21 @@ def test_uint8_adc_input():
     _check_all(case8, gpu, orc)
 
 
+def test_adc_offset():
+    """O1 with a nonzero ADC offset (kk_config.adc_offset: I = adc_scale·(code − adc_offset)): int16 codes
+    shifted by −1000 with adc_offset = −1000 — the same parity bar against the oracle run on the shifted codes."""
+    from gpu_case import receiver_for
+    from oracle import receiver as R
+    case = make_case(M=16, dl=32000.0, cspr=12.0, esn0=18.0, n=4 * F, seed=47)
+    o = case["ocfg"]
+    ocfg = R.OracleConfig(dispersion_ps_per_nm=case["dl"], adc_scale=o.adc_scale, ref_intensity=o.ref_intensity,
+                          formats=case["formats"], adc_offset=-1000.0)
+    case_o = dict(case, codes=(case["codes"].to(torch.int32) - 1000).to(torch.int16), ocfg=ocfg)
+    rx = receiver_for(case_o, keep=True, adc_offset=-1000.0)
+    gpu, orc = run_gpu(case_o, rx=rx), run_oracle(case_o)
+    _check_all(case_o, gpu, orc)
+
+
 @pytest.mark.parametrize("eq_mode", ["block_ls", "ddlms"])
 def test_per_frame_errors(eq_mode):
     case = make_case(M=64, dl=32000.0, cspr=12.0, esn0=22.0, n=6 * F, seed=43, eq_mode=eq_mode)

@@ -469,6 +469,29 @@ def test_r25_agc_gain_invariance():
         assert np.max(np.abs(o2["z"] - out["z"])) < 1e-9
 
 
+def test_o1_adc_offset_is_subtracted():
+    """O1 (kkrx.h kk_config.adc_offset: I = adc_scale·(code − adc_offset)): codes shifted by k with adc_offset = k
+    describe the same intensities — the whole chain's output is unchanged."""
+    out, cfg, g, ref = _chain(16, dl=32000.0, esn0=20.0, n=2 * 16384)
+    k = 1000.0
+    cfg2 = _cfg(dispersion_ps_per_nm=32000.0, adc_scale=cfg.adc_scale, ref_intensity=cfg.ref_intensity,
+                formats=(16,), adc_offset=k)
+    o2 = R.receive(g["codes"].numpy().astype(np.float64) + k, 2 * 16384, 2 * 16384, cfg2, ref=ref)
+    assert np.array_equal(o2["dec"], out["dec"])
+    assert np.max(np.abs(o2["z"] - out["z"])) < 1e-9
+
+
+def test_o10_bit_errors_are_label_bit_flips():
+    """O10: bit errors count flipped label bits, not symbols. Noiseless b2b 16-QAM decides every transmitted
+    label; against references with two label bits flipped (ref XOR 0b0101) every symbol is one symbol error
+    and exactly two bit errors."""
+    out, cfg, g, ref = _chain(16, dl=0.0, esn0=None, n=16384)
+    assert out["counts"]["sym_err"].sum() == 0
+    o2 = R.receive(g["codes"].numpy(), 2 * 16384, 16384, cfg, ref=(ref ^ 0b0101).astype(ref.dtype))
+    n = 16384 // 4
+    assert o2["counts"]["sym_err"].sum() == n and o2["counts"]["bit_err"].sum() == 2 * n
+
+
 def test_r7_clamp_floor_relative_to_iref():
     """R7: the log's floor ε = clamp_rel·I_ref is relative to the reference intensity, so the front end is
     scale-covariant: scaling the photocurrent AND I_ref by c leaves every clamp decision unchanged and shifts

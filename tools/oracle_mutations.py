@@ -103,6 +103,21 @@ MUTATIONS = [
     ("r10_training_on_unscaled", "oracle/receiver.py",
      "    # (4) pass 1 and decisions\n    y0 = Phi @ th0\n", "    # (4) pass 1 and decisions\n    y0 = Phi @ (th0 / g)\n",
      "R10/R25: training decisions on the pass-1 output before the AGC"),
+    ("o1_offset_sign", "oracle/receiver.py",
+     "return cfg.adc_scale * (codes.astype(np.float64) - cfg.adc_offset)",
+     "return cfg.adc_scale * (codes.astype(np.float64) + cfg.adc_offset)",
+     "O1: ADC offset added instead of subtracted"),
+    ("r9_lo_phase_origin", "oracle/receiver.py",
+     "    q = np.mod(cfg.lo_num * np.mod(n, cfg.lo_den), cfg.lo_den)\n    return e",
+     "    q = np.mod(cfg.lo_num * np.mod(n + 1, cfg.lo_den), cfg.lo_den)\n    return e",
+     "R9: LO phase origin one sample off the global grid"),
+    ("r4_half_span", "oracle/receiver.py",
+     "    half = cfg.rrc_span_sym * sps // 2\n", "    half = cfg.rrc_span_sym * sps // 4\n",
+     "R4: RRC truncated to half the span"),
+    ("o10_bits_as_symbols", "oracle/receiver.py",
+     "frame_err[fi] = (int(np.sum(lab != r)), int(np.sum(popcount(lab ^ r))))",
+     "frame_err[fi] = (int(np.sum(lab != r)), int(np.sum(lab != r)))",
+     "O10: bit errors counted as symbol errors"),
     ("seq_ddlms_no_carry", "oracle/receiver.py",
      "            seq_state = seq_next\n", "            seq_state = None\n",
      "NEXT-1: sequential DDLMS state not carried across frames"),
