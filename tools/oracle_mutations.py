@@ -118,6 +118,28 @@ MUTATIONS = [
      "frame_err[fi] = (int(np.sum(lab != r)), int(np.sum(popcount(lab ^ r))))",
      "frame_err[fi] = (int(np.sum(lab != r)), int(np.sum(lab != r)))",
      "O10: bit errors counted as symbol errors"),
+    ("r13_qam_norm", "oracle/constellation.py",
+     "norm = math.sqrt(2.0 * (M - 1) / 3.0)", "norm = math.sqrt(2.0 * (M - 1) / 3.0) * 1.05",
+     "R13: square-QAM points not at unit mean energy"),
+    ("next2_cd_sign", "oracle/receiver.py",
+     "    nu = np.fft.fftfreq(N, d=1.0 / cfg.fs_hz)\n    f_c = cfg.fs_hz * cfg.lo_num / cfg.lo_den\n    C = np.exp(-1j * (beta2L(cfg) / 2) * (2 * np.pi * (nu + cfg.sideband * f_c)) ** 2)",
+     "    nu = np.fft.fftfreq(N, d=1.0 / cfg.fs_hz)\n    f_c = cfg.fs_hz * cfg.lo_num / cfg.lo_den\n    C = np.exp(1j * (beta2L(cfg) / 2) * (2 * np.pi * (nu + cfg.sideband * f_c)) ** 2)",
+     "NEXT-2: static filter applies CD instead of its inverse"),
+    ("next2_cd_no_carrier_ref", "oracle/receiver.py",
+     "    nu = np.fft.fftfreq(N, d=1.0 / cfg.fs_hz)\n    f_c = cfg.fs_hz * cfg.lo_num / cfg.lo_den\n    C = np.exp(-1j * (beta2L(cfg) / 2) * (2 * np.pi * (nu + cfg.sideband * f_c)) ** 2)",
+     "    nu = np.fft.fftfreq(N, d=1.0 / cfg.fs_hz)\n    f_c = cfg.fs_hz * cfg.lo_num / cfg.lo_den\n    C = np.exp(-1j * (beta2L(cfg) / 2) * (2 * np.pi * nu) ** 2)",
+     "NEXT-2: CD inverse referenced to baseband instead of the carrier"),
+    ("r5_theta0_cd_sign", "oracle/receiver.py",
+     "    A = np.exp(-2j * np.pi * np.outer(nu, j) / (2 * cfg.baud_hz))\n    C = np.exp(-1j * (beta2L(cfg) / 2) * (2 * np.pi * (nu + cfg.sideband * f_c)) ** 2)",
+     "    A = np.exp(-2j * np.pi * np.outer(nu, j) / (2 * cfg.baud_hz))\n    C = np.exp(1j * (beta2L(cfg) / 2) * (2 * np.pi * (nu + cfg.sideband * f_c)) ** 2)",
+     "θ₀: the initial FIR approximates CD instead of its inverse"),
+    ("seq_ddlms_update_sign", "oracle/receiver.py",
+     "        out[i] = o\n        w = w + mu * e * np.conj(x)\n", "        out[i] = o\n        w = w - mu * e * np.conj(x)\n",
+     "NEXT-1: sequential DDLMS gradient step of the wrong sign"),
+    ("seq_ddlms_v_branch", "oracle/receiver.py",
+     "        if cfg.eq_widely_linear:\n            v = v + mu * e * x\n        cnt += 1",
+     "        if cfg.eq_widely_linear:\n            v = v + mu * e * np.conj(x)\n        cnt += 1",
+     "NEXT-1: widely-linear branch updated with conj(x)"),
     ("seq_ddlms_no_carry", "oracle/receiver.py",
      "            seq_state = seq_next\n", "            seq_state = None\n",
      "NEXT-1: sequential DDLMS state not carried across frames"),
