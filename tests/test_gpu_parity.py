@@ -306,6 +306,23 @@ def test_adc_offset():
     _check_all(case_o, gpu, orc)
 
 
+def test_joint_intensity_scale():
+    """The oracle's joint-scale covariance pin on the GPU: photocurrent (adc_scale) and I_ref both scaled by
+    2^-80 ≈ 8e-25 — every clamp/silent threshold is relative to I_ref, so the fp32 path still meets the parity
+    bar against the oracle of the scaled case (no frame turns silent, no sample clamps)."""
+    from gpu_case import receiver_for
+    from oracle import receiver as R
+    c = 2.0 ** -80
+    case = make_case(M=16, dl=32000.0, cspr=12.0, esn0=18.0, n=4 * F, seed=53)
+    o = case["ocfg"]
+    ocfg = R.OracleConfig(dispersion_ps_per_nm=case["dl"], adc_scale=o.adc_scale * c, ref_intensity=o.ref_intensity * c,
+                          formats=case["formats"])
+    case_s = dict(case, ocfg=ocfg)
+    gpu, orc = run_gpu(case_s, rx=receiver_for(case_s, keep=True)), run_oracle(case_s)
+    assert gpu["stats"]["bad_frames"] == 0 and orc["counts"]["bad_frames"] == 0
+    _check_all(case_s, gpu, orc)
+
+
 @pytest.mark.parametrize("eq_mode", ["block_ls", "ddlms"])
 def test_per_frame_errors(eq_mode):
     case = make_case(M=64, dl=32000.0, cspr=12.0, esn0=22.0, n=6 * F, seed=43, eq_mode=eq_mode)

@@ -492,6 +492,20 @@ def test_o10_bit_errors_are_label_bit_flips():
     assert o2["counts"]["sym_err"].sum() == n and o2["counts"]["bit_err"].sum() == 2 * n
 
 
+def test_chain_covariant_under_joint_intensity_scale():
+    """R7 + silent-frame rule: every threshold of the chain is relative to I_ref, so scaling the photocurrent
+    (adc_scale) AND I_ref by the same c — here 1e-24, far below any absolute float threshold — leaves every
+    decision unchanged: E, e and y scale by √c, the AGC divides it out; no frame turns silent or clamped."""
+    out, cfg, g, ref = _chain(16, dl=32000.0, esn0=20.0, n=2 * 16384)
+    for c in (1e-24, 1e12):
+        cfg2 = _cfg(dispersion_ps_per_nm=32000.0, adc_scale=cfg.adc_scale * c, ref_intensity=cfg.ref_intensity * c,
+                    formats=(16,))
+        o2 = R.receive(g["codes"].numpy(), 2 * 16384, 2 * 16384, cfg2, ref=ref)
+        assert o2["counts"]["bad_frames"] == 0 and o2["counts"]["clamped"] == out["counts"]["clamped"]
+        assert np.array_equal(o2["dec"], out["dec"])
+        assert np.max(np.abs(o2["z"] - out["z"])) < 1e-9
+
+
 def test_r7_clamp_floor_relative_to_iref():
     """R7: the log's floor ε = clamp_rel·I_ref is relative to the reference intensity, so the front end is
     scale-covariant: scaling the photocurrent AND I_ref by c leaves every clamp decision unchanged and shifts

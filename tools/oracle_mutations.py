@@ -140,6 +140,20 @@ MUTATIONS = [
      "        if cfg.eq_widely_linear:\n            v = v + mu * e * x\n        cnt += 1",
      "        if cfg.eq_widely_linear:\n            v = v + mu * e * np.conj(x)\n        cnt += 1",
      "NEXT-1: widely-linear branch updated with conj(x)"),
+    ("r26_schedule_shift", "oracle/receiver.py",
+     "return int(self.formats[(f // self.segment_frames) % len(self.formats)])",
+     "return int(self.formats[((f + 1) // self.segment_frames) % len(self.formats)])",
+     "R26: format schedule one frame early"),
+    ("pu_halfband_centre", "oracle/receiver.py",
+     "    f[k == 0] = 0.5\n", "    f[k == 0] = 1.0\n",
+     "KK upsampling: half-band centre tap 1 instead of ½ (DC gain 1.5)"),
+    ("silent_threshold_absolute", "oracle/receiver.py",
+     "if not (P0 > cfg.p0_min_rel * cfg.ref_intensity and np.isfinite(P0)):",
+     "if not (P0 > cfg.p0_min_rel and np.isfinite(P0)):",
+     "silent-frame rule: power threshold not relative to I_ref"),
+    # (Not listed: the restart form's μ schedule reversed — μ_warm on the kept symbols — still passes the
+    # restart-vs-sequential pin (≥ 99.9 % identical decisions, Q within 0.1 dB): at the pinned shapes the
+    # schedule's effect (steady-state misadjustment ∝ μ) is below the pins' resolution. A tuning reading.)
     ("seq_ddlms_no_carry", "oracle/receiver.py",
      "            seq_state = seq_next\n", "            seq_state = None\n",
      "NEXT-1: sequential DDLMS state not carried across frames"),
