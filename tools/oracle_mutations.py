@@ -154,6 +154,17 @@ MUTATIONS = [
     # (Not listed: the restart form's μ schedule reversed — μ_warm on the kept symbols — still passes the
     # restart-vs-sequential pin (≥ 99.9 % identical decisions, Q within 0.1 dB): at the pinned shapes the
     # schedule's effect (steady-state misadjustment ∝ μ) is below the pins' resolution. A tuning reading.)
+    ("p11_noise_per_axis", "oracle/theory.py",
+     "sig = math.sqrt(n0 / 2.0)                         # per-axis std",
+     "sig = math.sqrt(n0)                               # per-axis std",
+     "P11: closed-form BER with the full N0 on each axis"),
+    ("p11_natural_labels", "oracle/theory.py",
+     "e_axis = sum(P[i, j] * _hd(gray(i), gray(j)) for i in range(m) for j in range(m)) / m",
+     "e_axis = sum(P[i, j] * _hd(i, j) for i in range(m) for j in range(m)) / m",
+     "P11: closed-form square-QAM BER with natural instead of Gray label distances"),
+    ("p11_8qam_bits", "oracle/theory.py",
+     "return (eI + eQ) / 3.0", "return (eI + eQ) / 2.0",
+     "P11: 8-QAM BER divided by 2 bits instead of 3"),
     ("seq_ddlms_no_carry", "oracle/receiver.py",
      "            seq_state = seq_next\n", "            seq_state = None\n",
      "NEXT-1: sequential DDLMS state not carried across frames"),
