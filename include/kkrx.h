@@ -24,7 +24,8 @@
  *    reported at the next synchronising call (kk_stats) as KK_ERR_CUDA.
  *  - Calls on one context are not re-entrant (one host thread at a time). They may be queued on different
  *    streams without synchronisation: a call on another stream than the context's previous device call first
- *    waits (CUDA event) for the work queued there, since the calls share the context's scratch and counters.
+ *    waits (CUDA event) for the work queued there, since the calls share the context's scratch and counters
+ *    (a caller that destroys that stream first must synchronise it: its pending work can no longer be waited on).
  */
 #ifndef KKRX_H
 #define KKRX_H

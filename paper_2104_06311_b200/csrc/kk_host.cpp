@@ -617,6 +617,7 @@ static void order_after_last(kk_ctx* c, cudaStream_t s) {
   if (c->last_stream != nullptr && (c->last_stream == c->hs[0] || c->last_stream == c->hs[1])) return;
   if (!c->order_ev && cudaEventCreateWithFlags(&c->order_ev, cudaEventDisableTiming) != cudaSuccess) return;
   if (cudaEventRecord(c->order_ev, c->last_stream) == cudaSuccess) cudaStreamWaitEvent(s, c->order_ev, 0);
+  else (void)cudaGetLastError();   // e.g. the caller destroyed that stream: not an error of this call
 }
 static void set_last(kk_ctx* c, cudaStream_t s) { c->last_stream = s; c->have_stream = true; }
 
