@@ -76,13 +76,27 @@ MUTATIONS = [
      "  const uint32_t n1 = ((w >> 3) ^ w) & m28;                      // b[31 .. 58]",
      "  const uint32_t n1 = ((w >> 2) ^ w) & m28;                      // b[31 .. 58]",
      "kref: PRBS-31 feedback tap x^29 instead of x^28"),
+    ("k1u_hilbert_sign", "k1u_kk.cu",
+     "v[k] = h ? make_float2(-x.y, x.x) : make_float2(x.y, -x.x);",
+     "v[k] = h ? make_float2(x.y, -x.x) : make_float2(-x.y, x.x);",
+     "K1U: Hilbert multiplier +i·sgn instead of −i·sgn (2× upsampling path)"),
+    ("k2_ch_fold_alias_dropped", "k2_mf.cu",
+     "            cmac2(yv, b, __ldg(&Hc[j + 256 * (r + R3 / 2)]));\n", "",
+     "K2 (complex H, static-CD/DDLMS arrangements): the fold's alias term dropped"),
+    ("k3a_second_lag_pass_offset", "k3_eq.cu",
+     "              lag_acc(acc2, w, LA1, LA - LA1);", "              lag_acc(acc2, w, LA1 - 1, LA - LA1);",
+     "K3a (L ≥ 11): the second lag pass starts one lag early"),
+    # (Not listed: K3a's silent flag dropped is equivalent on every fp32-reachable input — a frame with
+    # P0 ≤ 1e-20·I_ref has y ≡ 0 in fp32, and the unflagged frame's failed solve (θ₀ fallback, counted bad)
+    # outputs the same z = 0 and D(0).)
 ]
 
 TESTS = ["tests/test_gpu_parity.py", "-x", "-q", "-k",
          "c1_b2b or format_parity or q_parity_large or uint8 or linear_only or per_frame_errors or decision_paths "
-         "or ddlms_mode_parity"]
-# the reference-label generator is checked by its own tests
+         "or ddlms_mode_parity or unaligned_reference_labels"]
+# the reference-label generator, the upsampling path and the silent-frame rule have their own test files
 TESTS_REF = ["tests/test_gpu_refprbs.py", "-x", "-q"]
+TESTS_UP = ["tests/test_gpu_upsample.py", "-x", "-q"]
 
 
 def build(names):
@@ -115,7 +129,7 @@ def build(names):
 def run(names, out):
     results = []
     t0 = time.time()                                      # the unmutated library must pass the same subset
-    for tests in (TESTS, TESTS_REF):
+    for tests in (TESTS, TESTS_REF, TESTS_UP):
         r = subprocess.run([sys.executable, "-m", "pytest", *tests], cwd=ROOT, capture_output=True, text=True)
         print(f"{'(unmutated library)':26s} {'passes' if r.returncode == 0 else 'FAILS'} {tests[0]} "
               f"({time.time() - t0:.0f} s)", flush=True)
@@ -130,7 +144,7 @@ def run(names, out):
             results.append(dict(name=name, what=what, status="not-built"))
             continue
         t0 = time.time()
-        tests = TESTS_REF if fn == "kref.cu" else TESTS
+        tests = TESTS_REF if fn == "kref.cu" else TESTS_UP if fn == "k1u_kk.cu" else TESTS
         r = subprocess.run([sys.executable, "-m", "pytest", *tests], cwd=ROOT, env=dict(os.environ, KK_LIB=lib),
                            capture_output=True, text=True)
         failed = [ln.split("::")[1].split()[0] for ln in r.stdout.splitlines() if ln.startswith("FAILED")]
